@@ -1,0 +1,236 @@
+/*
+ * dsp.h — C ABI of the B200-native Dynamic Sequence Parallelism (DSP) hot path.
+ *
+ * Paper: "DSP: Dynamic Sequence Parallelism for Multi-Dimensional Transformers"
+ * (arXiv 2403.10266).  Citations: P:n = line n of PAPER.md, S:n = line n of
+ * SPEC.md (interfaces only), R<k> = reading k in DESIGN.md §Readings.
+ *
+ * What the library computes (§3.1 System Design): the forward of one
+ * spatial-temporal (ST) transformer block whose activation X[B,T,S,C] (row-major,
+ * C innermost) is sharded over N ranks along ONE sequence dimension.  Spatial
+ * attention runs locally on T-shards; a dynamic switch ("a single AlltoAll
+ * operation ... when transitioning between computation stages") re-shards
+ * T->S; temporal attention and the MLP run locally on S-shards; a second switch
+ * goes back S->T ("two AlltoAll operations in total").
+ *
+ * Conventions (apply to every call unless stated):
+ *  - Pointers: arguments named *_dev / x_* / y_* / w_* / out / residual are DEVICE
+ *    pointers; arguments named *_host are HOST pointers (pinned memory recommended).
+ *    All device pointers must be 16-byte aligned.
+ *  - Layout: activations are contiguous row-major [B, T_local, S_local, C].  Rank r
+ *    holds the r-th contiguous chunk of the sharded axis (R11).  Weights use
+ *    the nn.Linear [out, in] layout; inside w_qkv rows [0,C) are q, [C,2C) k, [2C,3C) v
+ *    and head j owns rows j*Dh..(j+1)*Dh-1 of each (R8).
+ *  - Shapes: dsp_shape_t holds the GLOBAL shape and must be identical on all ranks.
+ *  - Dtypes: DSP_BF16 is the product path (bf16 storage, fp32 accumulation/softmax);
+ *    DSP_F32 is the fp32 check path (SIMT kernels, for the 1e-4 gate).
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    stream-ordered and asynchronous unless marked HOST-ONLY or SYNCHRONOUS; there is
+ *    no host synchronisation and no allocation on the hot path.
+ *  - Ownership: the caller owns every buffer (allocate with torch or cudaMalloc).  A
+ *    context BORROWS the NCCL communicator and peer pointers; it owns host state only.
+ *  - Collective calls (dsp_gather, dsp_switch, dsp_st_block_forward*) must be entered
+ *    by all N ranks in the same order with identical shape / dims / impl.
+ *    Argument validation depends only on those identical arguments, so every rank
+ *    returns the same error BEFORE any communication is enqueued.
+ *  - Errors: every call returns dsp_status_t; nothing throws across the ABI.  Detail
+ *    text for the last non-OK status of a context: dsp_last_error(ctx).  CUDA / NCCL
+ *    failures map to DSP_ERR_CUDA / DSP_ERR_NCCL.
+ *  - Determinism: split/switch/gather move bytes only and are bit-exact.  Compute
+ *    kernels use no atomics and no split-K: outputs are run-to-run deterministic and
+ *    independent of N (each output element's reduction order depends only on C, Dh, L).
+ */
+#ifndef DSP_H_
+#define DSP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dsp_ctx* dsp_ctx_t;
+
+typedef enum {
+  DSP_OK = 0,
+  DSP_ERR_NULL = 1,          /* a required pointer is NULL */
+  DSP_ERR_SHAPE = 2,         /* invalid shape (non-positive extent, C % num_heads != 0) */
+  DSP_ERR_DIVISIBILITY = 3,  /* N does not divide T or S (R12) */
+  DSP_ERR_SAME_DIM = 4,      /* switch from a dim to itself */
+  DSP_ERR_BAD_DIM = 5,       /* dim is not DSP_DIM_T / DSP_DIM_S */
+  DSP_ERR_UNSUPPORTED = 6,   /* valid request this build does not implement (reason in dsp_last_error) */
+  DSP_ERR_ALIGNMENT = 7,     /* pointer not 16-B aligned or row bytes not a multiple of 16 */
+  DSP_ERR_ALIAS = 8,         /* input and output buffers overlap where they must not */
+  DSP_ERR_WORKSPACE = 9,     /* workspace missing or smaller than dsp_workspace_bytes() */
+  DSP_ERR_CUDA = 10,         /* CUDA runtime / launch failure */
+  DSP_ERR_NCCL = 11,         /* NCCL failure or NCCL not available for world > 1 */
+  DSP_ERR_STATE = 12         /* context misuse (wrong device, peer buffers not set, ...) */
+} dsp_status_t;
+
+typedef enum { DSP_DIM_T = 1, DSP_DIM_S = 2 } dsp_dim_t;   /* axis index in [B,T,S,C] */
+typedef enum { DSP_BF16 = 0, DSP_F32 = 1 } dsp_dtype_t;
+/* Switch transport.  Explicit choice, no heuristic dispatch.
+ * NCCL: pack kernel -> ncclAlltoAll (bytes) -> unpack kernel (identity sides skipped).
+ * P2P : direct NVLink stores into the peers' symmetric buffers + signal-pad barriers. */
+typedef enum { DSP_SWITCH_NCCL = 0, DSP_SWITCH_P2P = 1 } dsp_switch_impl_t;
+
+/* GLOBAL shape of the activation; identical on all ranks. */
+typedef struct {
+  int64_t B, T, S, C;
+  int32_t num_heads;
+  dsp_dtype_t dtype;
+} dsp_shape_t;
+
+/* Weights of one ST block (MHA + MLP, LayerNorm before each layer, residuals),
+ * all device pointers in shape->dtype, nn.Linear [out,in] layout, no biases (R4). */
+typedef struct {
+  const void *ln1_w, *ln1_b, *w_qkv_s /*[3C,C]*/, *w_o_s /*[C,C]*/;
+  const void *ln2_w, *ln2_b, *w_qkv_t /*[3C,C]*/, *w_o_t /*[C,C]*/;
+  const void *ln3_w, *ln3_b, *w_fc1 /*[4C,C]*/, *w_fc2 /*[C,4C]*/;
+  float ln_eps;                                    /* 1e-5 (R3) */
+} dsp_block_weights_t;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create a context on CUDA device `device` for rank `rank` of `world`.
+ * nccl_comm: an ncclComm_t BORROWED from torch's ProcessGroupNCCL (_comm_ptr());
+ * may be NULL when world == 1.  Never destroyed by dsp.  NCCL symbols are resolved at
+ * run time from the libnccl.so.2 already loaded in the process (or $DSP_NCCL_LIBRARY).
+ * Errors: NULL (out), SHAPE (world < 1, rank out of range), NCCL (world > 1 and no
+ * comm or NCCL not loadable), CUDA (bad device).  SYNCHRONOUS. */
+dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, dsp_ctx_t* out);
+/* Destroy host state of the context.  Does not free caller buffers or the comm. */
+dsp_status_t dsp_ctx_destroy(dsp_ctx_t ctx);
+
+/* HOST-ONLY, pure: bytes of workspace dsp_st_block_forward needs per rank:
+ * tok_r * 6C * elem + 256 where tok_r = B*T*S/world (h: C, qkv+o / MLP hidden: 4C,
+ * S-sharded activation: C; the switch send/recv buffers alias dead regions). */
+size_t dsp_workspace_bytes(const dsp_shape_t* shape, int world);
+/* Attach caller-owned device workspace (kept by pointer, not copied). */
+dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* workspace_dev, size_t bytes);
+
+/* P2P switch only.  peer_base_dev[i] / peer_signal_dev[i] (HOST arrays of `world`
+ * device pointers, copied into the context) are rank i's symmetric data buffer and
+ * signal pad as mapped in THIS process (torch symmetric memory buffer_ptrs /
+ * signal_pad_ptrs, or cudaIpc mappings).  Every rank's data buffer has `bytes` bytes at
+ * the same offsets; signal pads need >= 2*world*8 bytes, zero-initialised.
+ * The switch destination (or the block's internal buffers) must lie inside the local
+ * data buffer peer_base_dev[rank].  For tests, several "virtual ranks" may share one
+ * device: pass one context per virtual rank. */
+dsp_status_t dsp_ctx_set_peer_buffers(dsp_ctx_t ctx, void* const* peer_base_dev,
+                                      void* const* peer_signal_dev, size_t bytes);
+
+const char* dsp_status_str(dsp_status_t status);
+const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
+int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
+#define DSP_ABI_VERSION 1
+
+/* ----------------------------------------------------------- layout (bytes) */
+
+/* x_local <- chunk `rank` of x_global along `dim` (R11).  Local, bit-exact.
+ * x_global [B,T,S,C] device; x_local [B,T/N,S,C] (dim T) or [B,T,S/N,C] (dim S).
+ * Errors: BAD_DIM, DIVISIBILITY, ALIGNMENT, ALIAS (overlap). */
+dsp_status_t dsp_split(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t dim,
+                       const void* x_global, void* x_local, void* stream);
+
+/* x_global <- concatenation in rank order along `dim`.  COLLECTIVE.
+ * ncclAllGather of the local shards; when the rank-major [N][local] order equals the
+ * global layout (dim T with B == 1) it lands directly in x_global, otherwise it lands
+ * in the workspace (>= B*T*S*C*elem bytes) and an unpack kernel scatters the runs.
+ * N == 1: a device copy.  Errors: as dsp_split; WORKSPACE; NCCL. */
+dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t dim,
+                        const void* x_local, void* x_global, void* stream);
+
+/* The dynamic switch (§3.1; Fig. 2).  COLLECTIVE.
+ * Pre: x_local is the `from_dim` chunk `rank` of a global X.  Post: y_local is the
+ * `to_dim` chunk `rank` of the same X, bit-identical bytes.  For from=T,to=S:
+ *   y[b, r*Tn + t', s', c] = (chunk received from rank r)[b, t', s', c], i.e.
+ *   Y_q[b,t,s',c] = X[b,t,q*Sn+s',c]   (SURVEY §8a "The switch as an exact index map").
+ * Volume: (N-1)*B*(T/N)*(S/N)*C elements sent and received per rank.
+ * impl NCCL: uses the workspace (>= 2*B*T*S*C/N*elem bytes) for pack/recv staging.
+ * impl P2P : y_local must lie inside the registered symmetric buffer.
+ * N == 1: a device copy (no-op if x == y).
+ * Errors: SAME_DIM, BAD_DIM, DIVISIBILITY, ALIGNMENT (C*elem % 16), ALIAS
+ * (x overlaps y, N > 1), WORKSPACE, STATE (P2P without peer buffers), NCCL. */
+dsp_status_t dsp_switch(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t from_dim,
+                        dsp_dim_t to_dim, const void* x_local, void* y_local,
+                        dsp_switch_impl_t impl, void* stream);
+
+/* HOST-ONLY, pure: off-rank bytes one switch sends and receives per rank,
+ * (N-1)*B*(T/N)*(S/N)*C*elem each (self-chunk excluded). */
+dsp_status_t dsp_switch_volume(const dsp_shape_t* shape, int world,
+                               int64_t* bytes_sent_per_rank, int64_t* bytes_recv_per_rank);
+
+/* HOST-ONLY, pure: the byte-run plan of one switch on `rank` — the host logic every
+ * transport executes.  A switch moves n0*n1*n2 runs of run_bytes contiguous bytes;
+ * run (i0,i1,i2) (i0 = peer, i1 = b, i2 = t') is read at
+ *   src_off = i0*src_stride[0] + i1*src_stride[1] + i2*src_stride[2]
+ * of this rank's x_local and written to
+ *   dst_off = i1*dst_stride[1] + i2*dst_stride[2] + dst_peer_off
+ * of PEER i0's y_local, where dst_peer_off = rank*dst_stride[0] (the slot this rank
+ * fills on every peer).  The NCCL transport realises it as pack (to chunk order
+ * [peer][b][t'][s'][c]) + AlltoAll + unpack; the P2P transport stores directly. */
+typedef struct {
+  int64_t n[3];
+  int64_t run_bytes;
+  int64_t src_stride[3];
+  int64_t dst_stride[3];
+  int64_t dst_peer_off;
+  int32_t pack_is_identity;     /* chunk order == x_local layout (no pack kernel) */
+  int32_t unpack_is_identity;   /* chunk order == y_local layout (no unpack kernel) */
+} dsp_switch_plan_t;
+dsp_status_t dsp_switch_plan(const dsp_shape_t* shape, int world, int rank,
+                             dsp_dim_t from_dim, dsp_dim_t to_dim, dsp_switch_plan_t* plan);
+
+/* --------------------------------------------------- local attention stages */
+
+/* out = (residual ? residual : 0) + MHA_S(h): spatial multi-head self-attention, one
+ * sequence over S per (b, t), on a T-sharded h_local [B, T/N, S, C].
+ * MHA(h) = concat_j softmax(q_j k_j^T / sqrt(Dh)) v_j  * w_o^T with [q|k|v] = h w_qkv^T
+ * (R6-R8).  No LayerNorm inside.  Local (no communication).  Uses the workspace for
+ * qkv and O (tok_r * 4C * elem bytes).  out may equal residual; out must not overlap h.
+ * bf16: tcgen05 QKV GEMM -> tcgen05 FMHA -> tcgen05 out-proj GEMM (+residual epilogue).
+ * Errors: SHAPE (C % num_heads), UNSUPPORTED (bf16 needs Dh % 16 == 0 or Dh in {72}
+ * ... see dsp_last_error; C % 64 == 0), ALIAS, WORKSPACE, DIVISIBILITY. */
+dsp_status_t dsp_spatial_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local,
+                              const void* w_qkv, const void* w_o, const void* residual,
+                              void* out, void* stream);
+
+/* As dsp_spatial_attn, temporal: one sequence over T per (b, s) on an S-sharded
+ * h_local [B, T, S/N, C] (frame stride S/N*C elements). */
+dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local,
+                               const void* w_qkv, const void* w_o, const void* residual,
+                               void* out, void* stream);
+
+/* ------------------------------------------------------------ the ST block */
+
+/* One ST block (R1, R10, R13, R14), x_local and y_local both
+ * T-sharded [B, T/N, S, C]:
+ *   y1 = x + MHA_S(LN1 x)            local on T-shards          (y1 stored in y_local)
+ *   switch T->S                      one all-to-all
+ *   y2 = y1 + MHA_T(LN2 y1)          local on S-shards
+ *   y  = y2 + MLP(LN3 y2)            MLP = gelu_tanh(. W1^T) W2^T (R5)
+ *   switch S->T                      second all-to-all
+ * COLLECTIVE.  x_local may equal y_local.  Workspace >= dsp_workspace_bytes().
+ * N == 1: no switch is executed (both layouts coincide).
+ * Errors: any of the above; WORKSPACE. */
+dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* shape,
+                                  const dsp_block_weights_t* w, const void* x_local,
+                                  void* y_local, dsp_switch_impl_t impl, void* stream);
+
+/* End-to-end variant through HOST buffers: copies x_local_host -> x_dev (H2D), runs
+ * dsp_st_block_forward(x_dev -> y_dev), copies y_dev -> y_local_host (D2H), all on
+ * `stream`; returns after enqueueing (synchronise the stream before reading y_host).
+ * x_dev / y_dev are caller-owned device staging buffers of the local shard size
+ * (may be equal).  COLLECTIVE. */
+dsp_status_t dsp_st_block_forward_host(dsp_ctx_t ctx, const dsp_shape_t* shape,
+                                       const dsp_block_weights_t* w,
+                                       const void* x_local_host, void* y_local_host,
+                                       void* x_dev, void* y_dev,
+                                       dsp_switch_impl_t impl, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSP_H_ */

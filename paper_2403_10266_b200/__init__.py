@@ -1,0 +1,275 @@
+"""paper_2403_10266_b200 — B200-native Dynamic Sequence Parallelism hot path.
+
+Thin ctypes binding over libdsp.so (include/dsp.h, include/dsp_kernels.h): every
+function here only marshals arguments (torch tensors -> device pointers, the current
+CUDA stream) and calls the C ABI of the same name; every step of the path runs in the
+library's CUDA kernels or NCCL.  There is no CPU fallback: if the library is missing
+or a tensor is not on a CUDA device, calls raise.
+
+Paper: arXiv 2403.10266 (DSP).  The block forward is §3.1: spatial
+attention local on T-shards -> dynamic switch (one all-to-all) -> temporal attention
++ MLP local on S-shards -> switch back ("two AlltoAll operations in total").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdsp.so")
+
+DSP_DIM_T, DSP_DIM_S = 1, 2
+DSP_BF16, DSP_F32 = 0, 1
+DSP_SWITCH_NCCL, DSP_SWITCH_P2P = 0, 1
+DSP_EPI_NONE, DSP_EPI_RESIDUAL, DSP_EPI_GELU = 0, 1, 2
+IMPLS = {"nccl": DSP_SWITCH_NCCL, "p2p": DSP_SWITCH_P2P}
+DIMS = {"T": DSP_DIM_T, "S": DSP_DIM_S, DSP_DIM_T: DSP_DIM_T, DSP_DIM_S: DSP_DIM_S}
+
+STATUS = {0: "DSP_OK", 1: "DSP_ERR_NULL", 2: "DSP_ERR_SHAPE", 3: "DSP_ERR_DIVISIBILITY", 4: "DSP_ERR_SAME_DIM",
+          5: "DSP_ERR_BAD_DIM", 6: "DSP_ERR_UNSUPPORTED", 7: "DSP_ERR_ALIGNMENT", 8: "DSP_ERR_ALIAS",
+          9: "DSP_ERR_WORKSPACE", 10: "DSP_ERR_CUDA", 11: "DSP_ERR_NCCL", 12: "DSP_ERR_STATE"}
+
+
+class DSPError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("T", ctypes.c_int64), ("S", ctypes.c_int64), ("C", ctypes.c_int64),
+                ("num_heads", ctypes.c_int32), ("dtype", ctypes.c_int)]
+
+
+class BlockWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("ln1_w", "ln1_b", "w_qkv_s", "w_o_s", "ln2_w", "ln2_b", "w_qkv_t",
+                                               "w_o_t", "ln3_w", "ln3_b", "w_fc1", "w_fc2")] + [("ln_eps", ctypes.c_float)]
+
+
+class SwitchPlan(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64 * 3), ("run_bytes", ctypes.c_int64), ("src_stride", ctypes.c_int64 * 3),
+                ("dst_stride", ctypes.c_int64 * 3), ("dst_peer_off", ctypes.c_int64),
+                ("pack_is_identity", ctypes.c_int32), ("unpack_is_identity", ctypes.c_int32)]
+
+
+WEIGHT_NAMES = tuple(n for n, _ in BlockWeights._fields_[:12])
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdsp.so (built in-tree by __graft_entry__.build()); raise if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2403_10266_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+        P = ctypes.POINTER
+        sig = {
+            "dsp_ctx_create": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, P(vp)],
+            "dsp_ctx_destroy": [vp],
+            "dsp_ctx_set_workspace": [vp, vp, ctypes.c_size_t],
+            "dsp_ctx_set_peer_buffers": [vp, P(vp), P(vp), ctypes.c_size_t],
+            "dsp_split": [vp, P(Shape), ctypes.c_int, vp, vp, vp],
+            "dsp_gather": [vp, P(Shape), ctypes.c_int, vp, vp, vp],
+            "dsp_switch": [vp, P(Shape), ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int, vp],
+            "dsp_switch_volume": [P(Shape), ctypes.c_int, P(i64), P(i64)],
+            "dsp_switch_plan": [P(Shape), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P(SwitchPlan)],
+            "dsp_spatial_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
+            "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
+            "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
+            "dsp_st_block_forward_host": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, ctypes.c_int, vp],
+            "dsp_layer_norm": [vp, ctypes.c_int, i64, i64, vp, vp, vp, ctypes.c_float, vp, vp],
+            "dsp_linear": [vp, ctypes.c_int, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp, vp],
+            "dsp_attention_core": [vp, ctypes.c_int, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.dsp_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
+        L.dsp_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_status_str.argtypes = [ctypes.c_int]
+        L.dsp_status_str.restype = ctypes.c_char_p
+        L.dsp_last_error.argtypes = [vp]
+        L.dsp_last_error.restype = ctypes.c_char_p
+        L.dsp_abi_version.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code: int, ctx_handle=None):
+    if code != 0:
+        msg = lib().dsp_last_error(ctx_handle).decode()
+        raise DSPError(code, msg)
+
+
+def _dtype_code(dt) -> int:
+    if dt in (torch.bfloat16, "bf16", DSP_BF16):
+        return DSP_BF16
+    if dt in (torch.float32, "f32", DSP_F32):
+        return DSP_F32
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def make_shape(B, T, S, C, num_heads, dtype) -> Shape:
+    return Shape(int(B), int(T), int(S), int(C), int(num_heads), _dtype_code(dtype))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError("dsp operates on CUDA tensors only (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("dsp needs contiguous tensors")
+    return t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def workspace_bytes(shape: Shape, world: int) -> int:
+    return int(lib().dsp_workspace_bytes(ctypes.byref(shape), int(world)))
+
+
+def switch_volume(shape: Shape, world: int):
+    s, r = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().dsp_switch_volume(ctypes.byref(shape), int(world), ctypes.byref(s), ctypes.byref(r)))
+    return s.value, r.value
+
+
+def switch_plan(shape: Shape, world: int, rank: int, from_dim, to_dim) -> SwitchPlan:
+    p = SwitchPlan()
+    _check(lib().dsp_switch_plan(ctypes.byref(shape), int(world), int(rank), DIMS[from_dim], DIMS[to_dim],
+                                 ctypes.byref(p)))
+    return p
+
+
+def nccl_comm_ptr(pg) -> int:
+    """ncclComm_t of an eagerly-initialised ProcessGroupNCCL (init_process_group(..., device_id=...))."""
+    backend = pg._get_backend(torch.device("cuda"))
+    return int(backend._comm_ptr())
+
+
+class Context:
+    """One dsp context per (process, device, communicator).
+
+    world == 1 needs no process group.  For world > 1 pass the NCCL process group
+    (initialised eagerly with device_id so its communicator exists); the context
+    borrows its ncclComm_t.  `rank`/`world` may be overridden to build "virtual
+    ranks" on one device for the P2P switch tests.
+    """
+
+    def __init__(self, pg=None, device=None, rank=None, world=None, comm_ptr=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("dsp needs a CUDA device")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   (device.index if isinstance(device, torch.device) else int(device)))
+        if pg is not None:
+            import torch.distributed as dist
+            rank = dist.get_rank(pg) if rank is None else rank
+            world = dist.get_world_size(pg) if world is None else world
+            if comm_ptr is None and world > 1:
+                comm_ptr = nccl_comm_ptr(pg)
+        self.rank = 0 if rank is None else int(rank)
+        self.world = 1 if world is None else int(world)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().dsp_ctx_create(comm_ptr, self.rank, self.world, self.device.index, ctypes.byref(h)))
+        self.handle = h
+        self._ws = None
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dsp_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _call(self, name, *args):
+        with torch.cuda.device(self.device):
+            _check(getattr(lib(), name)(self.handle, *args), self.handle)
+
+    # ---- resources
+    def set_workspace(self, ws: torch.Tensor):
+        self._ws = ws
+        _check(lib().dsp_ctx_set_workspace(self.handle, _ptr(ws), ws.numel() * ws.element_size()), self.handle)
+
+    def ensure_workspace(self, nbytes: int):
+        if self._ws is None or self._ws.numel() < nbytes:
+            self.set_workspace(torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device))
+        return self._ws
+
+    def set_peer_buffers(self, base_ptrs, signal_ptrs, nbytes: int):
+        n = len(base_ptrs)
+        B = (ctypes.c_void_p * n)(*base_ptrs)
+        S = (ctypes.c_void_p * n)(*signal_ptrs)
+        _check(lib().dsp_ctx_set_peer_buffers(self.handle, B, S, int(nbytes)), self.handle)
+
+    # ---- layout ops
+    def split(self, shape, dim, x_global, x_local, stream=None):
+        self._call("dsp_split", ctypes.byref(shape), DIMS[dim], _ptr(x_global), _ptr(x_local), _stream(stream))
+
+    def gather(self, shape, dim, x_local, x_global, stream=None):
+        self._call("dsp_gather", ctypes.byref(shape), DIMS[dim], _ptr(x_local), _ptr(x_global), _stream(stream))
+
+    def switch(self, shape, from_dim, to_dim, x_local, y_local, impl="nccl", stream=None):
+        self._call("dsp_switch", ctypes.byref(shape), DIMS[from_dim], DIMS[to_dim], _ptr(x_local), _ptr(y_local),
+                   IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    # ---- compute
+    def spatial_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):
+        self._call("dsp_spatial_attn", ctypes.byref(shape), _ptr(h), _ptr(w_qkv), _ptr(w_o), _ptr(residual),
+                   _ptr(out), _stream(stream))
+
+    def temporal_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):
+        self._call("dsp_temporal_attn", ctypes.byref(shape), _ptr(h), _ptr(w_qkv), _ptr(w_o), _ptr(residual),
+                   _ptr(out), _stream(stream))
+
+    @staticmethod
+    def block_weights(W: dict, eps: float = 1e-5) -> BlockWeights:
+        return BlockWeights(*[_ptr(W[n]) for n in WEIGHT_NAMES], ctypes.c_float(eps))
+
+    def st_block_forward(self, shape, weights, x_local, y_local, impl="nccl", stream=None):
+        bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
+        self._call("dsp_st_block_forward", ctypes.byref(shape), ctypes.byref(bw), _ptr(x_local), _ptr(y_local),
+                   IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def st_block_forward_host(self, shape, weights, x_host: torch.Tensor, y_host: torch.Tensor, x_dev, y_dev,
+                              impl="nccl", stream=None):
+        bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
+        for t in (x_host, y_host):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("host buffers must be contiguous CPU tensors (pinned recommended)")
+        self._call("dsp_st_block_forward_host", ctypes.byref(shape), ctypes.byref(bw), x_host.data_ptr(),
+                   y_host.data_ptr(), _ptr(x_dev), _ptr(y_dev), IMPLS[impl] if isinstance(impl, str) else int(impl),
+                   _stream(stream))
+
+    def layer_norm(self, x, gamma, beta, eps, y, stream=None):
+        rows, C = x.numel() // x.shape[-1], x.shape[-1]
+        self._call("dsp_layer_norm", _dtype_code(x.dtype), rows, C, _ptr(x), _ptr(gamma), _ptr(beta),
+                   ctypes.c_float(eps), _ptr(y), _stream(stream))
+
+    def linear(self, A, W, D, R=None, epi=DSP_EPI_NONE, stream=None):
+        M, K = A.numel() // A.shape[-1], A.shape[-1]
+        N = W.shape[0]
+        self._call("dsp_linear", _dtype_code(A.dtype), M, N, K, _ptr(A), _ptr(W), _ptr(R), int(epi), _ptr(D),
+                   _stream(stream))
+
+    def attention_core(self, B, T_loc, S_loc, C, num_heads, dim, qkv, o, stream=None):
+        self._call("dsp_attention_core", _dtype_code(qkv.dtype), B, T_loc, S_loc, C, num_heads, DIMS[dim],
+                   _ptr(qkv), _ptr(o), _stream(stream))

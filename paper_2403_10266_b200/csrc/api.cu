@@ -1,0 +1,576 @@
+// api.cu — the C ABI (include/dsp.h, include/dsp_kernels.h): validation, the switch
+// plan, transports (NCCL / P2P) and the composition of the ST block forward.
+// Every step of the path runs in this library's kernels (or NCCL); there is no host
+// compute and no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "dsp_internal.h"
+
+using namespace dsp;
+
+namespace {
+
+thread_local std::string g_no_ctx_error;
+
+dsp_status_t fail(dsp_ctx_t ctx, dsp_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->last_error = buf;
+  else g_no_ctx_error = buf;
+  return st;
+}
+
+dsp_status_t cuda_fail(dsp_ctx_t ctx, cudaError_t e, const char* what, const std::string& why = "") {
+  if (e == cudaErrorNotSupported)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "%s: %s", what, why.empty() ? "unsupported" : why.c_str());
+  return fail(ctx, DSP_ERR_CUDA, "%s: %s%s%s", what, cudaGetErrorString(e), why.empty() ? "" : " — ", why.c_str());
+}
+
+#define DSP_CUDA(ctx, expr, what)                        \
+  do {                                                   \
+    std::string _why;                                    \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what, _why); \
+  } while (0)
+#define DSP_CUDA_WHY(ctx, call, what)                    \
+  do {                                                   \
+    std::string _why;                                    \
+    cudaError_t _e = call;                               \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what, _why); \
+  } while (0)
+#define DSP_TRY(expr)                 \
+  do {                                \
+    dsp_status_t _s = (expr);         \
+    if (_s != DSP_OK) return _s;      \
+  } while (0)
+
+int64_t elem_bytes(dsp_dtype_t d) { return d == DSP_BF16 ? 2 : 4; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool overlap(const void* a, int64_t na, const void* b, int64_t nb) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + (uintptr_t)nb && y < x + (uintptr_t)na;
+}
+
+dsp_status_t check_shape(dsp_ctx_t ctx, const dsp_shape_t* s) {
+  if (!s) return fail(ctx, DSP_ERR_NULL, "shape is NULL");
+  if (s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1 || s->num_heads < 1)
+    return fail(ctx, DSP_ERR_SHAPE, "non-positive extent in shape (B=%lld T=%lld S=%lld C=%lld heads=%d)",
+                (long long)s->B, (long long)s->T, (long long)s->S, (long long)s->C, s->num_heads);
+  if (s->dtype != DSP_BF16 && s->dtype != DSP_F32) return fail(ctx, DSP_ERR_SHAPE, "unknown dtype %d", (int)s->dtype);
+  if ((s->C * elem_bytes(s->dtype)) % 16)
+    return fail(ctx, DSP_ERR_ALIGNMENT, "C*elem = %lld bytes is not a multiple of 16", (long long)(s->C * elem_bytes(s->dtype)));
+  return DSP_OK;
+}
+
+dsp_status_t check_dim(dsp_ctx_t ctx, int d) {
+  if (d != DSP_DIM_T && d != DSP_DIM_S) return fail(ctx, DSP_ERR_BAD_DIM, "dim %d is not DSP_DIM_T (1) or DSP_DIM_S (2)", d);
+  return DSP_OK;
+}
+
+dsp_status_t check_div(dsp_ctx_t ctx, const dsp_shape_t* s, int world) {
+  if (world < 1) return fail(ctx, DSP_ERR_SHAPE, "world %d < 1", world);
+  if (s->T % world || s->S % world)
+    return fail(ctx, DSP_ERR_DIVISIBILITY, "N=%d must divide T=%lld and S=%lld", world, (long long)s->T, (long long)s->S);
+  return DSP_OK;
+}
+
+dsp_status_t check_ctx(dsp_ctx_t ctx) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev != ctx->device)
+    return fail(ctx, DSP_ERR_STATE, "current CUDA device %d is not the context device %d", dev, ctx->device);
+  return DSP_OK;
+}
+
+int64_t shard_bytes(const dsp_shape_t* s, int world) { return s->B * s->T * s->S * s->C * elem_bytes(s->dtype) / world; }
+
+// bf16 tensor-core path constraints for one attention stage over sequences of length L
+dsp_status_t check_bf16_attn(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t L) {
+  if (s->C % s->num_heads) return fail(ctx, DSP_ERR_SHAPE, "C=%lld not divisible by num_heads=%d", (long long)s->C, s->num_heads);
+  const int64_t Dh = s->C / s->num_heads;
+  if (s->dtype == DSP_F32) {
+    if (Dh > 128) return fail(ctx, DSP_ERR_UNSUPPORTED, "fp32 check path supports Dh <= 128 (Dh=%lld)", (long long)Dh);
+    return DSP_OK;
+  }
+  if (Dh % 8 || Dh > 128) return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 attention needs Dh %% 8 == 0 and Dh <= 128 (Dh=%lld)", (long long)Dh);
+  if (s->C % 32) return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 path needs C %% 32 == 0 (C=%lld)", (long long)s->C);
+  if (!(L % 128 == 0 || 128 % L == 0))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 attention needs the sequence length (%lld) to divide 128 or be a multiple of 128", (long long)L);
+  return DSP_OK;
+}
+
+// ---------------------------------------------------------------- switch plan
+void make_plan(const dsp_shape_t* s, int N, int rank, int from, dsp_switch_plan_t* p) {
+  const int64_t e = elem_bytes(s->dtype), row = s->C * e, Tn = s->T / N, Sn = s->S / N, B = s->B, T = s->T, S = s->S;
+  memset(p, 0, sizeof(*p));
+  p->n[0] = N; p->n[1] = B; p->n[2] = Tn;
+  p->run_bytes = Sn * row;
+  if (from == DSP_DIM_T) {  // x [B,Tn,S,C] -> y [B,T,Sn,C]
+    p->src_stride[0] = Sn * row; p->src_stride[1] = Tn * S * row; p->src_stride[2] = S * row;
+    p->dst_stride[0] = Tn * Sn * row; p->dst_stride[1] = T * Sn * row; p->dst_stride[2] = Sn * row;
+    p->pack_is_identity = (N == 1 || B * Tn == 1);
+    p->unpack_is_identity = (N == 1 || B == 1);
+  } else {                  // x [B,T,Sn,C] -> y [B,Tn,S,C]
+    p->src_stride[0] = Tn * Sn * row; p->src_stride[1] = T * Sn * row; p->src_stride[2] = Sn * row;
+    p->dst_stride[0] = Sn * row; p->dst_stride[1] = Tn * S * row; p->dst_stride[2] = S * row;
+    p->pack_is_identity = (N == 1 || B == 1);
+    p->unpack_is_identity = (N == 1 || B * Tn == 1);
+  }
+  p->dst_peer_off = rank * p->dst_stride[0];
+}
+
+dsp_status_t validate_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int world, int from, int to) {
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_dim(ctx, from));
+  DSP_TRY(check_dim(ctx, to));
+  if (from == to) return fail(ctx, DSP_ERR_SAME_DIM, "switch from a dim to itself (S:283)");
+  return check_div(ctx, s, world);
+}
+
+bool in_region(const void* p, int64_t n, const void* base, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), b = reinterpret_cast<uintptr_t>(base);
+  return a >= b && a + (uintptr_t)n <= b + bytes;
+}
+
+// Execute a switch with explicit scratch (send/recv each >= shard bytes when needed).
+dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void* x, void* y, dsp_switch_impl_t impl,
+                       cudaStream_t st, void* scratch_send, void* scratch_recv) {
+  const int N = ctx->world;
+  const int64_t bytes = shard_bytes(s, N);
+  if (N == 1) {
+    if (x != y) DSP_CUDA(ctx, cudaMemcpyAsync(y, x, bytes, cudaMemcpyDeviceToDevice, st), "switch copy (N=1)");
+    return DSP_OK;
+  }
+  dsp_switch_plan_t p;
+  make_plan(s, N, ctx->rank, from, &p);
+  RunCopy rc;
+  for (int i = 0; i < 3; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
+  rc.run_bytes = p.run_bytes;
+  if (impl == DSP_SWITCH_P2P) {
+    if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P switch without dsp_ctx_set_peer_buffers");
+    void* base = ctx->peer_base.p[ctx->rank];
+    if (!in_region(y, bytes, base, ctx->peer_bytes))
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P switch destination is not inside the registered symmetric buffer");
+    const int64_t y_off = static_cast<uint8_t*>(y) - static_cast<uint8_t*>(base);
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p entry barrier");
+    DSP_CUDA(ctx, launch_p2p_put(x, ctx->peer_base, y_off + p.dst_peer_off, rc, ctx->num_sms, st), "p2p put");
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p exit barrier");
+    return DSP_OK;
+  }
+  if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
+  const int64_t chunk = p.n[1] * p.n[2] * p.run_bytes;  // bytes per peer
+  RunCopy pack = rc, unpack = rc;
+  pack.ds[0] = chunk; pack.ds[1] = p.n[2] * p.run_bytes; pack.ds[2] = p.run_bytes;
+  unpack.ss[0] = pack.ds[0]; unpack.ss[1] = pack.ds[1]; unpack.ss[2] = pack.ds[2];
+  const void* send = x;
+  void* recv = y;
+  if (!p.pack_is_identity) {
+    DSP_CUDA(ctx, launch_run_copy(x, scratch_send, pack, ctx->num_sms, st), "switch pack");
+    send = scratch_send;
+  }
+  if (!p.unpack_is_identity) recv = scratch_recv;
+  int r;
+  if (ctx->nccl.AlltoAll) {
+    r = ctx->nccl.AlltoAll(send, recv, (size_t)chunk, kNcclUint8, ctx->comm, st);
+  } else {
+    r = ctx->nccl.GroupStart();
+    for (int q = 0; q < N && r == 0; ++q) {
+      r = ctx->nccl.Send(static_cast<const uint8_t*>(send) + q * chunk, chunk, kNcclUint8, q, ctx->comm, st);
+      if (!r) r = ctx->nccl.Recv(static_cast<uint8_t*>(recv) + q * chunk, chunk, kNcclUint8, q, ctx->comm, st);
+    }
+    int r2 = ctx->nccl.GroupEnd();
+    if (!r) r = r2;
+  }
+  if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAlltoAll: %s", ctx->nccl.GetErrorString(r));
+  if (!p.unpack_is_identity) DSP_CUDA(ctx, launch_run_copy(recv, y, unpack, ctx->num_sms, st), "switch unpack");
+  return DSP_OK;
+}
+
+// one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C]
+dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
+                        const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
+                        cudaStream_t st) {
+  const int64_t tok = s->B * T_loc * S_loc, C = s->C;
+  const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
+  if (s->dtype == DSP_BF16) {
+    std::string why;
+    cudaError_t e = launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "qkv projection", why);
+    e = launch_fmha_bf16(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, dim, st, &why);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
+    e = launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "output projection", why);
+  } else {
+    DSP_CUDA(ctx, launch_gemm_f32((const float*)h, (const float*)w_qkv, nullptr, (float*)qkv, tok, 3 * C, C, DSP_EPI_NONE, st), "qkv projection f32");
+    DSP_CUDA(ctx, launch_attn_f32((const float*)qkv, (float*)o, s->B, T_loc, S_loc, C, s->num_heads, dim, st), "attention f32");
+    DSP_CUDA(ctx, launch_gemm_f32((const float*)o, (const float*)w_o, (const float*)res, (float*)out, tok, C, C, epi, st), "output projection f32");
+  }
+  return DSP_OK;
+}
+
+dsp_status_t linear(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t M, int64_t N, int64_t K, const void* A, const void* W,
+                    const void* R, int epi, void* D, cudaStream_t st) {
+  if (dt == DSP_BF16) {
+    std::string why;
+    cudaError_t e = launch_gemm_bf16(A, W, R, D, M, N, K, epi, ctx->num_sms, st, &why);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "linear", why);
+  } else {
+    DSP_CUDA(ctx, launch_gemm_f32((const float*)A, (const float*)W, (const float*)R, (float*)D, M, N, K, epi, st), "linear f32");
+  }
+  return DSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dsp_abi_version(void) { return DSP_ABI_VERSION; }
+
+const char* dsp_status_str(dsp_status_t s) {
+  switch (s) {
+    case DSP_OK: return "DSP_OK";
+    case DSP_ERR_NULL: return "DSP_ERR_NULL";
+    case DSP_ERR_SHAPE: return "DSP_ERR_SHAPE";
+    case DSP_ERR_DIVISIBILITY: return "DSP_ERR_DIVISIBILITY";
+    case DSP_ERR_SAME_DIM: return "DSP_ERR_SAME_DIM";
+    case DSP_ERR_BAD_DIM: return "DSP_ERR_BAD_DIM";
+    case DSP_ERR_UNSUPPORTED: return "DSP_ERR_UNSUPPORTED";
+    case DSP_ERR_ALIGNMENT: return "DSP_ERR_ALIGNMENT";
+    case DSP_ERR_ALIAS: return "DSP_ERR_ALIAS";
+    case DSP_ERR_WORKSPACE: return "DSP_ERR_WORKSPACE";
+    case DSP_ERR_CUDA: return "DSP_ERR_CUDA";
+    case DSP_ERR_NCCL: return "DSP_ERR_NCCL";
+    case DSP_ERR_STATE: return "DSP_ERR_STATE";
+  }
+  return "DSP_ERR_UNKNOWN";
+}
+
+const char* dsp_last_error(dsp_ctx_t ctx) { return ctx ? ctx->last_error.c_str() : g_no_ctx_error.c_str(); }
+
+dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, dsp_ctx_t* out) {
+  if (!out) return fail(nullptr, DSP_ERR_NULL, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, DSP_ERR_SHAPE, "bad rank %d / world %d", rank, world);
+  dsp_ctx* c = new dsp_ctx();
+  c->rank = rank; c->world = world; c->device = device; c->comm = nccl_comm;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    fail(nullptr, DSP_ERR_CUDA, "device %d: %s", device, cudaGetErrorString(e));
+    delete c;
+    return DSP_ERR_CUDA;
+  }
+  if (nccl_comm) {
+    std::string err;
+    if (!nccl_load(&c->nccl, &err)) {
+      fail(nullptr, DSP_ERR_NCCL, "%s", err.c_str());
+      delete c;
+      return DSP_ERR_NCCL;
+    }
+  }
+  *out = c;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_ctx_destroy(dsp_ctx_t ctx) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  delete ctx;
+  return DSP_OK;
+}
+
+size_t dsp_workspace_bytes(const dsp_shape_t* s, int world) {
+  if (!s || world < 1 || s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1) return 0;
+  const int64_t tok = s->B * s->T * s->S / world;
+  return (size_t)(tok * 6 * s->C * elem_bytes(s->dtype)) + 256;
+}
+
+dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* ws, size_t bytes) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (ws && !aligned16(ws)) return fail(ctx, DSP_ERR_ALIGNMENT, "workspace not 16-B aligned");
+  ctx->ws = ws;
+  ctx->ws_bytes = ws ? bytes : 0;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_ctx_set_peer_buffers(dsp_ctx_t ctx, void* const* base, void* const* sig, size_t bytes) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (!base || !sig) return fail(ctx, DSP_ERR_NULL, "peer pointer arrays are NULL");
+  if (ctx->world > kMaxPeers) return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P switch supports world <= %d", kMaxPeers);
+  for (int i = 0; i < ctx->world; ++i) {
+    if (!base[i] || !sig[i]) return fail(ctx, DSP_ERR_NULL, "peer %d pointer is NULL", i);
+    if (!aligned16(base[i]) || !aligned16(sig[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "peer %d pointer not 16-B aligned", i);
+    ctx->peer_base.p[i] = base[i];
+    ctx->peer_signal.p[i] = sig[i];
+  }
+  ctx->peer_bytes = bytes;
+  ctx->has_peers = true;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_switch_volume(const dsp_shape_t* s, int world, int64_t* sent, int64_t* recv) {
+  DSP_TRY(check_shape(nullptr, s));
+  DSP_TRY(check_div(nullptr, s, world));
+  if (!sent || !recv) return fail(nullptr, DSP_ERR_NULL, "output pointer is NULL");
+  const int64_t v = (int64_t)(world - 1) * s->B * (s->T / world) * (s->S / world) * s->C * elem_bytes(s->dtype);
+  *sent = v;
+  *recv = v;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_switch_plan(const dsp_shape_t* s, int world, int rank, dsp_dim_t from, dsp_dim_t to,
+                             dsp_switch_plan_t* plan) {
+  DSP_TRY(validate_switch(nullptr, s, world, from, to));
+  if (!plan) return fail(nullptr, DSP_ERR_NULL, "plan is NULL");
+  if (rank < 0 || rank >= world) return fail(nullptr, DSP_ERR_SHAPE, "rank %d out of range", rank);
+  make_plan(s, world, rank, from, plan);
+  return DSP_OK;
+}
+
+dsp_status_t dsp_split(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const void* xg, void* xl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_dim(ctx, dim));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!xg || !xl) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(xg) || !aligned16(xl)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int N = ctx->world, r = ctx->rank;
+  const int64_t e = elem_bytes(s->dtype), row = s->C * e, B = s->B, T = s->T, S = s->S, Tn = T / N, Sn = S / N;
+  if (overlap(xg, B * T * S * row, xl, B * T * S * row / N)) return fail(ctx, DSP_ERR_ALIAS, "x_local overlaps x_global");
+  RunCopy rc{};
+  if (dim == DSP_DIM_T) {
+    rc.n[0] = 1; rc.n[1] = B; rc.n[2] = 1; rc.run_bytes = Tn * S * row;
+    rc.ss[1] = T * S * row; rc.ds[1] = Tn * S * row;
+    xg = static_cast<const uint8_t*>(xg) + r * Tn * S * row;
+  } else {
+    rc.n[0] = 1; rc.n[1] = B; rc.n[2] = T; rc.run_bytes = Sn * row;
+    rc.ss[1] = T * S * row; rc.ss[2] = S * row; rc.ds[1] = T * Sn * row; rc.ds[2] = Sn * row;
+    xg = static_cast<const uint8_t*>(xg) + r * Sn * row;
+  }
+  DSP_CUDA(ctx, launch_run_copy(xg, xl, rc, ctx->num_sms, (cudaStream_t)stream), "split");
+  return DSP_OK;
+}
+
+dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const void* xl, void* xg, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_dim(ctx, dim));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!xg || !xl) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(xg) || !aligned16(xl)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int N = ctx->world;
+  const int64_t e = elem_bytes(s->dtype), row = s->C * e, B = s->B, T = s->T, S = s->S, Tn = T / N, Sn = S / N;
+  const int64_t local = B * T * S * row / N;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (overlap(xg, local * N, xl, local)) return fail(ctx, DSP_ERR_ALIAS, "x_local overlaps x_global");
+  if (N == 1) {
+    DSP_CUDA(ctx, cudaMemcpyAsync(xg, xl, local, cudaMemcpyDeviceToDevice, st), "gather copy (N=1)");
+    return DSP_OK;
+  }
+  if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "gather without a communicator");
+  const bool identity = (dim == DSP_DIM_T) ? (B == 1) : (B * T == 1);
+  void* stage = xg;
+  if (!identity) {
+    if (!ctx->ws || ctx->ws_bytes < (size_t)(local * N)) return fail(ctx, DSP_ERR_WORKSPACE, "gather needs %lld bytes of workspace", (long long)(local * N));
+    stage = ctx->ws;
+  }
+  int r = ctx->nccl.AllGather(xl, stage, (size_t)local, kNcclUint8, ctx->comm, st);
+  if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAllGather: %s", ctx->nccl.GetErrorString(r));
+  if (!identity) {
+    RunCopy rc{};
+    if (dim == DSP_DIM_T) {
+      rc.n[0] = N; rc.n[1] = B; rc.n[2] = 1; rc.run_bytes = Tn * S * row;
+      rc.ss[0] = local; rc.ss[1] = Tn * S * row; rc.ds[0] = Tn * S * row; rc.ds[1] = T * S * row;
+    } else {
+      rc.n[0] = N; rc.n[1] = B; rc.n[2] = T; rc.run_bytes = Sn * row;
+      rc.ss[0] = local; rc.ss[1] = T * Sn * row; rc.ss[2] = Sn * row;
+      rc.ds[0] = Sn * row; rc.ds[1] = T * S * row; rc.ds[2] = S * row;
+    }
+    DSP_CUDA(ctx, launch_run_copy(stage, xg, rc, ctx->num_sms, st), "gather unpack");
+  }
+  return DSP_OK;
+}
+
+dsp_status_t dsp_switch(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp_dim_t to, const void* x, void* y,
+                        dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(validate_switch(ctx, s, ctx->world, from, to));
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P) return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  if (!x || !y) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int64_t bytes = shard_bytes(s, ctx->world);
+  if (ctx->world > 1 && overlap(x, bytes, y, bytes)) return fail(ctx, DSP_ERR_ALIAS, "x_local overlaps y_local");
+  void* send = nullptr;
+  void* recv = nullptr;
+  if (ctx->world > 1 && impl == DSP_SWITCH_NCCL) {
+    dsp_switch_plan_t p;
+    make_plan(s, ctx->world, ctx->rank, from, &p);
+    const int64_t need = (p.pack_is_identity ? 0 : bytes) + (p.unpack_is_identity ? 0 : bytes);
+    if (need && (!ctx->ws || ctx->ws_bytes < (size_t)need))
+      return fail(ctx, DSP_ERR_WORKSPACE, "switch needs %lld bytes of workspace", (long long)need);
+    send = ctx->ws;
+    recv = static_cast<uint8_t*>(ctx->ws) + (p.pack_is_identity ? 0 : bytes);
+  }
+  return do_switch(ctx, s, from, x, y, impl, (cudaStream_t)stream, send, recv);
+}
+
+static dsp_status_t attn_public(dsp_ctx_t ctx, const dsp_shape_t* s, int dim, const void* h, const void* wqkv,
+                                const void* wo, const void* res, void* out, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!h || !wqkv || !wo || !out) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  const int N = ctx->world;
+  const int64_t T_loc = dim == DSP_DIM_S ? s->T / N : s->T, S_loc = dim == DSP_DIM_S ? s->S : s->S / N;
+  DSP_TRY(check_bf16_attn(ctx, s, dim == DSP_DIM_S ? S_loc : T_loc));
+  const int64_t e = elem_bytes(s->dtype), tok = s->B * T_loc * S_loc, act = tok * s->C * e;
+  if (!aligned16(h) || !aligned16(out) || (res && !aligned16(res))) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  if (overlap(h, act, out, act)) return fail(ctx, DSP_ERR_ALIAS, "out overlaps h");
+  if (res && res != out && overlap(res, act, out, act)) return fail(ctx, DSP_ERR_ALIAS, "out partially overlaps residual");
+  const int64_t need = tok * 4 * s->C * e;
+  if (!ctx->ws || ctx->ws_bytes < (size_t)need) return fail(ctx, DSP_ERR_WORKSPACE, "attention needs %lld bytes of workspace", (long long)need);
+  void* qkv = ctx->ws;
+  void* o = static_cast<uint8_t*>(ctx->ws) + tok * 3 * s->C * e;
+  return attn_stage(ctx, s, T_loc, S_loc, dim, h, wqkv, wo, res, out, qkv, o, (cudaStream_t)stream);
+}
+
+dsp_status_t dsp_spatial_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* h, const void* wqkv, const void* wo,
+                              const void* res, void* out, void* stream) {
+  return attn_public(ctx, s, DSP_DIM_S, h, wqkv, wo, res, out, stream);
+}
+
+dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* h, const void* wqkv, const void* wo,
+                               const void* res, void* out, void* stream) {
+  return attn_public(ctx, s, DSP_DIM_T, h, wqkv, wo, res, out, stream);
+}
+
+dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
+                                  void* y, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!w || !x || !y) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  const void* wp[12] = {w->ln1_w, w->ln1_b, w->w_qkv_s, w->w_o_s, w->ln2_w, w->ln2_b,
+                        w->w_qkv_t, w->w_o_t, w->ln3_w, w->ln3_b, w->w_fc1, w->w_fc2};
+  for (int i = 0; i < 12; ++i) {
+    if (!wp[i]) return fail(ctx, DSP_ERR_NULL, "weight %d is NULL", i);
+    if (!aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d not 16-B aligned", i);
+  }
+  if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int N = ctx->world;
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P) return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  DSP_TRY(check_bf16_attn(ctx, s, s->S));
+  DSP_TRY(check_bf16_attn(ctx, s, s->T));
+  const int64_t e = elem_bytes(s->dtype), C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * e;
+  const size_t need = dsp_workspace_bytes(s, N);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "block needs %zu bytes of workspace", need);
+  if (x != y && overlap(x, act, y, act)) return fail(ctx, DSP_ERR_ALIAS, "x_local partially overlaps y_local");
+  if (overlap(ctx->ws, need, x, act) || overlap(ctx->ws, need, y, act)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y");
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  void* h = ws;                      // [tok, C]
+  uint8_t* big = ws + act;           // [tok, 4C]: qkv + o | MLP hidden | switch scratch
+  void* qkv = big;
+  void* o = big + 3 * act;
+  void* ys = ws + 5 * act;           // [tok, C] S-sharded activation (N > 1)
+  if (N > 1 && impl == DSP_SWITCH_P2P) {
+    if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P block without dsp_ctx_set_peer_buffers");
+    void* base = ctx->peer_base.p[ctx->rank];
+    if (!in_region(ys, act, base, ctx->peer_bytes) || !in_region(y, act, base, ctx->peer_bytes))
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P block needs the workspace and y_local inside the symmetric buffer");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const float eps = w->ln_eps;
+  const int64_t Tn = s->T / N, Sn = s->S / N;
+  // a1-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
+  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
+  DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, h, w->w_qkv_s, w->w_o_s, x, y, qkv, o, st));
+  // a5: switch T -> S
+  void* cur = y;
+  if (N > 1) {
+    DSP_TRY(do_switch(ctx, s, DSP_DIM_T, y, ys, impl, st, big, big + act));
+    cur = ys;
+  }
+  // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place)
+  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
+  DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, h, w->w_qkv_t, w->w_o_t, cur, cur, qkv, o, st));
+  // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
+  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
+  DSP_TRY(linear(ctx, s->dtype, tok, 4 * C, C, h, w->w_fc1, nullptr, DSP_EPI_GELU, big, st));
+  DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));
+  // a11: switch S -> T back into y
+  if (N > 1) DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
+  return DSP_OK;
+}
+
+dsp_status_t dsp_st_block_forward_host(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w,
+                                       const void* xh, void* yh, void* xd, void* yd, dsp_switch_impl_t impl,
+                                       void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!xh || !yh || !xd || !yd) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  const int64_t act = shard_bytes(s, ctx->world);
+  cudaStream_t st = (cudaStream_t)stream;
+  DSP_CUDA(ctx, cudaMemcpyAsync(xd, xh, act, cudaMemcpyHostToDevice, st), "H2D x");
+  DSP_TRY(dsp_st_block_forward(ctx, s, w, xd, yd, impl, stream));
+  DSP_CUDA(ctx, cudaMemcpyAsync(yh, yd, act, cudaMemcpyDeviceToHost, st), "D2H y");
+  return DSP_OK;
+}
+
+dsp_status_t dsp_layer_norm(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t rows, int64_t C, const void* x, const void* g,
+                            const void* b, float eps, void* y, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!x || !g || !b || !y) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (rows < 0 || C < 1) return fail(ctx, DSP_ERR_SHAPE, "bad LN shape");
+  if (dt != DSP_BF16 && dt != DSP_F32) return fail(ctx, DSP_ERR_SHAPE, "unknown dtype");
+  if (dt == DSP_BF16 && (C * 2) % 16) return fail(ctx, DSP_ERR_ALIGNMENT, "bf16 LN needs C %% 8 == 0");
+  DSP_CUDA(ctx, launch_layer_norm(dt, rows, C, x, g, b, eps, y, (cudaStream_t)stream), "layer_norm");
+  return DSP_OK;
+}
+
+dsp_status_t dsp_linear(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t M, int64_t N, int64_t K, const void* A, const void* W,
+                        const void* R, dsp_epilogue_t epi, void* D, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!A || !W || !D || (epi == DSP_EPI_RESIDUAL && !R)) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (M < 0 || N < 1 || K < 1) return fail(ctx, DSP_ERR_SHAPE, "bad linear shape");
+  if (epi != DSP_EPI_NONE && epi != DSP_EPI_RESIDUAL && epi != DSP_EPI_GELU) return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown epilogue");
+  if (dt != DSP_BF16 && dt != DSP_F32) return fail(ctx, DSP_ERR_SHAPE, "unknown dtype");
+  const int64_t e = elem_bytes(dt);
+  if (overlap(D, M * N * e, A, M * K * e) || overlap(D, M * N * e, W, N * K * e)) return fail(ctx, DSP_ERR_ALIAS, "D overlaps A or W");
+  if (dt == DSP_BF16) {
+    if (K % 8 || N % 32) return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 linear needs K %% 8 == 0 and N %% 32 == 0");
+    if (!aligned16(A) || !aligned16(W) || !aligned16(D) || (R && !aligned16(R))) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  }
+  return linear(ctx, dt, M, N, K, A, W, R, epi, D, (cudaStream_t)stream);
+}
+
+dsp_status_t dsp_attention_core(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C,
+                                int32_t NH, dsp_dim_t dim, const void* qkv, void* o, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_dim(ctx, dim));
+  if (!qkv || !o) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  dsp_shape_t s{B, T_loc, S_loc, C, NH, dt};
+  DSP_TRY(check_shape(ctx, &s));
+  DSP_TRY(check_bf16_attn(ctx, &s, dim == DSP_DIM_S ? S_loc : T_loc));
+  if (!aligned16(qkv) || !aligned16(o)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == DSP_BF16) {
+    std::string why;
+    cudaError_t e = launch_fmha_bf16(qkv, o, B, T_loc, S_loc, C, NH, dim, st, &why);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
+  } else {
+    DSP_CUDA(ctx, launch_attn_f32((const float*)qkv, (float*)o, B, T_loc, S_loc, C, NH, dim, st), "attention f32");
+  }
+  return DSP_OK;
+}
+
+}  // extern "C"

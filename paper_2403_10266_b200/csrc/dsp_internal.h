@@ -1,0 +1,76 @@
+// dsp_internal.h — library-internal declarations (context, launchers, NCCL shim).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "dsp.h"
+#include "dsp_kernels.h"
+
+namespace dsp {
+
+constexpr int kMaxPeers = 8;  // one NVLink/NVSwitch box
+
+// ---- NCCL, resolved at run time from the libnccl.so.2 torch already loaded ----
+struct NcclApi {
+  bool ok = false;
+  int (*AlltoAll)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+bool nccl_load(NcclApi* api, std::string* err);
+constexpr int kNcclUint8 = 1;  // ncclUint8 in nccl.h
+
+struct PeerPtrs {
+  void* p[kMaxPeers];
+};
+
+// strided byte-run copy: run (i0,i1,i2) of run_bytes from src + sum(i*ss) to dst + sum(i*ds)
+struct RunCopy {
+  int64_t n[3];
+  int64_t run_bytes;
+  int64_t ss[3], ds[3];
+};
+
+// ---- launchers (return cudaGetLastError() after the launch) ----
+cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
+                             int epi, int num_sms, cudaStream_t st, std::string* why);
+cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
+                             int dim, cudaStream_t st, std::string* why);
+cudaError_t launch_gemm_f32(const float* A, const float* W, const float* R, float* D, int64_t M, int64_t N, int64_t K,
+                            int epi, cudaStream_t st);
+cudaError_t launch_attn_f32(const float* qkv, float* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
+                            int dim, cudaStream_t st);
+cudaError_t launch_layer_norm(int dtype, int64_t rows, int64_t C, const void* x, const void* g, const void* b,
+                              float eps, void* y, cudaStream_t st);
+cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int num_sms, cudaStream_t st);
+// P2P: run (i0=peer,i1,i2) stored to peer_base.p[i0] + dst_off + i1*ds[1] + i2*ds[2]
+cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t dst_off, const RunCopy& rc,
+                           int num_sms, cudaStream_t st);
+cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st);
+
+bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                    const uint32_t* box, CUtensorMapSwizzle swz, std::string* why);
+
+}  // namespace dsp
+
+struct dsp_ctx {
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  void* comm = nullptr;  // borrowed ncclComm_t
+  dsp::NcclApi nccl;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  dsp::PeerPtrs peer_base{}, peer_signal{};
+  bool has_peers = false;
+  size_t peer_bytes = 0;
+  uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
+  std::string last_error;
+};

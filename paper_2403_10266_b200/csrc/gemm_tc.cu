@@ -1,0 +1,288 @@
+// gemm_tc.cu — persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+// D[M,N] = epi(A[M,K] * W[N,K]^T), bf16 in / fp32 accumulate in TMEM / bf16 out.
+// Used for every dense contraction of the ST block:
+// QKV projection (plain), out-projection (+residual), FC1 (+GELU), FC2 (+residual).
+//
+// Roles (256 threads, 1 CTA per SM, grid = min(tiles, #SMs), static round-robin tiles):
+//   warp 0      TMA producer: A tile 128x64 and W tile BNx64 per k-block, SW128, into a
+//               STAGES-deep smem ring (full/empty mbarriers).
+//   warp 1      MMA issuer: one elected lane issues 4 x tcgen05.mma (M=128, N=BN, K=16)
+//               per k-block into one of two TMEM accumulators; tcgen05.commit frees the
+//               smem stage and, after the last k-block, signals the epilogue.
+//   warp 2      TMEM allocator.
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time (thread = accumulator row),
+//               fused residual / GELU, bf16 pack, 16-B global stores; then release the
+//               accumulator so the MMA warp can start the tile after next.
+// No split-K, no atomics: each output's reduction order depends only on K (N-invariance).
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "dsp_internal.h"
+#include "sm100.cuh"
+
+namespace dsp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one SW128 atom row
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 8 ? 8 : (220 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float gelu_tanh_f(float u) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * u * (1.f + fast_tanh(k0 * (u + k1 * u * u * u)));
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                        const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int tiles_m = (M + BM - 1) / BM;
+  const int tiles_n = N / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmW);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * BM;
+        const int n0 = (tile / tiles_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmW, &full[stage], kb * BK, n0);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, 0, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, SW_128B);
+            const uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, SW_128B);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == num_kb - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane_id();
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int m0 = (tile % tiles_m) * BM;
+      const int n0 = (tile / tiles_m) * BN;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int grow = m0 + row;
+      const bool live = grow < M;
+      __nv_bfloat16* drow = D + (size_t)grow * N + n0;
+      const __nv_bfloat16* rrow = R + (size_t)grow * N + n0;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait();
+        if (live) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          if (EPI == DSP_EPI_RESIDUAL) {
+            const uint4* rp = reinterpret_cast<const uint4*>(rrow + c * 32);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 rv = rp[j];
+              f[8 * j + 0] += bf16lo(rv.x);
+              f[8 * j + 1] += bf16hi(rv.x);
+              f[8 * j + 2] += bf16lo(rv.y);
+              f[8 * j + 3] += bf16hi(rv.y);
+              f[8 * j + 4] += bf16lo(rv.z);
+              f[8 * j + 5] += bf16hi(rv.z);
+              f[8 * j + 6] += bf16lo(rv.w);
+              f[8 * j + 7] += bf16hi(rv.w);
+            }
+          } else if (EPI == DSP_EPI_GELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = gelu_tanh_f(f[i]);
+          }
+          uint4* dp = reinterpret_cast<uint4*>(drow + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            dp[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                               pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+}  // namespace
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode;
+}
+
+// bf16 tensor map, dims/strides innermost first (strides in bytes for dims >= 1).
+bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                    const uint32_t* box, CUtensorMapSwizzle swz, std::string* why) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    if (why) *why = "cuTensorMapEncodeTiled unavailable (driver entry point)";
+    return false;
+  }
+  uint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (why) *why = "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
+template <int BN, int EPI>
+static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
+                            int num_sms, cudaStream_t st, std::string* why) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ta, tw;
+  uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
+  uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
+  uint32_t ba[2] = {BK, BM}, bw[2] = {BK, BN};
+  if (!make_tmap_bf16(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, why) ||
+      !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
+    return cudaErrorInvalidValue;
+  auto kern = gemm_bf16_tc_kernel<BN, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
+  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K);
+  return cudaGetLastError();
+}
+
+template <int EPI>
+static cudaError_t dispatch_bn(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                               int64_t K, int num_sms, cudaStream_t st, std::string* why) {
+  if (N % 256 == 0) return run_gemm<256, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+  if (N % 192 == 0) return run_gemm<192, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+  if (N % 128 == 0) return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+  if (N % 64 == 0) return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+  return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+}
+
+cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                             int64_t K, int epi, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  switch (epi) {
+    case DSP_EPI_NONE:
+      return dispatch_bn<DSP_EPI_NONE>(A, W, R, D, M, N, K, num_sms, st, why);
+    case DSP_EPI_RESIDUAL:
+      return dispatch_bn<DSP_EPI_RESIDUAL>(A, W, R, D, M, N, K, num_sms, st, why);
+    case DSP_EPI_GELU:
+      return dispatch_bn<DSP_EPI_GELU>(A, W, R, D, M, N, K, num_sms, st, why);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dsp

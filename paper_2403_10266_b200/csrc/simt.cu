@@ -1,0 +1,252 @@
+// simt.cu — fp32 check path: plain SIMT CUDA kernels for the
+// 1e-4 gate at the tiny config.  tcgen05 kind::tf32 is not used here (10-bit
+// mantissa would not meet 1e-4).  Same semantics as the bf16 tensor-core path.
+#include <cuda_bf16.h>
+#include <cmath>
+#include <type_traits>
+
+#include "dsp_internal.h"
+
+namespace dsp {
+namespace {
+
+// D[M,N] = epi(A[M,K] W[N,K]^T), 64x64 tile, 16x16 threads, 4x4 outputs per thread.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, const float* __restrict__ W,
+                                                       const float* R, float* D, int M, int N, int K) {
+  __shared__ float As[16][65];
+  __shared__ float Ws[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = threadIdx.x; i < 64 * 16; i += 256) {
+      const int r = i / 16, kk = i % 16;
+      As[kk][r] = (m0 + r < M && k0 + kk < K) ? A[(size_t)(m0 + r) * K + k0 + kk] : 0.f;
+      Ws[kk][r] = (n0 + r < N && k0 + kk < K) ? W[(size_t)(n0 + r) * K + k0 + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(As[kk][ty * 4 + i], Ws[kk][tx * 4 + j], acc[i][j]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, nn = n0 + tx * 4 + j;
+      if (m < M && nn < N) {
+        float v = acc[i][j];
+        if (EPI == DSP_EPI_RESIDUAL) v += R[(size_t)m * N + nn];
+        if (EPI == DSP_EPI_GELU) v = 0.5f * v * (1.f + tanhf(0.7978845608028654f * (v + 0.044715f * v * v * v)));
+        D[(size_t)m * N + nn] = v;
+      }
+    }
+}
+
+// One warp per (sequence, head, query row); exact softmax in two passes over keys.
+// qkv [tok, 3C]; token of position `pos` in sequence `seq`:
+//   tok = (seq / n_in) * stride_out + (seq % n_in) * stride_in + pos * pos_stride
+__global__ void attn_f32_kernel(const float* __restrict__ qkv, float* __restrict__ o, int nseq, int L, int NH, int Dh,
+                                int C, int n_in, long stride_out, long stride_in, long pos_stride) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long total = (long)nseq * NH * L;
+  if (gw >= total) return;
+  const int i = gw % L;
+  const int h = (gw / L) % NH;
+  const int seq = gw / (L * NH);
+  const long base = (seq / n_in) * stride_out + (long)(seq % n_in) * stride_in;
+  const float scale = 1.f / sqrtf((float)Dh);
+  const float* qrow = qkv + (base + i * pos_stride) * 3 * C + h * Dh;
+  float mx = -INFINITY;
+  for (int j = 0; j < L; ++j) {
+    const float* krow = qkv + (base + j * pos_stride) * 3 * C + C + h * Dh;
+    float d = 0.f;
+    for (int t = lane; t < Dh; t += 32) d = fmaf(qrow[t], krow[t], d);
+    for (int off = 16; off; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+    mx = fmaxf(mx, d * scale);
+  }
+  float accv[4] = {0.f, 0.f, 0.f, 0.f};  // Dh <= 128
+  float sum = 0.f;
+  for (int j = 0; j < L; ++j) {
+    const float* krow = qkv + (base + j * pos_stride) * 3 * C + C + h * Dh;
+    const float* vrow = krow + C;
+    float d = 0.f;
+    for (int t = lane; t < Dh; t += 32) d = fmaf(qrow[t], krow[t], d);
+    for (int off = 16; off; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
+    const float pj = expf(d * scale - mx);
+    sum += pj;
+    for (int t = lane, u = 0; t < Dh; t += 32, ++u) accv[u] = fmaf(pj, vrow[t], accv[u]);
+  }
+  float* orow = o + (base + i * pos_stride) * C + h * Dh;
+  for (int t = lane, u = 0; t < Dh; t += 32, ++u) orow[t] = accv[u] / sum;
+}
+
+// LayerNorm: one warp per row, fp32 math, two-pass (mean, then centred variance).
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p, long i);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p, long i) { return p[i]; }
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, long i) { return __bfloat162float(p[i]); }
+
+template <typename T>
+__global__ void layer_norm_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b, float eps,
+                                  T* y, long rows, int C) {
+  const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const T* xr = x + r * C;
+  constexpr int kMax = 48;  // up to C = 1536 held in registers for bf16
+  float v[kMax];
+  float s = 0.f;
+  int n = 0;
+  for (int c = lane; c < C; c += 32, ++n) {
+    const float f = ldf(xr, c);
+    if (n < kMax) v[n] = f;
+    s += f;
+  }
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const float mean = s / C;
+  float q = 0.f;
+  n = 0;
+  for (int c = lane; c < C; c += 32, ++n) {
+    const float d = (n < kMax ? v[n] : ldf(xr, c)) - mean;
+    q += d * d;
+  }
+  for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+  const float rstd = rsqrtf(q / C + eps);
+  T* yr = y + r * C;
+  n = 0;
+  for (int c = lane; c < C; c += 32, ++n) {
+    const float f = (n < kMax ? v[n] : ldf(xr, c));
+    const float o = (f - mean) * rstd * ldf(g, c) + ldf(b, c);
+    if constexpr (std::is_same<T, float>::value) yr[c] = o;
+    else yr[c] = __float2bfloat16_rn(o);
+  }
+}
+
+// bf16 LayerNorm specialised for C % 256 == 0 ... general C handled above; this variant
+// keeps 16-B vector accesses (C*2 % 16 == 0) and the whole row in registers (C <= 2048).
+__global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                                           const __nv_bfloat16* __restrict__ b, float eps, __nv_bfloat16* y, long rows,
+                                           int C) {
+  const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int nv = C / 8;  // 16-B vectors per row
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * C);
+  constexpr int kMaxV = 8;  // up to 8 vectors per lane -> C <= 2048
+  uint4 buf[kMaxV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      buf[k] = xr[vi];
+      const uint32_t w[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s += __uint_as_float(w[t] << 16) + __uint_as_float(w[t] & 0xFFFF0000u);
+    }
+  }
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const float mean = s / C;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      const uint32_t w[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float a = __uint_as_float(w[t] << 16) - mean, c = __uint_as_float(w[t] & 0xFFFF0000u) - mean;
+        q += a * a + c * c;
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+  const float rstd = rsqrtf(q / C + eps);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const uint4* bv = reinterpret_cast<const uint4*>(b);
+  uint4* yr = reinterpret_cast<uint4*>(y + r * C);
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      const uint4 gg = gv[vi], bb = bv[vi];
+      const uint32_t w[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
+      const uint32_t gw[4] = {gg.x, gg.y, gg.z, gg.w};
+      const uint32_t bw[4] = {bb.x, bb.y, bb.z, bb.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float lo = (__uint_as_float(w[t] << 16) - mean) * rstd * __uint_as_float(gw[t] << 16) +
+                         __uint_as_float(bw[t] << 16);
+        const float hi = (__uint_as_float(w[t] & 0xFFFF0000u) - mean) * rstd * __uint_as_float(gw[t] & 0xFFFF0000u) +
+                         __uint_as_float(bw[t] & 0xFFFF0000u);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(lo, hi);
+        o[t] = *reinterpret_cast<uint32_t*>(&p2);
+      }
+      yr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_f32(const float* A, const float* W, const float* R, float* D, int64_t M, int64_t N, int64_t K,
+                            int epi, cudaStream_t st) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+  switch (epi) {
+    case DSP_EPI_NONE: gemm_f32_kernel<DSP_EPI_NONE><<<grid, 256, 0, st>>>(A, W, R, D, (int)M, (int)N, (int)K); break;
+    case DSP_EPI_RESIDUAL: gemm_f32_kernel<DSP_EPI_RESIDUAL><<<grid, 256, 0, st>>>(A, W, R, D, (int)M, (int)N, (int)K); break;
+    case DSP_EPI_GELU: gemm_f32_kernel<DSP_EPI_GELU><<<grid, 256, 0, st>>>(A, W, R, D, (int)M, (int)N, (int)K); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_f32(const float* qkv, float* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
+                            int dim, cudaStream_t st) {
+  int nseq, L, n_in;
+  long so, si, ps;
+  if (dim == DSP_DIM_S) {  // sequences over S per frame
+    nseq = (int)(B * T_loc); L = (int)S_loc; n_in = 1; so = S_loc; si = 0; ps = 1;
+  } else {                 // sequences over T per (b, s)
+    nseq = (int)(B * S_loc); L = (int)T_loc; n_in = (int)S_loc; so = T_loc * S_loc; si = 1; ps = S_loc;
+  }
+  const long warps = (long)nseq * NH * L;
+  if (warps == 0) return cudaSuccess;
+  const int threads = 256;
+  const long blocks = (warps * 32 + threads - 1) / threads;
+  attn_f32_kernel<<<(unsigned)blocks, threads, 0, st>>>(qkv, o, nseq, L, NH, (int)(C / NH), (int)C, n_in, so, si, ps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_layer_norm(int dtype, int64_t rows, int64_t C, const void* x, const void* g, const void* b, float eps,
+                              void* y, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((rows * 32 + threads - 1) / threads);
+  if (dtype == DSP_F32) {
+    layer_norm_kernel<float><<<blocks, threads, 0, st>>>((const float*)x, (const float*)g, (const float*)b, eps,
+                                                         (float*)y, rows, (int)C);
+  } else if (C % 8 == 0 && C <= 2048) {
+    layer_norm_bf16_vec_kernel<<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
+                                                           (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows,
+                                                           (int)C);
+  } else {
+    layer_norm_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
+                                                                 (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows,
+                                                                 (int)C);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dsp

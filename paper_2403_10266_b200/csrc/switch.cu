@@ -1,0 +1,107 @@
+// switch.cu — byte-movement kernels of the dynamic switch (§3.1) and of
+// split / gather: a strided run copy (pack / unpack), the P2P direct-put over NVLink
+// peer mappings, and a signal-pad barrier.  All moves are 16-B vectorised and
+// coalesced: every run is Sn*C*elem contiguous bytes (SURVEY §8a "The switch as an
+// exact index map"), so no shared-memory transpose is needed.
+#include "dsp_internal.h"
+
+namespace dsp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// blockIdx.y = run index (i0*n1 + i1)*n2 + i2; blockIdx.x strides over the run's vectors.
+__global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                                            RunCopy rc, PeerPtrs peers, int use_peers, int64_t peer_off) {
+  const int64_t run = blockIdx.y;
+  const int64_t i2 = run % rc.n[2];
+  const int64_t i1 = (run / rc.n[2]) % rc.n[1];
+  const int64_t i0 = run / (rc.n[2] * rc.n[1]);
+  const uint4* s = reinterpret_cast<const uint4*>(src + i0 * rc.ss[0] + i1 * rc.ss[1] + i2 * rc.ss[2]);
+  uint8_t* dbase = use_peers ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
+  uint4* d = reinterpret_cast<uint4*>(dbase + i1 * rc.ds[1] + i2 * rc.ds[2]);
+  const int64_t nv = rc.run_bytes / 16;
+  const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
+  for (int64_t v0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; v0 < nv; v0 += step) {
+    uint4 buf[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * kThreads;
+      if (v < nv) buf[u] = ld_stream(s + v);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t v = v0 + u * kThreads;
+      if (v < nv) st_stream(d + v, buf[u]);
+    }
+  }
+}
+
+// Signal-pad barrier across `world` ranks (one block, one thread per peer):
+// release-store `epoch` into slot [rank] of every peer's pad, then acquire-spin until
+// every peer has written >= epoch into our own pad.  Bounded spin (no infinite hang).
+__global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64_t epoch) {
+  const int i = threadIdx.x;
+  if (i < world) {
+    __threadfence_system();
+    uint64_t* remote = static_cast<uint64_t*>(signals.p[i]) + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote), "l"(epoch) : "memory");
+    const uint64_t* mine = static_cast<const uint64_t*>(signals.p[rank]) + i;
+    uint64_t v = 0;
+    for (long spin = 0; spin < (1L << 26); ++spin) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= epoch) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+static cudaError_t launch_copy(const void* src, void* dst, const RunCopy& rc, const PeerPtrs& peers, int use_peers,
+                               int64_t peer_off, int num_sms, cudaStream_t st) {
+  const int64_t runs = rc.n[0] * rc.n[1] * rc.n[2];
+  if (runs == 0 || rc.run_bytes == 0) return cudaSuccess;
+  if (runs > 65535) return cudaErrorInvalidValue;
+  const int64_t nv = rc.run_bytes / 16;
+  int64_t bx = (nv + kThreads * kUnroll - 1) / (kThreads * kUnroll);
+  const int64_t want = (int64_t)num_sms * 8;  // ~8 resident CTAs per SM in total
+  int64_t cap = (want + runs - 1) / runs;
+  if (cap < 1) cap = 1;
+  if (bx > cap) bx = cap;
+  dim3 grid((unsigned)bx, (unsigned)runs);
+  run_copy_kernel<<<grid, kThreads, 0, st>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), rc, peers,
+                                             use_peers, peer_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int num_sms, cudaStream_t st) {
+  PeerPtrs none{};
+  return launch_copy(src, dst, rc, none, 0, 0, num_sms, st);
+}
+
+cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t dst_off, const RunCopy& rc, int num_sms,
+                           cudaStream_t st) {
+  return launch_copy(src, nullptr, rc, peer_base, 1, dst_off, num_sms, st);
+}
+
+cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st) {
+  p2p_barrier_kernel<<<1, 32, 0, st>>>(signals, rank, world, epoch);
+  return cudaGetLastError();
+}
+
+}  // namespace dsp

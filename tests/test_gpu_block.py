@@ -1,0 +1,182 @@
+"""GPU parity of the public stages and the ST block vs the float64 oracle.
+
+Multi-rank paths are exercised on ONE GPU with "virtual ranks": N contexts (rank r of
+world N) whose peer buffers are N local allocations, running concurrently on N
+streams, with the P2P switch transport (direct stores + signal-pad barriers).  The
+kernel logic is identical to the multi-GPU case; only the peer addresses are local.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import block as ob
+from oracle import switch as osw
+from tests.gpu_util import assert_block_close, bits16, to_dev, to_f64, weights_dev, weights_f64
+
+pytestmark = pytest.mark.gpu
+
+
+def dsp():
+    import paper_2403_10266_b200 as m
+    return m
+
+
+def _setup(sh: synth.BlockShape, seed=7, kappa=1.0):
+    Ws = synth.make_block_weights(sh, seed, kappa=kappa)
+    xs = synth.make_x(sh, seed)
+    return xs, Ws
+
+
+def _run_block_n1(sh, xs, Ws):
+    m = dsp()
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, sh.dtype)
+    Y = torch.empty_like(X)
+    ctx.st_block_forward(shape, weights_dev(Ws, sh.dtype), X, Y)
+    torch.cuda.synchronize()
+    return Y
+
+
+def test_block_tiny_f32_check_path():
+    """configs[0]: tiny ST block (T=4, S=16, C=64, 4 heads) fp32 check path, gate 1e-4."""
+    sh = synth.CONFIGS["tiny"]
+    xs, Ws = _setup(sh)
+    Y = _run_block_n1(sh, xs, Ws)
+    ref = ob.st_block(synth.to_f64(xs, "f32"), weights_f64(Ws, "f32"), sh.NH)
+    np.testing.assert_allclose(to_f64(Y), ref, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("sh", [synth.BlockShape(1, 16, 256, 1152, 16, "bf16"),
+                                synth.BlockShape(2, 8, 128, 256, 4, "bf16"),
+                                synth.BlockShape(1, 4, 64, 128, 2, "bf16")])
+def test_block_bf16_full_oracle(sh):
+    xs, Ws = _setup(sh)
+    Y = _run_block_n1(sh, xs, Ws)
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
+    print(assert_block_close(to_f64(Y), ref))
+
+
+def test_block_bf16_blk_sampled():
+    """configs[1] single ST block at full size (T=16, S=1024, C=1152) in the bench's launch
+    configuration: the oracle computes the spatial stage for every frame and the temporal
+    stage + MLP for 24 sampled spatial columns (slice independence)."""
+    sh = synth.CONFIGS["blk"]
+    xs, Ws = _setup(sh)
+    Y = to_f64(_run_block_n1(sh, xs, Ws))
+    W = weights_f64(Ws, "bf16")
+    y1 = ob.spatial_stage(synth.to_f64(xs, "bf16"), W, sh.NH)
+    cols = np.array(sorted(set([0, 1, 127, 128, 511, 1023] + list(np.random.default_rng(0).choice(1024, 18, replace=False)))))
+    y = ob.mlp_stage(ob.temporal_stage(y1[:, :, cols], W, sh.NH), W)
+    print(assert_block_close(Y[:, :, cols], y))
+
+
+@pytest.mark.parametrize("dim", ["S", "T"])
+def test_stage_attn_public(dim):
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, Ws = _setup(sh, seed=3)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, "bf16")
+    Out = torch.empty_like(X)
+    W = weights_dev(Ws, "bf16")
+    st = "s" if dim == "S" else "t"
+    fn = ctx.spatial_attn if dim == "S" else ctx.temporal_attn
+    fn(shape, X, W[f"w_qkv_{st}"], W[f"w_o_{st}"], X, Out)
+    torch.cuda.synchronize()
+    Wf = weights_f64(Ws, "bf16")
+    x = synth.to_f64(xs, "bf16")
+    f = ob.mha_spatial if dim == "S" else ob.mha_temporal
+    ref = x + f(x, Wf[f"w_qkv_{st}"], Wf[f"w_o_{st}"], sh.NH)
+    print(assert_block_close(to_f64(Out), ref))
+
+
+def test_block_repeat_run_bitwise():
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, Ws = _setup(sh)
+    a = bits16(_run_block_n1(sh, xs, Ws))
+    b = bits16(_run_block_n1(sh, xs, Ws))
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ virtual ranks
+class VirtualGroup:
+    """N contexts on one device, each with a private 'symmetric' buffer + signal pad."""
+
+    def __init__(self, N, region_bytes):
+        m = dsp()
+        self.N = N
+        self.ctx = [m.Context(rank=r, world=N) for r in range(N)]
+        self.region = [torch.zeros(region_bytes, dtype=torch.uint8, device="cuda") for _ in range(N)]
+        self.sig = [torch.zeros(2 * N, dtype=torch.int64, device="cuda") for _ in range(N)]
+        base = [t.data_ptr() for t in self.region]
+        sigp = [t.data_ptr() for t in self.sig]
+        for c in self.ctx:
+            c.set_peer_buffers(base, sigp, region_bytes)
+        self.streams = [torch.cuda.Stream() for _ in range(N)]
+
+    def view(self, r, offset, nbytes, dtype):
+        return self.region[r][offset:offset + nbytes].view(dtype)
+
+    def run(self, fn):
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for r in range(self.N):
+            with torch.cuda.stream(self.streams[r]):
+                fn(r)
+        for s in self.streams:
+            cur.wait_stream(s)
+        torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("B", [1, 2])
+def test_switch_p2p_virtual_ranks_bitexact(N, B):
+    m = dsp()
+    sh = synth.BlockShape(B, 16, 64, 64, 1, "bf16")
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, 1, "bf16")
+    x = synth.make_index_tagged(sh, 9)
+    nb = sh.M * 2 // N
+    g = VirtualGroup(N, 2 * nb)
+    tsh = osw.split(x, osw.DIM_T, N)
+    want_s = osw.switch(tsh, osw.DIM_T, osw.DIM_S)
+    for r in range(N):
+        g.view(r, 0, nb, torch.int16).copy_(torch.from_numpy(tsh[r].view(np.int16).reshape(-1)))
+    xin = [g.view(r, 0, nb, torch.bfloat16) for r in range(N)]
+    ys = [g.view(r, nb, nb, torch.bfloat16) for r in range(N)]
+    g.run(lambda r: g.ctx[r].switch(shape, "T", "S", xin[r], ys[r], impl="p2p"))
+    for r in range(N):
+        assert np.array_equal(bits16(ys[r]), want_s[r].view(np.int16).reshape(-1)), f"T->S rank {r}"
+    # and back: S -> T into the first half
+    g.run(lambda r: g.ctx[r].switch(shape, "S", "T", ys[r], xin[r], impl="p2p"))
+    for r in range(N):
+        assert np.array_equal(bits16(xin[r]), tsh[r].view(np.int16).reshape(-1)), f"S->T rank {r}"
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_block_p2p_virtual_ranks_n_invariant(N):
+    """DSP block over N virtual ranks == N=1 block bitwise (no reductions cross ranks,
+    no split-K: each output's reduction order is independent of N) and == oracle."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, Ws = _setup(sh)
+    ref1 = bits16(_run_block_n1(sh, xs, Ws))
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ws = m.workspace_bytes(shape, N)
+    ws = (ws + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    W = weights_dev(Ws, "bf16")
+    xsh = osw.split(xs, osw.DIM_T, N)
+    X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl="p2p"))
+    got = np.concatenate([bits16(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
