@@ -1,0 +1,412 @@
+"""bench.py — ST-block forward tokens/s of the DSP hot path on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dsp|reference]
+                    [--config blk|long|tiny] [--switch nccl|p2p]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+A step = one dsp_st_block_forward (LN1, spatial QKV GEMM,
+spatial FMHA, out-proj+residual, switch T->S, LN2, temporal QKV / FMHA / out-proj,
+LN3, FC1+GELU, FC2+residual, switch S->T) over one synthetic [B,T,S,C] activation
+already resident in HBM.  The global config is fixed as N grows (strong scaling, as in
+the paper's experiment P:153: "keep the batch size to 1 and sequence length constant").
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (oracle/) on a
+bounded sample of the same workload instead (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    "blk": (synth.CONFIGS["blk"], "configs[1] single ST block: B=1 T=16 S=1024 (32x32) C=1152 16 heads bf16"),
+    "long": (synth.CONFIGS["long"], "configs[3] long-video stress: B=1 T=128 S=4096 C=1152 16 heads bf16"),
+    "tiny": (synth.CONFIGS["tiny"], "configs[0] tiny ST block: B=1 T=4 S=16 C=64 4 heads fp32"),
+}
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ CPU oracle
+def oracle_sample(sh, seed, frames, cols, mlp_tokens):
+    """Time the float64 oracle on a bounded, stage-sampled slice of the block.
+
+    Each stage of the block touches every token once, so the per-token cost of the
+    block is the sum of the per-token costs of its stages: spatial stage (LN1 + MHA_S +
+    residual) on `frames` whole frames, temporal stage (LN2 + MHA_T + residual) on
+    `cols` whole columns, MLP stage on `mlp_tokens` tokens.  Slice independence
+    makes each sample a faithful piece of the full computation.
+    """
+    from oracle import block as ob
+    x = synth.to_f64(synth.make_x(sh, seed, t_range=(0, frames)), sh.dtype)
+    W = {k: synth.to_f64(v, sh.dtype) for k, v in synth.make_block_weights(sh, seed).items()}
+    t0 = time.perf_counter()
+    ob.spatial_stage(x, W, sh.NH)
+    t1 = time.perf_counter()
+    xc = synth.to_f64(synth.make_x(sh, seed, s_range=(0, cols)), sh.dtype)
+    ob.temporal_stage(xc, W, sh.NH)
+    t2 = time.perf_counter()
+    flat = xc.reshape(-1, sh.C)[:mlp_tokens]
+    ob.mlp_stage(flat, W)
+    t3 = time.perf_counter()
+    per_tok = (t1 - t0) / (sh.B * frames * sh.S) + (t2 - t1) / (sh.B * cols * sh.T) + (t3 - t2) / flat.shape[0]
+    return 1.0 / per_tok, t3 - t0
+
+
+def oracle_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def sample_sizes(sh, budget="baseline"):
+    if budget == "baseline":   # ~10-30 s of float64 numpy on 8 cores
+        return min(4, sh.T), min(256, sh.S), min(4096, sh.B * sh.T * sh.S)
+    return 1, min(64, sh.S), min(1024, sh.B * sh.T * sh.S)  # ~1-2 s per reference step
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sh, desc = CONFIGS[args.config]
+    frames, cols, toks = sample_sizes(sh, "step")
+    for _ in range(args.warmup):
+        oracle_sample(sh, args.seed, frames, cols, toks)
+    t0 = time.perf_counter()
+    rates = [oracle_sample(sh, args.seed, frames, cols, toks)[0] for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    v = float(np.mean(rates))
+    sample = (f"per step: oracle spatial stage on {frames} frame(s), temporal stage on {cols} columns, MLP stage on "
+              f"{toks} tokens (float64 numpy, BLAS threads = cores); tokens/s = 1 / sum of per-token stage costs")
+    out = {"impl": "reference", "metric": "ST-block fwd tokens/s", "value": v, "unit": "tokens/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": desc, "global_tokens": sh.B * sh.T * sh.S},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML polling thread (SM clock + throttle reasons) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def stage_work(name, sh, N):
+    """(algorithmic amount, unit, bound) per rank per launch of a block stage."""
+    B, T, S, C = sh.B, sh.T, sh.S, sh.C
+    tok = B * T * S // N
+    e = sh.elem_bytes
+    gem = {"QKV_S": 6, "QKV_T": 6, "PROJ_S": 2, "PROJ_T": 2, "FC1": 8, "FC2": 8}
+    if name in gem:
+        return gem[name] * tok * C * C, "flop", "tensor"
+    if name == "ATTN_S":
+        return 4 * B * (T // N) * S * S * C, "flop", "tensor"
+    if name == "ATTN_T":
+        return 4 * tok * C * e, "byte", "hbm"  # q, k, v read + o write, once each
+    if name.startswith("LN"):
+        return 2 * tok * C * e, "byte", "hbm"
+    if name.startswith("SWITCH"):
+        return (N - 1) * B * (T // N) * (S // N) * C * e, "byte", "nvlink"
+    return 0, "", ""
+
+
+def run_dsp(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_10266_b200 as dsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun --nproc-per-node {args.gpus}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    sh, desc = CONFIGS[args.config]
+    N = world
+    Tn = sh.T // N
+    ctx = dsp.Context(pg=pg, device=dev)
+    shape = dsp.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    tdt = torch.bfloat16 if sh.dtype == "bf16" else torch.float32
+
+    def to_dev(a):
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a.view(np.int16)).view(torch.bfloat16) if sh.dtype == "bf16" else torch.from_numpy(a)
+        return t.to(dev)
+
+    xs = synth.make_x(sh, args.seed, t_range=(rank * Tn, (rank + 1) * Tn))
+    W = {k: to_dev(v) for k, v in synth.make_block_weights(sh, args.seed).items()}
+    bw = ctx.block_weights(W)
+    X = to_dev(xs)
+    act_bytes = X.numel() * X.element_size()
+    ws_bytes = dsp.workspace_bytes(shape, N)
+    impl = args.switch
+    if impl == "p2p" and N > 1:
+        import torch.distributed._symmetric_memory as symm
+        ws_pad = (ws_bytes + 4095) // 4096 * 4096
+        buf = symm.empty(ws_pad + act_bytes, dtype=torch.uint8, device=dev)
+        hdl = symm.rendezvous(buf, dist.group.WORLD.group_name)
+        ctx.set_peer_buffers(hdl.buffer_ptrs, hdl.signal_pad_ptrs, ws_pad + act_bytes)
+        ctx.set_workspace(buf[:ws_pad])
+        Y = buf[ws_pad:ws_pad + act_bytes].view(tdt)
+    else:
+        ctx.ensure_workspace(ws_bytes)
+        Y = torch.empty_like(X)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        ctx.st_block_forward(shape, bw, X, Y, impl=impl)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # warm-up
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    barrier()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    l0 = ctx.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        for i in range(K):
+            flush.zero_()                      # L2 flush between timed steps (outside the events)
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        barrier()
+    launches = ctx.launch_count() - l0
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    tokens = sh.B * sh.T * sh.S
+    value = tokens * K / (t_ms / 1e3)
+
+    # per-stage timing pass (same launch configuration, stage events inside the block)
+    stage_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(dsp.STAGES))]
+    ctx.set_stage_events(stage_ev)
+    KP = max(3, min(K, 20))
+    acc = np.zeros(len(dsp.STAGES))
+    for _ in range(KP):
+        flush.zero_()
+        step()
+        torch.cuda.synchronize()
+        acc += [stage_ev[2 * i].elapsed_time(stage_ev[2 * i + 1]) for i in range(len(dsp.STAGES))]
+    ctx.set_stage_events(None)
+    stage_ms = acc / KP
+    if world > 1:
+        st = torch.tensor(stage_ms, dtype=torch.float64, device=dev)
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        stage_ms = st.cpu().numpy()
+    P, peak_src = peaks()
+    stages = {}
+    for i, name in enumerate(dsp.STAGES):
+        amt, unit, bound = stage_work(name, sh, N)
+        us = stage_ms[i] * 1e3
+        if amt == 0 or us <= 0.05:
+            stages[name] = {"us": round(us, 2)}
+            continue
+        if unit == "flop":
+            ach, pk, u = amt / (us * 1e-6) / 1e12, P["bf16_tflops"], "TFLOP/s"
+        elif bound == "hbm":
+            ach, pk, u = amt / (us * 1e-6) / 1e9, P["hbm_gbs"], "GB/s"
+        else:
+            ach, pk, u = amt / (us * 1e-6) / 1e9, 900.0, "GB/s"
+        stages[name] = {"us": round(us, 2), "achieved": round(ach, 1), "unit": u, "frac": round(ach / pk, 3),
+                        "bound": bound}
+    dom = max((n for n in stages if "frac" in stages[n]), key=lambda n: stages[n]["us"])
+    amt, unit, bound = stage_work(dom, sh, N)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    roof = {"kernel": dom, "bound": bound, "achieved": stages[dom]["achieved"],
+            "peak": P["bf16_tflops"] if unit == "flop" else P["hbm_gbs"], "unit": stages[dom]["unit"],
+            "frac": stages[dom]["frac"], "traffic": traffic, "peak_source": peak_src + ", burst",
+            "algorithmic_per_launch": amt, "algorithmic_unit": unit}
+    flops_block = 32 * tokens * sh.C ** 2 + 4 * sh.B * sh.T * sh.S ** 2 * sh.C + 4 * sh.B * sh.S * sh.T ** 2 * sh.C
+    t_roof_us = flops_block / N / (P["bf16_tflops"] * 1e12) * 1e6
+    nvl_us = 2 * (N - 1) * sh.M // (N * N) * sh.elem_bytes / 900e9 * 1e6
+    block_roof = {"t_roofline_us": round(max(t_roof_us, nvl_us), 1), "t_block_us": round(t_ms / K * 1e3, 1),
+                  "frac": round(max(t_roof_us, nvl_us) / (t_ms / K * 1e3), 3),
+                  "basis": "max(block FLOPs/N / measured bf16 peak, 2 switches' bytes / 900 GB/s)"}
+
+    # switch bus bandwidth (N > 1): busbw = (N-1)/N * shard_bytes / t
+    switch = None
+    if world > 1:
+        Z = torch.empty_like(X) if not (impl == "p2p") else None
+        if impl == "p2p":
+            Z = Y
+            src = torch.empty_like(X)
+        else:
+            src = Y
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for _ in range(3):
+            ctx.switch(shape, "T", "S", src, Z, impl=impl)
+        barrier()
+        for i in range(K):
+            evs[i][0].record()
+            ctx.switch(shape, "T", "S", src, Z, impl=impl)
+            evs[i][1].record()
+        barrier()
+        ts = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / K], dtype=torch.float64, device=dev)
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        sent, _ = dsp.switch_volume(shape, N)
+        switch = {"direction": "T->S", "impl": impl, "us": round(float(ts.item()) * 1e3, 2),
+                  "busbw_GBps": round(sent / (float(ts.item()) * 1e-3) / 1e9, 1),
+                  "algbw_GBps": round(act_bytes / (float(ts.item()) * 1e-3) / 1e9, 1),
+                  "nvlink_peak_GBps": 900.0, "bytes_sent_per_rank": sent}
+
+    # e2e through the C ABI with host buffers (H2D x + block + D2H y inside the timed region)
+    xh = torch.from_numpy(np.ascontiguousarray(xs).view(np.int16) if sh.dtype == "bf16" else xs).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    Xd, Yd = torch.empty_like(X), torch.empty_like(X)
+    if impl == "p2p" and N > 1:
+        Yd = Y
+    for _ in range(max(1, args.warmup)):
+        ctx.st_block_forward_host(shape, bw, xh, yh, Xd, Yd, impl=impl)
+    barrier()
+    eve = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for i in range(K):
+        flush.zero_()
+        eve[i][0].record()
+        ctx.st_block_forward_host(shape, bw, xh, yh, Xd, Yd, impl=impl)
+        eve[i][1].record()
+    barrier()
+    te = torch.tensor([sum(a.elapsed_time(b) for a, b in eve)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": tokens * K / (float(te.item()) / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": act_bytes,
+           "d2h_bytes_per_step": act_bytes, "per_rank": True}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            frames, cols, toks = sample_sizes(sh, "baseline")
+            v, secs = oracle_sample(sh, args.seed, frames, cols, toks)
+            cpu = {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
+                   "sample": f"float64 numpy oracle, stage-sampled: spatial stage on {frames} frames, temporal stage "
+                             f"on {cols} columns, MLP stage on {toks} tokens ({secs:.1f} s); tokens/s = 1 / sum of "
+                             f"per-token stage costs"}
+        out = {"metric": "ST-block fwd tokens/s", "value": value, "unit": "tokens/s", "n_gpus": N, "steps": K,
+               "warmup": args.warmup, "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": sh.dtype, "data": "synthetic",
+               "config": {"workload": desc, "B": sh.B, "T": sh.T, "S": sh.S, "C": sh.C, "num_heads": sh.NH,
+                          "global_tokens": tokens, "switch_impl": impl if N > 1 else "none (N=1)",
+                          "l2": "flushed between timed steps (256 MiB memset outside the events)"},
+               "roofline": roof, "block_roofline": block_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": launches, "launches_per_step": launches / K, "clocks": clocks.summary()}
+        if switch:
+            out["switch"] = switch
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
+    ap.add_argument("--config", default="blk", choices=list(CONFIGS))
+    ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_dsp(args)
+
+
+if __name__ == "__main__":
+    main()

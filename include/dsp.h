@@ -121,6 +121,20 @@ dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* workspace_dev, size_t by
 dsp_status_t dsp_ctx_set_peer_buffers(dsp_ctx_t ctx, void* const* peer_base_dev,
                                       void* const* peer_signal_dev, size_t bytes);
 
+/* Instrumentation (off the hot path).  Stage ids of dsp_st_block_forward, in order. */
+typedef enum {
+  DSP_STAGE_LN1 = 0, DSP_STAGE_QKV_S, DSP_STAGE_ATTN_S, DSP_STAGE_PROJ_S, DSP_STAGE_SWITCH_TS,
+  DSP_STAGE_LN2, DSP_STAGE_QKV_T, DSP_STAGE_ATTN_T, DSP_STAGE_PROJ_T, DSP_STAGE_LN3,
+  DSP_STAGE_FC1, DSP_STAGE_FC2, DSP_STAGE_SWITCH_ST, DSP_NUM_STAGES
+} dsp_stage_t;
+/* events: HOST array of 2*DSP_NUM_STAGES cudaEvent_t (caller-owned) or NULL to disable.
+ * When set, dsp_st_block_forward records events[2*i] / events[2*i+1] on its stream
+ * around stage i (both recorded even when a stage is skipped, e.g. switches at N=1). */
+dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n_events);
+/* Number of this library's own kernels launched through ctx since creation (NCCL kernels
+ * and cudaMemcpy excluded).  HOST-ONLY. */
+int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
+
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */

@@ -55,6 +55,8 @@ class SwitchPlan(ctypes.Structure):
                 ("pack_is_identity", ctypes.c_int32), ("unpack_is_identity", ctypes.c_int32)]
 
 
+STAGES = ("LN1", "QKV_S", "ATTN_S", "PROJ_S", "SWITCH_TS", "LN2", "QKV_T", "ATTN_T", "PROJ_T", "LN3", "FC1",
+          "FC2", "SWITCH_ST")
 WEIGHT_NAMES = tuple(n for n, _ in BlockWeights._fields_[:12])
 
 _lib = None
@@ -86,6 +88,7 @@ def lib() -> ctypes.CDLL:
             "dsp_layer_norm": [vp, ctypes.c_int, i64, i64, vp, vp, vp, ctypes.c_float, vp, vp],
             "dsp_linear": [vp, ctypes.c_int, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp, vp],
             "dsp_attention_core": [vp, ctypes.c_int, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp],
+            "dsp_ctx_set_stage_events": [vp, P(vp), ctypes.c_int],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -98,6 +101,8 @@ def lib() -> ctypes.CDLL:
         L.dsp_last_error.argtypes = [vp]
         L.dsp_last_error.restype = ctypes.c_char_p
         L.dsp_abi_version.restype = ctypes.c_int
+        L.dsp_ctx_launch_count.argtypes = [vp]
+        L.dsp_ctx_launch_count.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -219,6 +224,22 @@ class Context:
         B = (ctypes.c_void_p * n)(*base_ptrs)
         S = (ctypes.c_void_p * n)(*signal_ptrs)
         _check(lib().dsp_ctx_set_peer_buffers(self.handle, B, S, int(nbytes)), self.handle)
+
+    # ---- instrumentation
+    def launch_count(self) -> int:
+        return int(lib().dsp_ctx_launch_count(self.handle))
+
+    def set_stage_events(self, events):
+        """events: list of 2*len(STAGES) torch.cuda.Event(enable_timing=True), or None."""
+        if events is None:
+            _check(lib().dsp_ctx_set_stage_events(self.handle, None, 0), self.handle)
+            self._stage_events = None
+            return
+        for e in events:
+            e.record()  # materialise the underlying cudaEvent_t
+        arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+        self._stage_events = (events, arr)
+        _check(lib().dsp_ctx_set_stage_events(self.handle, arr, len(events)), self.handle)
 
     # ---- layout ops
     def split(self, shape, dim, x_global, x_local, stream=None):

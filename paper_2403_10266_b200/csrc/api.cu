@@ -40,12 +40,6 @@ dsp_status_t cuda_fail(dsp_ctx_t ctx, cudaError_t e, const char* what, const std
     cudaError_t _e = (expr);                             \
     if (_e != cudaSuccess) return cuda_fail(ctx, _e, what, _why); \
   } while (0)
-#define DSP_CUDA_WHY(ctx, call, what)                    \
-  do {                                                   \
-    std::string _why;                                    \
-    cudaError_t _e = call;                               \
-    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what, _why); \
-  } while (0)
 #define DSP_TRY(expr)                 \
   do {                                \
     dsp_status_t _s = (expr);         \
@@ -165,6 +159,7 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p entry barrier");
     DSP_CUDA(ctx, launch_p2p_put(x, ctx->peer_base, y_off + p.dst_peer_off, rc, ctx->num_sms, st), "p2p put");
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p exit barrier");
+    ctx->launches += 3;
     return DSP_OK;
   }
   if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
@@ -176,6 +171,7 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
   void* recv = y;
   if (!p.pack_is_identity) {
     DSP_CUDA(ctx, launch_run_copy(x, scratch_send, pack, ctx->num_sms, st), "switch pack");
+    ctx->launches += 1;
     send = scratch_send;
   }
   if (!p.unpack_is_identity) recv = scratch_recv;
@@ -192,29 +188,51 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
     if (!r) r = r2;
   }
   if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAlltoAll: %s", ctx->nccl.GetErrorString(r));
-  if (!p.unpack_is_identity) DSP_CUDA(ctx, launch_run_copy(recv, y, unpack, ctx->num_sms, st), "switch unpack");
+  if (!p.unpack_is_identity) {
+    DSP_CUDA(ctx, launch_run_copy(recv, y, unpack, ctx->num_sms, st), "switch unpack");
+    ctx->launches += 1;
+  }
   return DSP_OK;
 }
 
-// one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C]
+inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
+  if (ctx->has_stage_events && stage >= 0) cudaEventRecord((cudaEvent_t)ctx->stage_events[2 * stage + end], st);
+}
+
+// one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C].
+// stage0 >= 0: record stage events for (QKV, ATTN, PROJ) = stage0, stage0+1, stage0+2.
 dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
                         const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
-                        cudaStream_t st) {
+                        cudaStream_t st, int stage0 = -1) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
+  const int sq = stage0, sa = stage0 < 0 ? -1 : stage0 + 1, sp = stage0 < 0 ? -1 : stage0 + 2;
   if (s->dtype == DSP_BF16) {
     std::string why;
+    mark(ctx, sq, 0, st);
     cudaError_t e = launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "qkv projection", why);
-    e = launch_fmha_bf16(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, dim, st, &why);
+    mark(ctx, sq, 1, st);
+    mark(ctx, sa, 0, st);
+    e = launch_fmha_bf16(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, dim, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
+    mark(ctx, sa, 1, st);
+    mark(ctx, sp, 0, st);
     e = launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "output projection", why);
+    mark(ctx, sp, 1, st);
   } else {
+    mark(ctx, sq, 0, st);
     DSP_CUDA(ctx, launch_gemm_f32((const float*)h, (const float*)w_qkv, nullptr, (float*)qkv, tok, 3 * C, C, DSP_EPI_NONE, st), "qkv projection f32");
+    mark(ctx, sq, 1, st);
+    mark(ctx, sa, 0, st);
     DSP_CUDA(ctx, launch_attn_f32((const float*)qkv, (float*)o, s->B, T_loc, S_loc, C, s->num_heads, dim, st), "attention f32");
+    mark(ctx, sa, 1, st);
+    mark(ctx, sp, 0, st);
     DSP_CUDA(ctx, launch_gemm_f32((const float*)o, (const float*)w_o, (const float*)res, (float*)out, tok, C, C, epi, st), "output projection f32");
+    mark(ctx, sp, 1, st);
   }
+  if (tok > 0) ctx->launches += 3;
   return DSP_OK;
 }
 
@@ -227,6 +245,7 @@ dsp_status_t linear(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t M, int64_t N, int64_t
   } else {
     DSP_CUDA(ctx, launch_gemm_f32((const float*)A, (const float*)W, (const float*)R, (float*)D, M, N, K, epi, st), "linear f32");
   }
+  if (M > 0) ctx->launches += 1;
   return DSP_OK;
 }
 
@@ -294,6 +313,20 @@ size_t dsp_workspace_bytes(const dsp_shape_t* s, int world) {
   return (size_t)(tok * 6 * s->C * elem_bytes(s->dtype)) + 256;
 }
 
+dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (!events) {
+    ctx->has_stage_events = false;
+    return DSP_OK;
+  }
+  if (n != 2 * DSP_NUM_STAGES) return fail(ctx, DSP_ERR_SHAPE, "need %d events", 2 * DSP_NUM_STAGES);
+  for (int i = 0; i < n; ++i) ctx->stage_events[i] = events[i];
+  ctx->has_stage_events = true;
+  return DSP_OK;
+}
+
+int64_t dsp_ctx_launch_count(dsp_ctx_t ctx) { return ctx ? ctx->launches : -1; }
+
 dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* ws, size_t bytes) {
   if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
   if (ws && !aligned16(ws)) return fail(ctx, DSP_ERR_ALIGNMENT, "workspace not 16-B aligned");
@@ -357,6 +390,7 @@ dsp_status_t dsp_split(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const
     xg = static_cast<const uint8_t*>(xg) + r * Sn * row;
   }
   DSP_CUDA(ctx, launch_run_copy(xg, xl, rc, ctx->num_sms, (cudaStream_t)stream), "split");
+  ctx->launches += 1;
   return DSP_OK;
 }
 
@@ -396,6 +430,7 @@ dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, cons
       rc.ds[0] = Sn * row; rc.ds[1] = T * S * row; rc.ds[2] = S * row;
     }
     DSP_CUDA(ctx, launch_run_copy(stage, xg, rc, ctx->num_sms, st), "gather unpack");
+    ctx->launches += 1;
   }
   return DSP_OK;
 }
@@ -491,23 +526,40 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   const float eps = w->ln_eps;
   const int64_t Tn = s->T / N, Sn = s->S / N;
   // a1-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
+  mark(ctx, DSP_STAGE_LN1, 0, st);
   DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
-  DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, h, w->w_qkv_s, w->w_o_s, x, y, qkv, o, st));
+  ctx->launches += 1;
+  mark(ctx, DSP_STAGE_LN1, 1, st);
+  DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, h, w->w_qkv_s, w->w_o_s, x, y, qkv, o, st, DSP_STAGE_QKV_S));
   // a5: switch T -> S
   void* cur = y;
+  mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
   if (N > 1) {
     DSP_TRY(do_switch(ctx, s, DSP_DIM_T, y, ys, impl, st, big, big + act));
     cur = ys;
   }
+  mark(ctx, DSP_STAGE_SWITCH_TS, 1, st);
   // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place)
+  mark(ctx, DSP_STAGE_LN2, 0, st);
   DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
-  DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, h, w->w_qkv_t, w->w_o_t, cur, cur, qkv, o, st));
+  ctx->launches += 1;
+  mark(ctx, DSP_STAGE_LN2, 1, st);
+  DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, h, w->w_qkv_t, w->w_o_t, cur, cur, qkv, o, st, DSP_STAGE_QKV_T));
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
+  mark(ctx, DSP_STAGE_LN3, 0, st);
   DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
+  ctx->launches += 1;
+  mark(ctx, DSP_STAGE_LN3, 1, st);
+  mark(ctx, DSP_STAGE_FC1, 0, st);
   DSP_TRY(linear(ctx, s->dtype, tok, 4 * C, C, h, w->w_fc1, nullptr, DSP_EPI_GELU, big, st));
+  mark(ctx, DSP_STAGE_FC1, 1, st);
+  mark(ctx, DSP_STAGE_FC2, 0, st);
   DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));
+  mark(ctx, DSP_STAGE_FC2, 1, st);
   // a11: switch S -> T back into y
+  mark(ctx, DSP_STAGE_SWITCH_ST, 0, st);
   if (N > 1) DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
+  mark(ctx, DSP_STAGE_SWITCH_ST, 1, st);
   return DSP_OK;
 }
 
@@ -534,6 +586,7 @@ dsp_status_t dsp_layer_norm(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t rows, int64_t
   if (dt != DSP_BF16 && dt != DSP_F32) return fail(ctx, DSP_ERR_SHAPE, "unknown dtype");
   if (dt == DSP_BF16 && (C * 2) % 16) return fail(ctx, DSP_ERR_ALIGNMENT, "bf16 LN needs C %% 8 == 0");
   DSP_CUDA(ctx, launch_layer_norm(dt, rows, C, x, g, b, eps, y, (cudaStream_t)stream), "layer_norm");
+  if (rows > 0) ctx->launches += 1;
   return DSP_OK;
 }
 
@@ -565,11 +618,12 @@ dsp_status_t dsp_attention_core(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t B, int64_
   cudaStream_t st = (cudaStream_t)stream;
   if (dt == DSP_BF16) {
     std::string why;
-    cudaError_t e = launch_fmha_bf16(qkv, o, B, T_loc, S_loc, C, NH, dim, st, &why);
+    cudaError_t e = launch_fmha_bf16(qkv, o, B, T_loc, S_loc, C, NH, dim, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
   } else {
     DSP_CUDA(ctx, launch_attn_f32((const float*)qkv, (float*)o, B, T_loc, S_loc, C, NH, dim, st), "attention f32");
   }
+  ctx->launches += 1;
   return DSP_OK;
 }
 

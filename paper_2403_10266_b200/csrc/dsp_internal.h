@@ -44,7 +44,7 @@ struct RunCopy {
 cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
                              int epi, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
-                             int dim, cudaStream_t st, std::string* why);
+                             int dim, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_gemm_f32(const float* A, const float* W, const float* R, float* D, int64_t M, int64_t N, int64_t K,
                             int epi, cudaStream_t st);
 cudaError_t launch_attn_f32(const float* qkv, float* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
@@ -71,6 +71,9 @@ struct dsp_ctx {
   dsp::PeerPtrs peer_base{}, peer_signal{};
   bool has_peers = false;
   size_t peer_bytes = 0;
+  int64_t launches = 0;            // own kernels launched (instrumentation)
+  void* stage_events[2 * DSP_NUM_STAGES] = {};
+  bool has_stage_events = false;
   uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
   std::string last_error;
 };

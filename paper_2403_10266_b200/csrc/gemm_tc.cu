@@ -1,19 +1,26 @@
-// gemm_tc.cu — persistent warp-specialised tcgen05 GEMM for sm_100a.
+// gemm_tc.cu — persistent warp-specialised tcgen05 GEMM for sm_100a, CTA-pair (2-SM) MMA.
 //
 // D[M,N] = epi(A[M,K] * W[N,K]^T), bf16 in / fp32 accumulate in TMEM / bf16 out.
 // Used for every dense contraction of the ST block:
 // QKV projection (plain), out-projection (+residual), FC1 (+GELU), FC2 (+residual).
 //
-// Roles (256 threads, 1 CTA per SM, grid = min(tiles, #SMs), static round-robin tiles):
-//   warp 0      TMA producer: A tile 128x64 and W tile BNx64 per k-block, SW128, into a
-//               STAGES-deep smem ring (full/empty mbarriers).
-//   warp 1      MMA issuer: one elected lane issues 4 x tcgen05.mma (M=128, N=BN, K=16)
-//               per k-block into one of two TMEM accumulators; tcgen05.commit frees the
-//               smem stage and, after the last k-block, signals the epilogue.
-//   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time (thread = accumulator row),
-//               fused residual / GELU, bf16 pack, 16-B global stores; then release the
-//               accumulator so the MMA warp can start the tile after next.
+// Why CTA pairs: with single-CTA 128xBN tiles every operand byte crosses the SM's shared
+// memory twice (TMA write + UMMA read), which caps the tensor pipe near 60% of peak on
+// B200.  A cluster of 2 CTAs computes a 256xBN tile with tcgen05.mma.cta_group::2: each
+// CTA stages its own 128 rows of A and HALF of the BN rows of W, so per-SM smem traffic
+// per MMA drops by ~30% at BN=192/256.
+//
+// Roles (256 threads per CTA, grid = 2 x min(tiles, #SMs/2), static round-robin tiles):
+//   warp 0      TMA producer (both CTAs): A rows [m0+128r, +128) and W rows
+//               [n0 + r*BN/2, +BN/2) per 64-wide k-block into a STAGES-deep ring; the
+//               bytes complete on the LEADER's full barrier.
+//   warp 1      TMEM allocator (both CTAs, cta_group::2) and, in the leader only, the MMA
+//               issuer: 4 x tcgen05.mma (M=256, N=BN, K=16) per k-block into one of two
+//               TMEM accumulators; multicast commits free the smem stage in both CTAs and,
+//               after the last k-block, signal both epilogues.
+//   warps 4-7   epilogue (both CTAs): tcgen05.ld 32 columns at a time (thread = accumulator
+//               row), fused residual / GELU, bf16 pack, 16-B global stores; then arrive on
+//               the leader's accumulator-empty barrier.
 // No split-K, no atomics: each output's reduction order depends only on K (N-invariance).
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -27,16 +34,17 @@ namespace dsp {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one SW128 atom row
+constexpr int BM = 128;  // rows per CTA (256 per pair)
+constexpr int BK = 64;   // 64 bf16 = 128 B = one SW128 atom row
 
 template <int BN>
 struct GemmCfg {
+  static constexpr int BNH = BN / 2;                    // W rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 8 ? 8 : (220 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 };
 
@@ -62,10 +70,13 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = warp_id();
-  const int tiles_m = (M + BM - 1) / BM;
+  const uint32_t rank = cluster_ctarank();  // 0 = leader of the CTA pair
+  const bool leader = rank == 0;
+  const int tiles_m = (M + 2 * BM - 1) / (2 * BM);
   const int tiles_n = N / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch(&tmA);
@@ -76,16 +87,16 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 2 * 128);  // both CTAs' epilogue threads
     }
     fence_barrier_init();
   }
-  if (warp == 2) {
-    tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
-    tmem_relinquish();
+  if (warp == 1) {
+    tmem_alloc_2sm(tmem_holder, Cfg::TMEM_COLS);
+    tmem_relinquish_2sm();
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
@@ -93,14 +104,14 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * BM;
-        const int n0 = (tile / tiles_m) * BN;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        const int m0 = (tile % tiles_m) * (2 * BM) + rank * BM;
+        const int n0 = (tile / tiles_m) * BN + rank * Cfg::BNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
-          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmW, &full[stage], kb * BK, n0);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          tma_load_2d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          tma_load_2d_2sm(sB + stage * Cfg::B_BYTES, &tmW, &full[stage], kb * BK, n0);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -109,34 +120,36 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int acc = it & 1;
-      mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(&full[stage], phase);
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+        const uint32_t d_tmem = tmem + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, SW_128B);
-            const uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, SW_128B);
-            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, SW_128B);
+              const uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, SW_128B);
+              umma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+            umma_commit_2sm_mc(&empty[stage], 0x3);
+            if (kb == num_kb - 1) umma_commit_2sm_mc(&tfull[acc], 0x3);
           }
-          umma_commit(&empty[stage]);
-          if (kb == num_kb - 1) umma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -144,9 +157,9 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane_id();
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
-      const int m0 = (tile % tiles_m) * BM;
+      const int m0 = (tile % tiles_m) * (2 * BM) + rank * BM;
       const int n0 = (tile / tiles_m) * BN;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -190,15 +203,16 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (leader) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
     }
   }
 
   tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
+  cluster_sync();
+  if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, Cfg::TMEM_COLS);
+    tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
   }
 }
 
@@ -244,7 +258,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   CUtensorMap ta, tw;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
-  uint32_t ba[2] = {BK, BM}, bw[2] = {BK, BN};
+  uint32_t ba[2] = {BK, BM}, bw[2] = {BK, Cfg::BNH};
   if (!make_tmap_bf16(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, why) ||
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
@@ -255,10 +269,21 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int64_t tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = (int)(tiles < num_sms ? tiles : num_sms);
-  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K);
-  return cudaGetLastError();
+  const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K);
 }
 
 template <int EPI>

@@ -51,7 +51,7 @@ def test_block_tiny_f32_check_path():
 
 @pytest.mark.parametrize("sh", [synth.BlockShape(1, 16, 256, 1152, 16, "bf16"),
                                 synth.BlockShape(2, 8, 128, 256, 4, "bf16"),
-                                synth.BlockShape(1, 4, 64, 128, 2, "bf16")])
+                                synth.BlockShape(1, 4, 128, 1152, 16, "bf16")])
 def test_block_bf16_full_oracle(sh):
     xs, Ws = _setup(sh)
     Y = _run_block_n1(sh, xs, Ws)
