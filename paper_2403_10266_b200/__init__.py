@@ -18,7 +18,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdsp.so")
+LIB_PATH = os.environ.get("DSP_LIB_OVERRIDE") or os.path.join(_HERE, "libdsp.so")  # override: A/B experiments only
 
 DSP_DIM_T, DSP_DIM_S = 1, 2
 DSP_BF16, DSP_F32 = 0, 1

@@ -109,6 +109,234 @@ __device__ __forceinline__ float max8(const float* v) {
   return fmaxf(a, b);
 }
 
+// Geometry of the key columns one softmax thread touches.
+struct SoftmaxGeom {
+  int row;            // query row of this thread in the tile (= TMEM lane)
+  uint32_t lane_off;  // TMEM lane offset of this warp's quadrant
+  bool diag;          // block-diagonal packing (G > 1)
+  int wc0, nhalf, hcols, L, my_blk;
+  float sl2;          // log2(e) / sqrt(Dh)
+};
+
+__device__ __forceinline__ SoftmaxGeom make_geom(const FmhaParams& p, int warp, float sl2) {
+  SoftmaxGeom g;
+  const int q = warp & 3;
+  g.row = q * 32 + lane_id();
+  g.lane_off = (uint32_t)(q * 32) << 16;
+  g.diag = p.G > 1;
+  const int wcols = g.diag ? (p.L > 32 ? p.L : 32) : 128;
+  g.wc0 = g.diag ? (q * 32 / wcols) * wcols : 0;
+  g.nhalf = (wcols + 63) / 64;
+  g.hcols = wcols < 64 ? wcols : 64;
+  g.L = p.L;
+  g.my_blk = g.row / (p.L < 128 ? p.L : 128);
+  g.sl2 = sl2;
+  return g;
+}
+
+// One online-softmax step on S_j (in TMEM at tS): row max, lazy O rescale (after PV_{j-1}
+// completed, signalled on o_done), P_j = exp2(S*scale - m) as bf16 into the SW128 smem tile
+// sP, running sum l.  Returns after the P stores are fenced for the async proxy.
+template <int DP>
+__device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
+                                             float& m, float& l, uint64_t* o_done, uint32_t& no) {
+  const int row = G.row;
+  const uint32_t lane_off = G.lane_off;
+  const bool diag = G.diag;
+  const int wc0 = G.wc0, nhalf = G.nhalf, hcols = G.hcols, my_blk = G.my_blk;
+  const float sl2 = G.sl2;
+  uint8_t* prow = sP + row * 128;
+  // pass 1: row max over this thread's valid columns
+  float mx = -INFINITY;
+  for (int hf = 0; hf < nhalf; ++hf) {
+    float s[64];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (c * 32 < hcols) {
+        uint32_t v[32];
+        tmem_ld32(tS + lane_off + wc0 + hf * 64 + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = -INFINITY;
+      }
+    }
+    if (diag) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if ((wc0 + hf * 64 + i) / G.L != my_blk) s[i] = -INFINITY;
+    }
+    float t8[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) t8[a] = max8(s + 8 * a);
+    mx = fmaxf(mx, max8(t8));
+  }
+  const float mx2 = mx * sl2;
+  const bool bump = (j == 0) || (mx2 > m + 8.f);
+  const float m_new = bump ? mx2 : m;
+  const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
+  m = m_new;
+  if (j > 0) {
+    mbar_wait(o_done, no & 1);  // PV_{j-1} done: O stable, P buffer free
+    ++no;
+    tc_fence_after();
+    if (__any_sync(0xffffffffu, bump)) {
+      const float a = bump ? alpha : 1.f;
+#pragma unroll
+      for (int c = 0; c < DP / 16; ++c) {
+        uint32_t v[16];
+        tmem_ld16(tO + lane_off + c * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a);
+        tmem_st16(tO + lane_off + c * 16, v);
+      }
+      tmem_st_wait();
+    }
+  }
+  // pass 2: exponentiate, row-sum, P (bf16) -> smem.  SW128 K-major: 16-B chunk c of
+  // row r lives at chunk position c ^ (r & 7) of the row's 128-B line.
+  float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int hf = 0; hf < nhalf; ++hf) {
+    const int col0 = wc0 + hf * 64;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (c * 32 < hcols) {
+        uint32_t v[32];
+        tmem_ld32(tS + lane_off + col0 + c * 32, v);
+        tmem_ld_wait();
+        float e[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float x = __uint_as_float(v[i]);
+          if (diag && (col0 + c * 32 + i) / G.L != my_blk) x = -INFINITY;
+          e[i] = fast_exp2(fmaf(x, sl2, -m_new));
+          rs8[i & 7] += e[i];
+        }
+        const int colb = col0 + c * 32;  // multiple of 32
+        uint8_t* line = prow + (colb >> 6) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int chunk = ((colb & 63) >> 3) + u;
+          uint4 w = make_uint4(pack_bf16x2(e[8 * u + 0], e[8 * u + 1]), pack_bf16x2(e[8 * u + 2], e[8 * u + 3]),
+                               pack_bf16x2(e[8 * u + 4], e[8 * u + 5]), pack_bf16x2(e[8 * u + 6], e[8 * u + 7]));
+          *reinterpret_cast<uint4*>(line + ((chunk ^ (row & 7)) << 4)) = w;
+        }
+      }
+    }
+  }
+  const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+  l = l * alpha + rs;
+  fence_proxy_async_smem();
+  tc_fence_before();
+}
+
+// Non-diagonal tiles (L >= 128): single pass with the whole 128-column S row in registers.
+// All four TMEM loads are in flight before one wait; the exponentials are computed before
+// waiting for PV_{j-1} (only the O rescale and the P store need it).
+template <int DP>
+__device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
+                                                  float& m, float& l, uint64_t* o_done, uint32_t& no) {
+  const int row = G.row;
+  const uint32_t lane_off = G.lane_off;
+  const float sl2 = G.sl2;
+  uint32_t v[128];
+  tmem_ld32(tS + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+  tmem_ld32(tS + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tmem_ld32(tS + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
+  tmem_ld32(tS + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
+  tmem_ld_wait();
+  float t16[16];
+#pragma unroll
+  for (int a = 0; a < 16; ++a) {
+    const float* f = reinterpret_cast<const float*>(v + 8 * a);
+    t16[a] = max8(f);
+  }
+  float mx = fmaxf(max8(t16), max8(t16 + 8));
+  const float mx2 = mx * sl2;
+  const bool bump = (j == 0) || (mx2 > m + 8.f);
+  const float m_new = bump ? mx2 : m;
+  const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
+  m = m_new;
+  float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t pk[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const float e0 = fast_exp2(fmaf(__uint_as_float(v[2 * i]), sl2, -m_new));
+    const float e1 = fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -m_new));
+    rs8[(2 * i) & 7] += e0;
+    rs8[(2 * i + 1) & 7] += e1;
+    pk[i] = pack_bf16x2(e0, e1);
+  }
+  const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+  l = l * alpha + rs;
+  if (j > 0) {
+    mbar_wait(o_done, no & 1);  // PV_{j-1} done: O stable, P buffer free
+    ++no;
+    tc_fence_after();
+    if (__any_sync(0xffffffffu, bump)) {
+      const float a = bump ? alpha : 1.f;
+#pragma unroll
+      for (int c = 0; c < DP / 16; ++c) {
+        uint32_t o[16];
+        tmem_ld16(tO + lane_off + c * 16, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+        tmem_st16(tO + lane_off + c * 16, o);
+      }
+      tmem_st_wait();
+    }
+  }
+  // P (bf16) -> smem, SW128 K-major: 16-B chunk c of row r at chunk position c ^ (r & 7)
+#ifdef DSP_P_GENERIC_STORE
+  uint8_t* prow = sP + row * 128;
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    *reinterpret_cast<uint4*>(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4)) =
+        make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+#else
+  const uint32_t prow = smem_u32(sP) + row * 128;
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    st_shared_v4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                 pk[4 * c + 3]);
+#endif
+  fence_proxy_async_smem();
+  tc_fence_before();
+}
+
+// O / l -> bf16 -> o[tok, h*Dh + d] for this thread's row (after the last PV completed).
+template <int DP>
+__device__ __forceinline__ void store_o(const FmhaParams& p, const TileCoord& t, int row, uint32_t tO,
+                                        uint32_t lane_off, float l) {
+  const long tok = row_token(p, t, row);
+  const float inv_l = 1.f / l;
+  __nv_bfloat16* orow = p.o + tok * p.C + t.h * p.Dh;
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) {
+    uint32_t v[16];
+    tmem_ld16(tO + lane_off + c * 16, v);
+    tmem_ld_wait();
+    if (tok >= 0) {
+#pragma unroll
+      for (int h8 = 0; h8 < 2; ++h8) {
+        const int d = c * 16 + h8 * 8;
+        if (d < p.Dh) {
+          const uint32_t* w = v + h8 * 8;
+          uint4 o4 = make_uint4(pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l),
+                                pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l),
+                                pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l),
+                                pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l));
+          *reinterpret_cast<uint4*>(orow + d) = o4;
+        }
+      }
+    }
+  }
+}
+
 template <int NA, int RB>
 __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
     fmha_bf16_tc_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
@@ -251,140 +479,21 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int row = q * 32 + lane_id();
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const float sl2 = p.scale_log2;
-    // key columns this warp touches: all 128, or (diagonal blocks) a 32/64-wide window
-    const bool diag = p.G > 1;
-    const int wcols = diag ? (p.L > 32 ? p.L : 32) : 128;
-    const int wc0 = diag ? (q * 32 / wcols) * wcols : 0;
-    const int nhalf = (wcols + 63) / 64;          // 64-column halves
-    const int hcols = wcols < 64 ? wcols : 64;    // columns per half (32 or 64)
-    const int my_blk = row / (p.L < 128 ? p.L : 128);
-    uint8_t* prow = sP + row * 128;
-    uint32_t ns = 0, no = 0, nit = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++nit) {
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    uint32_t ns = 0, no = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         mbar_wait(s_full, ns & 1);
         ++ns;
         tc_fence_after();
-        // pass 1: row max over this thread's valid columns
-        float mx = -INFINITY;
-        for (int hf = 0; hf < nhalf; ++hf) {
-          float s[64];
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            if (c * 32 < hcols) {
-              uint32_t v[32];
-              tmem_ld32(tS + lane_off + wc0 + hf * 64 + c * 32, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) s[c * 32 + i] = -INFINITY;
-            }
-          }
-          if (diag) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if ((wc0 + hf * 64 + i) / p.L != my_blk) s[i] = -INFINITY;
-          }
-          float t8[8];
-#pragma unroll
-          for (int a = 0; a < 8; ++a) t8[a] = max8(s + 8 * a);
-          mx = fmaxf(mx, max8(t8));
-        }
-        const float mx2 = mx * sl2;
-        const bool bump = (j == 0) || (mx2 > m + 8.f);
-        const float m_new = bump ? mx2 : m;
-        const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
-        m = m_new;
-        if (j > 0) {
-          mbar_wait(o_done, no & 1);  // PV_{j-1} done: O stable, P buffer free
-          ++no;
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, bump)) {
-            const float a = bump ? alpha : 1.f;
-#pragma unroll
-            for (int c = 0; c < Cfg::DP / 16; ++c) {
-              uint32_t v[16];
-              tmem_ld16(tO + lane_off + c * 16, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * a);
-              tmem_st16(tO + lane_off + c * 16, v);
-            }
-            tmem_st_wait();
-          }
-        }
-        // pass 2: exponentiate, row-sum, P (bf16) -> smem.  SW128 K-major: 16-B chunk c of
-        // row r lives at chunk position c ^ (r & 7) of the row's 128-B line.
-        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int hf = 0; hf < nhalf; ++hf) {
-          const int col0 = wc0 + hf * 64;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            if (c * 32 < hcols) {
-              uint32_t v[32];
-              tmem_ld32(tS + lane_off + col0 + c * 32, v);
-              tmem_ld_wait();
-              float e[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                float x = __uint_as_float(v[i]);
-                if (diag && (col0 + c * 32 + i) / p.L != my_blk) x = -INFINITY;
-                e[i] = fast_exp2(fmaf(x, sl2, -m_new));
-                rs8[i & 7] += e[i];
-              }
-              const int colb = col0 + c * 32;  // multiple of 32
-              uint8_t* line = prow + (colb >> 6) * 16384;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int chunk = ((colb & 63) >> 3) + u;
-                uint4 w = make_uint4(pack_bf16x2(e[8 * u + 0], e[8 * u + 1]), pack_bf16x2(e[8 * u + 2], e[8 * u + 3]),
-                                     pack_bf16x2(e[8 * u + 4], e[8 * u + 5]), pack_bf16x2(e[8 * u + 6], e[8 * u + 7]));
-                *reinterpret_cast<uint4*>(line + ((chunk ^ (row & 7)) << 4)) = w;
-              }
-            }
-          }
-        }
-        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-        l = l * alpha + rs;
-        fence_proxy_async_smem();
-        tc_fence_before();
+        softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no);
         mbar_arrive(p_full);
       }
-      // epilogue: O / l -> bf16 -> o[tok, h*Dh + d]
       mbar_wait(o_done, no & 1);
       ++no;
       tc_fence_after();
-      const TileCoord t = tile_coord(p, item, -1);
-      const long tok = row_token(p, t, row);
-      const float inv_l = 1.f / l;
-      __nv_bfloat16* orow = p.o + tok * p.C + t.h * p.Dh;
-#pragma unroll
-      for (int c = 0; c < Cfg::DP / 16; ++c) {
-        uint32_t v[16];
-        tmem_ld16(tO + lane_off + c * 16, v);
-        tmem_ld_wait();
-        if (tok >= 0) {
-#pragma unroll
-          for (int h8 = 0; h8 < 2; ++h8) {
-            const int d = c * 16 + h8 * 8;
-            if (d < p.Dh) {
-              const uint32_t* w = v + h8 * 8;
-              uint4 o4 = make_uint4(pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l));
-              *reinterpret_cast<uint4*>(orow + d) = o4;
-            }
-          }
-        }
-      }
+      store_o<Cfg::DP>(p, tile_coord(p, item, -1), G.row, tO, G.lane_off, l);
       tc_fence_before();
       mbar_arrive(o_free);
     }
@@ -395,6 +504,227 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Long sequences (L % 256 == 0): one CTA per SM works on TWO 128-row query tiles
+// ("slots") of the same (sequence, head), sharing one K/V stream (2-stage ring).  TMEM
+// (512 columns) holds S0, S1 (128 columns each) and O0, O1.  Each slot's softmax is split
+// over two warpgroups, one per 64-key half of the tile (row max exchanged through smem
+// and a named barrier), so every SMSP has four softmax warps to keep the MUFU (exp2)
+// pipe busy, while the tensor pipe runs S_{j+1} of both slots, then both P_j V_j.
+//   warp 0       TMA producer        warp 1       MMA issuer + TMEM allocator
+//   warps 4-11   slot 0 (halves 0,1) warps 12-19  slot 1 (halves 0,1)
+template <int NA, int RB>
+struct PairCfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP, P_BYTES = Base::P_BYTES;
+  static constexpr int RED_BYTES = 2 * 2 * 2 * 128 * 4;   // [max | sum][slot][half][row] floats
+  static constexpr int SMEM = 1024 + 6 * TILE /*Q0,Q1,K x2,V x2*/ + 2 * P_BYTES + RED_BYTES + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024;
+  static constexpr int THREADS = 384;
+};
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(384, 1)
+    fmha_pair_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
+                     const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
+                     const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                     const FmhaParams p) {
+  using Cfg = PairCfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                       // 2 tiles
+  uint8_t* sK = sQ + 2 * Cfg::TILE;         // 2 stages
+  uint8_t* sV = sK + 2 * Cfg::TILE;         // 2 stages
+  uint8_t* sP = sV + 2 * Cfg::TILE;         // 2 x 32 KB
+  float* red = reinterpret_cast<float*>(sP + 2 * Cfg::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * Cfg::P_BYTES + Cfg::RED_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [2] per slot
+  uint64_t* p_full = bars + 12;   // [2]
+  uint64_t* o_done = bars + 14;   // [2]
+  uint64_t* o_free = bars + 16;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = warp_id();
+  const int n = p.n_kv;
+  const int npairs = p.items / 2;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
+    if (RB) { tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b); }
+    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  // launch allocation is 168 regs x 384 threads; 56 x 128 + 224 x 256 == 168 x 384 exactly
+  if (warp == 0) {
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      uint32_t nq = 0, kv = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+        mbar_wait_sleep(q_empty, (nq & 1) ^ 1);
+        ++nq;
+        mbar_arrive_expect_tx(q_full, 2 * Cfg::TX);
+        load_tile<NA, RB>(sQ, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip, -1));
+        load_tile<NA, RB>(sQ + Cfg::TILE, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip + 1, -1));
+        for (int j = 0; j < n; ++j, ++kv) {
+          const int st = kv & 1;
+          const uint32_t ph = (kv >> 1) & 1;
+          const TileCoord t = tile_coord(p, 2 * ip, j);
+          mbar_wait_sleep(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::TX);
+          load_tile<NA, RB>(sK + st * Cfg::TILE, &tk_a, &tk_b, &k_full[st], t);
+          mbar_wait_sleep(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::TX);
+          load_tile<NA, RB>(sV + st * Cfg::TILE, &tv_a, &tv_b, &v_full[st], t);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    setmaxnreg_dec<56>();
+    {
+      constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
+      constexpr uint32_t idPVb = make_idesc_bf16(128, RB == 0 ? 16 : RB, 0, 1);
+      const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
+      auto issue_s = [&](int slot, int st) {  // S_slot = Q_slot K^T
+        if (elect_one()) {
+          const uint32_t qa = q0 + slot * Cfg::TILE, ka = k0 + st * Cfg::TILE, d = tmem + slot * 128;
+          int step = 0;
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k, ++step)
+              umma_bf16_ss(d, make_sdesc(qa + i * 16384 + k * 32, 16, 1024, SW_128B),
+                           make_sdesc(ka + i * 16384 + k * 32, 16, 1024, SW_128B), idS, step != 0);
+          if (RB) {
+#pragma unroll
+            for (int k = 0; k < RB / 16; ++k, ++step)
+              umma_bf16_ss(d, make_sdesc(qa + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
+                           make_sdesc(ka + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+          }
+          umma_commit(&s_full[slot]);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int slot, int st, bool acc0) {  // O_slot (+)= P_slot V
+        if (elect_one()) {
+          const uint32_t pa = p0 + slot * Cfg::P_BYTES, va = v0 + st * Cfg::TILE, o = tmem + 256 + slot * 128;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t ad = make_sdesc(pa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SW_128B);
+#pragma unroll
+            for (int i = 0; i < NA; ++i)
+              umma_bf16_ss(o + 64 * i, ad, make_sdesc(va + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+                           acc0 || k != 0);
+            if (RB)
+              umma_bf16_ss(o + 64 * NA, ad,
+                           make_sdesc(va + NA * 16384 + k * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
+                           idPVb, acc0 || k != 0);
+          }
+          umma_commit(&o_done[slot]);
+        }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
+        __syncwarp();
+      };
+      uint32_t nq = 0, np0 = 0, np1 = 0, nit = 0, kvbase = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x, ++nit, kvbase += n) {
+        mbar_wait(q_full, nq & 1);
+        ++nq;
+        const uint32_t kv0 = kvbase;
+        mbar_wait(&k_full[kv0 & 1], (kv0 >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, kv0 & 1);
+        issue_s(1, kv0 & 1);
+        commit(&k_empty[kv0 & 1]);
+        if (n == 1) commit(q_empty);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t kj = kvbase + j, kn = kj + 1;
+          // S_{j+1} of both tiles first (they gate the softmax warpgroups), then the PVs.
+          mbar_wait(&p_full[0], np0 & 1);
+          ++np0;
+          if (j + 1 < n) {
+            mbar_wait(&k_full[kn & 1], (kn >> 1) & 1);
+            tc_fence_after();
+            issue_s(0, kn & 1);
+          }
+          mbar_wait(&p_full[1], np1 & 1);
+          ++np1;
+          tc_fence_after();
+          if (j + 1 < n) {
+            issue_s(1, kn & 1);
+            commit(&k_empty[kn & 1]);
+            if (j + 2 == n) commit(q_empty);
+          }
+          mbar_wait(&v_full[kj & 1], (kj >> 1) & 1);
+          if (j == 0) {
+            mbar_wait(&o_free[0], (nit & 1) ^ 1);
+            mbar_wait(&o_free[1], (nit & 1) ^ 1);
+          }
+          tc_fence_after();
+          issue_pv(0, kj & 1, j > 0);
+          issue_pv(1, kj & 1, j > 0);
+          commit(&v_empty[kj & 1]);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    setmaxnreg_dec<56>();
+  } else {
+    setmaxnreg_inc<224>();
+    const int slot = (warp - 4) >> 2;
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128;
+    uint8_t* sPs = sP + slot * Cfg::P_BYTES;
+    uint32_t ns = 0, no = 0;
+    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(&s_full[slot], ns & 1);
+        ++ns;
+        tc_fence_after();
+        softmax_tile_full<Cfg::DP>(G, tS, tO, sPs, j, m, l, &o_done[slot], no);
+        mbar_arrive(&p_full[slot]);
+      }
+      mbar_wait(&o_done[slot], no & 1);
+      ++no;
+      tc_fence_after();
+      store_o<Cfg::DP>(p, tile_coord(p, 2 * ip + slot, -1), G.row, tO, G.lane_off, l);
+      tc_fence_before();
+      mbar_arrive(&o_free[slot]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -416,6 +746,21 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
         return cudaErrorInvalidValue;
     } else {
       m[2 * part + 1] = m[2 * part];
+    }
+  }
+  if constexpr (PairCfg<NA, RB>::OK) {
+    if (p.G == 1 && p.n_qt % 2 == 0) {
+      auto kp = fmha_pair_kernel<NA, RB>;
+      static bool attr_p = false;
+      if (!attr_p) {
+        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<NA, RB>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_p = true;
+      }
+      const int npairs = p.items / 2;
+      const int grid = npairs < num_sms ? npairs : num_sms;
+      kp<<<grid, PairCfg<NA, RB>::THREADS, PairCfg<NA, RB>::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+      return cudaGetLastError();
     }
   }
   auto kern = fmha_bf16_tc_kernel<NA, RB>;

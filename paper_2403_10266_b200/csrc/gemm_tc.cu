@@ -21,6 +21,9 @@
 //   warps 4-7   epilogue (both CTAs): tcgen05.ld 32 columns at a time (thread = accumulator
 //               row), fused residual / GELU, bf16 pack, 16-B global stores; then arrive on
 //               the leader's accumulator-empty barrier.
+// Tiles are rasterised n-fastest: concurrently running pairs share A row blocks and the
+// (L2-resident, <= 21 MB) weight matrix, so A streams from HBM once even when it is larger
+// than L2 (FC2: A = 151 MB at the single-block config).
 // No split-K, no atomics: each output's reduction order depends only on K (N-invariance).
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -105,8 +108,8 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-        const int m0 = (tile % tiles_m) * (2 * BM) + rank * BM;
-        const int n0 = (tile / tiles_m) * BN + rank * Cfg::BNH;
+        const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
+        const int n0 = (tile % tiles_n) * BN + rank * Cfg::BNH;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
@@ -159,15 +162,21 @@ __global__ void __launch_bounds__(256, 1)
     int it = 0;
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
-      const int m0 = (tile % tiles_m) * (2 * BM) + rank * BM;
-      const int n0 = (tile / tiles_m) * BN;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
-      tc_fence_after();
+      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
+      const int n0 = (tile % tiles_n) * BN;
       const int grow = m0 + row;
       const bool live = grow < M;
       __nv_bfloat16* drow = D + (size_t)grow * N + n0;
-      const __nv_bfloat16* rrow = R + (size_t)grow * N + n0;
-#pragma unroll 1
+      // residual row segment is independent of the accumulator: fetch it before waiting
+      uint4 rv[EPI == DSP_EPI_RESIDUAL ? BN / 8 : 1];
+      if (EPI == DSP_EPI_RESIDUAL && live) {
+        const uint4* rp = reinterpret_cast<const uint4*>(R + (size_t)grow * N + n0);
+#pragma unroll
+        for (int j = 0; j < BN / 8; ++j) rv[j] = rp[j];
+      }
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
@@ -177,18 +186,17 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
           if (EPI == DSP_EPI_RESIDUAL) {
-            const uint4* rp = reinterpret_cast<const uint4*>(rrow + c * 32);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              uint4 rv = rp[j];
-              f[8 * j + 0] += bf16lo(rv.x);
-              f[8 * j + 1] += bf16hi(rv.x);
-              f[8 * j + 2] += bf16lo(rv.y);
-              f[8 * j + 3] += bf16hi(rv.y);
-              f[8 * j + 4] += bf16lo(rv.z);
-              f[8 * j + 5] += bf16hi(rv.z);
-              f[8 * j + 6] += bf16lo(rv.w);
-              f[8 * j + 7] += bf16hi(rv.w);
+              const uint4 r4 = rv[c * 4 + j];
+              f[8 * j + 0] += bf16lo(r4.x);
+              f[8 * j + 1] += bf16hi(r4.x);
+              f[8 * j + 2] += bf16lo(r4.y);
+              f[8 * j + 3] += bf16hi(r4.y);
+              f[8 * j + 4] += bf16lo(r4.z);
+              f[8 * j + 5] += bf16hi(r4.z);
+              f[8 * j + 6] += bf16lo(r4.w);
+              f[8 * j + 7] += bf16hi(r4.w);
             }
           } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll

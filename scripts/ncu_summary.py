@@ -1,0 +1,31 @@
+"""Summarise an ncu report (run here, no GPU): key metrics per kernel + top stalls."""
+import csv, io, subprocess, sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "sm__cycles_elapsed.avg.per_second",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")][:90]
+        print("==", name)
+        for k in KEYS:
+            if k in hdr:
+                print(f"   {k:70s} {r[hdr.index(k)]}")
+        st = [(h, float(r[i] or 0)) for i, h in enumerate(hdr)
+              if h.startswith("smsp__pcsamp_warps_issue_stalled") and not h.endswith("not_issued")]
+        st.sort(key=lambda x: -x[1])
+        print("   stalls:", ", ".join(f"{h.replace('smsp__pcsamp_warps_issue_stalled_', '')}={int(v)}" for h, v in st[:8]))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
