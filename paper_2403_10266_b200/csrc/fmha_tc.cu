@@ -30,6 +30,12 @@
 #include "dsp_internal.h"
 #include "sm100.cuh"
 
+// fraction of the softmax exponentials computed with poly_exp2 on the FMA pipe
+#ifndef DSP_POLY_NUM
+#define DSP_POLY_NUM 5  // 5/16 measured best on B200 (1/4: 118.8 us, 5/16: 114.4, 3/8: 117.0, 1/2: 126.8)
+#define DSP_POLY_DEN 16
+#endif
+
 namespace dsp {
 namespace {
 
@@ -45,7 +51,15 @@ struct FmhaParams {
   int items;     // n_outer * NH * n_qt
   float scale_log2;
   __nv_bfloat16* o;
+  unsigned long long* trace;  // DSP_FMHA_TRACE builds only: per-phase clock64 stamps of CTA 0
 };
+
+#ifdef DSP_FMHA_TRACE
+#define FMHA_STAMP(buf, idx) \
+  do { if ((buf) && blockIdx.x == 0 && lane_id() == 0 && (threadIdx.x & 127) == 0) (buf)[idx] = clock64(); } while (0)
+#else
+#define FMHA_STAMP(buf, idx) do { } while (0)
+#endif
 
 template <int NA, int RB>
 struct FmhaCfg {
@@ -238,7 +252,9 @@ __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, 
 // waiting for PV_{j-1} (only the O rescale and the P store need it).
 template <int DP>
 __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
-                                                  float& m, float& l, uint64_t* o_done, uint32_t& no) {
+                                                  float& m, float& l, uint64_t* o_done, uint32_t& no,
+                                                  unsigned long long* tr = nullptr, uint64_t* s_free = nullptr,
+                                                  int* store_pending = nullptr, uint32_t bar_id = 0) {
   const int row = G.row;
   const uint32_t lane_off = G.lane_off;
   const float sl2 = G.sl2;
@@ -248,6 +264,10 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
   tmem_ld32(tS + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
   tmem_ld32(tS + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
   tmem_ld_wait();
+  if (s_free) {  // the whole S row is in registers: the MMA may overwrite S with S_{j+1}
+    tc_fence_before();
+    mbar_arrive(s_free);
+  }
   float t16[16];
 #pragma unroll
   for (int a = 0; a < 16; ++a) {
@@ -260,22 +280,33 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
   const float m_new = bump ? mx2 : m;
   const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
   m = m_new;
-  float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   uint32_t pk[64];
+  const float2 sl2x2 = make_float2(sl2, sl2), mx2n = make_float2(-m_new, -m_new);
 #pragma unroll
   for (int i = 0; i < 64; ++i) {
-    const float e0 = fast_exp2(fmaf(__uint_as_float(v[2 * i]), sl2, -m_new));
-    const float e1 = fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), sl2, -m_new));
-    rs8[(2 * i) & 7] += e0;
-    rs8[(2 * i + 1) & 7] += e1;
-    pk[i] = pack_bf16x2(e0, e1);
+    // x = s * scale*log2(e) - m on pairs; DSP_POLY_NUM/DSP_POLY_DEN of the pairs exponentiated on
+    // the FMA pipe (poly_exp2_x2), the rest on the MUFU (ex2.approx)
+    const float2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2, mx2n);
+    float2 e;
+    if ((i % DSP_POLY_DEN) < DSP_POLY_NUM) {
+      e = poly_exp2_x2(x);
+    } else {
+      e.x = fast_exp2(x.x);
+      e.y = fast_exp2(x.y);
+    }
+    rs4[i & 3] = fadd2(rs4[i & 3], e);
+    pk[i] = pack_bf16x2(e.x, e.y);
   }
-  const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+  const float2 rsa = fadd2(fadd2(rs4[0], rs4[1]), fadd2(rs4[2], rs4[3]));
+  const float rs = rsa.x + rsa.y;
   l = l * alpha + rs;
+  FMHA_STAMP(tr, 1);
   if (j > 0) {
     mbar_wait(o_done, no & 1);  // PV_{j-1} done: O stable, P buffer free
     ++no;
     tc_fence_after();
+    FMHA_STAMP(tr, 2);
     if (__any_sync(0xffffffffu, bump)) {
       const float a = bump ? alpha : 1.f;
 #pragma unroll
@@ -289,6 +320,11 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
       }
       tmem_st_wait();
     }
+  }
+  if (store_pending && *store_pending) {  // previous item's O TMA store must have read the P buffer
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+    named_bar_sync(bar_id, 128);
+    *store_pending = 0;
   }
   // P (bf16) -> smem, SW128 K-major: 16-B chunk c of row r at chunk position c ^ (r & 7)
 #ifdef DSP_P_GENERIC_STORE
@@ -531,6 +567,7 @@ __global__ void __launch_bounds__(384, 1)
     fmha_pair_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
                      const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
                      const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                     const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
                      const FmhaParams p) {
   using Cfg = PairCfg<NA, RB>;
   using Base = FmhaCfg<NA, RB>;
@@ -552,6 +589,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = bars + 12;   // [2]
   uint64_t* o_done = bars + 14;   // [2]
   uint64_t* o_free = bars + 16;   // [2]
+  uint64_t* s_free = bars + 18;   // [2] S row fully in registers
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = warp_id();
@@ -566,6 +604,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&p_full[t], 128);
       mbar_init(&o_done[t], 1);
       mbar_init(&o_free[t], 128);
+      mbar_init(&s_free[t], 128);
     }
     fence_barrier_init();
   }
@@ -652,7 +691,7 @@ __global__ void __launch_bounds__(384, 1)
         if (elect_one()) umma_commit(bar);
         __syncwarp();
       };
-      uint32_t nq = 0, np0 = 0, np1 = 0, nit = 0, kvbase = 0;
+      uint32_t nq = 0, np0 = 0, np1 = 0, nf0 = 0, nf1 = 0, nit = 0, kvbase = 0;
       for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x, ++nit, kvbase += n) {
         mbar_wait(q_full, nq & 1);
         ++nq;
@@ -665,29 +704,31 @@ __global__ void __launch_bounds__(384, 1)
         if (n == 1) commit(q_empty);
         for (int j = 0; j < n; ++j) {
           const uint32_t kj = kvbase + j, kn = kj + 1;
-          // S_{j+1} of both tiles first (they gate the softmax warpgroups), then the PVs.
-          mbar_wait(&p_full[0], np0 & 1);
-          ++np0;
+          // S_{j+1} as soon as each slot has S_j in registers (overlaps its exp phase) ...
           if (j + 1 < n) {
+            mbar_wait(&s_free[0], nf0 & 1);
             mbar_wait(&k_full[kn & 1], (kn >> 1) & 1);
             tc_fence_after();
             issue_s(0, kn & 1);
-          }
-          mbar_wait(&p_full[1], np1 & 1);
-          ++np1;
-          tc_fence_after();
-          if (j + 1 < n) {
+            mbar_wait(&s_free[1], nf1 & 1);
+            tc_fence_after();
             issue_s(1, kn & 1);
             commit(&k_empty[kn & 1]);
             if (j + 2 == n) commit(q_empty);
           }
+          ++nf0;
+          ++nf1;
+          // ... then O += P_j V_j once each slot has stored P_j
+          mbar_wait(&p_full[0], np0 & 1);
+          ++np0;
           mbar_wait(&v_full[kj & 1], (kj >> 1) & 1);
-          if (j == 0) {
-            mbar_wait(&o_free[0], (nit & 1) ^ 1);
-            mbar_wait(&o_free[1], (nit & 1) ^ 1);
-          }
+          if (j == 0) mbar_wait(&o_free[0], (nit & 1) ^ 1);
           tc_fence_after();
           issue_pv(0, kj & 1, j > 0);
+          mbar_wait(&p_full[1], np1 & 1);
+          ++np1;
+          if (j == 0) mbar_wait(&o_free[1], (nit & 1) ^ 1);
+          tc_fence_after();
           issue_pv(1, kj & 1, j > 0);
           commit(&v_empty[kj & 1]);
         }
@@ -701,23 +742,75 @@ __global__ void __launch_bounds__(384, 1)
     const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
     const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128;
     uint8_t* sPs = sP + slot * Cfg::P_BYTES;
+    const uint32_t bar_id = 1 + slot;
+    const bool store_leader = (threadIdx.x & 127) == 0;
+    int store_pending = 0;
     uint32_t ns = 0, no = 0;
     for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
+        unsigned long long* tr = p.trace ? p.trace + ((size_t)(slot * 64 + (ns & 63)) * 8) : nullptr;
+        FMHA_STAMP(tr, 0);
         mbar_wait(&s_full[slot], ns & 1);
         ++ns;
         tc_fence_after();
-        softmax_tile_full<Cfg::DP>(G, tS, tO, sPs, j, m, l, &o_done[slot], no);
+        FMHA_STAMP(tr, 3);
+        softmax_tile_full<Cfg::DP>(G, tS, tO, sPs, j, m, l, &o_done[slot], no, tr, &s_free[slot], &store_pending,
+                                   bar_id);
+        FMHA_STAMP(tr, 4);
         mbar_arrive(&p_full[slot]);
       }
-      mbar_wait(&o_done[slot], no & 1);
+      unsigned long long* te = p.trace ? p.trace + ((size_t)(slot * 64 + ((ns - 1) & 63)) * 8) : nullptr;
+      FMHA_STAMP(te, 5);
+      mbar_wait(&o_done[slot], no & 1);  // last PV done: O final, P buffer free
       ++no;
       tc_fence_after();
-      store_o<Cfg::DP>(p, tile_coord(p, 2 * ip + slot, -1), G.row, tO, G.lane_off, l);
+      FMHA_STAMP(te, 6);
+      // O / l -> bf16 -> smem in the TMA tile layout (SW128 64-column part + swizzled rest),
+      // then one elected thread stores the tile with TMA (columns >= Dh are out of bounds).
+      const int row = G.row;
+      const float inv_l = 1.f / l;
+      const uint32_t st0 = smem_u32(sPs);
+#pragma unroll
+      for (int c = 0; c < Cfg::DP / 16; ++c) {
+        uint32_t o[16];
+        tmem_ld16(tO + G.lane_off + c * 16, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8) {
+          const int d = c * 16 + h8 * 8;
+          const uint32_t* w = o + h8 * 8;
+          const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
+          const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
+          const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
+          const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
+          uint32_t addr;
+          if (d < NA * 64) {
+            const int blk = d >> 6, ch = (d & 63) >> 3;
+            addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
+          } else {
+            const int ch = (d - NA * 64) >> 3;  // RB = 16: SW32 (2 chunks/row), RB = 32: SW64 (4 chunks/row)
+            addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
+                            : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
+          }
+          st_shared_v4(addr, a0, a1, a2, a3);
+        }
+      }
       tc_fence_before();
-      mbar_arrive(&o_free[slot]);
+      mbar_arrive(&o_free[slot]);  // O is in registers/smem: the MMA may start the next item's PV
+      fence_proxy_async_smem();
+      named_bar_sync(bar_id, 128);
+      if (store_leader) {
+        const TileCoord t = tile_coord(p, 2 * ip + slot, -1);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) tma_store_5d(&to_a, sPs + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
+        if (RB) tma_store_5d(&to_b, sPs + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
+        bulk_commit_group();
+      }
+      store_pending = 1;
+      FMHA_STAMP(te, 7);
     }
+    if (store_leader) bulk_wait_group_read0();
   }
 
   tc_fence_before();
@@ -750,6 +843,19 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
   }
   if constexpr (PairCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0) {
+      // output maps: same 5-D view as q/k/v but over o [tok, C] (row pitch C)
+      CUtensorMap mo[2];
+      uint64_t ostr[4] = {strides[0], strides[1] / 3, strides[2] / 3, strides[3] / 3};
+      uint32_t boxa[5] = {64, 1, box_rows[0], box_rows[1], 1};
+      uint32_t boxb[5] = {(uint32_t)(RB ? RB : 16), 1, box_rows[0], box_rows[1], 1};
+      if (!make_tmap_bf16(&mo[0], p.o, 5, dims, ostr, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why)) return cudaErrorInvalidValue;
+      if (RB) {
+        if (!make_tmap_bf16(&mo[1], p.o, 5, dims, ostr, boxb,
+                            RB == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, why))
+          return cudaErrorInvalidValue;
+      } else {
+        mo[1] = mo[0];
+      }
       auto kp = fmha_pair_kernel<NA, RB>;
       static bool attr_p = false;
       if (!attr_p) {
@@ -759,7 +865,8 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       }
       const int npairs = p.items / 2;
       const int grid = npairs < num_sms ? npairs : num_sms;
-      kp<<<grid, PairCfg<NA, RB>::THREADS, PairCfg<NA, RB>::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+      kp<<<grid, PairCfg<NA, RB>::THREADS, PairCfg<NA, RB>::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], mo[0],
+                                                                          mo[1], p);
       return cudaGetLastError();
     }
   }
@@ -778,6 +885,11 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
 
 }  // namespace
 
+#ifdef DSP_FMHA_TRACE
+unsigned long long* g_fmha_trace = nullptr;
+extern "C" void* dsp_debug_fmha_trace() { return g_fmha_trace; }
+#endif
+
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
                              int dim, int num_sms, cudaStream_t st, std::string* why) {
   FmhaParams p{};
@@ -788,6 +900,16 @@ cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc,
   p.T_loc = (int)T_loc;
   p.B = (int)B;
   p.o = static_cast<__nv_bfloat16*>(o);
+  p.trace = nullptr;
+#ifdef DSP_FMHA_TRACE
+  {
+    static unsigned long long* tbuf = nullptr;
+    if (!tbuf) cudaMalloc(&tbuf, 2 * 64 * 8 * sizeof(unsigned long long));
+    p.trace = tbuf;
+    extern unsigned long long* g_fmha_trace;
+    g_fmha_trace = tbuf;
+  }
+#endif
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
   p.spatial = (dim == DSP_DIM_S);
   p.L = (int)(p.spatial ? S_loc : T_loc);
