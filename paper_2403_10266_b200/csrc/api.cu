@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -87,6 +88,32 @@ dsp_status_t check_ctx(dsp_ctx_t ctx) {
 }
 
 int64_t shard_bytes(const dsp_shape_t* s, int world) { return s->B * s->T * s->S * s->C * elem_bytes(s->dtype) / world; }
+
+int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+// Block workspace layout (bytes).  act = tok_r * C * elem.
+//   [0, act)          h: LN output (f32 path) / switch scratch
+//   [act, 5 act)      big: qkv [tok,3C] + o [tok,C] | MLP hidden [tok,4C] | switch send/recv
+//   [5 act, 6 act)    ys: S-sharded activation (N > 1)
+//   fold region       (bf16) W o gamma for w_qkv_s, w_qkv_t, w_fc1; u, v vectors; row stats
+struct BlockWs {
+  int64_t act, h, big, ys, wf_s, wf_t, wf_1, uv, stats, total;
+};
+BlockWs block_ws(const dsp_shape_t* s, int world) {
+  BlockWs w{};
+  const int64_t tok = s->B * s->T * s->S / world, C = s->C, e = elem_bytes(s->dtype);
+  w.act = tok * C * e;
+  w.h = 0;
+  w.big = w.act;
+  w.ys = 5 * w.act;
+  w.wf_s = align256(6 * w.act);
+  w.wf_t = w.wf_s + align256(3 * C * C * 2);
+  w.wf_1 = w.wf_t + align256(3 * C * C * 2);
+  w.uv = w.wf_1 + align256(4 * C * C * 2);
+  w.stats = w.uv + align256(2 * 10 * C * 4);
+  w.total = w.stats + align256(tok * 8) + 256;
+  return w;
+}
 
 // bf16 tensor-core path constraints for one attention stage over sequences of length L
 dsp_status_t check_bf16_attn(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t L) {
@@ -203,14 +230,16 @@ inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
 // stage0 >= 0: record stage events for (QKV, ATTN, PROJ) = stage0, stage0+1, stage0+2.
 dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
                         const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
-                        cudaStream_t st, int stage0 = -1) {
+                        cudaStream_t st, int stage0 = -1, const EpiVec* ln = nullptr) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
   const int sq = stage0, sa = stage0 < 0 ? -1 : stage0 + 1, sp = stage0 < 0 ? -1 : stage0 + 2;
   if (s->dtype == DSP_BF16) {
     std::string why;
     mark(ctx, sq, 0, st);
-    cudaError_t e = launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    // ln != nullptr: h is the raw (un-normalised) input and w_qkv the LN-folded weight
+    cudaError_t e = ln ? launch_gemm_bf16_ln(h, w_qkv, *ln, qkv, tok, 3 * C, C, false, ctx->num_sms, st, &why)
+                       : launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "qkv projection", why);
     mark(ctx, sq, 1, st);
     mark(ctx, sa, 0, st);
@@ -282,6 +311,8 @@ dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, ds
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, DSP_ERR_SHAPE, "bad rank %d / world %d", rank, world);
   dsp_ctx* c = new dsp_ctx();
   c->rank = rank; c->world = world; c->device = device; c->comm = nccl_comm;
+  const char* fl = std::getenv("DSP_FOLD_LN");
+  c->fold_ln = fl && fl[0] == '1';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
@@ -309,8 +340,7 @@ dsp_status_t dsp_ctx_destroy(dsp_ctx_t ctx) {
 
 size_t dsp_workspace_bytes(const dsp_shape_t* s, int world) {
   if (!s || world < 1 || s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1) return 0;
-  const int64_t tok = s->B * s->T * s->S / world;
-  return (size_t)(tok * 6 * s->C * elem_bytes(s->dtype)) + 256;
+  return (size_t)block_ws(s, world).total;
 }
 
 dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n) {
@@ -510,12 +540,13 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "block needs %zu bytes of workspace", need);
   if (x != y && overlap(x, act, y, act)) return fail(ctx, DSP_ERR_ALIAS, "x_local partially overlaps y_local");
   if (overlap(ctx->ws, need, x, act) || overlap(ctx->ws, need, y, act)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y");
+  const BlockWs L = block_ws(s, N);
   uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
-  void* h = ws;                      // [tok, C]
-  uint8_t* big = ws + act;           // [tok, 4C]: qkv + o | MLP hidden | switch scratch
+  void* h = ws + L.h;                // [tok, C]
+  uint8_t* big = ws + L.big;         // [tok, 4C]: qkv + o | MLP hidden | switch scratch
   void* qkv = big;
   void* o = big + 3 * act;
-  void* ys = ws + 5 * act;           // [tok, C] S-sharded activation (N > 1)
+  void* ys = ws + L.ys;              // [tok, C] S-sharded activation (N > 1)
   if (N > 1 && impl == DSP_SWITCH_P2P) {
     if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P block without dsp_ctx_set_peer_buffers");
     void* base = ctx->peer_base.p[ctx->rank];
@@ -525,12 +556,34 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   cudaStream_t st = (cudaStream_t)stream;
   const float eps = w->ln_eps;
   const int64_t Tn = s->T / N, Sn = s->S / N;
-  // a1-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
+  // LayerNorm folded into the following GEMM (explicit opt-in, DSP_FOLD_LN=1).  Measured on B200
+  // at the single-block config it is slower than LN + plain GEMM (809 vs 754 us: the folded
+  // epilogue lengthens the QKV/FC1 GEMMs more than the removed LN traffic saves), so the
+  // default keeps the LayerNorm kernel.  Row-stats kernel holds rows of <= 1280 channels.
+  const bool fold = ctx->fold_ln && s->dtype == DSP_BF16 && C % 8 == 0 && C <= 1280;
+  float* uv = reinterpret_cast<float*>(ws + L.uv);
+  float2* stats = reinterpret_cast<float2*>(ws + L.stats);
+  EpiVec ev1{stats, uv, uv + 3 * C}, ev2{stats, uv + 6 * C, uv + 9 * C}, ev3{stats, uv + 12 * C, uv + 16 * C};
+  void* wf_s = ws + L.wf_s;
+  void* wf_t = ws + L.wf_t;
+  void* wf_1 = ws + L.wf_1;
+  // a1: LN1 (folded: row statistics of x + LN-folded weights of all three LN->linear pairs)
   mark(ctx, DSP_STAGE_LN1, 0, st);
-  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
-  ctx->launches += 1;
+  if (fold) {
+    LnFold jobs[3] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, wf_s, uv, uv + 3 * C, 3 * C},
+                      {w->w_qkv_t, w->ln2_w, w->ln2_b, wf_t, uv + 6 * C, uv + 9 * C, 3 * C},
+                      {w->w_fc1, w->ln3_w, w->ln3_b, wf_1, uv + 12 * C, uv + 16 * C, 4 * C}};
+    DSP_CUDA(ctx, launch_fold_ln_weights(3, jobs, C, st), "fold LN weights");
+    DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
+    ctx->launches += 2;
+  } else {
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
+    ctx->launches += 1;
+  }
   mark(ctx, DSP_STAGE_LN1, 1, st);
-  DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, h, w->w_qkv_s, w->w_o_s, x, y, qkv, o, st, DSP_STAGE_QKV_S));
+  // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
+  DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, fold ? x : h, fold ? wf_s : w->w_qkv_s, w->w_o_s, x, y, qkv, o,
+                     st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr));
   // a5: switch T -> S
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
@@ -541,17 +594,27 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   mark(ctx, DSP_STAGE_SWITCH_TS, 1, st);
   // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place)
   mark(ctx, DSP_STAGE_LN2, 0, st);
-  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
+  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN2 stats");
+  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
   ctx->launches += 1;
   mark(ctx, DSP_STAGE_LN2, 1, st);
-  DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, h, w->w_qkv_t, w->w_o_t, cur, cur, qkv, o, st, DSP_STAGE_QKV_T));
+  DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, fold ? cur : h, fold ? wf_t : w->w_qkv_t, w->w_o_t, cur, cur, qkv,
+                     o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr));
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
   mark(ctx, DSP_STAGE_LN3, 0, st);
-  DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
+  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN3 stats");
+  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
   ctx->launches += 1;
   mark(ctx, DSP_STAGE_LN3, 1, st);
   mark(ctx, DSP_STAGE_FC1, 0, st);
-  DSP_TRY(linear(ctx, s->dtype, tok, 4 * C, C, h, w->w_fc1, nullptr, DSP_EPI_GELU, big, st));
+  if (fold) {
+    std::string why;
+    cudaError_t e2 = launch_gemm_bf16_ln(cur, wf_1, ev3, big, tok, 4 * C, C, true, ctx->num_sms, st, &why);
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "FC1 (LN3 folded)", why);
+    ctx->launches += 1;
+  } else {
+    DSP_TRY(linear(ctx, s->dtype, tok, 4 * C, C, h, w->w_fc1, nullptr, DSP_EPI_GELU, big, st));
+  }
   mark(ctx, DSP_STAGE_FC1, 1, st);
   mark(ctx, DSP_STAGE_FC2, 0, st);
   DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));

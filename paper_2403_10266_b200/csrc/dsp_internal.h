@@ -57,6 +57,28 @@ cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t d
                            int num_sms, cudaStream_t st);
 cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st);
 
+// LayerNorm folded into the following GEMM (bf16 path)
+struct LnFold {
+  const void* W;      // [N, K] bf16 weight of the linear layer
+  const void* gamma;  // [K] bf16
+  const void* beta;   // [K] bf16
+  void* Wf;           // [N, K] bf16 out: W * gamma
+  float* u;           // [N] out: row sums of Wf
+  float* v;           // [N] out: W beta
+  int64_t N;
+};
+cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
+cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
+// GEMM epilogue codes beyond the public dsp_epilogue_t
+enum { EPI_LN = 3, EPI_LN_GELU = 4 };
+struct EpiVec {
+  const float2* row_stats;  // [M] (mean, rstd)
+  const float* col_u;       // [N]
+  const float* col_v;       // [N]
+};
+cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,
+                                int64_t K, bool gelu, int num_sms, cudaStream_t st, std::string* why);
+
 bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle swz, std::string* why);
 
@@ -74,6 +96,7 @@ struct dsp_ctx {
   int64_t launches = 0;            // own kernels launched (instrumentation)
   void* stage_events[2 * DSP_NUM_STAGES] = {};
   bool has_stage_events = false;
+  bool fold_ln = false;  // DSP_FOLD_LN=1: LayerNorm folded into the following GEMM
   uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
   std::string last_error;
 };

@@ -153,7 +153,8 @@ __device__ __forceinline__ SoftmaxGeom make_geom(const FmhaParams& p, int warp, 
 // sP, running sum l.  Returns after the P stores are fenced for the async proxy.
 template <int DP>
 __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
-                                             float& m, float& l, uint64_t* o_done, uint32_t& no) {
+                                             float& m, float& l, uint64_t* o_done, uint32_t& no,
+                                             int* store_pending = nullptr, uint32_t bar_id = 0) {
   const int row = G.row;
   const uint32_t lane_off = G.lane_off;
   const bool diag = G.diag;
@@ -210,9 +211,25 @@ __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, 
       tmem_st_wait();
     }
   }
+  if (store_pending && *store_pending) {  // previous item's O TMA store must have read the P buffer
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+    named_bar_sync(bar_id, 128);
+    *store_pending = 0;
+  }
   // pass 2: exponentiate, row-sum, P (bf16) -> smem.  SW128 K-major: 16-B chunk c of
-  // row r lives at chunk position c ^ (r & 7) of the row's 128-B line.
+  // row r lives at chunk position c ^ (r & 7) of the row's 128-B line.  In the diagonal
+  // mode the whole row is written (zeros outside this thread's window) so the buffer can
+  // also serve as the O staging tile.
   float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const uint32_t prow_s = smem_u32(prow);
+  if (diag) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const int col = c * 8;
+      if (col < wc0 || col >= wc0 + nhalf * hcols)
+        st_shared_v4(prow_s + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), 0u, 0u, 0u, 0u);
+    }
+  }
   for (int hf = 0; hf < nhalf; ++hf) {
     const int col0 = wc0 + hf * 64;
 #pragma unroll
@@ -230,13 +247,13 @@ __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, 
           rs8[i & 7] += e[i];
         }
         const int colb = col0 + c * 32;  // multiple of 32
-        uint8_t* line = prow + (colb >> 6) * 16384;
+        const uint32_t line = prow_s + (colb >> 6) * 16384;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int chunk = ((colb & 63) >> 3) + u;
-          uint4 w = make_uint4(pack_bf16x2(e[8 * u + 0], e[8 * u + 1]), pack_bf16x2(e[8 * u + 2], e[8 * u + 3]),
-                               pack_bf16x2(e[8 * u + 4], e[8 * u + 5]), pack_bf16x2(e[8 * u + 6], e[8 * u + 7]));
-          *reinterpret_cast<uint4*>(line + ((chunk ^ (row & 7)) << 4)) = w;
+          st_shared_v4(line + ((chunk ^ (row & 7)) << 4), pack_bf16x2(e[8 * u + 0], e[8 * u + 1]),
+                       pack_bf16x2(e[8 * u + 2], e[8 * u + 3]), pack_bf16x2(e[8 * u + 4], e[8 * u + 5]),
+                       pack_bf16x2(e[8 * u + 6], e[8 * u + 7]));
         }
       }
     }
@@ -344,6 +361,58 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
   tc_fence_before();
 }
 
+// Epilogue through TMA: O / l -> bf16 -> smem staging tile in the TMA box layout (the SW128
+// 64-column chunks, then the SW32 / SW64 remainder), fence, named barrier over the 128
+// threads of the tile, one elected thread issues the bulk tensor stores (columns >= Dh and
+// padding rows are out of bounds and not written).  `o_free` is arrived as soon as O has
+// been read from TMEM.  The staging buffer may only be rewritten after
+// bulk_wait_group_read0() (tracked by store_pending).
+template <int NA, int RB>
+__device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CUtensorMap* to_a,
+                                                   const CUtensorMap* to_b, uint8_t* stage, uint32_t tO,
+                                                   uint32_t lane_off, int row, float l, uint32_t bar_id,
+                                                   const TileCoord& t, uint64_t* o_free, int& store_pending) {
+  constexpr int DP = NA * 64 + RB;
+  const float inv_l = 1.f / l;
+  const uint32_t st0 = smem_u32(stage);
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) {
+    uint32_t o[16];
+    tmem_ld16(tO + lane_off + c * 16, o);
+    tmem_ld_wait();
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      const int d = c * 16 + h8 * 8;
+      const uint32_t* w = o + h8 * 8;
+      const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
+      const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
+      const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
+      const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
+      uint32_t addr;
+      if (d < NA * 64) {
+        const int blk = d >> 6, ch = (d & 63) >> 3;
+        addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
+      } else {
+        const int ch = (d - NA * 64) >> 3;  // RB = 16: SW32 (2 chunks/row), RB = 32: SW64 (4 chunks/row)
+        addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
+                        : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
+      }
+      st_shared_v4(addr, a0, a1, a2, a3);
+    }
+  }
+  tc_fence_before();
+  mbar_arrive(o_free);
+  fence_proxy_async_smem();
+  named_bar_sync(bar_id, 128);
+  if ((threadIdx.x & 127) == 0) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) tma_store_5d(to_a, stage + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
+    if (RB) tma_store_5d(to_b, stage + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
+    bulk_commit_group();
+  }
+  store_pending = 1;
+}
+
 // O / l -> bf16 -> o[tok, h*Dh + d] for this thread's row (after the last PV completed).
 template <int DP>
 __device__ __forceinline__ void store_o(const FmhaParams& p, const TileCoord& t, int row, uint32_t tO,
@@ -378,6 +447,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
     fmha_bf16_tc_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
                         const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
                         const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                        const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
                         const FmhaParams p) {
   using Cfg = FmhaCfg<NA, RB>;
   extern __shared__ uint8_t smem_raw[];
@@ -517,22 +587,23 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   } else if (warp >= 4) {
     const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
     uint32_t ns = 0, no = 0;
+    int store_pending = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         mbar_wait(s_full, ns & 1);
         ++ns;
         tc_fence_after();
-        softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no);
+        softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
         mbar_arrive(p_full);
       }
       mbar_wait(o_done, no & 1);
       ++no;
       tc_fence_after();
-      store_o<Cfg::DP>(p, tile_coord(p, item, -1), G.row, tO, G.lane_off, l);
-      tc_fence_before();
-      mbar_arrive(o_free);
+      epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sP, tO, G.lane_off, G.row, l, 1, tile_coord(p, item, -1), o_free,
+                                 store_pending);
     }
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
   }
 
   tc_fence_before();
@@ -766,48 +837,8 @@ __global__ void __launch_bounds__(384, 1)
       ++no;
       tc_fence_after();
       FMHA_STAMP(te, 6);
-      // O / l -> bf16 -> smem in the TMA tile layout (SW128 64-column part + swizzled rest),
-      // then one elected thread stores the tile with TMA (columns >= Dh are out of bounds).
-      const int row = G.row;
-      const float inv_l = 1.f / l;
-      const uint32_t st0 = smem_u32(sPs);
-#pragma unroll
-      for (int c = 0; c < Cfg::DP / 16; ++c) {
-        uint32_t o[16];
-        tmem_ld16(tO + G.lane_off + c * 16, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int h8 = 0; h8 < 2; ++h8) {
-          const int d = c * 16 + h8 * 8;
-          const uint32_t* w = o + h8 * 8;
-          const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
-          const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
-          const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
-          const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
-          uint32_t addr;
-          if (d < NA * 64) {
-            const int blk = d >> 6, ch = (d & 63) >> 3;
-            addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
-          } else {
-            const int ch = (d - NA * 64) >> 3;  // RB = 16: SW32 (2 chunks/row), RB = 32: SW64 (4 chunks/row)
-            addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
-                            : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
-          }
-          st_shared_v4(addr, a0, a1, a2, a3);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&o_free[slot]);  // O is in registers/smem: the MMA may start the next item's PV
-      fence_proxy_async_smem();
-      named_bar_sync(bar_id, 128);
-      if (store_leader) {
-        const TileCoord t = tile_coord(p, 2 * ip + slot, -1);
-#pragma unroll
-        for (int i = 0; i < NA; ++i) tma_store_5d(&to_a, sPs + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
-        if (RB) tma_store_5d(&to_b, sPs + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
-        bulk_commit_group();
-      }
-      store_pending = 1;
+      epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sPs, tO, G.lane_off, G.row, l, bar_id,
+                                 tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
       FMHA_STAMP(te, 7);
     }
     if (store_leader) bulk_wait_group_read0();
@@ -841,21 +872,23 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       m[2 * part + 1] = m[2 * part];
     }
   }
+  // output maps: same 5-D view as q/k/v but over o [tok, C] (row pitch C instead of 3C)
+  CUtensorMap mo[2];
+  {
+    uint64_t ostr[4] = {strides[0], strides[1] / 3, strides[2] / 3, strides[3] / 3};
+    uint32_t boxa[5] = {64, 1, box_rows[0], box_rows[1], 1};
+    uint32_t boxb[5] = {(uint32_t)(RB ? RB : 16), 1, box_rows[0], box_rows[1], 1};
+    if (!make_tmap_bf16(&mo[0], p.o, 5, dims, ostr, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why)) return cudaErrorInvalidValue;
+    if (RB) {
+      if (!make_tmap_bf16(&mo[1], p.o, 5, dims, ostr, boxb,
+                          RB == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, why))
+        return cudaErrorInvalidValue;
+    } else {
+      mo[1] = mo[0];
+    }
+  }
   if constexpr (PairCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0) {
-      // output maps: same 5-D view as q/k/v but over o [tok, C] (row pitch C)
-      CUtensorMap mo[2];
-      uint64_t ostr[4] = {strides[0], strides[1] / 3, strides[2] / 3, strides[3] / 3};
-      uint32_t boxa[5] = {64, 1, box_rows[0], box_rows[1], 1};
-      uint32_t boxb[5] = {(uint32_t)(RB ? RB : 16), 1, box_rows[0], box_rows[1], 1};
-      if (!make_tmap_bf16(&mo[0], p.o, 5, dims, ostr, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why)) return cudaErrorInvalidValue;
-      if (RB) {
-        if (!make_tmap_bf16(&mo[1], p.o, 5, dims, ostr, boxb,
-                            RB == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B, why))
-          return cudaErrorInvalidValue;
-      } else {
-        mo[1] = mo[0];
-      }
       auto kp = fmha_pair_kernel<NA, RB>;
       static bool attr_p = false;
       if (!attr_p) {
@@ -879,7 +912,7 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
   }
   const int slots = Cfg::CTAS_PER_SM * num_sms;
   const int grid = p.items < slots ? p.items : slots;
-  kern<<<grid, 256, Cfg::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+  kern<<<grid, 256, Cfg::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], mo[0], mo[1], p);
   return cudaGetLastError();
 }
 

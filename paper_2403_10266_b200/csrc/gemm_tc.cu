@@ -46,9 +46,10 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 8 ? 8 : (220 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 8 ? 8 : (216 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr int EPI_VEC_BYTES = 2 * 2 * BN * 4;  // per-accumulator copies of u, v (LN-folded epilogue)
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + EPI_VEC_BYTES;
 };
 
 __device__ __forceinline__ float gelu_tanh_f(float u) {
@@ -59,7 +60,8 @@ __device__ __forceinline__ float gelu_tanh_f(float u) {
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                        const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K) {
+                        const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
+                        const EpiVec ev) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -71,6 +73,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* evec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + 256);  // [2 acc][u | v][BN]
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();  // 0 = leader of the CTA pair
@@ -174,6 +177,19 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int j = 0; j < BN / 8; ++j) rv[j] = rp[j];
       }
+      // LayerNorm folded into this GEMM: per-row (mean, rstd) of the raw input row; the tile's
+      // per-column u, v staged once in smem (one copy per accumulator, so a slow warp of the
+      // previous tile never sees them overwritten)
+      float2 rstat = make_float2(0.f, 0.f);
+      float* eu = evec + acc * 2 * BN;
+      if (EPI == EPI_LN || EPI == EPI_LN_GELU) {
+        if (live) rstat = ev.row_stats[grow];
+        for (int i = threadIdx.x - 128; i < BN; i += 128) {
+          eu[i] = ev.col_u[n0 + i];
+          eu[BN + i] = ev.col_v[n0 + i];
+        }
+        named_bar_sync(1, 128);
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
 #pragma unroll
@@ -201,6 +217,21 @@ __global__ void __launch_bounds__(256, 1)
           } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) f[i] = gelu_tanh_f(f[i]);
+          } else if (EPI == EPI_LN || EPI == EPI_LN_GELU) {
+            // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, warp-uniform loads)
+            const float4* u4 = reinterpret_cast<const float4*>(eu + c * 32);
+            const float4* v4 = reinterpret_cast<const float4*>(eu + BN + c * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 uu = u4[q4], vv = v4[q4];
+              const float us[4] = {uu.x, uu.y, uu.z, uu.w}, vs[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                float y = fmaf(rstat.y, fmaf(-rstat.x, us[t], f[4 * q4 + t]), vs[t]);
+                if (EPI == EPI_LN_GELU) y = gelu_tanh_f(y);
+                f[4 * q4 + t] = y;
+              }
+            }
           }
           uint4* dp = reinterpret_cast<uint4*>(drow + c * 32);
 #pragma unroll
@@ -261,7 +292,7 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* 
 
 template <int BN, int EPI>
 static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
-                            int num_sms, cudaStream_t st, std::string* why) {
+                            int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{}) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ta, tw;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
@@ -291,17 +322,26 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K,
+                            ev);
 }
 
 template <int EPI>
 static cudaError_t dispatch_bn(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
-                               int64_t K, int num_sms, cudaStream_t st, std::string* why) {
-  if (N % 256 == 0) return run_gemm<256, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
-  if (N % 192 == 0) return run_gemm<192, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
-  if (N % 128 == 0) return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
-  if (N % 64 == 0) return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
-  return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why);
+                               int64_t K, int num_sms, cudaStream_t st, std::string* why,
+                               const EpiVec& ev = EpiVec{}) {
+  if (N % 256 == 0) return run_gemm<256, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+  if (N % 192 == 0) return run_gemm<192, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+  if (N % 128 == 0) return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+  if (N % 64 == 0) return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+  return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+}
+
+cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,
+                                int64_t K, bool gelu, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  if (gelu) return dispatch_bn<EPI_LN_GELU>(A, Wf, nullptr, D, M, N, K, num_sms, st, why, ev);
+  return dispatch_bn<EPI_LN>(A, Wf, nullptr, D, M, N, K, num_sms, st, why, ev);
 }
 
 cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,

@@ -197,6 +197,104 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
   }
 }
 
+
+// Per-row LayerNorm statistics (mean, rstd) of a bf16 [rows, C] activation, two-pass in
+// registers like the LayerNorm kernel; 8 bytes out per row.  Used to fold LN into the GEMM
+// that consumes it (LN(x) W^T = rstd (x (W o gamma)^T - mean u) + W beta).
+__global__ void __launch_bounds__(256) row_stats_bf16_kernel(const __nv_bfloat16* __restrict__ x, float eps,
+                                                             float2* __restrict__ stats, long rows, int C) {
+  // 4 rows per warp, all loads issued before any reduction (memory-level parallelism)
+  constexpr int R = 4, kMaxV = 5;  // C <= 1280
+  const long r0 = (((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R;
+  const int lane = threadIdx.x & 31;
+  const int nv = C / 8;
+  uint4 buf[R][kMaxV];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (r0 + q) * C);
+#pragma unroll
+    for (int k = 0; k < kMaxV; ++k) {
+      const int vi = lane + 32 * k;
+      buf[q][k] = (r0 + q < rows && vi < nv) ? xr[vi] : make_uint4(0, 0, 0, 0);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxV; ++k) {
+      const uint32_t w[4] = {buf[q][k].x, buf[q][k].y, buf[q][k].z, buf[q][k].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s += __uint_as_float(w[t] << 16) + __uint_as_float(w[t] & 0xFFFF0000u);
+    }
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float mean = s / C;
+    float qq = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxV; ++k) {
+      if (lane + 32 * k < nv) {
+        const uint32_t w[4] = {buf[q][k].x, buf[q][k].y, buf[q][k].z, buf[q][k].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float a = __uint_as_float(w[t] << 16) - mean, c = __uint_as_float(w[t] & 0xFFFF0000u) - mean;
+          qq += a * a + c * c;
+        }
+      }
+    }
+    for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, off);
+    if (lane == 0 && r0 + q < rows) stats[r0 + q] = make_float2(mean, rsqrtf(qq / C + eps));
+  }
+}
+
+// Fold a LayerNorm's affine parameters into the weight of the following linear layer:
+//   W'[n, c] = bf16(W[n, c] * gamma[c]),  u[n] = sum_c W'[n, c],  v[n] = sum_c W[n, c] * beta[c]
+// One warp per output row n; up to 3 matrices per launch (blockIdx.y).
+struct FoldJob {
+  const __nv_bfloat16* W;
+  const __nv_bfloat16* gamma;
+  const __nv_bfloat16* beta;
+  __nv_bfloat16* Wf;
+  float* u;
+  float* v;
+  int N;
+};
+struct FoldJobs {
+  FoldJob j[3];
+};
+__global__ void fold_ln_weights_kernel(FoldJobs jobs, int K) {
+  const FoldJob& J = jobs.j[blockIdx.y];
+  const long n = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (n >= J.N) return;
+  const uint4* wr = reinterpret_cast<const uint4*>(J.W + n * K);
+  const uint4* g4 = reinterpret_cast<const uint4*>(J.gamma);
+  const uint4* b4 = reinterpret_cast<const uint4*>(J.beta);
+  uint4* wf = reinterpret_cast<uint4*>(J.Wf + n * K);
+  float su = 0.f, sv = 0.f;
+  for (int vi = lane; vi < K / 8; vi += 32) {
+    const uint4 w = wr[vi], g = g4[vi], b = b4[vi];
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w}, gg[4] = {g.x, g.y, g.z, g.w}, bb[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float w0 = __uint_as_float(ww[t] << 16), w1 = __uint_as_float(ww[t] & 0xFFFF0000u);
+      const float p0 = w0 * __uint_as_float(gg[t] << 16), p1 = w1 * __uint_as_float(gg[t] & 0xFFFF0000u);
+      __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+      o[t] = *reinterpret_cast<uint32_t*>(&pb);
+      su += __low2float(pb) + __high2float(pb);
+      sv += w0 * __uint_as_float(bb[t] << 16) + w1 * __uint_as_float(bb[t] & 0xFFFF0000u);
+    }
+    wf[vi] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  for (int off = 16; off; off >>= 1) {
+    su += __shfl_xor_sync(0xffffffffu, su, off);
+    sv += __shfl_xor_sync(0xffffffffu, sv, off);
+  }
+  if (lane == 0) {
+    J.u[n] = su;
+    J.v[n] = sv;
+  }
+}
 }  // namespace
 
 cudaError_t launch_gemm_f32(const float* A, const float* W, const float* R, float* D, int64_t M, int64_t N, int64_t K,
@@ -246,6 +344,35 @@ cudaError_t launch_layer_norm(int dtype, int64_t rows, int64_t C, const void* x,
                                                                  (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows,
                                                                  (int)C);
   }
+  return cudaGetLastError();
+}
+
+}  // namespace dsp
+
+namespace dsp {
+
+cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  const int threads = 256;
+  const long warps = (rows + 3) / 4;
+  const unsigned blocks = (unsigned)((warps * 32 + threads - 1) / threads);
+  if (C % 8 || C > 1280) return cudaErrorNotSupported;
+  row_stats_bf16_kernel<<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {
+  FoldJobs fj{};
+  int maxN = 0;
+  for (int i = 0; i < njobs; ++i) {
+    fj.j[i] = FoldJob{(const __nv_bfloat16*)jobs[i].W, (const __nv_bfloat16*)jobs[i].gamma,
+                      (const __nv_bfloat16*)jobs[i].beta, (__nv_bfloat16*)jobs[i].Wf, jobs[i].u, jobs[i].v,
+                      (int)jobs[i].N};
+    if (jobs[i].N > maxN) maxN = (int)jobs[i].N;
+  }
+  const int threads = 256;
+  dim3 grid((unsigned)((maxN * 32 + threads - 1) / threads), (unsigned)njobs);
+  fold_ln_weights_kernel<<<grid, threads, 0, st>>>(fj, (int)K);
   return cudaGetLastError();
 }
 

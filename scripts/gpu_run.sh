@@ -1,1 +1,4 @@
-for v in "" p3_8 p7_16 p1_2; do echo "variant $v"; if [ -n "$v" ]; then export DSP_LIB_OVERRIDE=$PWD/paper_2403_10266_b200/libdsp_$v.so; fi; timeout 90 python scripts/quick_time.py | grep -E "fmha s"; timeout 90 python -m pytest tests -m gpu -q -x --timeout 60 -k "attention_core and 1024" 2>&1 | tail -1; done
+timeout 300 python -m pytest tests -m gpu -q -x --timeout 120 -k "layer_norm or block_bf16_full" 2>&1 | tail -2
+timeout 90 python scripts/quick_time.py | grep -E "block|layernorm"
+DSP_FOLD_LN=1 timeout 90 python scripts/quick_time.py | grep -E "block"
+timeout 300 python bench.py --steps 20 --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step']); [print(k, v) for k,v in d['stages'].items()]"
