@@ -230,7 +230,7 @@ def run_dsp(args):
         Y = torch.empty_like(X)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
+    def step_eager():
         ctx.st_block_forward(shape, bw, X, Y, impl=impl)
 
     def barrier():
@@ -239,11 +239,30 @@ def run_dsp(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    # warm-up
+    # warm-up (eager), then capture one block in a CUDA graph: replay removes the host launch
+    # overhead of the ~13 launches per block (the kernels and NCCL calls are the same)
     for _ in range(args.warmup):
         flush.zero_()
-        step()
+        step_eager()
     barrier()
+    step, graph_note, per_step_launches = step_eager, "eager", None
+    if args.graph:
+        try:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            l0 = ctx.launch_count()
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    step_eager()
+            per_step_launches = ctx.launch_count() - l0
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            step, graph_note = g.replay, "cuda graph replay of one captured dsp_st_block_forward"
+        except Exception as e:  # noqa: BLE001 - fall back to eager launches
+            step, graph_note = step_eager, f"eager (graph capture failed: {str(e)[:120]})"
+        barrier()
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     l0 = ctx.launch_count()
@@ -255,7 +274,7 @@ def run_dsp(args):
             step()
             ev[i][1].record()
         barrier()
-    launches = ctx.launch_count() - l0
+    launches = ctx.launch_count() - l0 if per_step_launches is None else per_step_launches * K
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -264,14 +283,15 @@ def run_dsp(args):
     tokens = sh.B * sh.T * sh.S
     value = tokens * K / (t_ms / 1e3)
 
-    # per-stage timing pass (same launch configuration, stage events inside the block)
+    # per-stage timing pass (same kernels and launch configuration, eager launches with stage
+    # events recorded inside the block; events add small gaps, so shares matter, not the sum)
     stage_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(dsp.STAGES))]
     ctx.set_stage_events(stage_ev)
     KP = max(3, min(K, 20))
     acc = np.zeros(len(dsp.STAGES))
     for _ in range(KP):
         flush.zero_()
-        step()
+        step_eager()
         torch.cuda.synchronize()
         acc += [stage_ev[2 * i].elapsed_time(stage_ev[2 * i + 1]) for i in range(len(dsp.STAGES))]
     ctx.set_stage_events(None)
@@ -378,7 +398,8 @@ def run_dsp(args):
                "vs_baseline": None, "dtype": sh.dtype, "data": "synthetic",
                "config": {"workload": desc, "B": sh.B, "T": sh.T, "S": sh.S, "C": sh.C, "num_heads": sh.NH,
                           "global_tokens": tokens, "switch_impl": impl if N > 1 else "none (N=1)",
-                          "l2": "flushed between timed steps (256 MiB memset outside the events)"},
+                          "l2": "flushed between timed steps (256 MiB memset outside the events)",
+                          "launch": graph_note},
                "roofline": roof, "block_roofline": block_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launches_per_step": launches / K, "clocks": clocks.summary()}
         if switch:
@@ -399,6 +420,7 @@ def main():
     ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of graph replay")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
