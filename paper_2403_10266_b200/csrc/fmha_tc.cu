@@ -494,6 +494,8 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
   const uint32_t tS = tmem;        // 128 columns
   const uint32_t tO = tmem + 128;  // DP columns
 
@@ -687,6 +689,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
 
   // launch allocation is 168 regs x 384 threads; 56 x 128 + 224 x 256 == 168 x 384 exactly
   if (warp == 0) {
@@ -898,9 +902,8 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       }
       const int npairs = p.items / 2;
       const int grid = npairs < num_sms ? npairs : num_sms;
-      kp<<<grid, PairCfg<NA, RB>::THREADS, PairCfg<NA, RB>::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], mo[0],
-                                                                          mo[1], p);
-      return cudaGetLastError();
+      return launch_k(kp, dim3(grid), dim3(PairCfg<NA, RB>::THREADS), PairCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2],
+                      m[3], m[4], m[5], mo[0], mo[1], p);
     }
   }
   auto kern = fmha_bf16_tc_kernel<NA, RB>;
@@ -912,8 +915,7 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
   }
   const int slots = Cfg::CTAS_PER_SM * num_sms;
   const int grid = p.items < slots ? p.items : slots;
-  kern<<<grid, 256, Cfg::SMEM, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], mo[0], mo[1], p);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(grid), dim3(256), Cfg::SMEM, st, 1, m[0], m[1], m[2], m[3], m[4], m[5], mo[0], mo[1], p);
 }
 
 }  // namespace

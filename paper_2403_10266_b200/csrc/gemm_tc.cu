@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -310,20 +312,8 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   }
   const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(2 * pairs));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = Cfg::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tw, (const __nv_bfloat16*)R, (__nv_bfloat16*)D, (int)M, (int)N, (int)K,
-                            ev);
+  return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, (const __nv_bfloat16*)R,
+                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ev);
 }
 
 template <int EPI>

@@ -6,6 +6,7 @@
 #include <type_traits>
 
 #include "dsp_internal.h"
+#include "sm100.cuh"
 
 namespace dsp {
 namespace {
@@ -98,6 +99,8 @@ __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p, long
 template <typename T>
 __global__ void layer_norm_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b, float eps,
                                   T* y, long rows, int C) {
+  griddep_wait();
+  griddep_launch_dependents();
   const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -136,6 +139,8 @@ __global__ void layer_norm_kernel(const T* __restrict__ x, const T* __restrict__
 __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                                            const __nv_bfloat16* __restrict__ b, float eps, __nv_bfloat16* y, long rows,
                                            int C) {
+  griddep_wait();
+  griddep_launch_dependents();
   const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -203,6 +208,8 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
 // that consumes it (LN(x) W^T = rstd (x (W o gamma)^T - mean u) + W beta).
 __global__ void __launch_bounds__(256) row_stats_bf16_kernel(const __nv_bfloat16* __restrict__ x, float eps,
                                                              float2* __restrict__ stats, long rows, int C) {
+  griddep_wait();
+  griddep_launch_dependents();
   // 4 rows per warp, all loads issued before any reduction (memory-level parallelism)
   constexpr int R = 4, kMaxV = 5;  // C <= 1280
   const long r0 = (((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R;
@@ -262,6 +269,8 @@ struct FoldJobs {
   FoldJob j[3];
 };
 __global__ void fold_ln_weights_kernel(FoldJobs jobs, int K) {
+  griddep_wait();
+  griddep_launch_dependents();
   const FoldJob& J = jobs.j[blockIdx.y];
   const long n = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -333,16 +342,14 @@ cudaError_t launch_layer_norm(int dtype, int64_t rows, int64_t C, const void* x,
   const int threads = 256;
   const unsigned blocks = (unsigned)((rows * 32 + threads - 1) / threads);
   if (dtype == DSP_F32) {
-    layer_norm_kernel<float><<<blocks, threads, 0, st>>>((const float*)x, (const float*)g, (const float*)b, eps,
-                                                         (float*)y, rows, (int)C);
+    return launch_k(layer_norm_kernel<float>, dim3(blocks), dim3(threads), 0, st, 1, (const float*)x, (const float*)g,
+                    (const float*)b, eps, (float*)y, rows, (int)C);
   } else if (C % 8 == 0 && C <= 2048) {
-    layer_norm_bf16_vec_kernel<<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
-                                                           (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows,
-                                                           (int)C);
+    return launch_k(layer_norm_bf16_vec_kernel, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x,
+                    (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows, (int)C);
   } else {
-    layer_norm_kernel<__nv_bfloat16><<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
-                                                                 (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows,
-                                                                 (int)C);
+    return launch_k(layer_norm_kernel<__nv_bfloat16>, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x,
+                    (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows, (int)C);
   }
   return cudaGetLastError();
 }
@@ -357,8 +364,8 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
   const long warps = (rows + 3) / 4;
   const unsigned blocks = (unsigned)((warps * 32 + threads - 1) / threads);
   if (C % 8 || C > 1280) return cudaErrorNotSupported;
-  row_stats_bf16_kernel<<<blocks, threads, 0, st>>>((const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C);
-  return cudaGetLastError();
+  return launch_k(row_stats_bf16_kernel, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, eps,
+                  (float2*)stats, rows, (int)C);
 }
 
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {
@@ -372,8 +379,7 @@ cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cud
   }
   const int threads = 256;
   dim3 grid((unsigned)((maxN * 32 + threads - 1) / threads), (unsigned)njobs);
-  fold_ln_weights_kernel<<<grid, threads, 0, st>>>(fj, (int)K);
-  return cudaGetLastError();
+  return launch_k(fold_ln_weights_kernel, grid, dim3(threads), 0, st, 1, fj, (int)K);
 }
 
 }  // namespace dsp

@@ -4,6 +4,7 @@
 // coalesced: every run is Sn*C*elem contiguous bytes (SURVEY §8a "The switch as an
 // exact index map"), so no shared-memory transpose is needed.
 #include "dsp_internal.h"
+#include "sm100.cuh"
 
 namespace dsp {
 namespace {
@@ -26,6 +27,8 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 // blockIdx.y = run index (i0*n1 + i1)*n2 + i2; blockIdx.x strides over the run's vectors.
 __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                             RunCopy rc, PeerPtrs peers, int use_peers, int64_t peer_off) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int64_t run = blockIdx.y;
   const int64_t i2 = run % rc.n[2];
   const int64_t i1 = (run / rc.n[2]) % rc.n[1];
@@ -54,6 +57,7 @@ __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __res
 // release-store `epoch` into slot [rank] of every peer's pad, then acquire-spin until
 // every peer has written >= epoch into our own pad.  Bounded spin (no infinite hang).
 __global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64_t epoch) {
+  griddep_wait();
   const int i = threadIdx.x;
   if (i < world) {
     __threadfence_system();
@@ -84,9 +88,8 @@ static cudaError_t launch_copy(const void* src, void* dst, const RunCopy& rc, co
   if (cap < 1) cap = 1;
   if (bx > cap) bx = cap;
   dim3 grid((unsigned)bx, (unsigned)runs);
-  run_copy_kernel<<<grid, kThreads, 0, st>>>(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), rc, peers,
-                                             use_peers, peer_off);
-  return cudaGetLastError();
+  return launch_k(run_copy_kernel, grid, dim3(kThreads), 0, st, 1, static_cast<const uint8_t*>(src),
+                  static_cast<uint8_t*>(dst), rc, peers, use_peers, peer_off);
 }
 
 cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int num_sms, cudaStream_t st) {
@@ -100,8 +103,7 @@ cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t d
 }
 
 cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st) {
-  p2p_barrier_kernel<<<1, 32, 0, st>>>(signals, rank, world, epoch);
-  return cudaGetLastError();
+  return launch_k(p2p_barrier_kernel, dim3(1), dim3(32), 0, st, 1, signals, rank, world, epoch);
 }
 
 }  // namespace dsp
