@@ -217,7 +217,7 @@ def run_dsp(args):
     act_bytes = X.numel() * X.element_size()
     ws_bytes = dsp.workspace_bytes(shape, N)
     impl = args.switch
-    if impl == "p2p" and N > 1:
+    if impl in ("p2p", "fused") and N > 1:
         import torch.distributed._symmetric_memory as symm
         ws_pad = (ws_bytes + 4095) // 4096 * 4096
         buf = symm.empty(ws_pad + act_bytes, dtype=torch.uint8, device=dev)
@@ -339,8 +339,8 @@ def run_dsp(args):
     # switch bus bandwidth (N > 1): busbw = (N-1)/N * shard_bytes / t
     switch = None
     if world > 1:
-        Z = torch.empty_like(X) if not (impl == "p2p") else None
-        if impl == "p2p":
+        Z = torch.empty_like(X) if impl == "nccl" else None
+        if impl != "nccl":
             Z = Y
             src = torch.empty_like(X)
         else:
@@ -366,7 +366,7 @@ def run_dsp(args):
     xh = torch.from_numpy(np.ascontiguousarray(xs).view(np.int16) if sh.dtype == "bf16" else xs).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
     Xd, Yd = torch.empty_like(X), torch.empty_like(X)
-    if impl == "p2p" and N > 1:
+    if impl != "nccl" and N > 1:
         Yd = Y
     for _ in range(max(1, args.warmup)):
         ctx.st_block_forward_host(shape, bw, xh, yh, Xd, Yd, impl=impl)
@@ -417,7 +417,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
     ap.add_argument("--config", default="blk", choices=list(CONFIGS))
-    ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p", "fused"])
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of graph replay")

@@ -71,9 +71,15 @@ typedef enum {
 typedef enum { DSP_DIM_T = 1, DSP_DIM_S = 2 } dsp_dim_t;   /* axis index in [B,T,S,C] */
 typedef enum { DSP_BF16 = 0, DSP_F32 = 1 } dsp_dtype_t;
 /* Switch transport.  Explicit choice, no heuristic dispatch.
- * NCCL: pack kernel -> ncclAlltoAll (bytes) -> unpack kernel (identity sides skipped).
- * P2P : direct NVLink stores into the peers' symmetric buffers + signal-pad barriers. */
-typedef enum { DSP_SWITCH_NCCL = 0, DSP_SWITCH_P2P = 1 } dsp_switch_impl_t;
+ * NCCL : pack kernel -> ncclAlltoAll (bytes) -> unpack kernel (identity sides skipped).
+ * P2P  : direct NVLink stores into the peers' symmetric buffers + signal-pad barriers.
+ * FUSED: (dsp_st_block_forward only) no separate switch: the spatial out-projection
+ *        epilogue stores every output row directly at its final address in the S-shard
+ *        owner's buffer, and the FC2 epilogue stores directly into the T-shard owner's
+ *        y_local, over the peer mappings (the NVLink transfer overlaps the GEMM tiles);
+ *        one signal-pad barrier after each of the two GEMMs.  Needs the peer buffers of
+ *        DSP_SWITCH_P2P; dsp_switch treats FUSED as P2P. */
+typedef enum { DSP_SWITCH_NCCL = 0, DSP_SWITCH_P2P = 1, DSP_SWITCH_FUSED = 2 } dsp_switch_impl_t;
 
 /* GLOBAL shape of the activation; identical on all ranks. */
 typedef struct {

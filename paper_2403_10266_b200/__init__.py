@@ -22,9 +22,9 @@ LIB_PATH = os.environ.get("DSP_LIB_OVERRIDE") or os.path.join(_HERE, "libdsp.so"
 
 DSP_DIM_T, DSP_DIM_S = 1, 2
 DSP_BF16, DSP_F32 = 0, 1
-DSP_SWITCH_NCCL, DSP_SWITCH_P2P = 0, 1
+DSP_SWITCH_NCCL, DSP_SWITCH_P2P, DSP_SWITCH_FUSED = 0, 1, 2
 DSP_EPI_NONE, DSP_EPI_RESIDUAL, DSP_EPI_GELU = 0, 1, 2
-IMPLS = {"nccl": DSP_SWITCH_NCCL, "p2p": DSP_SWITCH_P2P}
+IMPLS = {"nccl": DSP_SWITCH_NCCL, "p2p": DSP_SWITCH_P2P, "fused": DSP_SWITCH_FUSED}
 DIMS = {"T": DSP_DIM_T, "S": DSP_DIM_S, DSP_DIM_T: DSP_DIM_T, DSP_DIM_S: DSP_DIM_S}
 
 STATUS = {0: "DSP_OK", 1: "DSP_ERR_NULL", 2: "DSP_ERR_SHAPE", 3: "DSP_ERR_DIVISIBILITY", 4: "DSP_ERR_SAME_DIM",

@@ -230,7 +230,8 @@ inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
 // stage0 >= 0: record stage events for (QKV, ATTN, PROJ) = stage0, stage0+1, stage0+2.
 dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
                         const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
-                        cudaStream_t st, int stage0 = -1, const EpiVec* ln = nullptr) {
+                        cudaStream_t st, int stage0 = -1, const EpiVec* ln = nullptr,
+                        const RemoteMap* remote = nullptr) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
   const int sq = stage0, sa = stage0 < 0 ? -1 : stage0 + 1, sp = stage0 < 0 ? -1 : stage0 + 2;
@@ -247,7 +248,9 @@ dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int6
     if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
     mark(ctx, sa, 1, st);
     mark(ctx, sp, 0, st);
-    e = launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
+    // remote != nullptr: switch fused into this epilogue (rows stored at their owner rank)
+    e = remote ? launch_gemm_bf16_remote(o, w_o, res, *remote, tok, C, C, ctx->num_sms, st, &why)
+               : launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "output projection", why);
     mark(ctx, sp, 1, st);
   } else {
@@ -469,7 +472,9 @@ dsp_status_t dsp_switch(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp
                         dsp_switch_impl_t impl, void* stream) {
   DSP_TRY(check_ctx(ctx));
   DSP_TRY(validate_switch(ctx, s, ctx->world, from, to));
-  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P) return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  if (impl == DSP_SWITCH_FUSED) impl = DSP_SWITCH_P2P;  // a standalone switch has nothing to fuse with
   if (!x || !y) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
   const int64_t bytes = shard_bytes(s, ctx->world);
@@ -532,7 +537,8 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   }
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
   const int N = ctx->world;
-  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P) return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
   DSP_TRY(check_bf16_attn(ctx, s, s->S));
   DSP_TRY(check_bf16_attn(ctx, s, s->T));
   const int64_t e = elem_bytes(s->dtype), C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * e;
@@ -547,11 +553,20 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   void* qkv = big;
   void* o = big + 3 * act;
   void* ys = ws + L.ys;              // [tok, C] S-sharded activation (N > 1)
-  if (N > 1 && impl == DSP_SWITCH_P2P) {
+  const bool fused = N > 1 && impl == DSP_SWITCH_FUSED;
+  RemoteMap rm_ts{}, rm_st{};
+  if (N > 1 && (impl == DSP_SWITCH_P2P || fused)) {
     if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P block without dsp_ctx_set_peer_buffers");
     void* base = ctx->peer_base.p[ctx->rank];
     if (!in_region(ys, act, base, ctx->peer_bytes) || !in_region(y, act, base, ctx->peer_bytes))
       return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P block needs the workspace and y_local inside the symmetric buffer");
+    if (fused) {
+      if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "fused switch needs the bf16 path");
+      const int64_t ys_off = static_cast<uint8_t*>(ys) - static_cast<uint8_t*>(base);
+      const int64_t y_off = static_cast<uint8_t*>(y) - static_cast<uint8_t*>(base);
+      rm_ts = RemoteMap{ctx->peer_base, ys_off, 1, ctx->rank, (int)s->B, (int)s->T, (int)s->S, (int)(s->T / N), (int)(s->S / N)};
+      rm_st = RemoteMap{ctx->peer_base, y_off, 2, ctx->rank, (int)s->B, (int)s->T, (int)s->S, (int)(s->T / N), (int)(s->S / N)};
+    }
   }
   cudaStream_t st = (cudaStream_t)stream;
   const float eps = w->ln_eps;
@@ -583,11 +598,15 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   mark(ctx, DSP_STAGE_LN1, 1, st);
   // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
   DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, fold ? x : h, fold ? wf_s : w->w_qkv_s, w->w_o_s, x, y, qkv, o,
-                     st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr));
-  // a5: switch T -> S
+                     st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr, fused ? &rm_ts : nullptr));
+  // a5: switch T -> S (fused: the out-projection already stored every row at its owner)
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
-  if (N > 1) {
+  if (fused) {
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "fused switch barrier");
+    ctx->launches += 1;
+    cur = ys;
+  } else if (N > 1) {
     DSP_TRY(do_switch(ctx, s, DSP_DIM_T, y, ys, impl, st, big, big + act));
     cur = ys;
   }
@@ -617,11 +636,23 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   }
   mark(ctx, DSP_STAGE_FC1, 1, st);
   mark(ctx, DSP_STAGE_FC2, 0, st);
-  DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));
+  if (fused) {  // FC2 epilogue stores y = y2 + MLP rows straight into the T-shard owners' y_local
+    std::string why;
+    cudaError_t e2 = launch_gemm_bf16_remote(big, w->w_fc2, cur, rm_st, tok, C, 4 * C, ctx->num_sms, st, &why);
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "FC2 (switch fused)", why);
+    ctx->launches += 1;
+  } else {
+    DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));
+  }
   mark(ctx, DSP_STAGE_FC2, 1, st);
   // a11: switch S -> T back into y
   mark(ctx, DSP_STAGE_SWITCH_ST, 0, st);
-  if (N > 1) DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
+  if (fused) {
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "fused switch barrier");
+    ctx->launches += 1;
+  } else if (N > 1) {
+    DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
+  }
   mark(ctx, DSP_STAGE_SWITCH_ST, 1, st);
   return DSP_OK;
 }

@@ -72,7 +72,17 @@ struct LnFold {
 cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
 // GEMM epilogue codes beyond the public dsp_epilogue_t
-enum { EPI_LN = 3, EPI_LN_GELU = 4 };
+enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5 };
+// Residual epilogue whose output rows go straight to their owner rank after a switch
+// (switch fused into the GEMM): mode 1 = T->S (rows of [B,Tn,S] -> peers' [B,T,Sn]),
+// mode 2 = S->T (rows of [B,T,Sn] -> peers' [B,Tn,S]).  Row bytes = C * 2.
+struct RemoteMap {
+  PeerPtrs base;
+  int64_t dst_off;  // offset of the destination buffer inside every peer's symmetric buffer
+  int mode, rank, B, T, S, Tn, Sn;
+};
+cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,
+                                    int64_t N, int64_t K, int num_sms, cudaStream_t st, std::string* why);
 struct EpiVec {
   const float2* row_stats;  // [M] (mean, rstd)
   const float* col_u;       // [N]

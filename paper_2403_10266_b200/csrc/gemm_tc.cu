@@ -61,7 +61,7 @@ template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                         const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
-                        const EpiVec ev) {
+                        const EpiVec ev, const RemoteMap rm) {
   using Cfg = GemmCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -172,9 +172,25 @@ __global__ void __launch_bounds__(256, 1)
       const int grow = m0 + row;
       const bool live = grow < M;
       __nv_bfloat16* drow = D + (size_t)grow * N + n0;
+      if (EPI == EPI_RES_REMOTE && live) {
+        // switch fused into the epilogue: this row's owner rank q and row index there
+        int64_t dst;
+        int q;
+        if (rm.mode == 1) {  // T-sharded [B,Tn,S] row -> S-shard owner's [B,T,Sn]
+          const int64_t ts = (int64_t)rm.Tn * rm.S, b = grow / ts, rem = grow % ts, t = rem / rm.S, sx = rem % rm.S;
+          q = (int)(sx / rm.Sn);
+          dst = (b * rm.T + (int64_t)rm.rank * rm.Tn + t) * rm.Sn + sx % rm.Sn;
+        } else {             // S-sharded [B,T,Sn] row -> T-shard owner's [B,Tn,S]
+          const int64_t ts = (int64_t)rm.T * rm.Sn, b = grow / ts, rem = grow % ts, t = rem / rm.Sn, sx = rem % rm.Sn;
+          q = (int)(t / rm.Tn);
+          dst = (b * rm.Tn + t % rm.Tn) * rm.S + (int64_t)rm.rank * rm.Sn + sx;
+        }
+        drow = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(rm.base.p[q]) + rm.dst_off) + dst * N + n0;
+      }
       // residual row segment is independent of the accumulator: fetch it before waiting
-      uint4 rv[EPI == DSP_EPI_RESIDUAL ? BN / 8 : 1];
-      if (EPI == DSP_EPI_RESIDUAL && live) {
+      constexpr bool kRes = EPI == DSP_EPI_RESIDUAL || EPI == EPI_RES_REMOTE;
+      uint4 rv[kRes ? BN / 8 : 1];
+      if (kRes && live) {
         const uint4* rp = reinterpret_cast<const uint4*>(R + (size_t)grow * N + n0);
 #pragma unroll
         for (int j = 0; j < BN / 8; ++j) rv[j] = rp[j];
@@ -203,7 +219,7 @@ __global__ void __launch_bounds__(256, 1)
           float f[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          if (EPI == DSP_EPI_RESIDUAL) {
+          if (kRes) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const uint4 r4 = rv[c * 4 + j];
@@ -294,7 +310,8 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* 
 
 template <int BN, int EPI>
 static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
-                            int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{}) {
+                            int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{},
+                            const RemoteMap& rm = RemoteMap{}) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ta, tw;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
@@ -313,7 +330,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, (const __nv_bfloat16*)R,
-                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ev);
+                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ev, rm);
 }
 
 template <int EPI>
@@ -325,6 +342,17 @@ static cudaError_t dispatch_bn(const void* A, const void* W, const void* R, void
   if (N % 128 == 0) return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
   if (N % 64 == 0) return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
   return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+}
+
+cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,
+                                    int64_t N, int64_t K, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  const EpiVec ev{};
+  if (N % 256 == 0) return run_gemm<256, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
+  if (N % 192 == 0) return run_gemm<192, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
+  if (N % 128 == 0) return run_gemm<128, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
+  if (N % 64 == 0) return run_gemm<64, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
+  return run_gemm<32, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
 }
 
 cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,

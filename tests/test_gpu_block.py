@@ -159,9 +159,11 @@ def test_switch_p2p_virtual_ranks_bitexact(N, B):
 
 
 @pytest.mark.parametrize("N", [2, 4])
-def test_block_p2p_virtual_ranks_n_invariant(N):
+@pytest.mark.parametrize("impl", ["p2p", "fused"])
+def test_block_p2p_virtual_ranks_n_invariant(N, impl):
     """DSP block over N virtual ranks == N=1 block bitwise (no reductions cross ranks,
-    no split-K: each output's reduction order is independent of N) and == oracle."""
+    no split-K: each output's reduction order is independent of N).  `fused`: the switch is
+    done by the out-projection / FC2 epilogues storing rows at their owner rank."""
     m = dsp()
     sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
     xs, Ws = _setup(sh)
@@ -177,6 +179,6 @@ def test_block_p2p_virtual_ranks_n_invariant(N):
     Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
     for r in range(N):
         g.ctx[r].set_workspace(g.region[r][:ws])
-    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl="p2p"))
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl=impl))
     got = np.concatenate([bits16(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
