@@ -68,7 +68,10 @@ struct FmhaCfg {
   static constexpr int TILE = NA * 16384 + RB_BYTES;            // one 128-row operand tile
   static constexpr int TX = 128 * DP * 2;                        // TMA bytes per tile
   static constexpr int P_BYTES = 2 * 16384;
-  static constexpr int SMEM = 1024 + 3 * TILE /*Q,K,V*/ + P_BYTES + 256;
+  // Q, K, V x 2 stages, P, barriers.  No alignment slack: dynamic smem starts right after the
+  // 1 KB system-reserved block and is therefore 1024-B aligned (checked in the kernel), which
+  // keeps two CTAs per SM at Dh = 72 (115,712 B available per CTA).
+  static constexpr int SMEM = 5 * TILE /*Q,K,V0,V1*/ - TILE + P_BYTES + 256;
   static constexpr uint32_t RB_SW = RB == 16 ? SW_32B : SW_64B;
   static constexpr uint32_t RB_ROW = RB * 2;                     // bytes per row in the rem chunk
   static constexpr int CTAS_PER_SM = SMEM <= 113 * 1024 ? 2 : 1;  // Dh <= 96: two CTAs per SM
@@ -413,6 +416,64 @@ __device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CU
   store_pending = 1;
 }
 
+// Block-diagonal tiles (G sequences of length L < 128 per tile, rows sequence-major): this
+// thread's keys are the columns [lo, lo + L) of its diagonal block, inside the warp's 32-
+// or 64-column window.  Single pass from registers, range-compare mask (no division), the
+// full P row is written (zeros outside the block) so the buffer can stage O afterwards.
+template <int DP>
+__device__ __forceinline__ void softmax_tile_diag(const SoftmaxGeom& G, uint32_t tS, uint8_t* sP, float& m, float& l,
+                                                  int* store_pending, uint32_t bar_id) {
+  const int row = G.row;
+  const int lo = G.my_blk * G.L, hi = lo + G.L;
+  const int wcols = G.nhalf * G.hcols;  // 32 or 64
+  uint32_t v[64];
+  tmem_ld32(tS + G.lane_off + G.wc0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+  if (wcols > 32) tmem_ld32(tS + G.lane_off + G.wc0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tmem_ld_wait();
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const int col = G.wc0 + i;
+    if (i < wcols && col >= lo && col < hi) mx = fmaxf(mx, __uint_as_float(v[i]));
+  }
+  const float m_new = mx * G.sl2;
+  float rs = 0.f;
+  uint32_t pk[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c0 = G.wc0 + 2 * i;
+    const float x0 = (2 * i < wcols && c0 >= lo && c0 < hi) ? fmaf(__uint_as_float(v[2 * i]), G.sl2, -m_new) : -INFINITY;
+    const float x1 = (2 * i + 1 < wcols && c0 + 1 >= lo && c0 + 1 < hi)
+                         ? fmaf(__uint_as_float(v[2 * i + 1]), G.sl2, -m_new) : -INFINITY;
+    const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+    rs += e0 + e1;
+    pk[i] = pack_bf16x2(e0, e1);
+  }
+  m = m_new;
+  l = rs;
+  if (store_pending && *store_pending) {  // previous item's O TMA store must have read the P buffer
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+    named_bar_sync(bar_id, 128);
+    *store_pending = 0;
+  }
+  const uint32_t prow = smem_u32(sP) + row * 128;
+  const int c0w = G.wc0 >> 3, ncw = wcols >> 3;  // window = chunks [c0w, c0w + ncw) of 8 keys
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    if (u < ncw) {
+      const int c = c0w + u;
+      st_shared_v4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
+                   pk[4 * u + 3]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 16; ++c)  // zeros outside the window
+    if (c < c0w || c >= c0w + ncw)
+      st_shared_v4(prow + (c >> 3) * 16384 + (((c & 7) ^ (row & 7)) << 4), 0u, 0u, 0u, 0u);
+  fence_proxy_async_smem();
+  tc_fence_before();
+}
+
 // O / l -> bf16 -> o[tok, h*Dh + d] for this thread's row (after the last PV completed).
 template <int DP>
 __device__ __forceinline__ void store_o(const FmhaParams& p, const TileCoord& t, int row, uint32_t tO,
@@ -450,24 +511,25 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
                         const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
                         const FmhaParams p) {
   using Cfg = FmhaCfg<NA, RB>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // layout assumes a 1024-B aligned base
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + Cfg::TILE;
-  uint8_t* sV = sK + Cfg::TILE;
-  uint8_t* sP = sV + Cfg::TILE;  // 2 x [128 rows x 128 B] SW128, K-major
+  uint8_t* sV = sK + Cfg::TILE;      // 2 stages
+  uint8_t* sP = sV + 2 * Cfg::TILE;  // 2 x [128 rows x 128 B] SW128, K-major
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* k_full = bars + 2;
   uint64_t* k_empty = bars + 3;
-  uint64_t* v_full = bars + 4;
-  uint64_t* v_empty = bars + 5;
-  uint64_t* s_full = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
-  uint64_t* o_free = bars + 9;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* v_full = bars + 4;   // [2]
+  uint64_t* v_empty = bars + 6;  // [2]
+  uint64_t* s_full = bars + 8;
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_done = bars + 10;
+  uint64_t* o_free = bars + 11;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = warp_id();
   const int n = p.n_kv;
@@ -475,7 +537,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
     if (RB) { tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b); }
-    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], 1);
     mbar_init(p_full, 128);
     mbar_init(o_done, 1);
     mbar_init(o_free, 128);
@@ -513,10 +575,11 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
           ++nk;
           mbar_arrive_expect_tx(k_full, Cfg::TX);
           load_tile<NA, RB>(sK, &tk_a, &tk_b, k_full, t);
-          mbar_wait(v_empty, (nv & 1) ^ 1);
+          const int vs = nv & 1;  // V is double-buffered: V_{j+1} streams in while PV_j runs
+          mbar_wait(&v_empty[vs], ((nv >> 1) & 1) ^ 1);
           ++nv;
-          mbar_arrive_expect_tx(v_full, Cfg::TX);
-          load_tile<NA, RB>(sV, &tv_a, &tv_b, v_full, t);
+          mbar_arrive_expect_tx(&v_full[vs], Cfg::TX);
+          load_tile<NA, RB>(sV + vs * Cfg::TILE, &tv_a, &tv_b, &v_full[vs], t);
         }
       }
     }
@@ -563,25 +626,27 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
           if (j + 2 == n && elect_one()) umma_commit(q_empty);
           __syncwarp();
         }
-        mbar_wait(v_full, nv & 1);
+        const int vs = nv & 1;
+        mbar_wait(&v_full[vs], (nv >> 1) & 1);
         ++nv;
         if (j == 0) mbar_wait(o_free, (nit & 1) ^ 1);  // previous item's epilogue has read O
         tc_fence_after();
         if (elect_one()) {
+          const uint32_t vb = v0 + vs * Cfg::TILE;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {  // 128 keys in steps of 16
             const uint64_t ad = make_sdesc(p0 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SW_128B);
 #pragma unroll
             for (int i = 0; i < NA; ++i)
-              umma_bf16_ss(tO + 64 * i, ad, make_sdesc(v0 + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+              umma_bf16_ss(tO + 64 * i, ad, make_sdesc(vb + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
                            (j | k) != 0);
             if (RB)
               umma_bf16_ss(tO + 64 * NA, ad,
-                           make_sdesc(v0 + NA * 16384 + k * 16 * Cfg::RB_ROW, 16384, 8 * Cfg::RB_ROW, Cfg::RB_SW),
+                           make_sdesc(vb + NA * 16384 + k * 16 * Cfg::RB_ROW, 16384, 8 * Cfg::RB_ROW, Cfg::RB_SW),
                            idPVb, (j | k) != 0);
           }
           umma_commit(o_done);
-          umma_commit(v_empty);
+          umma_commit(&v_empty[vs]);
         }
         __syncwarp();
       }
@@ -592,18 +657,25 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
     int store_pending = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       float m = -INFINITY, l = 0.f;
+      unsigned long long* tr = p.trace ? p.trace + ((size_t)(ns & 127) * 8) : nullptr;
+      FMHA_STAMP(tr, 0);
       for (int j = 0; j < n; ++j) {
         mbar_wait(s_full, ns & 1);
         ++ns;
         tc_fence_after();
-        softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
+        FMHA_STAMP(tr, 1);
+        if (G.diag) softmax_tile_diag<Cfg::DP>(G, tS, sP, m, l, &store_pending, 1);  // n == 1 in this mode
+        else softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
+        FMHA_STAMP(tr, 2);
         mbar_arrive(p_full);
       }
       mbar_wait(o_done, no & 1);
       ++no;
       tc_fence_after();
+      FMHA_STAMP(tr, 3);
       epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sP, tO, G.lane_off, G.row, l, 1, tile_coord(p, item, -1), o_free,
                                  store_pending);
+      FMHA_STAMP(tr, 4);
     }
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
   }
