@@ -378,11 +378,13 @@ __device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CU
   constexpr int DP = NA * 64 + RB;
   const float inv_l = 1.f / l;
   const uint32_t st0 = smem_u32(stage);
+  uint32_t ov[DP];  // all TMEM loads in flight before one wait
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16));
+  tmem_ld_wait();
 #pragma unroll
   for (int c = 0; c < DP / 16; ++c) {
-    uint32_t o[16];
-    tmem_ld16(tO + lane_off + c * 16, o);
-    tmem_ld_wait();
+    const uint32_t* o = ov + c * 16;
 #pragma unroll
     for (int h8 = 0; h8 < 2; ++h8) {
       const int d = c * 16 + h8 * 8;
@@ -420,12 +422,12 @@ __device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CU
 // thread's keys are the columns [lo, lo + L) of its diagonal block, inside the warp's 32-
 // or 64-column window.  Single pass from registers, range-compare mask (no division), the
 // full P row is written (zeros outside the block) so the buffer can stage O afterwards.
-template <int DP>
+template <int W>  // window width: 32 or 64 columns
 __device__ __forceinline__ void softmax_tile_diag(const SoftmaxGeom& G, uint32_t tS, uint8_t* sP, float& m, float& l,
                                                   int* store_pending, uint32_t bar_id) {
   const int row = G.row;
   const int lo = G.my_blk * G.L, hi = lo + G.L;
-  const int wcols = G.nhalf * G.hcols;  // 32 or 64
+  constexpr int wcols = W;
   uint32_t v[64];
   tmem_ld32(tS + G.lane_off + G.wc0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
   if (wcols > 32) tmem_ld32(tS + G.lane_off + G.wc0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
@@ -664,8 +666,12 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
         ++ns;
         tc_fence_after();
         FMHA_STAMP(tr, 1);
-        if (G.diag) softmax_tile_diag<Cfg::DP>(G, tS, sP, m, l, &store_pending, 1);  // n == 1 in this mode
-        else softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
+        if (G.diag) {  // n == 1 in this mode
+          if (G.nhalf * G.hcols > 32) softmax_tile_diag<64>(G, tS, sP, m, l, &store_pending, 1);
+          else softmax_tile_diag<32>(G, tS, sP, m, l, &store_pending, 1);
+        } else {
+          softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
+        }
         FMHA_STAMP(tr, 2);
         mbar_arrive(p_full);
       }

@@ -46,10 +46,13 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (216 * 1024) / STAGE_BYTES > 8 ? 8 : (216 * 1024) / STAGE_BYTES;
+  static constexpr int E_BYTES = BN * 256;  // epilogue staging: 128 rows x BN bf16 as BN/EB boxes
+  static constexpr int EB = BN < 64 ? BN : 64;          // box width (columns): SW128 at 64, SW64 at 32
+  static constexpr int E_BOX = 128 * EB * 2;
+  static constexpr int STAGES = (216 * 1024 - E_BYTES) / STAGE_BYTES > 8 ? 8 : (216 * 1024 - E_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int EPI_VEC_BYTES = 2 * 2 * BN * 4;  // per-accumulator copies of u, v (LN-folded epilogue)
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/ + EPI_VEC_BYTES;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + E_BYTES + 256 /*barriers*/ + EPI_VEC_BYTES;
 };
 
 __device__ __forceinline__ float gelu_tanh_f(float u) {
@@ -60,6 +63,7 @@ __device__ __forceinline__ float gelu_tanh_f(float u) {
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                        const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
                         const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
                         const EpiVec ev, const RemoteMap rm) {
   using Cfg = GemmCfg<BN>;
@@ -68,12 +72,14 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sE = smem + STAGES * Cfg::STAGE_BYTES;  // epilogue staging tile (residual in, output out)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sE + Cfg::E_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* evec = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + 256);  // [2 acc][u | v][BN]
+  uint64_t* r_full = tempty + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(r_full + 1);
+  float* evec = reinterpret_cast<float*>(sE + Cfg::E_BYTES + 256);  // [2 acc][u | v][BN]
 
   const int warp = warp_id();
   const uint32_t rank = cluster_ctarank();  // 0 = leader of the CTA pair
@@ -87,6 +93,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmW);
+    tma_prefetch(&tmD);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -95,6 +102,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * 128);  // both CTAs' epilogue threads
     }
+    mbar_init(r_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -161,6 +169,79 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+  } else if (warp >= 4 && (EPI == DSP_EPI_NONE || EPI == DSP_EPI_RESIDUAL || EPI == DSP_EPI_GELU)) {
+    // Bulk-tensor epilogue: the residual tile arrives by TMA into the staging tile sE (issued
+    // by this warpgroup as soon as the previous tile's store has been read out of sE), each
+    // thread adds its accumulator row in place (SW128 layout: 16-B chunk c of row r at
+    // c ^ (r & 7)), and one thread TMA-stores the tile (rows >= M are clipped).
+    constexpr bool kRes = EPI == DSP_EPI_RESIDUAL;
+    const int q = warp & 3;
+    const int row = q * 32 + lane_id();
+    const bool elected = threadIdx.x == 128;
+    const uint32_t e0 = smem_u32(sE);
+    int it = 0;
+    auto load_res = [&](int tile) {
+      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM, n0 = (tile % tiles_n) * BN;
+      mbar_arrive_expect_tx(r_full, Cfg::E_BYTES);
+#pragma unroll
+      for (int b = 0; b < BN / Cfg::EB; ++b) tma_load_2d(sE + b * Cfg::E_BOX, &tmR, r_full, n0 + Cfg::EB * b, m0);
+    };
+    if (kRes && elected && pair < num_tiles) load_res(pair);
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+      const int acc = it & 1;
+      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
+      const int n0 = (tile % tiles_n) * BN;
+      if (kRes) {
+        mbar_wait(r_full, it & 1);
+      } else if (it > 0) {  // the previous tile's store must have been read out of sE
+        if (elected) bulk_wait_group_read0();
+        named_bar_sync(1, 128);
+      }
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait();
+        // chunk c (32 columns = 4 x 16 B) of this row inside box c / (EB / 32)
+        const uint32_t line = e0 + (c / (Cfg::EB / 32)) * Cfg::E_BOX + row * (Cfg::EB * 2);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = (c % (Cfg::EB / 32)) * 4 + u;
+          const uint32_t addr = line + ((Cfg::EB == 64 ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3))) << 4);
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * u + i]);
+          if (kRes) {
+            uint32_t r0, r1, r2, r3;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+            f[0] += bf16lo(r0); f[1] += bf16hi(r0); f[2] += bf16lo(r1); f[3] += bf16hi(r1);
+            f[4] += bf16lo(r2); f[5] += bf16hi(r2); f[6] += bf16lo(r3); f[7] += bf16hi(r3);
+          } else if (EPI == DSP_EPI_GELU) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
+          }
+          st_shared_v4(addr, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                       pack_bf16x2(f[6], f[7]));
+        }
+      }
+      tc_fence_before();
+      if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next
+      else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (elected) {
+#pragma unroll
+        for (int b = 0; b < BN / Cfg::EB; ++b) tma_store_2d(&tmD, sE + b * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
+        bulk_commit_group();
+        if (kRes && tile + num_pairs < num_tiles) {
+          bulk_wait_group_read0();  // sE read out: bring in the next tile's residual
+          load_res(tile + num_pairs);
+        }
+      }
+    }
+    if (elected) bulk_wait_group_read0();
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane_id();
@@ -313,13 +394,22 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
                             int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{},
                             const RemoteMap& rm = RemoteMap{}) {
   using Cfg = GemmCfg<BN>;
-  CUtensorMap ta, tw;
+  CUtensorMap ta, tw, td, tr;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
-  uint32_t ba[2] = {BK, BM}, bw[2] = {BK, Cfg::BNH};
+  uint64_t dd[2] = {(uint64_t)N, (uint64_t)M}, sd[1] = {(uint64_t)N * 2};
+  uint32_t ba[2] = {BK, BM}, bw[2] = {BK, Cfg::BNH}, bd[2] = {Cfg::EB, BM};
+  const CUtensorMapSwizzle esw = Cfg::EB == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   if (!make_tmap_bf16(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, why) ||
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
+  td = ta;
+  tr = ta;
+  if (EPI == DSP_EPI_NONE || EPI == DSP_EPI_RESIDUAL || EPI == DSP_EPI_GELU) {
+    if (!make_tmap_bf16(&td, D, 2, dd, sd, bd, esw, why)) return cudaErrorInvalidValue;
+    if (EPI == DSP_EPI_RESIDUAL && !make_tmap_bf16(&tr, R, 2, dd, sd, bd, esw, why))
+      return cudaErrorInvalidValue;
+  }
   auto kern = gemm_bf16_tc_kernel<BN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -329,7 +419,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   }
   const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
-  return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, (const __nv_bfloat16*)R,
+  return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, td, tr, (const __nv_bfloat16*)R,
                   (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ev, rm);
 }
 
