@@ -95,6 +95,10 @@ typedef struct {
   const void *ln2_w, *ln2_b, *w_qkv_t /*[3C,C]*/, *w_o_t /*[C,C]*/;
   const void *ln3_w, *ln3_b, *w_fc1 /*[4C,C]*/, *w_fc2 /*[C,4C]*/;
   float ln_eps;                                    /* 1e-5 (R3) */
+  /* NULL: the block runs three LayerNorm kernels.  Otherwise a buffer filled by
+   * dsp_st_block_prepare() from THESE weights (bf16 only): every LayerNorm is folded into
+   * the GEMM that consumes it (R30).  Stale if the weights change after preparing. */
+  const void* prepared;
 } dsp_block_weights_t;
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -144,7 +148,7 @@ int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
-#define DSP_ABI_VERSION 1
+#define DSP_ABI_VERSION 2  /* 2: dsp_block_weights_t.prepared, block preparation */
 
 /* ----------------------------------------------------------- layout (bytes) */
 
@@ -238,6 +242,22 @@ dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const vo
 dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* shape,
                                   const dsp_block_weights_t* w, const void* x_local,
                                   void* y_local, dsp_switch_impl_t impl, void* stream);
+
+/* Bytes of the prepared-weights buffer for one bf16 block of this shape (0 for f32). */
+size_t dsp_block_prepared_bytes(const dsp_shape_t* shape);
+
+/* LayerNorm folding of one block's weights (R30), a one-time step per set of
+ * weights (inference: weights are constant across the sampling steps).  With
+ * LN(x) = (x - mean) * rstd * gamma + beta (R3) and a bias-free linear W [N, K]:
+ *   LN(x) W^T = rstd * (x (W o gamma)^T - mean * u) + v,  u = (W o gamma) 1,  v = W beta,
+ * so the GEMM reads the raw activation and applies rstd, mean, u, v in its epilogue.
+ * Writes into `prepared` (device, caller-owned, 256-B aligned, >= dsp_block_prepared_bytes):
+ *   [3C, C] bf16 w_qkv_s o ln1_w | [3C, C] bf16 w_qkv_t o ln2_w | [4C, C] bf16 w_fc1 o ln3_w
+ *   (each 256-B aligned) | f32 u_s[3C] v_s[3C] u_t[3C] v_t[3C] u_1[4C] v_1[4C].
+ * Enqueued on `stream`.  Errors: NULL, UNSUPPORTED (f32, C % 8 != 0, C > 1280),
+ * WORKSPACE (prepared_bytes too small), ALIGNMENT, CUDA. */
+dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* w,
+                                  void* prepared, size_t prepared_bytes, void* stream);
 
 /* End-to-end variant through HOST buffers: copies x_local_host -> x_dev (H2D), runs
  * dsp_st_block_forward(x_dev -> y_dev), copies y_dev -> y_local_host (D2H), all on

@@ -46,7 +46,8 @@ class Shape(ctypes.Structure):
 
 class BlockWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("ln1_w", "ln1_b", "w_qkv_s", "w_o_s", "ln2_w", "ln2_b", "w_qkv_t",
-                                               "w_o_t", "ln3_w", "ln3_b", "w_fc1", "w_fc2")] + [("ln_eps", ctypes.c_float)]
+                                               "w_o_t", "ln3_w", "ln3_b", "w_fc1", "w_fc2")] + [
+        ("ln_eps", ctypes.c_float), ("prepared", ctypes.c_void_p)]
 
 
 class SwitchPlan(ctypes.Structure):
@@ -85,6 +86,7 @@ def lib() -> ctypes.CDLL:
             "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
             "dsp_st_block_forward_host": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, ctypes.c_int, vp],
+            "dsp_st_block_prepare": [vp, P(Shape), P(BlockWeights), vp, ctypes.c_size_t, vp],
             "dsp_layer_norm": [vp, ctypes.c_int, i64, i64, vp, vp, vp, ctypes.c_float, vp, vp],
             "dsp_linear": [vp, ctypes.c_int, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp, vp],
             "dsp_attention_core": [vp, ctypes.c_int, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp],
@@ -96,6 +98,8 @@ def lib() -> ctypes.CDLL:
             f.restype = ctypes.c_int
         L.dsp_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
         L.dsp_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_block_prepared_bytes.argtypes = [P(Shape)]
+        L.dsp_block_prepared_bytes.restype = ctypes.c_size_t
         L.dsp_status_str.argtypes = [ctypes.c_int]
         L.dsp_status_str.restype = ctypes.c_char_p
         L.dsp_last_error.argtypes = [vp]
@@ -144,6 +148,11 @@ def _stream(stream=None) -> int:
 
 def workspace_bytes(shape: Shape, world: int) -> int:
     return int(lib().dsp_workspace_bytes(ctypes.byref(shape), int(world)))
+
+
+def prepared_bytes(shape: Shape) -> int:
+    """Size of the LayerNorm-folded weights buffer of one bf16 block (dsp_block_prepared_bytes)."""
+    return int(lib().dsp_block_prepared_bytes(ctypes.byref(shape)))
 
 
 def switch_volume(shape: Shape, world: int):
@@ -263,7 +272,20 @@ class Context:
 
     @staticmethod
     def block_weights(W: dict, eps: float = 1e-5) -> BlockWeights:
-        return BlockWeights(*[_ptr(W[n]) for n in WEIGHT_NAMES], ctypes.c_float(eps))
+        """W: the 12 weight tensors by name, plus optionally "prepared" (from prepare_block)."""
+        prep = W.get("prepared")
+        return BlockWeights(*[_ptr(W[n]) for n in WEIGHT_NAMES], ctypes.c_float(eps),
+                            None if prep is None else _ptr(prep))
+
+    def prepare_block(self, shape, W: dict, prepared=None, stream=None) -> torch.Tensor:
+        """dsp_st_block_prepare: fold the three LayerNorms into their GEMMs' weights once.
+        Returns the prepared buffer; pass it as W["prepared"] to st_block_forward."""
+        if prepared is None:  # f32 shapes: 0 bytes -> the C call reports DSP_ERR_UNSUPPORTED
+            prepared = torch.empty(max(prepared_bytes(shape), 256), dtype=torch.uint8, device=self.device)
+        bw = self.block_weights({k: W[k] for k in WEIGHT_NAMES})
+        self._call("dsp_st_block_prepare", ctypes.byref(shape), ctypes.byref(bw), _ptr(prepared),
+                   prepared.numel() * prepared.element_size(), _stream(stream))
+        return prepared
 
     def st_block_forward(self, shape, weights, x_local, y_local, impl="nccl", stream=None):
         bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)

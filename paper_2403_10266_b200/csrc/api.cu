@@ -92,12 +92,13 @@ int64_t shard_bytes(const dsp_shape_t* s, int world) { return s->B * s->T * s->S
 int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 // Block workspace layout (bytes).  act = tok_r * C * elem.
-//   [0, act)          h: LN output (f32 path) / switch scratch
+//   [0, act)          h: LN output (unprepared path) / switch scratch
 //   [act, 5 act)      big: qkv [tok,3C] + o [tok,C] | MLP hidden [tok,4C] | switch send/recv
 //   [5 act, 6 act)    ys: S-sharded activation (N > 1)
-//   fold region       (bf16) W o gamma for w_qkv_s, w_qkv_t, w_fc1; u, v vectors; row stats
+//   stats             [tok] float2 (mean, rstd) of a LayerNorm input (prepared path)
+//   parts             [tok, C / BN] float2 per-row partials from the out-projection epilogues
 struct BlockWs {
-  int64_t act, h, big, ys, wf_s, wf_t, wf_1, uv, stats, total;
+  int64_t act, h, big, ys, stats, parts, total;
 };
 BlockWs block_ws(const dsp_shape_t* s, int world) {
   BlockWs w{};
@@ -106,13 +107,25 @@ BlockWs block_ws(const dsp_shape_t* s, int world) {
   w.h = 0;
   w.big = w.act;
   w.ys = 5 * w.act;
-  w.wf_s = align256(6 * w.act);
-  w.wf_t = w.wf_s + align256(3 * C * C * 2);
-  w.wf_1 = w.wf_t + align256(3 * C * C * 2);
-  w.uv = w.wf_1 + align256(4 * C * C * 2);
-  w.stats = w.uv + align256(2 * 10 * C * 4);
-  w.total = w.stats + align256(tok * 8) + 256;
+  w.stats = align256(6 * w.act);
+  w.parts = w.stats + align256(tok * 8);
+  w.total = w.parts + align256(tok * (C / gemm_bn_for(C)) * 8) + 256;
   return w;
+}
+
+// Prepared (LayerNorm-folded) weights of one bf16 block: W o gamma for the three
+// LayerNorm -> linear pairs and their per-output-column u = (W o gamma) 1, v = W beta.
+struct PrepLayout {
+  int64_t wf_s, wf_t, wf_1, uv, total;
+};
+PrepLayout prep_layout(int64_t C) {
+  PrepLayout p{};
+  p.wf_s = 0;
+  p.wf_t = align256(3 * C * C * 2);
+  p.wf_1 = p.wf_t + align256(3 * C * C * 2);
+  p.uv = p.wf_1 + align256(4 * C * C * 2);
+  p.total = p.uv + align256(20 * C * 4);
+  return p;
 }
 
 // bf16 tensor-core path constraints for one attention stage over sequences of length L
@@ -231,7 +244,7 @@ inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
 dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
                         const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
                         cudaStream_t st, int stage0 = -1, const EpiVec* ln = nullptr,
-                        const RemoteMap* remote = nullptr) {
+                        const RemoteMap* remote = nullptr, float2* part_out = nullptr) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
   const int sq = stage0, sa = stage0 < 0 ? -1 : stage0 + 1, sp = stage0 < 0 ? -1 : stage0 + 2;
@@ -249,8 +262,9 @@ dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int6
     mark(ctx, sa, 1, st);
     mark(ctx, sp, 0, st);
     // remote != nullptr: switch fused into this epilogue (rows stored at their owner rank)
-    e = remote ? launch_gemm_bf16_remote(o, w_o, res, *remote, tok, C, C, ctx->num_sms, st, &why)
-               : launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
+    e = remote     ? launch_gemm_bf16_remote(o, w_o, res, *remote, tok, C, C, ctx->num_sms, st, &why)
+        : part_out ? launch_gemm_bf16_res_stats(o, w_o, res, out, tok, C, C, part_out, ctx->num_sms, st, &why)
+                   : launch_gemm_bf16(o, w_o, res, out, tok, C, C, epi, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "output projection", why);
     mark(ctx, sp, 1, st);
   } else {
@@ -314,8 +328,6 @@ dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, ds
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, DSP_ERR_SHAPE, "bad rank %d / world %d", rank, world);
   dsp_ctx* c = new dsp_ctx();
   c->rank = rank; c->world = world; c->device = device; c->comm = nccl_comm;
-  const char* fl = std::getenv("DSP_FOLD_LN");
-  c->fold_ln = fl && fl[0] == '1';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
@@ -536,6 +548,9 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     if (!aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d not 16-B aligned", i);
   }
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
+  if (w->prepared && (s->C % 8 || s->C > 1280 || s->C / gemm_bn_for(s->C) > 8))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= 1280 and C / BN <= 8");
   const int N = ctx->world;
   if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
     return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
@@ -571,34 +586,42 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   cudaStream_t st = (cudaStream_t)stream;
   const float eps = w->ln_eps;
   const int64_t Tn = s->T / N, Sn = s->S / N;
-  // LayerNorm folded into the following GEMM (explicit opt-in, DSP_FOLD_LN=1).  Measured on B200
-  // at the single-block config it is slower than LN + plain GEMM (809 vs 754 us: the folded
-  // epilogue lengthens the QKV/FC1 GEMMs more than the removed LN traffic saves), so the
-  // default keeps the LayerNorm kernel.  Row-stats kernel holds rows of <= 1280 channels.
-  const bool fold = ctx->fold_ln && s->dtype == DSP_BF16 && C % 8 == 0 && C <= 1280;
-  float* uv = reinterpret_cast<float*>(ws + L.uv);
+  // Prepared weights (dsp_st_block_prepare): every LayerNorm is folded into the GEMM that
+  // consumes it.  LN1: row statistics of x; LN2 (N == 1) and LN3: combined in the consuming
+  // epilogue from per-row partials the out-projection epilogues write; LN2 at N > 1: row
+  // statistics after the switch (the rows moved).
+  const bool fold = w->prepared != nullptr;
+  const PrepLayout P = prep_layout(C);
+  const uint8_t* prep = static_cast<const uint8_t*>(w->prepared);
+  const float* uv = fold ? reinterpret_cast<const float*>(prep + P.uv) : nullptr;
   float2* stats = reinterpret_cast<float2*>(ws + L.stats);
-  EpiVec ev1{stats, uv, uv + 3 * C}, ev2{stats, uv + 6 * C, uv + 9 * C}, ev3{stats, uv + 12 * C, uv + 16 * C};
-  void* wf_s = ws + L.wf_s;
-  void* wf_t = ws + L.wf_t;
-  void* wf_1 = ws + L.wf_1;
-  // a1: LN1 (folded: row statistics of x + LN-folded weights of all three LN->linear pairs)
-  mark(ctx, DSP_STAGE_LN1, 0, st);
+  float2* parts = reinterpret_cast<float2*>(ws + L.parts);
+  const int nparts = (int)(C / gemm_bn_for(C));
+  EpiVec ev1{}, ev2{}, ev3{};
   if (fold) {
-    LnFold jobs[3] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, wf_s, uv, uv + 3 * C, 3 * C},
-                      {w->w_qkv_t, w->ln2_w, w->ln2_b, wf_t, uv + 6 * C, uv + 9 * C, 3 * C},
-                      {w->w_fc1, w->ln3_w, w->ln3_b, wf_1, uv + 12 * C, uv + 16 * C, 4 * C}};
-    DSP_CUDA(ctx, launch_fold_ln_weights(3, jobs, C, st), "fold LN weights");
-    DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
-    ctx->launches += 2;
-  } else {
-    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
-    ctx->launches += 1;
+    ev1.row_stats = stats; ev1.col_u = uv; ev1.col_v = uv + 3 * C;
+    ev2.col_u = uv + 6 * C; ev2.col_v = uv + 9 * C;
+    ev3.col_u = uv + 12 * C; ev3.col_v = uv + 16 * C;
+    ev3.part_in = parts; ev3.nparts_in = nparts; ev3.part_cnt = (int)(C / nparts); ev3.eps = eps;
+    if (N == 1) {
+      ev2.part_in = parts; ev2.nparts_in = nparts; ev2.part_cnt = (int)(C / nparts); ev2.eps = eps;
+    } else {
+      ev2.row_stats = stats;
+    }
   }
+  const void* wf_s = fold ? prep + P.wf_s : nullptr;
+  const void* wf_t = fold ? prep + P.wf_t : nullptr;
+  const void* wf_1 = fold ? prep + P.wf_1 : nullptr;
+  // a1: LN1 (prepared: row statistics of x only)
+  mark(ctx, DSP_STAGE_LN1, 0, st);
+  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
+  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
+  ctx->launches += 1;
   mark(ctx, DSP_STAGE_LN1, 1, st);
-  // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y
+  // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y (N == 1 prepared: + LN2 partials)
   DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, fold ? x : h, fold ? wf_s : w->w_qkv_s, w->w_o_s, x, y, qkv, o,
-                     st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr, fused ? &rm_ts : nullptr));
+                     st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr, fused ? &rm_ts : nullptr,
+                     fold && N == 1 ? parts : nullptr));
   // a5: switch T -> S (fused: the out-projection already stored every row at its owner)
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
@@ -611,26 +634,31 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     cur = ys;
   }
   mark(ctx, DSP_STAGE_SWITCH_TS, 1, st);
-  // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place)
+  // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place; prepared: + LN3 partials)
   mark(ctx, DSP_STAGE_LN2, 0, st);
-  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN2 stats");
-  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
-  ctx->launches += 1;
+  if (!fold) {
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
+    ctx->launches += 1;
+  } else if (N > 1) {
+    DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN2 stats");
+    ctx->launches += 1;
+  }
   mark(ctx, DSP_STAGE_LN2, 1, st);
   DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, fold ? cur : h, fold ? wf_t : w->w_qkv_t, w->w_o_t, cur, cur, qkv,
-                     o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr));
+                     o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr, nullptr, fold ? parts : nullptr));
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
   mark(ctx, DSP_STAGE_LN3, 0, st);
-  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN3 stats");
-  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
-  ctx->launches += 1;
+  if (!fold) {
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
+    ctx->launches += 1;
+  }
   mark(ctx, DSP_STAGE_LN3, 1, st);
   mark(ctx, DSP_STAGE_FC1, 0, st);
   if (fold) {
     std::string why;
     cudaError_t e2 = launch_gemm_bf16_ln(cur, wf_1, ev3, big, tok, 4 * C, C, true, ctx->num_sms, st, &why);
     if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "FC1 (LN3 folded)", why);
-    ctx->launches += 1;
+    if (tok > 0) ctx->launches += 1;
   } else {
     DSP_TRY(linear(ctx, s->dtype, tok, 4 * C, C, h, w->w_fc1, nullptr, DSP_EPI_GELU, big, st));
   }
@@ -654,6 +682,35 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
   }
   mark(ctx, DSP_STAGE_SWITCH_ST, 1, st);
+  return DSP_OK;
+}
+
+size_t dsp_block_prepared_bytes(const dsp_shape_t* s) {
+  if (!s || s->C < 1 || s->dtype != DSP_BF16) return 0;
+  return (size_t)prep_layout(s->C).total;
+}
+
+dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, void* prep,
+                                  size_t prep_bytes, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  if (!w || !prep) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
+  const int64_t C = s->C;
+  if (C % 8 || C > 1280) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0 and C <= 1280 (C=%lld)", (long long)C);
+  const PrepLayout P = prep_layout(C);
+  if (prep_bytes < (size_t)P.total) return fail(ctx, DSP_ERR_WORKSPACE, "prepared buffer needs %lld bytes", (long long)P.total);
+  if (reinterpret_cast<uintptr_t>(prep) % 256) return fail(ctx, DSP_ERR_ALIGNMENT, "prepared buffer must be 256-B aligned");
+  const void* wp[9] = {w->ln1_w, w->ln1_b, w->w_qkv_s, w->ln2_w, w->ln2_b, w->w_qkv_t, w->ln3_w, w->ln3_b, w->w_fc1};
+  for (int i = 0; i < 9; ++i)
+    if (!wp[i]) return fail(ctx, DSP_ERR_NULL, "weight %d is NULL", i);
+  uint8_t* p = static_cast<uint8_t*>(prep);
+  float* uv = reinterpret_cast<float*>(p + P.uv);
+  LnFold jobs[3] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, p + P.wf_s, uv, uv + 3 * C, 3 * C},
+                    {w->w_qkv_t, w->ln2_w, w->ln2_b, p + P.wf_t, uv + 6 * C, uv + 9 * C, 3 * C},
+                    {w->w_fc1, w->ln3_w, w->ln3_b, p + P.wf_1, uv + 12 * C, uv + 16 * C, 4 * C}};
+  DSP_CUDA(ctx, launch_fold_ln_weights(3, jobs, C, (cudaStream_t)stream), "fold LN weights");
+  ctx->launches += 1;
   return DSP_OK;
 }
 

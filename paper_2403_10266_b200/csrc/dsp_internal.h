@@ -83,11 +83,23 @@ struct RemoteMap {
 };
 cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,
                                     int64_t N, int64_t K, int num_sms, cudaStream_t st, std::string* why);
+// Epilogue vectors.  LN-folded GEMM (EPI_LN*): per-row statistics either as (mean, rstd) in
+// row_stats, or (row_stats == nullptr) combined in the epilogue from part_in: nparts_in
+// per-row partials (mean_p, M2_p) over part_cnt columns each, written by the residual
+// epilogue of the GEMM that produced the rows (part_out, one partial per BN-column tile).
 struct EpiVec {
   const float2* row_stats;  // [M] (mean, rstd)
   const float* col_u;       // [N]
   const float* col_v;       // [N]
+  const float2* part_in;    // [M, nparts_in] (mean_p, M2_p)
+  int nparts_in, part_cnt;
+  float eps;
+  float2* part_out;         // residual epilogue: [M, N / BN] partials of the stored (bf16) rows
 };
+// BN (output-tile width) the GEMM dispatch picks for N output columns
+int gemm_bn_for(int64_t N);
+cudaError_t launch_gemm_bf16_res_stats(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                                       int64_t K, float2* part_out, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,
                                 int64_t K, bool gelu, int num_sms, cudaStream_t st, std::string* why);
 
@@ -145,7 +157,6 @@ struct dsp_ctx {
   int64_t launches = 0;            // own kernels launched (instrumentation)
   void* stage_events[2 * DSP_NUM_STAGES] = {};
   bool has_stage_events = false;
-  bool fold_ln = false;  // DSP_FOLD_LN=1: LayerNorm folded into the following GEMM
   uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
   std::string last_error;
 };

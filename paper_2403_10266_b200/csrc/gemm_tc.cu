@@ -169,12 +169,13 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp >= 4 && (EPI == DSP_EPI_NONE || EPI == DSP_EPI_RESIDUAL || EPI == DSP_EPI_GELU)) {
+  } else if (warp >= 4 && EPI != EPI_RES_REMOTE) {
     // Bulk-tensor epilogue: the residual tile arrives by TMA into the staging tile sE (issued
     // by this warpgroup as soon as the previous tile's store has been read out of sE), each
     // thread adds its accumulator row in place (SW128 layout: 16-B chunk c of row r at
     // c ^ (r & 7)), and one thread TMA-stores the tile (rows >= M are clipped).
     constexpr bool kRes = EPI == DSP_EPI_RESIDUAL;
+    constexpr bool kLn = EPI == EPI_LN || EPI == EPI_LN_GELU;
     const int q = warp & 3;
     const int row = q * 32 + lane_id();
     const bool elected = threadIdx.x == 128;
@@ -191,14 +192,49 @@ __global__ void __launch_bounds__(256, 1)
       const int acc = it & 1;
       const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
       const int n0 = (tile % tiles_n) * BN;
+      // LayerNorm folded into this GEMM: per-row (mean, rstd) of the raw input row; the tile's
+      // per-column u, v staged in smem (one copy per accumulator: the other copy may still be
+      // read by a slower warp of the previous tile)
+      float2 rstat = make_float2(0.f, 0.f);
+      float* eu = evec + acc * 2 * BN;
+      if (kLn) {
+        if (m0 + row < M) {
+          if (ev.row_stats) {
+            rstat = ev.row_stats[m0 + row];
+          } else {  // Chan et al. combination of equal-count partials (mean_p, M2_p), <= 8 of them
+            const float2* pp = ev.part_in + (size_t)(m0 + row) * ev.nparts_in;
+            float2 pv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pv[i] = i < ev.nparts_in ? pp[i] : make_float2(0.f, 0.f);
+            float mean = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mean += pv[i].x;
+            mean /= ev.nparts_in;
+            float m2 = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float d = pv[i].x - mean;
+              if (i < ev.nparts_in) m2 += pv[i].y + ev.part_cnt * d * d;
+            }
+            rstat = make_float2(mean, rsqrtf(m2 / (float)(ev.nparts_in * ev.part_cnt) + ev.eps));
+          }
+        }
+        for (int i = threadIdx.x - 128; i < BN; i += 128) {
+          st_shared_f32(smem_u32(eu + i), ev.col_u[n0 + i]);
+          st_shared_f32(smem_u32(eu + BN + i), ev.col_v[n0 + i]);
+        }
+      }
       if (kRes) {
         mbar_wait(r_full, it & 1);
-      } else if (it > 0) {  // the previous tile's store must have been read out of sE
-        if (elected) bulk_wait_group_read0();
+      } else if (it > 0 || kLn) {  // the previous tile's store must have been read out of sE
+        if (elected && it > 0) bulk_wait_group_read0();
         named_bar_sync(1, 128);
       }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
+      // row statistics of the stored (bf16-rounded) values, shifted by the first one
+      const bool kStats = kRes && ev.part_out != nullptr;
+      float2 sh = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
@@ -221,10 +257,41 @@ __global__ void __launch_bounds__(256, 1)
           } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
+          } else if (kLn) {
+            // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, broadcast loads)
+            const uint32_t ua = smem_u32(eu + c * 32 + 8 * u), va = smem_u32(eu + BN + c * 32 + 8 * u);
+            const float2 nm = make_float2(-rstat.x, -rstat.x), rs = make_float2(rstat.y, rstat.y);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float4 uu = ld_shared_f32x4(ua + 16 * h), vv = ld_shared_f32x4(va + 16 * h);
+              const float2 y0 = ffma2(rs, ffma2(nm, make_float2(uu.x, uu.y), make_float2(f[4 * h], f[4 * h + 1])),
+                                      make_float2(vv.x, vv.y));
+              const float2 y1 = ffma2(rs, ffma2(nm, make_float2(uu.z, uu.w), make_float2(f[4 * h + 2], f[4 * h + 3])),
+                                      make_float2(vv.z, vv.w));
+              f[4 * h] = y0.x; f[4 * h + 1] = y0.y; f[4 * h + 2] = y1.x; f[4 * h + 3] = y1.y;
+              if (EPI == EPI_LN_GELU) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) f[4 * h + t] = gelu_tanh_f(f[4 * h + t]);
+              }
+            }
           }
           st_shared_v4(addr, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
                        pack_bf16x2(f[6], f[7]));
+          if (kStats) {  // shifted sums of the fp32 row values (R30), packed pairs
+            if (c == 0 && u == 0) sh = make_float2(-f[0], -f[0]);
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 d = fadd2(make_float2(f[i], f[i + 1]), sh);
+              s1 = fadd2(s1, d);
+              s2 = ffma2(d, d, s2);
+            }
+          }
         }
+      }
+      if (kStats && m0 + row < M) {
+        const float a = s1.x + s1.y, mp = a * (1.f / BN);
+        ev.part_out[(size_t)(m0 + row) * tiles_n + (tile % tiles_n)] =
+            make_float2(mp - sh.x, fmaxf(s2.x + s2.y - a * mp, 0.f));
       }
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next
@@ -405,7 +472,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
     return cudaErrorInvalidValue;
   td = ta;
   tr = ta;
-  if (EPI == DSP_EPI_NONE || EPI == DSP_EPI_RESIDUAL || EPI == DSP_EPI_GELU) {
+  if (EPI != EPI_RES_REMOTE) {
     if (!make_tmap_bf16(&td, D, 2, dd, sd, bd, esw, why)) return cudaErrorInvalidValue;
     if (EPI == DSP_EPI_RESIDUAL && !make_tmap_bf16(&tr, R, 2, dd, sd, bd, esw, why))
       return cudaErrorInvalidValue;
@@ -450,6 +517,18 @@ cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev,
   if (M == 0) return cudaSuccess;
   if (gelu) return dispatch_bn<EPI_LN_GELU>(A, Wf, nullptr, D, M, N, K, num_sms, st, why, ev);
   return dispatch_bn<EPI_LN>(A, Wf, nullptr, D, M, N, K, num_sms, st, why, ev);
+}
+
+int gemm_bn_for(int64_t N) {
+  return N % 256 == 0 ? 256 : N % 192 == 0 ? 192 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 32;
+}
+
+cudaError_t launch_gemm_bf16_res_stats(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                                       int64_t K, float2* part_out, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  EpiVec ev{};
+  ev.part_out = part_out;
+  return dispatch_bn<DSP_EPI_RESIDUAL>(A, W, R, D, M, N, K, num_sms, st, why, ev);
 }
 
 cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,

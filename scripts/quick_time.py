@@ -17,6 +17,9 @@ def t(fn, n=20):
 tok = 16384; C = 1152
 us = t(lambda: ctx.st_block_forward(shape, W, X, Y))
 print(f"block: {us:.1f} us  -> {tok/us*1e6/1e6:.2f} M tok/s; roofline 462 us -> frac {462/us:.3f}")
+WP = dict(W); WP["prepared"] = ctx.prepare_block(shape, W)
+us = t(lambda: ctx.st_block_forward(shape, WP, X, Y))
+print(f"block prepared: {us:.1f} us  -> {tok/us*1e6/1e6:.2f} M tok/s; roofline 462 us -> frac {462/us:.3f}")
 H = torch.empty(tok, C, dtype=torch.bfloat16, device="cuda"); QKV = torch.empty(tok, 3*C, dtype=torch.bfloat16, device="cuda")
 O = torch.empty(tok, C, dtype=torch.bfloat16, device="cuda"); HID = torch.empty(tok, 4*C, dtype=torch.bfloat16, device="cuda")
 for name, fn, fl in [("qkv gemm", lambda: ctx.linear(X, W["w_qkv_s"], QKV), 2*tok*3*C*C),

@@ -28,14 +28,17 @@ def _setup(sh: synth.BlockShape, seed=7, kappa=1.0):
     return xs, Ws
 
 
-def _run_block_n1(sh, xs, Ws):
+def _run_block_n1(sh, xs, Ws, prepared=False):
     m = dsp()
     ctx = m.Context()
     shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
     ctx.ensure_workspace(m.workspace_bytes(shape, 1))
     X = to_dev(xs, sh.dtype)
     Y = torch.empty_like(X)
-    ctx.st_block_forward(shape, weights_dev(Ws, sh.dtype), X, Y)
+    W = weights_dev(Ws, sh.dtype)
+    if prepared:
+        W["prepared"] = ctx.prepare_block(shape, W)
+    ctx.st_block_forward(shape, W, X, Y)
     torch.cuda.synchronize()
     return Y
 
@@ -55,6 +58,18 @@ def test_block_tiny_f32_check_path():
 def test_block_bf16_full_oracle(sh):
     xs, Ws = _setup(sh)
     Y = _run_block_n1(sh, xs, Ws)
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
+    print(assert_block_close(to_f64(Y), ref))
+
+
+@pytest.mark.parametrize("sh", [synth.BlockShape(1, 16, 256, 1152, 16, "bf16"),
+                                synth.BlockShape(2, 8, 128, 256, 4, "bf16")])
+def test_block_bf16_prepared_layernorm_folded(sh):
+    """Prepared weights (dsp_st_block_prepare, R30): every LayerNorm folded into the GEMM that
+    consumes it -- LN1 from row statistics, LN2/LN3 from the out-projection epilogues' per-row
+    partials -- against the same oracle block."""
+    xs, Ws = _setup(sh)
+    Y = _run_block_n1(sh, xs, Ws, prepared=True)
     ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
     print(assert_block_close(to_f64(Y), ref))
 
@@ -182,3 +197,29 @@ def test_block_p2p_virtual_ranks_n_invariant(N, impl):
     g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl=impl))
     got = np.concatenate([bits16(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
+
+
+@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("impl", ["p2p", "fused"])
+def test_block_prepared_virtual_ranks_vs_oracle(N, impl):
+    """Prepared (LayerNorm-folded) block over N virtual ranks: LN2 statistics are recomputed
+    after the switch (rows moved), LN3 from partials; checked against the oracle."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, Ws = _setup(sh)
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    W = weights_dev(Ws, "bf16")
+    W["prepared"] = g.ctx[0].prepare_block(shape, W)
+    torch.cuda.synchronize()
+    xsh = osw.split(xs, osw.DIM_T, N)
+    X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl=impl))
+    got = np.concatenate([to_f64(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    print(assert_block_close(got, ref))
