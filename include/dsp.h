@@ -139,7 +139,9 @@ typedef enum {
 } dsp_stage_t;
 /* events: HOST array of 2*DSP_NUM_STAGES cudaEvent_t (caller-owned) or NULL to disable.
  * When set, dsp_st_block_forward records events[2*i] / events[2*i+1] on its stream
- * around stage i (both recorded even when a stage is skipped, e.g. switches at N=1). */
+ * around stage i (both recorded even when a stage is skipped, e.g. switches at N=1).
+ * NULL entries are skipped, so a caller can time one stage per pass: every event record
+ * is a point where the next kernel's programmatic dependent launch cannot overlap. */
 dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n_events);
 /* Number of this library's own kernels launched through ctx since creation (NCCL kernels
  * and cudaMemcpy excluded).  HOST-ONLY. */

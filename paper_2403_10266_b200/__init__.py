@@ -239,14 +239,16 @@ class Context:
         return int(lib().dsp_ctx_launch_count(self.handle))
 
     def set_stage_events(self, events):
-        """events: list of 2*len(STAGES) torch.cuda.Event(enable_timing=True), or None."""
+        """events: list of 2*len(STAGES) torch.cuda.Event(enable_timing=True) (entries may be None:
+        that boundary is not recorded), or None to switch stage events off."""
         if events is None:
             _check(lib().dsp_ctx_set_stage_events(self.handle, None, 0), self.handle)
             self._stage_events = None
             return
         for e in events:
-            e.record()  # materialise the underlying cudaEvent_t
-        arr = (ctypes.c_void_p * len(events))(*[e.cuda_event for e in events])
+            if e is not None:
+                e.record()  # materialise the underlying cudaEvent_t
+        arr = (ctypes.c_void_p * len(events))(*[None if e is None else e.cuda_event for e in events])
         self._stage_events = (events, arr)
         _check(lib().dsp_ctx_set_stage_events(self.handle, arr, len(events)), self.handle)
 

@@ -236,7 +236,8 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
 }
 
 inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
-  if (ctx->has_stage_events && stage >= 0) cudaEventRecord((cudaEvent_t)ctx->stage_events[2 * stage + end], st);
+  if (ctx->has_stage_events && stage >= 0 && ctx->stage_events[2 * stage + end])
+    cudaEventRecord((cudaEvent_t)ctx->stage_events[2 * stage + end], st);
 }
 
 // one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C].
@@ -549,8 +550,8 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   }
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
   if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
-  if (w->prepared && (s->C % 8 || s->C > 1280 || s->C / gemm_bn_for(s->C) > 8))
-    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= 1280 and C / BN <= 8");
+  if (w->prepared && (s->C % 8 || s->C > 1280 || s->C / gemm_bn_for(s->C) > kMaxParts))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= 1280 and C / BN <= %d", kMaxParts);
   const int N = ctx->world;
   if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
     return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);

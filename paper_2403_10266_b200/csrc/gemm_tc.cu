@@ -47,7 +47,9 @@ struct GemmCfg {
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int E_BYTES = BN * 256;  // epilogue staging: 128 rows x BN bf16 as BN/EB boxes
-  static constexpr int EB = BN < 64 ? BN : 64;          // box width (columns): SW128 at 64, SW64 at 32
+  // store/residual box width (columns): SW128 at 64, SW64 at 32, SW32 at 16 (BN = 144)
+  static constexpr int EB = BN % 64 == 0 ? 64 : BN % 32 == 0 ? 32 : 16;
+  static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
   static constexpr int STAGES = (216 * 1024 - E_BYTES) / STAGE_BYTES > 8 ? 8 : (216 * 1024 - E_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
@@ -201,18 +203,18 @@ __global__ void __launch_bounds__(256, 1)
         if (m0 + row < M) {
           if (ev.row_stats) {
             rstat = ev.row_stats[m0 + row];
-          } else {  // Chan et al. combination of equal-count partials (mean_p, M2_p), <= 8 of them
+          } else {  // Chan et al. combination of equal-count partials (mean_p, M2_p), <= kMaxParts
             const float2* pp = ev.part_in + (size_t)(m0 + row) * ev.nparts_in;
-            float2 pv[8];
+            float2 pv[kMaxParts];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) pv[i] = i < ev.nparts_in ? pp[i] : make_float2(0.f, 0.f);
+            for (int i = 0; i < kMaxParts; ++i) pv[i] = i < ev.nparts_in ? pp[i] : make_float2(0.f, 0.f);
             float mean = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) mean += pv[i].x;
+            for (int i = 0; i < kMaxParts; ++i) mean += pv[i].x;
             mean /= ev.nparts_in;
             float m2 = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < kMaxParts; ++i) {
               const float d = pv[i].x - mean;
               if (i < ev.nparts_in) m2 += pv[i].y + ev.part_cnt * d * d;
             }
@@ -235,17 +237,22 @@ __global__ void __launch_bounds__(256, 1)
       // row statistics of the stored (bf16-rounded) values, shifted by the first one
       const bool kStats = kRes && ev.part_out != nullptr;
       float2 sh = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
+      constexpr int CW = Cfg::CW;
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+      for (int c = 0; c < BN / CW; ++c) {
+        uint32_t v[CW];
+        if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
+        else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
         tmem_ld_wait();
-        // chunk c (32 columns = 4 x 16 B) of this row inside box c / (EB / 32)
-        const uint32_t line = e0 + (c / (Cfg::EB / 32)) * Cfg::E_BOX + row * (Cfg::EB * 2);
+        // chunk c (CW columns = CW/8 x 16 B) of this row inside box (c * CW) / EB
+        const int col0 = c * CW;
+        const uint32_t line = e0 + (col0 / Cfg::EB) * Cfg::E_BOX + row * (Cfg::EB * 2);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = (c % (Cfg::EB / 32)) * 4 + u;
-          const uint32_t addr = line + ((Cfg::EB == 64 ? (j ^ (row & 7)) : (j ^ ((row >> 1) & 3))) << 4);
+        for (int u = 0; u < CW / 8; ++u) {
+          const int j = (col0 % Cfg::EB) / 8 + u;
+          const uint32_t addr =
+              line + ((Cfg::EB == 64 ? (j ^ (row & 7)) : Cfg::EB == 32 ? (j ^ ((row >> 1) & 3)) : (j ^ ((row >> 2) & 1)))
+                      << 4);
           float f[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * u + i]);
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
           } else if (kLn) {
             // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, broadcast loads)
-            const uint32_t ua = smem_u32(eu + c * 32 + 8 * u), va = smem_u32(eu + BN + c * 32 + 8 * u);
+            const uint32_t ua = smem_u32(eu + col0 + 8 * u), va = smem_u32(eu + BN + col0 + 8 * u);
             const float2 nm = make_float2(-rstat.x, -rstat.x), rs = make_float2(rstat.y, rstat.y);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -358,19 +365,21 @@ __global__ void __launch_bounds__(256, 1)
       }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
+      constexpr int CW = Cfg::CW;
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+      for (int c = 0; c < BN / CW; ++c) {
+        uint32_t v[CW];
+        if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
+        else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
         tmem_ld_wait();
         if (live) {
-          float f[32];
+          float f[CW];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          for (int i = 0; i < CW; ++i) f[i] = __uint_as_float(v[i]);
           if (kRes) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint4 r4 = rv[c * 4 + j];
+            for (int j = 0; j < CW / 8; ++j) {
+              const uint4 r4 = rv[c * (CW / 8) + j];
               f[8 * j + 0] += bf16lo(r4.x);
               f[8 * j + 1] += bf16hi(r4.x);
               f[8 * j + 2] += bf16lo(r4.y);
@@ -382,13 +391,13 @@ __global__ void __launch_bounds__(256, 1)
             }
           } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = gelu_tanh_f(f[i]);
+            for (int i = 0; i < CW; ++i) f[i] = gelu_tanh_f(f[i]);
           } else if (EPI == EPI_LN || EPI == EPI_LN_GELU) {
             // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, warp-uniform loads)
-            const float4* u4 = reinterpret_cast<const float4*>(eu + c * 32);
-            const float4* v4 = reinterpret_cast<const float4*>(eu + BN + c * 32);
+            const float4* u4 = reinterpret_cast<const float4*>(eu + c * CW);
+            const float4* v4 = reinterpret_cast<const float4*>(eu + BN + c * CW);
 #pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4) {
+            for (int q4 = 0; q4 < CW / 4; ++q4) {
               const float4 uu = u4[q4], vv = v4[q4];
               const float us[4] = {uu.x, uu.y, uu.z, uu.w}, vs[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
@@ -399,9 +408,9 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          uint4* dp = reinterpret_cast<uint4*>(drow + c * 32);
+          uint4* dp = reinterpret_cast<uint4*>(drow + c * CW);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < CW / 8; ++j) {
             dp[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
                                pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
           }
@@ -466,7 +475,9 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
   uint64_t dd[2] = {(uint64_t)N, (uint64_t)M}, sd[1] = {(uint64_t)N * 2};
   uint32_t ba[2] = {BK, BM}, bw[2] = {BK, Cfg::BNH}, bd[2] = {Cfg::EB, BM};
-  const CUtensorMapSwizzle esw = Cfg::EB == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapSwizzle esw = Cfg::EB == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : Cfg::EB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                 : CU_TENSOR_MAP_SWIZZLE_32B;
   if (!make_tmap_bf16(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, why) ||
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
@@ -493,23 +504,21 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
 template <int EPI>
 static cudaError_t dispatch_bn(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
                                int64_t K, int num_sms, cudaStream_t st, std::string* why,
-                               const EpiVec& ev = EpiVec{}) {
-  if (N % 256 == 0) return run_gemm<256, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
-  if (N % 192 == 0) return run_gemm<192, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
-  if (N % 128 == 0) return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
-  if (N % 64 == 0) return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
-  return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev);
+                               const EpiVec& ev = EpiVec{}, const RemoteMap& rm = RemoteMap{}) {
+  switch (gemm_bn_for(N)) {
+    case 256: return run_gemm<256, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+    case 192: return run_gemm<192, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+    case 144: return run_gemm<144, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+    case 128: return run_gemm<128, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+    case 64: return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+    default: return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
+  }
 }
 
 cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,
                                     int64_t N, int64_t K, int num_sms, cudaStream_t st, std::string* why) {
   if (M == 0) return cudaSuccess;
-  const EpiVec ev{};
-  if (N % 256 == 0) return run_gemm<256, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
-  if (N % 192 == 0) return run_gemm<192, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
-  if (N % 128 == 0) return run_gemm<128, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
-  if (N % 64 == 0) return run_gemm<64, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
-  return run_gemm<32, EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, ev, rm);
+  return dispatch_bn<EPI_RES_REMOTE>(A, W, R, nullptr, M, N, K, num_sms, st, why, EpiVec{}, rm);
 }
 
 cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,
@@ -520,7 +529,17 @@ cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev,
 }
 
 int gemm_bn_for(int64_t N) {
-  return N % 256 == 0 ? 256 : N % 192 == 0 ? 192 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 32;
+#ifdef DSP_GEMM_BN_1152
+  if (N == 1152) return DSP_GEMM_BN_1152;  // A/B experiments only
+#endif
+  // A function of N only (never of M): the tile width fixes how many LayerNorm partials a
+  // residual epilogue writes, and the block must not depend on the shard size (N-invariance).
+  // 144-wide tiles (8 column tiles at C = 1152, 6.9 waves of 74 pairs instead of 5.2 -> 6 at
+  // 192) were measured slower on B200 (FC2 134 vs 128 us): the mainloop is bound by the bytes
+  // staged per k-block, which do not shrink with BN (A is 16 KB either way).  Selectable with
+  // -DDSP_GEMM_BN_1152=144 for experiments.
+  if (N % 256 == 0) return 256;
+  return N % 192 == 0 ? 192 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 32;
 }
 
 cudaError_t launch_gemm_bf16_res_stats(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,

@@ -275,6 +275,9 @@ __device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // per-warpgroup register budget (all 4 warps of the warpgroup execute it)
 template <int N>
@@ -294,6 +297,32 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// three-input max (sm_100 FMNMX3): a 128-value row max in 64 instructions
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+template <int N>
+__device__ __forceinline__ float max_tree3(const float* x) {
+  if constexpr (N == 1) {
+    return x[0];
+  } else if constexpr (N == 2) {
+    return fmaxf(x[0], x[1]);
+  } else {
+    constexpr int M = N / 3, R = N % 3;
+    float y[M + R];
+#pragma unroll
+    for (int i = 0; i < M; ++i) y[i] = fmax3f(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+#pragma unroll
+    for (int i = 0; i < R; ++i) y[M + i] = x[3 * M + i];
+    return max_tree3<M + R>(y);
+  }
+}
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;

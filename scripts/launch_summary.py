@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (gpu__time_duration per launch) into per-kernel shares of
 the ST-block step: only this library's kernels (gemm / fmha / layer_norm / run_copy / p2p)."""
-import csv, io, json, sys
+import csv, io, json, re, sys
 from collections import defaultdict
 
 def load(path):
@@ -8,13 +8,21 @@ def load(path):
     txt = txt[txt.index('"ID"'):]
     return list(csv.DictReader(io.StringIO(txt)))
 
+EPI = {"0": "plain", "1": "+residual", "2": "+GELU", "3": "LN folded", "4": "LN folded+GELU", "5": "+residual, remote rows"}
+ROLE = {"3": "QKV_S/QKV_T", "1": "PROJ_S/PROJ_T/FC2", "4": "FC1", "2": "FC1 (raw weights)", "0": "QKV (raw weights)",
+        "5": "PROJ_S/FC2 (fused switch)"}
+
+
 def kind(name):
-    for k in ("gemm_bf16_tc_kernel<192, 0>", "gemm_bf16_tc_kernel<192, 1>", "gemm_bf16_tc_kernel<256, 2>",
-              "gemm_bf16_tc_kernel<256, 0>", "fmha_pair_kernel", "fmha_bf16_tc_kernel", "layer_norm", "run_copy",
-              "p2p_barrier", "gemm_bf16_tc_kernel"):
+    m = re.search(r"gemm_bf16_tc_kernel<(\d+), (\d+)>", name)
+    if m:
+        return f"gemm BN={m.group(1)} {EPI.get(m.group(2), m.group(2))} [{ROLE.get(m.group(2), '?')}]"
+    for k in ("fmha_pair_kernel", "fmha_bf16_tc_kernel", "row_stats", "layer_norm", "run_copy", "p2p_barrier",
+              "p2p_put", "fold_ln_weights"):
         if k in name:
             return k
     return None
+
 
 rows = [r for r in load(sys.argv[1]) if r["Metric Name"] == "gpu__time_duration.sum"]
 per = defaultdict(list)

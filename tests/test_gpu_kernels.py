@@ -28,7 +28,8 @@ def _rand_bf16(shape, seed, scale=1.0, tid=1):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 192, 64), (300, 1152, 1152), (16384, 3456, 1152), (2048, 4608, 1152),
-                                   (2048, 1152, 4608), (77, 96, 72), (256, 32, 16), (1000, 256, 520)])
+                                   (2048, 1152, 4608), (77, 96, 72), (256, 32, 16), (1000, 256, 520),
+                                   (333, 288, 200)])
 @pytest.mark.parametrize("epi", [0, 1, 2])
 def test_linear_bf16(ctx, M, N, K, epi):
     import paper_2403_10266_b200 as dsp
