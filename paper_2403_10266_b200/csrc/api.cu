@@ -236,8 +236,14 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
 }
 
 inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
-  if (ctx->has_stage_events && stage >= 0 && ctx->stage_events[2 * stage + end])
-    cudaEventRecord((cudaEvent_t)ctx->stage_events[2 * stage + end], st);
+  if (ctx->has_stage_events && stage >= 0 && ctx->stage_events[2 * stage + end]) {
+    // inside a stream capture the record becomes an external event node of the graph, so a
+    // replayed graph timestamps the stage boundary
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    cudaEventRecordWithFlags((cudaEvent_t)ctx->stage_events[2 * stage + end], st,
+                             cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
+  }
 }
 
 // one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C].

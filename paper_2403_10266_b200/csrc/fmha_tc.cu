@@ -717,12 +717,13 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
 // ---------------------------------------------------------------------------------
 // Long sequences (L % 256 == 0): one CTA per SM works on TWO 128-row query tiles
 // ("slots") of the same (sequence, head), sharing one K/V stream (2-stage ring).  TMEM
-// (512 columns) holds S0, S1 (128 columns each) and O0, O1.  Each slot's softmax is split
-// over two warpgroups, one per 64-key half of the tile (row max exchanged through smem
-// and a named barrier), so every SMSP has four softmax warps to keep the MUFU (exp2)
-// pipe busy, while the tensor pipe runs S_{j+1} of both slots, then both P_j V_j.
+// (512 columns) holds S0, S1 (128 columns each) and O0, O1.  One softmax warpgroup per slot,
+// thread = query row with the whole 128-key S row in registers; the tensor pipe runs
+// S_{j+1} of a slot as soon as that slot holds S_j in registers, then both P_j V_j.
+// ONES (Dh <= DP - 8): the row sums come from the tensor core (R31), see softmax_tile_full.
 //   warp 0       TMA producer        warp 1       MMA issuer + TMEM allocator
-//   warps 4-11   slot 0 (halves 0,1) warps 12-19  slot 1 (halves 0,1)
+//   warp 2       V patcher (ONES)    warp 3       idle
+//   warps 4-7    slot 0 softmax      warps 8-11   slot 1 softmax
 template <int NA, int RB>
 struct PairCfg {
   using Base = FmhaCfg<NA, RB>;
