@@ -272,6 +272,23 @@ dsp_status_t dsp_st_block_forward_host(dsp_ctx_t ctx, const dsp_shape_t* shape,
                                        void* x_dev, void* y_dev,
                                        dsp_switch_impl_t impl, void* stream);
 
+/* Pipelined end-to-end path for a stream of n independent inputs (serving): for each i,
+ * H2D x_local_host[i] -> x_dev[i % 2] on a context-owned copy-in stream, the block on `stream`
+ * (x_dev[i % 2] -> y_dev[i % 2]), D2H y_dev[i % 2] -> y_local_host[i] on a context-owned
+ * copy-out stream.  Events order every reuse of a staging buffer, so the copies of steps
+ * i + 1 and i - 1 overlap the block of step i (PCIe is full duplex).  x_dev[2], y_dev[2]:
+ * HOST arrays of four distinct, non-overlapping device buffers of the local shard size;
+ * x_local_host / y_local_host: HOST arrays of n host pointers (pinned for overlap).  Work the
+ * caller enqueued on `stream` before the call completes before the first copy; `stream`
+ * completes only after the last D2H, so synchronising `stream` means every y is on the host.
+ * COLLECTIVE (n blocks, same n on all ranks).  Errors: as dsp_st_block_forward; NULL; SHAPE
+ * (n < 0); ALIAS (staging buffers overlap). */
+dsp_status_t dsp_st_block_forward_host_pipelined(dsp_ctx_t ctx, const dsp_shape_t* shape,
+                                                 const dsp_block_weights_t* w, int n,
+                                                 const void* const* x_local_host, void* const* y_local_host,
+                                                 void* const* x_dev, void* const* y_dev,
+                                                 dsp_switch_impl_t impl, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

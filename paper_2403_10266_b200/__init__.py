@@ -87,6 +87,8 @@ def lib() -> ctypes.CDLL:
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
             "dsp_st_block_forward_host": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, ctypes.c_int, vp],
             "dsp_st_block_prepare": [vp, P(Shape), P(BlockWeights), vp, ctypes.c_size_t, vp],
+            "dsp_st_block_forward_host_pipelined": [vp, P(Shape), P(BlockWeights), ctypes.c_int, P(vp), P(vp),
+                                                    P(vp), P(vp), ctypes.c_int, vp],
             "dsp_layer_norm": [vp, ctypes.c_int, i64, i64, vp, vp, vp, ctypes.c_float, vp, vp],
             "dsp_linear": [vp, ctypes.c_int, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp, vp],
             "dsp_attention_core": [vp, ctypes.c_int, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp],
@@ -303,6 +305,23 @@ class Context:
         self._call("dsp_st_block_forward_host", ctypes.byref(shape), ctypes.byref(bw), x_host.data_ptr(),
                    y_host.data_ptr(), _ptr(x_dev), _ptr(y_dev), IMPLS[impl] if isinstance(impl, str) else int(impl),
                    _stream(stream))
+
+    def st_block_forward_host_pipelined(self, shape, weights, x_hosts, y_hosts, x_devs, y_devs, impl="nccl",
+                                        stream=None):
+        """dsp_st_block_forward_host_pipelined: len(x_hosts) independent blocks with their H2D / D2H
+        copies overlapped across steps (x_devs, y_devs: two device staging buffers each)."""
+        bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
+        n = len(x_hosts)
+        if len(y_hosts) != n or len(x_devs) != 2 or len(y_devs) != 2:
+            raise ValueError("need n host inputs, n host outputs, 2 + 2 device staging buffers")
+        for t in list(x_hosts) + list(y_hosts):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("host buffers must be contiguous CPU tensors (pinned recommended)")
+        arr = lambda ptrs: (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+        self._call("dsp_st_block_forward_host_pipelined", ctypes.byref(shape), ctypes.byref(bw), n,
+                   arr([t.data_ptr() for t in x_hosts]), arr([t.data_ptr() for t in y_hosts]),
+                   arr([_ptr(t) for t in x_devs]), arr([_ptr(t) for t in y_devs]),
+                   IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
 
     def layer_norm(self, x, gamma, beta, eps, y, stream=None):
         rows, C = x.numel() // x.shape[-1], x.shape[-1]

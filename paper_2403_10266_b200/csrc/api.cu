@@ -354,6 +354,14 @@ dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, ds
   return DSP_OK;
 }
 
+dsp_ctx::~dsp_ctx() {
+  for (int b = 0; b < 2; ++b)
+    for (void* e : {ev_in[b], ev_xfree[b], ev_out[b], ev_yfree[b]})
+      if (e) cudaEventDestroy((cudaEvent_t)e);
+  if (h2d_stream) cudaStreamDestroy((cudaStream_t)h2d_stream);
+  if (d2h_stream) cudaStreamDestroy((cudaStream_t)d2h_stream);
+}
+
 dsp_status_t dsp_ctx_destroy(dsp_ctx_t ctx) {
   if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
   delete ctx;
@@ -733,6 +741,62 @@ dsp_status_t dsp_st_block_forward_host(dsp_ctx_t ctx, const dsp_shape_t* s, cons
   DSP_CUDA(ctx, cudaMemcpyAsync(xd, xh, act, cudaMemcpyHostToDevice, st), "H2D x");
   DSP_TRY(dsp_st_block_forward(ctx, s, w, xd, yd, impl, stream));
   DSP_CUDA(ctx, cudaMemcpyAsync(yh, yd, act, cudaMemcpyDeviceToHost, st), "D2H y");
+  return DSP_OK;
+}
+
+dsp_status_t dsp_st_block_forward_host_pipelined(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w,
+                                                 int n, const void* const* xh, void* const* yh, void* const* xd,
+                                                 void* const* yd, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (n < 0) return fail(ctx, DSP_ERR_SHAPE, "n = %d < 0", n);
+  if (n == 0) return DSP_OK;
+  if (!xh || !yh || !xd || !yd || !xd[0] || !xd[1] || !yd[0] || !yd[1]) return fail(ctx, DSP_ERR_NULL, "NULL buffer array");
+  for (int i = 0; i < n; ++i)
+    if (!xh[i] || !yh[i]) return fail(ctx, DSP_ERR_NULL, "NULL host buffer %d", i);
+  const int64_t act = shard_bytes(s, ctx->world);
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b)
+      if (overlap(xd[a], act, yd[b], act)) return fail(ctx, DSP_ERR_ALIAS, "x_dev[%d] overlaps y_dev[%d]", a, b);
+  if (overlap(xd[0], act, xd[1], act) || overlap(yd[0], act, yd[1], act))
+    return fail(ctx, DSP_ERR_ALIAS, "the two staging buffers of a pair overlap");
+  if (!ctx->h2d_stream) {
+    cudaStream_t a, b;
+    DSP_CUDA(ctx, cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking), "copy-in stream");
+    ctx->h2d_stream = a;
+    DSP_CUDA(ctx, cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking), "copy-out stream");
+    ctx->d2h_stream = b;
+    for (int k = 0; k < 2; ++k)
+      for (void** e : {&ctx->ev_in[k], &ctx->ev_xfree[k], &ctx->ev_out[k], &ctx->ev_yfree[k]}) {
+        cudaEvent_t ev;
+        DSP_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "pipeline event");
+        *e = ev;
+      }
+  }
+  cudaStream_t st = (cudaStream_t)stream, hs = (cudaStream_t)ctx->h2d_stream, ds = (cudaStream_t)ctx->d2h_stream;
+  auto ev = [](void* e) { return (cudaEvent_t)e; };
+  // the staging buffers may still be in use by work the caller enqueued earlier on `stream`
+  DSP_CUDA(ctx, cudaEventRecord(ev(ctx->ev_xfree[0]), st), "pipeline start");
+  DSP_CUDA(ctx, cudaStreamWaitEvent(hs, ev(ctx->ev_xfree[0]), 0), "pipeline start");
+  DSP_CUDA(ctx, cudaStreamWaitEvent(ds, ev(ctx->ev_xfree[0]), 0), "pipeline start");
+  for (int i = 0; i < n; ++i) {
+    const int b = i & 1;
+    if (i >= 2) DSP_CUDA(ctx, cudaStreamWaitEvent(hs, ev(ctx->ev_xfree[b]), 0), "wait x_dev free");
+    DSP_CUDA(ctx, cudaMemcpyAsync(xd[b], xh[i], act, cudaMemcpyHostToDevice, hs), "H2D x");
+    DSP_CUDA(ctx, cudaEventRecord(ev(ctx->ev_in[b]), hs), "x ready");
+    DSP_CUDA(ctx, cudaStreamWaitEvent(st, ev(ctx->ev_in[b]), 0), "wait x ready");
+    if (i >= 2) DSP_CUDA(ctx, cudaStreamWaitEvent(st, ev(ctx->ev_yfree[b]), 0), "wait y_dev free");
+    DSP_TRY(dsp_st_block_forward(ctx, s, w, xd[b], yd[b], impl, stream));
+    DSP_CUDA(ctx, cudaEventRecord(ev(ctx->ev_xfree[b]), st), "x consumed");
+    DSP_CUDA(ctx, cudaEventRecord(ev(ctx->ev_out[b]), st), "y ready");
+    DSP_CUDA(ctx, cudaStreamWaitEvent(ds, ev(ctx->ev_out[b]), 0), "wait y ready");
+    DSP_CUDA(ctx, cudaMemcpyAsync(yh[i], yd[b], act, cudaMemcpyDeviceToHost, ds), "D2H y");
+    DSP_CUDA(ctx, cudaEventRecord(ev(ctx->ev_yfree[b]), ds), "y copied");
+  }
+  // `stream` completes only after every result has reached the host
+  DSP_CUDA(ctx, cudaStreamWaitEvent(st, ev(ctx->ev_yfree[(n - 1) & 1]), 0), "pipeline end");
+  if (n >= 2) DSP_CUDA(ctx, cudaStreamWaitEvent(st, ev(ctx->ev_yfree[n & 1]), 0), "pipeline end");
   return DSP_OK;
 }
 

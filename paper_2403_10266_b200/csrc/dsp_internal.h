@@ -160,5 +160,14 @@ struct dsp_ctx {
   void* stage_events[2 * DSP_NUM_STAGES] = {};
   bool has_stage_events = false;
   uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
+  // pipelined host path (dsp_st_block_forward_host_pipelined): copy-in / copy-out streams and
+  // per-staging-buffer events, created on first use, destroyed with the context
+  void* h2d_stream = nullptr;
+  void* d2h_stream = nullptr;
+  void* ev_in[2] = {};      // x_dev[b] filled (copy-in stream)
+  void* ev_xfree[2] = {};   // x_dev[b] consumed by the block (compute stream)
+  void* ev_out[2] = {};     // y_dev[b] written by the block (compute stream)
+  void* ev_yfree[2] = {};   // y_dev[b] copied out (copy-out stream)
   std::string last_error;
+  ~dsp_ctx();
 };

@@ -223,3 +223,35 @@ def test_block_prepared_virtual_ranks_vs_oracle(N, impl):
     g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl=impl))
     got = np.concatenate([to_f64(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     print(assert_block_close(got, ref))
+
+
+def test_block_host_pipelined_equals_device_path():
+    """dsp_st_block_forward_host_pipelined (e2e serving path: H2D / block / D2H of adjacent steps
+    overlapped on three streams, two staging buffers each way) returns, for every one of five
+    different inputs, exactly the bytes of dsp_st_block_forward on device-resident input."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    Ws = synth.make_block_weights(sh, 7)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    W = weights_dev(Ws, sh.dtype)
+    W["prepared"] = ctx.prepare_block(shape, W)
+    xs = [synth.make_x(sh, 100 + i) for i in range(5)]
+    want = []
+    for x in xs:
+        X = to_dev(x, sh.dtype)
+        Y = torch.empty_like(X)
+        ctx.st_block_forward(shape, W, X, Y)
+        want.append(Y.view(torch.int16).cpu())
+    xh = [to_dev(x, sh.dtype).view(torch.int16).cpu().pin_memory() for x in xs]
+    yh = [torch.empty_like(t).pin_memory() for t in xh]
+    ref = to_dev(xs[0], sh.dtype)
+    xd = [torch.empty_like(ref) for _ in range(2)]
+    yd = [torch.empty_like(ref) for _ in range(2)]
+    ctx.st_block_forward_host_pipelined(shape, W, xh, yh, xd, yd)
+    torch.cuda.current_stream().synchronize()
+    for i in range(5):
+        assert torch.equal(yh[i], want[i]), f"step {i}"
+    with pytest.raises(m.DSPError):  # staging buffers must not overlap
+        ctx.st_block_forward_host_pipelined(shape, W, xh[:2], yh[:2], [xd[0], xd[1]], [xd[0], yd[1]])
