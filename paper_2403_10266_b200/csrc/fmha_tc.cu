@@ -36,6 +36,12 @@
 // 107-112; split + ping-pong: 107-112) and therefore off by default.  The exp loop itself is
 // the bound: scripts/micro/exp_loop.cu measures 3.8 exps/clk/SMSP with two warps per SMSP and
 // 4.8 with four, against 32768 exps per SM per K/V step.
+// fmha_kv1_kernel (3-stage Q|K|V ring, one CTA per SM) for single-K/V-tile sequences: correct
+// but measured slower than fmha_bf16_tc_kernel at the temporal blk shape (36.3 vs 32.8 us) and
+// equal at T = 128 (467 us), so off by default.
+#ifndef DSP_FMHA_KV1
+#define DSP_FMHA_KV1 0
+#endif
 #ifndef DSP_FMHA_SPLIT
 #define DSP_FMHA_SPLIT 0
 #endif
@@ -1400,6 +1406,255 @@ __global__ void __launch_bounds__(640, 1)
   }
 }
 
+// O / l -> bf16 -> a staging tile in the TMA box layout (the SW128 64-column chunks, then the
+// SW32 / SW64 remainder), fenced for the async proxy; `o_free` is arrived once O is in
+// registers.  The caller signals the thread that issues the TMA store.
+template <int NA, int RB>
+__device__ __forceinline__ void stage_o(uint8_t* stage, uint32_t tO, uint32_t lane_off, int row, float l,
+                                        uint64_t* o_free) {
+  constexpr int DP = NA * 64 + RB;
+  const float inv_l = 1.f / l;
+  const uint32_t st0 = smem_u32(stage);
+  uint32_t ov[DP];
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16));
+  tmem_ld_wait();
+  tc_fence_before();
+  mbar_arrive(o_free);
+#pragma unroll
+  for (int c = 0; c < DP / 16; ++c) {
+#pragma unroll
+    for (int h8 = 0; h8 < 2; ++h8) {
+      const int d = c * 16 + h8 * 8;
+      const uint32_t* w = ov + d;
+      const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
+      const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
+      const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
+      const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
+      uint32_t addr;
+      if (d < NA * 64) {
+        const int blk = d >> 6, ch = (d & 63) >> 3;
+        addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
+      } else {
+        const int ch = (d - NA * 64) >> 3;
+        addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
+                        : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
+      }
+      st_shared_v4(addr, a0, a1, a2, a3);
+    }
+  }
+  fence_proxy_async_smem();
+}
+
+// ---------------------------------------------------------------------------------
+// Sequences that fit one K/V tile (n_kv == 1: temporal T = 16 packed 8 per tile, or L = 128):
+// HBM-bound (q, k, v read once, o written once), so the design goal is bytes in flight.
+// One CTA per SM keeps a ring of NS = 3 stages, each holding the Q, K and V tiles of one
+// work item (3 x 20 KB at Dh = 72), so up to three items' loads are in flight per SM while
+// two are computed: S and O of the two compute slots fill the 512 TMEM columns.  After
+// S = Q K^T the stage's Q/K bytes are dead and hold P (SW128, 32 KB); after P V they hold
+// the O staging tile for the TMA store.  A store warp issues that store and frees the stage
+// once the store has read it.
+//   warp 0 TMA producer   warp 1 MMA (S_{k+1} before P_k V_k)   warp 2 O store   warp 3 idle
+//   warps 4-7 softmax + epilogue of even items, warps 8-11 odd items (thread = query row)
+template <int NA, int RB>
+struct Kv1Cfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int NS = 3;
+  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP;
+  static constexpr int STAGE = 3 * TILE;  // Q | K | V; P and the O staging tile alias Q|K
+  static constexpr int SMEM = 1024 + NS * STAGE + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024 && 2 * TILE >= Base::P_BYTES;
+};
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(384, 1)
+    fmha_kv1_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
+                    const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
+                    const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                    const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
+                    const FmhaParams p) {
+  using Cfg = Kv1Cfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  constexpr int NS = Cfg::NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
+  uint64_t* full = bars;              // [NS] Q, K, V of the stage landed
+  uint64_t* stage_free = bars + 3;    // [NS] the stage's O store has read the staging tile
+  uint64_t* o_staged = bars + 6;      // [NS] O staging tile written (128 softmax threads)
+  uint64_t* s_full = bars + 9;        // [2] per slot
+  uint64_t* p_full = bars + 11;       // [2]
+  uint64_t* o_done = bars + 13;       // [2]
+  uint64_t* o_free = bars + 15;       // [2] O read out of TMEM
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
+  const int warp = warp_id();
+  auto stage_ptr = [&](int st) { return smem + st * Cfg::STAGE; };
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a); tma_prefetch(&to_a);
+    if (RB) { tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b); tma_prefetch(&to_b); }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&stage_free[i], 1);
+      mbar_init(&o_staged[i], 128);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
+
+  if (warp == 0) {
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      int k = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+        const int st = k % NS;
+        mbar_wait_sleep(&stage_free[st], ((k / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], 3 * Cfg::TX);
+        uint8_t* sb = stage_ptr(st);
+        const TileCoord t = tile_coord(p, item, 0);
+        load_tile<NA, RB>(sb, &tq_a, &tq_b, &full[st], tile_coord(p, item, -1));
+        load_tile<NA, RB>(sb + Cfg::TILE, &tk_a, &tk_b, &full[st], t);
+        load_tile<NA, RB>(sb + 2 * Cfg::TILE, &tv_a, &tv_b, &full[st], t);
+      }
+    }
+  } else if (warp == 1) {
+    setmaxnreg_dec<56>();
+    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
+    constexpr uint32_t idPVb = make_idesc_bf16(128, RB == 0 ? 16 : RB, 0, 1);
+    auto issue_s = [&](int k) {  // full[k % NS] observed complete by the caller
+      const int st = k % NS, sl = k & 1;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t q0 = smem_u32(stage_ptr(st)), k0 = q0 + Cfg::TILE, d = tmem + sl * 256;
+        int step = 0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk, ++step)
+            umma_bf16_ss(d, make_sdesc(q0 + i * 16384 + kk * 32, 16, 1024, SW_128B),
+                         make_sdesc(k0 + i * 16384 + kk * 32, 16, 1024, SW_128B), idS, step != 0);
+#pragma unroll
+        for (int kk = 0; kk < RB / 16; ++kk, ++step)
+          umma_bf16_ss(d, make_sdesc(q0 + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
+                       make_sdesc(k0 + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+        umma_commit(&s_full[sl]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int k) {  // p_full / o_free observed by the caller
+      const int st = k % NS, sl = k & 1;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t p0 = smem_u32(stage_ptr(st)), vb = p0 + 2 * Cfg::TILE, o = tmem + sl * 256 + 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = make_sdesc(p0 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B);
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            umma_bf16_ss(o + 64 * i, ad, make_sdesc(vb + i * 16384 + kk * 2048, 16384, 1024, SW_128B), idPVa, kk != 0);
+          if (RB)
+            umma_bf16_ss(o + 64 * NA, ad,
+                         make_sdesc(vb + NA * 16384 + kk * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
+                         idPVb, kk != 0);
+        }
+        umma_commit(&o_done[sl]);
+      }
+      __syncwarp();
+    };
+    int nmine = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) ++nmine;
+    // Event loop: S_j may run once its stage has landed and slot j & 1's previous S was consumed
+    // (PV_{j-2} issued, i.e. j <= npv + 1); PV_k once P_k is written and O of the slot is free.
+    // Neither waits for the other's unrelated condition (an item whose load is late does not
+    // hold back the P.V of an item that is ready).
+    int ns = 0, npv = 0;
+    while (npv < nmine) {
+      if (ns < nmine && ns <= npv + 1 && mbar_test(&full[ns % NS], (ns / NS) & 1)) {
+        issue_s(ns);
+        ++ns;
+        continue;
+      }
+      if (npv < ns && mbar_test(&p_full[npv & 1], (npv >> 1) & 1) &&
+          (npv < 2 || mbar_test(&o_free[npv & 1], ((npv >> 1) & 1) ^ 1))) {
+        issue_pv(npv);
+        ++npv;
+        continue;
+      }
+      __nanosleep(40);  // nothing ready: do not steal issue slots from the softmax warps on this SMSP
+    }
+  } else if (warp == 2) {
+    setmaxnreg_dec<56>();
+    if (elect_one()) {  // O store: staging tile -> global, then the stage may be refilled
+      int k = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+        const int st = k % NS;
+        mbar_wait(&o_staged[st], (k / NS) & 1);
+        const TileCoord t = tile_coord(p, item, -1);
+        uint8_t* sb = stage_ptr(st);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) tma_store_5d(&to_a, sb + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
+        if (RB) tma_store_5d(&to_b, sb + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
+        bulk_commit_group();
+        bulk_wait_group_read0();
+        mbar_arrive(&stage_free[st]);
+      }
+      bulk_wait_group_read0();
+    }
+  } else if (warp == 3) {
+    setmaxnreg_dec<56>();
+  } else {
+    setmaxnreg_inc<224>();
+    const int sl = (warp - 4) >> 2;
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    const uint32_t tS = tmem + sl * 256, tO = tmem + sl * 256 + 128;
+    uint32_t no_dummy = 0;
+    int k = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+      if ((k & 1) != sl) continue;
+      const int st = k % NS;
+      uint8_t* sb = stage_ptr(st);
+      float m = -INFINITY, l = 0.f;
+      mbar_wait(&s_full[sl], (k >> 1) & 1);
+      tc_fence_after();
+      if (G.diag) {
+        if (G.nhalf * G.hcols > 32) softmax_tile_diag<64>(G, tS, sb, m, l, nullptr, 0);
+        else softmax_tile_diag<32>(G, tS, sb, m, l, nullptr, 0);
+      } else {
+        softmax_tile<Cfg::DP>(G, tS, tO, sb, 0, m, l, nullptr, no_dummy, nullptr, 0);
+      }
+      mbar_arrive(&p_full[sl]);
+      mbar_wait(&o_done[sl], (k >> 1) & 1);
+      tc_fence_after();
+      stage_o<NA, RB>(sb, tO, G.lane_off, G.row, l, &o_free[sl]);
+      mbar_arrive(&o_staged[st]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 template <int NA, int RB>
 cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims, const uint64_t* strides,
                      const uint32_t* box_rows, int num_sms, cudaStream_t st, std::string* why) {
@@ -1465,6 +1720,20 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       const int grid = npairs < num_sms ? npairs : num_sms;
       return launch_k(kp, dim3(grid), dim3(PairCfg<NA, RB>::THREADS), PairCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2],
                       m[3], m[4], m[5], mo[0], mo[1], p);
+    }
+  }
+  if constexpr (Kv1Cfg<NA, RB>::OK) {
+    if (DSP_FMHA_KV1 && p.n_kv == 1) {
+      auto k1 = fmha_kv1_kernel<NA, RB>;
+      static bool attr_1 = false;
+      if (!attr_1) {
+        cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, Kv1Cfg<NA, RB>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_1 = true;
+      }
+      const int grid = p.items < num_sms ? p.items : num_sms;
+      return launch_k(k1, dim3(grid), dim3(384), Kv1Cfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2], m[3], m[4], m[5],
+                      mo[0], mo[1], p);
     }
   }
   auto kern = fmha_bf16_tc_kernel<NA, RB>;
