@@ -96,10 +96,13 @@ def run_reference(args):
     t0 = time.perf_counter()
     rates = [oracle_sample(sh, args.seed, frames, cols, toks)[0] for _ in range(args.steps)]
     wall = time.perf_counter() - t0
-    v = float(np.mean(rates))
+    layers = getattr(args, "layers", 1)
+    v = float(np.mean(rates)) / layers
     sample = (f"per step: oracle spatial stage on {frames} frame(s), temporal stage on {cols} columns, MLP stage on "
-              f"{toks} tokens (float64 numpy, BLAS threads = cores); tokens/s = 1 / sum of per-token stage costs")
-    out = {"impl": "reference", "metric": "ST-block fwd tokens/s", "value": v, "unit": "tokens/s",
+              f"{toks} tokens (float64 numpy, BLAS threads = cores); tokens/s = 1 / sum of per-token stage costs"
+              + (f", divided by {layers} layers" if layers > 1 else ""))
+    metric = "ST-block fwd tokens/s" if layers == 1 else f"{layers}-layer ST-DiT forward tokens/s"
+    out = {"impl": "reference", "metric": metric, "value": v, "unit": "tokens/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -457,13 +460,96 @@ def run_dsp(args):
         dist.destroy_process_group()
 
 
+def run_model(args):
+    """configs[2]: the 28-layer ST-DiT-XL/2-shaped forward (28 blocks at the single-block shape,
+    per-layer weights, prepared), one dsp_st_model_forward per step, CUDA-graph replay."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_10266_b200 as dsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    sh, L, N = synth.CONFIGS["blk"], 28, world
+    Tn = sh.T // N
+    ctx = dsp.Context(pg=pg, device=dev)
+    shape = dsp.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    to_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+    layers = []
+    for layer in range(L):
+        W = {k: to_dev(v) for k, v in synth.make_block_weights(sh, args.seed, layer=layer).items()}
+        W["prepared"] = ctx.prepare_block(shape, W)
+        layers.append(W)
+    bws = [ctx.block_weights(W) for W in layers]
+    X = to_dev(synth.make_x(sh, args.seed, t_range=(rank * Tn, (rank + 1) * Tn)))
+    Y = torch.empty_like(X)
+    ctx.ensure_workspace(dsp.workspace_bytes(shape, N))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    step_eager = lambda: ctx.st_model_forward(shape, bws, X, Y, impl="nccl")
+    for _ in range(args.warmup):
+        step_eager()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    l0 = ctx.launch_count()
+    with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+        step_eager()
+    per_step = ctx.launch_count() - l0
+    torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+        for a, b in ev:
+            flush.zero_()
+            a.record()
+            g.replay()
+            b.record()
+        torch.cuda.synchronize()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    tokens = sh.B * sh.T * sh.S
+    P, _ = peaks()
+    flops = L * (32 * tokens * sh.C ** 2 + 4 * sh.B * sh.T * sh.S ** 2 * sh.C + 4 * sh.B * sh.S * sh.T ** 2 * sh.C)
+    t_roof = flops / N / (P["bf16_tflops"] * 1e12) * 1e3
+    if rank == 0:
+        print(json.dumps({"metric": "28-layer ST-DiT forward tokens/s", "value": tokens * K / (t_ms / 1e3),
+                          "unit": "tokens/s", "n_gpus": N, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic",
+                          "config": {"workload": "configs[2] ST-DiT-XL/2-shaped: 28 blocks, B=1 T=16 S=1024 C=1152 "
+                                                 "16 heads, per-layer weights, prepared (LN folded; LN1 of blocks "
+                                                 "1..27 from the previous FC2 epilogue at N=1)",
+                                     "l2": "flushed between timed steps", "launch": "cuda graph replay"},
+                          "block_equivalent_us": round(t_ms / K / L * 1e3, 1),
+                          "roofline": {"t_roofline_ms": round(t_roof, 3), "frac": round(t_roof / (t_ms / K), 3),
+                                       "basis": "28 x block FLOPs / N / measured bf16 peak"},
+                          "gpu_launches": per_step * K, "clocks": clocks.summary()}), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
-    ap.add_argument("--config", default="blk", choices=list(CONFIGS))
+    ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28"])
     ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p", "fused"])
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -474,7 +560,11 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
+        if args.config == "model28":  # 28 blocks of the blk shape: the oracle's block cost x 28
+            args.config, args.layers = "blk", 28
         run_reference(args)
+    elif args.config == "model28":
+        run_model(args)
     else:
         run_dsp(args)
 

@@ -245,6 +245,16 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* shape,
                                   const dsp_block_weights_t* w, const void* x_local,
                                   void* y_local, dsp_switch_impl_t impl, void* stream);
 
+/* Forward of a stack of L ST blocks, y = block_{L-1}( ... block_0(x)) (BASELINE configs[2]:
+ * the 28-layer ST-DiT-XL/2-shaped model), x and y T-sharded as for one block (x may
+ * equal y; blocks 1.. run in place on y).  w: HOST array of L block-weight structs.  With
+ * prepared weights (R30) at N == 1, block l's FC2 epilogue also writes the per-row LayerNorm
+ * partials of its output and block l + 1 folds LN1 from them (no statistics pass between
+ * blocks).  Workspace as for one block (reused by every layer).  COLLECTIVE (2 switches per
+ * layer).  Errors: as dsp_st_block_forward; SHAPE (L < 1); NULL. */
+dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* const* w,
+                                  int L, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
+
 /* Bytes of the prepared-weights buffer for one bf16 block of this shape (0 for f32). */
 size_t dsp_block_prepared_bytes(const dsp_shape_t* shape);
 

@@ -85,6 +85,7 @@ def lib() -> ctypes.CDLL:
             "dsp_spatial_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
+            "dsp_st_model_forward": [vp, P(Shape), P(P(BlockWeights)), ctypes.c_int, vp, vp, ctypes.c_int, vp],
             "dsp_st_block_forward_host": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, ctypes.c_int, vp],
             "dsp_st_block_prepare": [vp, P(Shape), P(BlockWeights), vp, ctypes.c_size_t, vp],
             "dsp_st_block_forward_host_pipelined": [vp, P(Shape), P(BlockWeights), ctypes.c_int, P(vp), P(vp),
@@ -294,6 +295,14 @@ class Context:
     def st_block_forward(self, shape, weights, x_local, y_local, impl="nccl", stream=None):
         bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
         self._call("dsp_st_block_forward", ctypes.byref(shape), ctypes.byref(bw), _ptr(x_local), _ptr(y_local),
+                   IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def st_model_forward(self, shape, layers, x_local, y_local, impl="nccl", stream=None):
+        """dsp_st_model_forward: layers = list of per-layer weights (dicts or BlockWeights)."""
+        bws = [w if isinstance(w, BlockWeights) else self.block_weights(w) for w in layers]
+        arr = (ctypes.POINTER(BlockWeights) * len(bws))(*[ctypes.pointer(b) for b in bws])
+        self._keep_model = (bws, arr)
+        self._call("dsp_st_model_forward", ctypes.byref(shape), arr, len(bws), _ptr(x_local), _ptr(y_local),
                    IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
 
     def st_block_forward_host(self, shape, weights, x_host: torch.Tensor, y_host: torch.Tensor, x_dev, y_dev,

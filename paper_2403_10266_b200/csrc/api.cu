@@ -550,8 +550,13 @@ dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* 
   return attn_public(ctx, s, DSP_DIM_T, h, wqkv, wo, res, out, stream);
 }
 
-dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
-                                  void* y, dsp_switch_impl_t impl, void* stream) {
+// One block.  Chaining flags of dsp_st_model_forward (prepared weights, N == 1 only):
+//   ln1_from_parts: the LN1 statistics of x are combined from per-row partials already in the
+//                   workspace (written by the previous block's FC2 epilogue) -- no stats pass;
+//   emit_parts:     the FC2 epilogue writes the per-row partials of y for the next block's LN1.
+static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
+                                  void* y, dsp_switch_impl_t impl, void* stream, bool ln1_from_parts,
+                                  bool emit_parts) {
   DSP_TRY(check_ctx(ctx));
   DSP_TRY(check_shape(ctx, s));
   DSP_TRY(check_div(ctx, s, ctx->world));
@@ -613,8 +618,13 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   float2* parts = reinterpret_cast<float2*>(ws + L.parts);
   const int nparts = (int)(C / gemm_bn_for(C));
   EpiVec ev1{}, ev2{}, ev3{};
+  const bool chain_in = fold && N == 1 && ln1_from_parts, chain_out = fold && N == 1 && emit_parts;
   if (fold) {
     ev1.row_stats = stats; ev1.col_u = uv; ev1.col_v = uv + 3 * C;
+    if (chain_in) {
+      ev1.row_stats = nullptr;
+      ev1.part_in = parts; ev1.nparts_in = nparts; ev1.part_cnt = (int)(C / nparts); ev1.eps = eps;
+    }
     ev2.col_u = uv + 6 * C; ev2.col_v = uv + 9 * C;
     ev3.col_u = uv + 12 * C; ev3.col_v = uv + 16 * C;
     ev3.part_in = parts; ev3.nparts_in = nparts; ev3.part_cnt = (int)(C / nparts); ev3.eps = eps;
@@ -629,9 +639,11 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   const void* wf_1 = fold ? prep + P.wf_1 : nullptr;
   // a1: LN1 (prepared: row statistics of x only)
   mark(ctx, DSP_STAGE_LN1, 0, st);
-  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
-  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
-  ctx->launches += 1;
+  if (!chain_in) {
+    if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
+    else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
+    ctx->launches += 1;
+  }
   mark(ctx, DSP_STAGE_LN1, 1, st);
   // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y (N == 1 prepared: + LN2 partials)
   DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, fold ? x : h, fold ? wf_s : w->w_qkv_s, w->w_o_s, x, y, qkv, o,
@@ -684,6 +696,11 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     cudaError_t e2 = launch_gemm_bf16_remote(big, w->w_fc2, cur, rm_st, tok, C, 4 * C, ctx->num_sms, st, &why);
     if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "FC2 (switch fused)", why);
     ctx->launches += 1;
+  } else if (chain_out) {  // + LN partials of y for the next block's LN1
+    std::string why;
+    cudaError_t e2 = launch_gemm_bf16_res_stats(big, w->w_fc2, cur, cur, tok, C, 4 * C, parts, ctx->num_sms, st, &why);
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "FC2 (+LN partials)", why);
+    if (tok > 0) ctx->launches += 1;
   } else {
     DSP_TRY(linear(ctx, s->dtype, tok, C, 4 * C, big, w->w_fc2, cur, DSP_EPI_RESIDUAL, cur, st));
   }
@@ -697,6 +714,27 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
   }
   mark(ctx, DSP_STAGE_SWITCH_ST, 1, st);
+  return DSP_OK;
+}
+
+dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
+                                  void* y, dsp_switch_impl_t impl, void* stream) {
+  return block_forward(ctx, s, w, x, y, impl, stream, false, false);
+}
+
+dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* const* w, int L,
+                                  const void* x, void* y, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (L < 1) return fail(ctx, DSP_ERR_SHAPE, "L = %d < 1", L);
+  if (!w) return fail(ctx, DSP_ERR_NULL, "NULL weights array");
+  for (int l = 0; l < L; ++l)
+    if (!w[l]) return fail(ctx, DSP_ERR_NULL, "weights of layer %d are NULL", l);
+  for (int l = 0; l < L; ++l) {
+    // LN1 of block l + 1 from block l's FC2 partials when both sides are prepared (N == 1)
+    const bool in = l > 0 && w[l - 1]->prepared && w[l]->prepared;
+    const bool out = l + 1 < L && w[l]->prepared && w[l + 1]->prepared;
+    DSP_TRY(block_forward(ctx, s, w[l], l == 0 ? x : y, y, impl, stream, in, out));
+  }
   return DSP_OK;
 }
 

@@ -282,13 +282,14 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          st_shared_v4(addr, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                       pack_bf16x2(f[6], f[7]));
-          if (kStats) {  // shifted sums of the fp32 row values (R30), packed pairs
-            if (c == 0 && u == 0) sh = make_float2(-f[0], -f[0]);
+          const uint32_t pk[4] = {pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                  pack_bf16x2(f[6], f[7])};
+          st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
+          if (kStats) {  // shifted sums of the STORED (bf16-rounded) row values (R30), packed pairs
+            if (c == 0 && u == 0) sh = make_float2(-bf16lo(pk[0]), -bf16lo(pk[0]));
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-              const float2 d = fadd2(make_float2(f[i], f[i + 1]), sh);
+            for (int i = 0; i < 4; ++i) {
+              const float2 d = fadd2(make_float2(bf16lo(pk[i]), bf16hi(pk[i])), sh);
               s1 = fadd2(s1, d);
               s2 = ffma2(d, d, s2);
             }
