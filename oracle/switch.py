@@ -8,6 +8,11 @@ ranks (S:171: "real message exchange ... so the ledger is a measurement"), not
 as slicing of a global tensor.  Chunk -> rank map: rank r holds the r-th
 contiguous chunk along the sharded axis (R11).  Self-sends are not
 communication.  Axis numbering follows [B, T, S, C]: T = 1, S = 2.
+
+split_nd / switch_nd: the same operations on an N-D activation [d0, ..., d_{k-1}, C]
+(any number of sequence dims, channel last) -- P:93: "our method can generalize to all
+multi-dimensional transformers beyond the demonstrated spatial-temporal transformer"
+(e.g. [B, T, H, W, C] with attention along T, H and W separately).
 """
 from __future__ import annotations
 
@@ -59,9 +64,32 @@ def _check_dim(dim):
         raise DSPOracleError(f"bad dim {dim}: only T (1) and S (2) are sequence dims")
 
 
+def _check_dim_nd(dim, ndim):
+    if not (0 <= dim < ndim - 1):
+        raise DSPOracleError(f"bad dim {dim}: the sharded / switched dims are 0..{ndim - 2} (the last is the channel)")
+
+
+def split_nd(x: np.ndarray, dim: int, world: int) -> list:
+    """N-D split: rank r takes chunk r of x along any non-channel dim."""
+    _check_dim_nd(dim, x.ndim)
+    return _split(x, dim, world)
+
+
+def switch_nd(shards: list, from_dim: int, to_dim: int, ledger: Ledger | None = None,
+              tag: str = "switch", elem_bytes: int = 2) -> list:
+    """N-D dynamic switch between any two non-channel dims (see switch())."""
+    _check_dim_nd(from_dim, shards[0].ndim)
+    _check_dim_nd(to_dim, shards[0].ndim)
+    return _switch(shards, from_dim, to_dim, ledger, tag, elem_bytes)
+
+
 def split(x: np.ndarray, dim: int, world: int) -> list:
     """Rank r takes chunk r of x along dim."""
     _check_dim(dim)
+    return _split(x, dim, world)
+
+
+def _split(x: np.ndarray, dim: int, world: int) -> list:
     if x.shape[dim] % world:
         raise DSPOracleError(f"divisibility: N={world} does not divide extent {x.shape[dim]}")
     n = x.shape[dim] // world
@@ -96,6 +124,10 @@ def switch(shards: list, from_dim: int, to_dim: int, ledger: Ledger | None = Non
     """
     _check_dim(from_dim)
     _check_dim(to_dim)
+    return _switch(shards, from_dim, to_dim, ledger, tag, elem_bytes)
+
+
+def _switch(shards, from_dim, to_dim, ledger, tag, elem_bytes):
     if from_dim == to_dim:
         raise DSPOracleError("switching to the current axis (S:283)")
     N = len(shards)

@@ -18,6 +18,11 @@ import paper_2403_10266_b200 as dsp
 import synth
 
 NVLINK_GBS = float(os.environ.get("NVLINK_GBS", "770"))  # measured peer copy per direction (B200_PROFILING.md)
+try:
+    PEAK_TFLOPS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                              "MEASURED_PEAKS.json")))["bf16_tflops"]
+except Exception:
+    PEAK_TFLOPS = 1590.0  # B200_PROFILING.md fallback
 
 
 def main():
@@ -96,7 +101,7 @@ def main():
         sw_bytes = 2 * (N - 1) * sh.M // (N * N) * 2
         sw_us = sw_bytes / (NVLINK_GBS * 1e3)
         flops = (32 * B * T * S * C * C + 4 * B * T * S * S * C + 4 * B * S * T * T * C) / N
-        roof = max(flops / 1674.9e12 * 1e6, sw_bytes / 900e3)
+        roof = max(flops / PEAK_TFLOPS / 1e12 * 1e6, sw_bytes / 900e3)
         est = comp + sw_us
         res[N] = {"compute_us": round(comp, 1), "switch_us_at_%dGBps" % NVLINK_GBS: round(sw_us, 1),
                   "block_us_est": round(est, 1), "tokens_per_s_est": round(B * T * S / est * 1e6),

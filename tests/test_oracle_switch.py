@@ -88,3 +88,80 @@ def test_errors():
         osw.switch(osw.split(np.zeros((1, 4, 6, 2)), DIM_T, 4), DIM_T, DIM_S)  # 4 does not divide S=6
     with pytest.raises(osw.DSPOracleError):
         osw.split(x, 3, 2)
+
+
+# ---------------------------------------------------------------- N-D switch
+def _tagged_nd(dims, seed=3):
+    """int64 tensor whose every element holds its own global flat index (plus a seeded offset)."""
+    return np.arange(int(np.prod(dims)), dtype=np.int64).reshape(dims) * 7 + seed
+
+
+@pytest.mark.parametrize("dims", [(2, 4, 8, 4, 3), (1, 8, 4, 2, 4, 2), (4, 4, 4, 5)])
+@pytest.mark.parametrize("N", [2, 4])
+def test_switch_nd_closed_form_all_pairs(dims, N):
+    """Every ordered pair (a, b) of non-channel dims: after switch_nd(a -> b), rank q holds exactly
+    the elements whose index along b lies in [q*db/N, (q+1)*db/N), in their original relative order
+    -- checked element by element from the index tag against the explicit index map."""
+    x = _tagged_nd(dims)
+    nd = len(dims)
+    for a in range(nd - 1):
+        for b in range(nd - 1):
+            if a == b or dims[a] % N or dims[b] % N:
+                continue
+            sh = osw.split_nd(x, a, N)
+            out = osw.switch_nd(sh, a, b)
+            nb = dims[b] // N
+            for q in range(N):
+                got = out[q]
+                exp_shape = list(dims)
+                exp_shape[b] = nb
+                assert list(got.shape) == exp_shape
+                # decode every element's global index and compare with the map (i_b = q*nb + local i_b)
+                flat = (got - 3) // 7
+                idx = np.array(np.unravel_index(flat.reshape(-1), dims)).T.reshape(*got.shape, nd)
+                loc = np.indices(got.shape).transpose(*range(1, nd + 1), 0)
+                want = loc.copy()
+                want[..., b] += q * nb
+                assert np.array_equal(idx, want), (a, b, q)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+def test_switch_nd_equals_4d_switch_and_round_trips(N):
+    sh = synth.BlockShape(2, 16, 32, 4, 1, "bf16")
+    x = synth.make_index_tagged(sh, 5)
+    t = osw.split(x, DIM_T, N)
+    assert all(np.array_equal(u, v) for u, v in zip(osw.switch_nd(t, 1, 2), osw.switch(t, DIM_T, DIM_S)))
+    dims = (2, 8, 8, 8, 4)
+    g = _tagged_nd(dims)
+    if N > 8 or 8 % N:
+        return
+    s0 = osw.split_nd(g, 1, N)
+    back = osw.switch_nd(osw.switch_nd(s0, 1, 3), 3, 1)
+    assert all(np.array_equal(u, v) for u, v in zip(back, s0))
+    # composition: 1 -> 2 -> 3 equals 1 -> 3
+    via = osw.switch_nd(osw.switch_nd(s0, 1, 2), 2, 3)
+    direct = osw.switch_nd(s0, 1, 3)
+    assert all(np.array_equal(u, v) for u, v in zip(via, direct))
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+def test_switch_nd_ledger_volume(N):
+    """Off-rank elements sent per rank per switch = (N-1) M / N^2 for any pair of dims."""
+    dims = (1, 8, 16, 8, 4)
+    M = int(np.prod(dims))
+    x = np.zeros(dims, dtype=np.int16)
+    for a, b in [(1, 2), (3, 1), (2, 3)]:
+        led = osw.Ledger()
+        osw.switch_nd(osw.split_nd(x, a, N), a, b, led, "t")
+        for r in range(N):
+            assert led.sent(r) == (N - 1) * M // (N * N)
+
+
+def test_switch_nd_errors():
+    x = np.zeros((2, 4, 4, 3))
+    with pytest.raises(osw.DSPOracleError):
+        osw.split_nd(x, 3, 2)          # the channel dim is never sharded
+    with pytest.raises(osw.DSPOracleError):
+        osw.switch_nd(osw.split_nd(x, 1, 2), 1, 1)
+    with pytest.raises(osw.DSPOracleError):
+        osw.switch_nd(osw.split_nd(x, 1, 2), 1, 3)
