@@ -245,6 +245,38 @@ dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* shape,
                                   const dsp_block_weights_t* w, const void* x_local,
                                   void* y_local, dsp_switch_impl_t impl, void* stream);
 
+/* ---------------------------------------------------------------- N-D switch
+ * DSP on a multi-dimensional activation [d_0, ..., d_{n-2}, C] with any number of sequence
+ * dims ("our method can generalize to all multi-dimensional transformers beyond the
+ * demonstrated spatial-temporal transformer"; e.g. [B, T, H, W, C] with attention along T, H
+ * and W separately).  Sharding convention as for the 4-D switch: rank r holds the r-th
+ * contiguous chunk along the sharded dim (R11).  dims: HOST array of the GLOBAL extents,
+ * outermost first, the last one is the channel dim (never sharded); elem_bytes: bytes per
+ * element.  from_dim / to_dim in [0, ndim - 2], distinct. */
+#define DSP_ND_MAX_DIMS 8
+typedef struct {
+  int64_t n[4];            /* loop extents: [peer, outer, rows of the outer switched dim, middle] */
+  int64_t run_bytes;       /* contiguous bytes moved per run */
+  int64_t src_stride[4];   /* bytes, in x_local */
+  int64_t dst_stride[4];   /* bytes, in the destination's y_local; [0] = offset per source rank */
+  int64_t dst_peer_off;    /* this rank's offset in every destination: rank * dst_stride[0] */
+  int32_t pack_is_identity, unpack_is_identity;
+} dsp_switch_nd_plan_t;
+/* HOST-ONLY, pure: the byte plan of rank `rank`'s N-D switch.  Errors: NULL, SHAPE (ndim
+ * outside [3, DSP_ND_MAX_DIMS], an extent < 1, elem_bytes < 1), BAD_DIM, SAME_DIM,
+ * DIVISIBILITY (world does not divide d[from] or d[to]), ALIGNMENT (a run is not a multiple
+ * of 16 bytes: needs d[max(from,to)] / world * prod(d after it) * elem_bytes % 16 == 0). */
+dsp_status_t dsp_switch_nd_plan(const int64_t* dims, int ndim, int elem_bytes, int world, int rank,
+                                int from_dim, int to_dim, dsp_switch_nd_plan_t* plan);
+/* N-D dynamic switch: x_local = chunk `rank` of the global X along from_dim (extent
+ * d[from]/world there), y_local = chunk `rank` along to_dim, bit-identical bytes.  Transport
+ * as dsp_switch (NCCL: pack -> ncclAlltoAll -> unpack through the context workspace, which
+ * must hold 2 local shards unless pack/unpack are identities; P2P: y_local inside the
+ * registered symmetric buffer).  x, y 16-B aligned, non-overlapping (world > 1).
+ * COLLECTIVE.  Errors: as dsp_switch_nd_plan, plus NULL, ALIAS, WORKSPACE, STATE, NCCL, CUDA. */
+dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int elem_bytes, int from_dim,
+                           int to_dim, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
+
 /* Forward of a stack of L ST blocks, y = block_{L-1}( ... block_0(x)) (BASELINE configs[2]:
  * the 28-layer ST-DiT-XL/2-shaped model), x and y T-sharded as for one block (x may
  * equal y; blocks 1.. run in place on y).  w: HOST array of L block-weight structs.  With

@@ -56,6 +56,12 @@ class SwitchPlan(ctypes.Structure):
                 ("pack_is_identity", ctypes.c_int32), ("unpack_is_identity", ctypes.c_int32)]
 
 
+class SwitchNdPlan(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64 * 4), ("run_bytes", ctypes.c_int64), ("src_stride", ctypes.c_int64 * 4),
+                ("dst_stride", ctypes.c_int64 * 4), ("dst_peer_off", ctypes.c_int64),
+                ("pack_is_identity", ctypes.c_int32), ("unpack_is_identity", ctypes.c_int32)]
+
+
 STAGES = ("LN1", "QKV_S", "ATTN_S", "PROJ_S", "SWITCH_TS", "LN2", "QKV_T", "ATTN_T", "PROJ_T", "LN3", "FC1",
           "FC2", "SWITCH_ST")
 WEIGHT_NAMES = tuple(n for n, _ in BlockWeights._fields_[:12])
@@ -82,6 +88,10 @@ def lib() -> ctypes.CDLL:
             "dsp_switch": [vp, P(Shape), ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int, vp],
             "dsp_switch_volume": [P(Shape), ctypes.c_int, P(i64), P(i64)],
             "dsp_switch_plan": [P(Shape), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P(SwitchPlan)],
+            "dsp_switch_nd_plan": [P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, P(SwitchNdPlan)],
+            "dsp_switch_nd": [vp, P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
+                              vp],
             "dsp_spatial_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
@@ -168,6 +178,15 @@ def switch_plan(shape: Shape, world: int, rank: int, from_dim, to_dim) -> Switch
     p = SwitchPlan()
     _check(lib().dsp_switch_plan(ctypes.byref(shape), int(world), int(rank), DIMS[from_dim], DIMS[to_dim],
                                  ctypes.byref(p)))
+    return p
+
+
+def switch_nd_plan(dims, elem_bytes: int, world: int, rank: int, from_dim: int, to_dim: int) -> SwitchNdPlan:
+    """dsp_switch_nd_plan (host-only): the byte plan of an N-D switch (dims = global extents, channel last)."""
+    p = SwitchNdPlan()
+    d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
+    _check(lib().dsp_switch_nd_plan(d, len(dims), int(elem_bytes), int(world), int(rank), int(from_dim), int(to_dim),
+                                    ctypes.byref(p)))
     return p
 
 
@@ -265,6 +284,12 @@ class Context:
     def switch(self, shape, from_dim, to_dim, x_local, y_local, impl="nccl", stream=None):
         self._call("dsp_switch", ctypes.byref(shape), DIMS[from_dim], DIMS[to_dim], _ptr(x_local), _ptr(y_local),
                    IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def switch_nd(self, dims, from_dim: int, to_dim: int, x_local, y_local, impl="nccl", stream=None):
+        """dsp_switch_nd: N-D dynamic switch of the global [dims] tensor (channel last) between two dims."""
+        d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
+        self._call("dsp_switch_nd", d, len(dims), x_local.element_size(), int(from_dim), int(to_dim), _ptr(x_local),
+                   _ptr(y_local), IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
 
     # ---- compute
     def spatial_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):

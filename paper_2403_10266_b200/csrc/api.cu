@@ -177,19 +177,13 @@ bool in_region(const void* p, int64_t n, const void* base, size_t bytes) {
 }
 
 // Execute a switch with explicit scratch (send/recv each >= shard bytes when needed).
-dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void* x, void* y, dsp_switch_impl_t impl,
-                       cudaStream_t st, void* scratch_send, void* scratch_recv) {
+// Execute a switch plan (4-level strided runs, level 0 = peer): P2P = entry barrier, direct
+// stores of every run at its final address in the peer's buffer, exit barrier; NCCL = pack into
+// per-peer chunks (skipped when identity) -> ncclAlltoAll (bytes) -> unpack (skipped when identity).
+dsp_status_t do_switch_plan(dsp_ctx_t ctx, const RunCopy& rc, int64_t dst_peer_off, bool pack_identity,
+                            bool unpack_identity, int64_t bytes, const void* x, void* y, dsp_switch_impl_t impl,
+                            cudaStream_t st, void* scratch_send, void* scratch_recv) {
   const int N = ctx->world;
-  const int64_t bytes = shard_bytes(s, N);
-  if (N == 1) {
-    if (x != y) DSP_CUDA(ctx, cudaMemcpyAsync(y, x, bytes, cudaMemcpyDeviceToDevice, st), "switch copy (N=1)");
-    return DSP_OK;
-  }
-  dsp_switch_plan_t p;
-  make_plan(s, N, ctx->rank, from, &p);
-  RunCopy rc;
-  for (int i = 0; i < 3; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
-  rc.run_bytes = p.run_bytes;
   if (impl == DSP_SWITCH_P2P) {
     if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P switch without dsp_ctx_set_peer_buffers");
     void* base = ctx->peer_base.p[ctx->rank];
@@ -197,24 +191,25 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
       return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P switch destination is not inside the registered symmetric buffer");
     const int64_t y_off = static_cast<uint8_t*>(y) - static_cast<uint8_t*>(base);
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p entry barrier");
-    DSP_CUDA(ctx, launch_p2p_put(x, ctx->peer_base, y_off + p.dst_peer_off, rc, ctx->num_sms, st), "p2p put");
+    DSP_CUDA(ctx, launch_p2p_put(x, ctx->peer_base, y_off + dst_peer_off, rc, ctx->num_sms, st), "p2p put");
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p exit barrier");
     ctx->launches += 3;
     return DSP_OK;
   }
   if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
-  const int64_t chunk = p.n[1] * p.n[2] * p.run_bytes;  // bytes per peer
+  const int64_t chunk = rc.n[1] * rc.n[2] * rc.n[3] * rc.run_bytes;  // bytes per peer
   RunCopy pack = rc, unpack = rc;
-  pack.ds[0] = chunk; pack.ds[1] = p.n[2] * p.run_bytes; pack.ds[2] = p.run_bytes;
-  unpack.ss[0] = pack.ds[0]; unpack.ss[1] = pack.ds[1]; unpack.ss[2] = pack.ds[2];
+  pack.ds[0] = chunk; pack.ds[1] = rc.n[2] * rc.n[3] * rc.run_bytes; pack.ds[2] = rc.n[3] * rc.run_bytes;
+  pack.ds[3] = rc.run_bytes;
+  for (int i = 0; i < 4; ++i) unpack.ss[i] = pack.ds[i];
   const void* send = x;
   void* recv = y;
-  if (!p.pack_is_identity) {
+  if (!pack_identity) {
     DSP_CUDA(ctx, launch_run_copy(x, scratch_send, pack, ctx->num_sms, st), "switch pack");
     ctx->launches += 1;
     send = scratch_send;
   }
-  if (!p.unpack_is_identity) recv = scratch_recv;
+  if (!unpack_identity) recv = scratch_recv;
   int r;
   if (ctx->nccl.AlltoAll) {
     r = ctx->nccl.AlltoAll(send, recv, (size_t)chunk, kNcclUint8, ctx->comm, st);
@@ -228,11 +223,28 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
     if (!r) r = r2;
   }
   if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAlltoAll: %s", ctx->nccl.GetErrorString(r));
-  if (!p.unpack_is_identity) {
+  if (!unpack_identity) {
     DSP_CUDA(ctx, launch_run_copy(recv, y, unpack, ctx->num_sms, st), "switch unpack");
     ctx->launches += 1;
   }
   return DSP_OK;
+}
+
+dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void* x, void* y, dsp_switch_impl_t impl,
+                       cudaStream_t st, void* scratch_send, void* scratch_recv) {
+  const int N = ctx->world;
+  const int64_t bytes = shard_bytes(s, N);
+  if (N == 1) {
+    if (x != y) DSP_CUDA(ctx, cudaMemcpyAsync(y, x, bytes, cudaMemcpyDeviceToDevice, st), "switch copy (N=1)");
+    return DSP_OK;
+  }
+  dsp_switch_plan_t p;
+  make_plan(s, N, ctx->rank, from, &p);
+  RunCopy rc;
+  for (int i = 0; i < 3; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
+  rc.run_bytes = p.run_bytes;
+  return do_switch_plan(ctx, rc, p.dst_peer_off, p.pack_is_identity, p.unpack_is_identity, bytes, x, y, impl, st,
+                        scratch_send, scratch_recv);
 }
 
 inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
@@ -493,6 +505,101 @@ dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, cons
     ctx->launches += 1;
   }
   return DSP_OK;
+}
+
+// N-D plan (see include/dsp.h).  With a = from, b = to, inner = prod(d after max(a, b)) * elem:
+//   a < b: runs of (d_b/N)*inner bytes over (peer q, outer, i_a in [0, d_a/N), middle); peer q
+//          gets the i_b block q; lands at i_a + rank*d_a/N in q's [.., d_a, .., d_b/N, ..];
+//   a > b: runs of (d_a/N)*inner bytes over (peer q, outer, i_b in block q, middle); lands at
+//          i_b - q*d_b/N, with the run at offset rank*(d_a/N)*inner, in q's [.., d_b/N, .., d_a, ..].
+static dsp_status_t make_plan_nd(dsp_ctx_t ctx, const int64_t* d, int nd, int e, int N, int rank, int a, int b,
+                                 dsp_switch_nd_plan_t* p) {
+  if (!d || !p) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  if (nd < 3 || nd > DSP_ND_MAX_DIMS) return fail(ctx, DSP_ERR_SHAPE, "ndim %d outside [3, %d]", nd, DSP_ND_MAX_DIMS);
+  if (e < 1 || N < 1) return fail(ctx, DSP_ERR_SHAPE, "elem_bytes %d / world %d < 1", e, N);
+  for (int i = 0; i < nd; ++i)
+    if (d[i] < 1) return fail(ctx, DSP_ERR_SHAPE, "extent %d is %lld", i, (long long)d[i]);
+  if (a < 0 || a > nd - 2 || b < 0 || b > nd - 2) return fail(ctx, DSP_ERR_BAD_DIM, "switch dims must be in [0, %d]", nd - 2);
+  if (a == b) return fail(ctx, DSP_ERR_SAME_DIM, "switch from a dim to itself (S:283)");
+  if (rank < 0 || rank >= N) return fail(ctx, DSP_ERR_SHAPE, "rank %d outside [0, %d)", rank, N);
+  if (d[a] % N || d[b] % N) return fail(ctx, DSP_ERR_DIVISIBILITY, "world %d does not divide d[%d]=%lld / d[%d]=%lld", N, a,
+                                        (long long)d[a], b, (long long)d[b]);
+  const int lo = a < b ? a : b, hi = a < b ? b : a;
+  int64_t outer = 1, mid = 1, inner = e;
+  for (int i = 0; i < lo; ++i) outer *= d[i];
+  for (int i = lo + 1; i < hi; ++i) mid *= d[i];
+  for (int i = hi + 1; i < nd; ++i) inner *= d[i];
+  const int64_t ra = d[a] / N, rb = d[b] / N;
+  memset(p, 0, sizeof(*p));
+  p->n[0] = N; p->n[1] = outer; p->n[3] = mid;
+  if (a < b) {  // x [outer, d_a/N, mid, d_b, inner] -> y [outer, d_a, mid, d_b/N, inner]
+    p->n[2] = ra;
+    p->run_bytes = rb * inner;
+    p->src_stride[0] = rb * inner; p->src_stride[1] = ra * mid * d[b] * inner;
+    p->src_stride[2] = mid * d[b] * inner; p->src_stride[3] = d[b] * inner;
+    p->dst_stride[1] = d[a] * mid * rb * inner; p->dst_stride[2] = mid * rb * inner; p->dst_stride[3] = rb * inner;
+    p->dst_stride[0] = ra * p->dst_stride[2];
+  } else {      // x [outer, d_b, mid, d_a/N, inner] -> y [outer, d_b/N, mid, d_a, inner]
+    p->n[2] = rb;
+    p->run_bytes = ra * inner;
+    p->src_stride[0] = rb * mid * ra * inner; p->src_stride[1] = d[b] * mid * ra * inner;
+    p->src_stride[2] = mid * ra * inner; p->src_stride[3] = ra * inner;
+    p->dst_stride[1] = rb * mid * d[a] * inner; p->dst_stride[2] = mid * d[a] * inner; p->dst_stride[3] = d[a] * inner;
+    p->dst_stride[0] = ra * inner;
+  }
+  p->dst_peer_off = rank * p->dst_stride[0];
+  if (p->run_bytes % 16) return fail(ctx, DSP_ERR_ALIGNMENT, "switch runs of %lld bytes are not 16-B multiples", (long long)p->run_bytes);
+  // pack is an identity when peer q's runs already sit contiguously at q * chunk in x; unpack
+  // when the received [source rank][outer][rows][middle] layout is y's own layout
+  const int64_t R = p->run_bytes, chunk = p->n[1] * p->n[2] * p->n[3] * R;
+  auto same = [&](const int64_t* st) {
+    return (p->n[3] == 1 || st[3] == R) && (p->n[2] == 1 || st[2] == p->n[3] * R) &&
+           (p->n[1] == 1 || st[1] == p->n[2] * p->n[3] * R) && st[0] == chunk;
+  };
+  p->pack_is_identity = N == 1 || same(p->src_stride);
+  p->unpack_is_identity = N == 1 || same(p->dst_stride);
+  return DSP_OK;
+}
+
+dsp_status_t dsp_switch_nd_plan(const int64_t* dims, int ndim, int elem_bytes, int world, int rank, int from_dim,
+                                int to_dim, dsp_switch_nd_plan_t* plan) {
+  return make_plan_nd(nullptr, dims, ndim, elem_bytes, world, rank, from_dim, to_dim, plan);
+}
+
+dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int elem_bytes, int from_dim, int to_dim,
+                           const void* x, void* y, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  dsp_switch_nd_plan_t p;
+  DSP_TRY(make_plan_nd(ctx, dims, ndim, elem_bytes, ctx->world, ctx->rank, from_dim, to_dim, &p));
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
+  if (impl == DSP_SWITCH_FUSED) impl = DSP_SWITCH_P2P;
+  if (!x || !y) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int N = ctx->world;
+  int64_t bytes = elem_bytes;
+  for (int i = 0; i < ndim; ++i) bytes *= dims[i];
+  bytes /= N;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N == 1) {
+    if (x != y) DSP_CUDA(ctx, cudaMemcpyAsync(y, x, bytes, cudaMemcpyDeviceToDevice, st), "switch copy (N=1)");
+    return DSP_OK;
+  }
+  if (overlap(x, bytes, y, bytes)) return fail(ctx, DSP_ERR_ALIAS, "x_local overlaps y_local");
+  void* send = nullptr;
+  void* recv = nullptr;
+  if (impl == DSP_SWITCH_NCCL) {
+    const int64_t need = (p.pack_is_identity ? 0 : bytes) + (p.unpack_is_identity ? 0 : bytes);
+    if (need && (!ctx->ws || ctx->ws_bytes < (size_t)need))
+      return fail(ctx, DSP_ERR_WORKSPACE, "switch needs %lld bytes of workspace", (long long)need);
+    send = ctx->ws;
+    recv = static_cast<uint8_t*>(ctx->ws) + (p.pack_is_identity ? 0 : bytes);
+  }
+  RunCopy rc;
+  for (int i = 0; i < 4; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
+  rc.run_bytes = p.run_bytes;
+  return do_switch_plan(ctx, rc, p.dst_peer_off, p.pack_is_identity, p.unpack_is_identity, bytes, x, y, impl, st, send,
+                        recv);
 }
 
 dsp_status_t dsp_switch(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp_dim_t to, const void* x, void* y,

@@ -36,10 +36,12 @@ struct PeerPtrs {
 };
 
 // strided byte-run copy: run (i0,i1,i2) of run_bytes from src + sum(i*ss) to dst + sum(i*ds)
+// Strided run copy: runs (i0, i1, i2, i3) over extents n[], each run_bytes contiguous bytes at
+// src + sum(i_k * ss[k]) -> dst + sum(i_k * ds[k]) (level 0 selects the peer in a P2P put).
 struct RunCopy {
-  int64_t n[3];
-  int64_t run_bytes;
-  int64_t ss[3], ds[3];
+  int64_t n[4] = {1, 1, 1, 1};
+  int64_t run_bytes = 0;
+  int64_t ss[4] = {0, 0, 0, 0}, ds[4] = {0, 0, 0, 0};
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----

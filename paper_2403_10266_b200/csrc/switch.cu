@@ -24,31 +24,35 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
                : "memory");
 }
 
-// blockIdx.y = run index (i0*n1 + i1)*n2 + i2; blockIdx.x strides over the run's vectors.
+// run index (((i0*n1 + i1)*n2 + i2)*n3 + i3) = blockIdx.y + k*gridDim.y; blockIdx.x strides over
+// the run's 16-B vectors.
 __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
                                                             RunCopy rc, PeerPtrs peers, int use_peers, int64_t peer_off) {
   griddep_wait();
   griddep_launch_dependents();
-  const int64_t run = blockIdx.y;
-  const int64_t i2 = run % rc.n[2];
-  const int64_t i1 = (run / rc.n[2]) % rc.n[1];
-  const int64_t i0 = run / (rc.n[2] * rc.n[1]);
-  const uint4* s = reinterpret_cast<const uint4*>(src + i0 * rc.ss[0] + i1 * rc.ss[1] + i2 * rc.ss[2]);
-  uint8_t* dbase = use_peers ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
-  uint4* d = reinterpret_cast<uint4*>(dbase + i1 * rc.ds[1] + i2 * rc.ds[2]);
+  const int64_t runs = rc.n[0] * rc.n[1] * rc.n[2] * rc.n[3];
   const int64_t nv = rc.run_bytes / 16;
   const int64_t step = (int64_t)gridDim.x * kThreads * kUnroll;
-  for (int64_t v0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; v0 < nv; v0 += step) {
-    uint4 buf[kUnroll];
+  for (int64_t run = blockIdx.y; run < runs; run += gridDim.y) {
+    const int64_t i3 = run % rc.n[3];
+    const int64_t i2 = (run / rc.n[3]) % rc.n[2];
+    const int64_t i1 = (run / (rc.n[3] * rc.n[2])) % rc.n[1];
+    const int64_t i0 = run / (rc.n[3] * rc.n[2] * rc.n[1]);
+    const uint4* s = reinterpret_cast<const uint4*>(src + i0 * rc.ss[0] + i1 * rc.ss[1] + i2 * rc.ss[2] + i3 * rc.ss[3]);
+    uint8_t* dbase = use_peers ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
+    uint4* d = reinterpret_cast<uint4*>(dbase + i1 * rc.ds[1] + i2 * rc.ds[2] + i3 * rc.ds[3]);
+    for (int64_t v0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; v0 < nv; v0 += step) {
+      uint4 buf[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t v = v0 + u * kThreads;
-      if (v < nv) buf[u] = ld_stream(s + v);
-    }
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t v = v0 + u * kThreads;
+        if (v < nv) buf[u] = ld_stream(s + v);
+      }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t v = v0 + u * kThreads;
-      if (v < nv) st_stream(d + v, buf[u]);
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t v = v0 + u * kThreads;
+        if (v < nv) st_stream(d + v, buf[u]);
+      }
     }
   }
 }
@@ -78,16 +82,17 @@ __global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64
 
 static cudaError_t launch_copy(const void* src, void* dst, const RunCopy& rc, const PeerPtrs& peers, int use_peers,
                                int64_t peer_off, int num_sms, cudaStream_t st) {
-  const int64_t runs = rc.n[0] * rc.n[1] * rc.n[2];
+  const int64_t runs = rc.n[0] * rc.n[1] * rc.n[2] * rc.n[3];
   if (runs == 0 || rc.run_bytes == 0) return cudaSuccess;
-  if (runs > 65535) return cudaErrorInvalidValue;
+  if (rc.run_bytes % 16) return cudaErrorInvalidValue;
   const int64_t nv = rc.run_bytes / 16;
   int64_t bx = (nv + kThreads * kUnroll - 1) / (kThreads * kUnroll);
   const int64_t want = (int64_t)num_sms * 8;  // ~8 resident CTAs per SM in total
   int64_t cap = (want + runs - 1) / runs;
   if (cap < 1) cap = 1;
   if (bx > cap) bx = cap;
-  dim3 grid((unsigned)bx, (unsigned)runs);
+  const int64_t gy = runs < 65535 ? runs : 65535;  // runs beyond gridDim.y are strided over
+  dim3 grid((unsigned)bx, (unsigned)gy);
   return launch_k(run_copy_kernel, grid, dim3(kThreads), 0, st, 1, static_cast<const uint8_t*>(src),
                   static_cast<uint8_t*>(dst), rc, peers, use_peers, peer_off);
 }

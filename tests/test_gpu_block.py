@@ -255,3 +255,30 @@ def test_block_host_pipelined_equals_device_path():
         assert torch.equal(yh[i], want[i]), f"step {i}"
     with pytest.raises(m.DSPError):  # staging buffers must not overlap
         ctx.st_block_forward_host_pipelined(shape, W, xh[:2], yh[:2], [xd[0], xd[1]], [xd[0], yd[1]])
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_switch_nd_p2p_virtual_ranks_bitexact(N):
+    """dsp_switch_nd through the P2P kernels (virtual ranks) on a 5-D [B, T, H, W, C] activation,
+    every ordered pair of sequence dims, bit-exact against the oracle's N-D switch; round trip."""
+    m = dsp()
+    dims = (2, 8, 8, 16, 64)
+    g = (np.arange(int(np.prod(dims)), dtype=np.int64) * 2654435761 % 65521).astype(np.int16).reshape(dims)
+    nb = g.nbytes // N
+    grp = VirtualGroup(N, 2 * nb)
+    for a in range(1, 4):
+        for b in range(1, 4):
+            if a == b:
+                continue
+            sh = osw.split_nd(g, a, N)
+            want = osw.switch_nd(sh, a, b)
+            for r in range(N):
+                grp.view(r, 0, nb, torch.int16).copy_(torch.from_numpy(sh[r].reshape(-1)))
+            xin = [grp.view(r, 0, nb, torch.int16) for r in range(N)]
+            ys = [grp.view(r, nb, nb, torch.int16) for r in range(N)]
+            grp.run(lambda r: grp.ctx[r].switch_nd(dims, a, b, xin[r], ys[r], impl="p2p"))
+            for r in range(N):
+                assert np.array_equal(ys[r].cpu().numpy(), want[r].reshape(-1)), (a, b, r)
+            grp.run(lambda r: grp.ctx[r].switch_nd(dims, b, a, ys[r], xin[r], impl="p2p"))
+            for r in range(N):
+                assert np.array_equal(xin[r].cpu().numpy(), sh[r].reshape(-1)), ("back", a, b, r)
