@@ -17,6 +17,8 @@ What it computes (PAPER.md = P:line, SPEC.md = S:line):
   * sharded.py — the DSP schedule over N simulated ranks (Fig. 1/2):
                  split -> spatial stage on T-shards -> switch T->S -> temporal stage
                  + MLP on S-shards -> switch S->T -> gather.
+  * block_nd.py — the multi-dimensional block (attention along any list of dims)
+                 and its DSP schedule with N-D switches (P:93 generalisation).
   * volume.py  — the communication-volume analysis of §3.2 / Table 1.
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`) tie each function to something
