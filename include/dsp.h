@@ -277,6 +277,27 @@ dsp_status_t dsp_switch_nd_plan(const int64_t* dims, int ndim, int elem_bytes, i
 dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int elem_bytes, int from_dim,
                            int to_dim, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
 
+/* ---------------------------------------------------------------- N-D block
+ * Multi-dimensional transformer block on x [d_0, ..., d_{n-2}, C] with attention
+ * along each of the dims attn_dims[0..n_stages-1] in that order (pre-LN + residual, R1-R8),
+ * then the MLP (ratio 4, tanh-GELU):  for k in attn_dims: x += MHA_k(LN_k x);  y = x + MLP(LN x).
+ * DSP schedule (generalised): x_local / y_local are chunk `rank` along shard_dim; stages
+ * along other dims are local; before the stage along shard_dim ONE N-D switch to the dim
+ * attended just before it, and after the MLP one switch back -- two per block, none
+ * if shard_dim is not attended.  shard_dim != attn_dims[0].  dsp_st_block_forward is the
+ * case [B, T, S, C], attn_dims = {S, T}, shard_dim = T (raw weights).  Workspace >=
+ * dsp_nd_workspace_bytes.  COLLECTIVE.  Errors: NULL, SHAPE (ndim, dims, heads, stages),
+ * BAD_DIM (a dim outside [0, n-2], repeated, or shard_dim == attn_dims[0]), DIVISIBILITY,
+ * UNSUPPORTED (bf16 attention length / head-dim limits as dsp_spatial_attn), ALIGNMENT,
+ * ALIAS, WORKSPACE, STATE, NCCL, CUDA. */
+typedef struct { const void *ln_w, *ln_b, *w_qkv /*[3C, C]*/, *w_o /*[C, C]*/; } dsp_attn_weights_t;
+typedef struct { const void *ln_w, *ln_b, *w_fc1 /*[4C, C]*/, *w_fc2 /*[C, 4C]*/; } dsp_mlp_weights_t;
+size_t dsp_nd_workspace_bytes(const int64_t* dims, int ndim, dsp_dtype_t dtype, int world);  /* host-only */
+dsp_status_t dsp_nd_block_forward(dsp_ctx_t ctx, const int64_t* dims, int ndim, int num_heads, dsp_dtype_t dtype,
+                                  int n_stages, const int* attn_dims, const dsp_attn_weights_t* attn,
+                                  const dsp_mlp_weights_t* mlp, float ln_eps, int shard_dim, const void* x_local,
+                                  void* y_local, dsp_switch_impl_t impl, void* stream);
+
 /* Forward of a stack of L ST blocks, y = block_{L-1}( ... block_0(x)) (BASELINE configs[2]:
  * the 28-layer ST-DiT-XL/2-shaped model), x and y T-sharded as for one block (x may
  * equal y; blocks 1.. run in place on y).  w: HOST array of L block-weight structs.  With

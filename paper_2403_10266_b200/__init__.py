@@ -62,6 +62,14 @@ class SwitchNdPlan(ctypes.Structure):
                 ("pack_is_identity", ctypes.c_int32), ("unpack_is_identity", ctypes.c_int32)]
 
 
+class AttnWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("ln_w", "ln_b", "w_qkv", "w_o")]
+
+
+class MlpWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("ln_w", "ln_b", "w_fc1", "w_fc2")]
+
+
 STAGES = ("LN1", "QKV_S", "ATTN_S", "PROJ_S", "SWITCH_TS", "LN2", "QKV_T", "ATTN_T", "PROJ_T", "LN3", "FC1",
           "FC2", "SWITCH_ST")
 WEIGHT_NAMES = tuple(n for n, _ in BlockWeights._fields_[:12])
@@ -92,6 +100,9 @@ def lib() -> ctypes.CDLL:
                                    ctypes.c_int, P(SwitchNdPlan)],
             "dsp_switch_nd": [vp, P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
                               vp],
+            "dsp_nd_block_forward": [vp, P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     P(ctypes.c_int), P(AttnWeights), P(MlpWeights), ctypes.c_float, ctypes.c_int, vp,
+                                     vp, ctypes.c_int, vp],
             "dsp_spatial_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
@@ -111,6 +122,8 @@ def lib() -> ctypes.CDLL:
             f.restype = ctypes.c_int
         L.dsp_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
         L.dsp_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_nd_workspace_bytes.argtypes = [P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        L.dsp_nd_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_block_prepared_bytes.argtypes = [P(Shape)]
         L.dsp_block_prepared_bytes.restype = ctypes.c_size_t
         L.dsp_status_str.argtypes = [ctypes.c_int]
@@ -179,6 +192,11 @@ def switch_plan(shape: Shape, world: int, rank: int, from_dim, to_dim) -> Switch
     _check(lib().dsp_switch_plan(ctypes.byref(shape), int(world), int(rank), DIMS[from_dim], DIMS[to_dim],
                                  ctypes.byref(p)))
     return p
+
+
+def nd_workspace_bytes(dims, dtype, world: int) -> int:
+    d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
+    return int(lib().dsp_nd_workspace_bytes(d, len(dims), _dtype_code(dtype), int(world)))
 
 
 def switch_nd_plan(dims, elem_bytes: int, world: int, rank: int, from_dim: int, to_dim: int) -> SwitchNdPlan:
@@ -290,6 +308,19 @@ class Context:
         d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
         self._call("dsp_switch_nd", d, len(dims), x_local.element_size(), int(from_dim), int(to_dim), _ptr(x_local),
                    _ptr(y_local), IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    # ---- N-D block (multi-dimensional transformer; DSP schedule P:93)
+    def nd_block_forward(self, dims, num_heads: int, attn_dims, stages, mlp, shard_dim: int, x_local, y_local,
+                         impl="nccl", eps: float = 1e-5, stream=None):
+        """stages: per attended dim, dict(ln_w, ln_b, w_qkv, w_o); mlp: dict(ln_w, ln_b, w_fc1, w_fc2)."""
+        d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
+        order = (ctypes.c_int * len(attn_dims))(*[int(k) for k in attn_dims])
+        aw = (AttnWeights * len(stages))(*[AttnWeights(*[_ptr(w[n]) for n in ("ln_w", "ln_b", "w_qkv", "w_o")])
+                                           for w in stages])
+        mw = MlpWeights(*[_ptr(mlp[n]) for n in ("ln_w", "ln_b", "w_fc1", "w_fc2")])
+        self._call("dsp_nd_block_forward", d, len(dims), int(num_heads), _dtype_code(x_local.dtype), len(stages),
+                   order, aw, ctypes.byref(mw), ctypes.c_float(eps), int(shard_dim), _ptr(x_local), _ptr(y_local),
+                   IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
 
     # ---- compute
     def spatial_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):

@@ -845,6 +845,128 @@ dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   return DSP_OK;
 }
 
+size_t dsp_nd_workspace_bytes(const int64_t* dims, int ndim, dsp_dtype_t dtype, int world) {
+  if (!dims || ndim < 3 || ndim > DSP_ND_MAX_DIMS || world < 1) return 0;
+  int64_t tok = 1;
+  for (int i = 0; i < ndim - 1; ++i) {
+    if (dims[i] < 1) return 0;
+    tok *= dims[i];
+  }
+  if (dims[ndim - 1] < 1) return 0;
+  return (size_t)(6 * (tok / world) * dims[ndim - 1] * elem_bytes(dtype) + 256);  // h | qkv + o / hidden | ys
+}
+
+dsp_status_t dsp_nd_block_forward(dsp_ctx_t ctx, const int64_t* d, int nd, int num_heads, dsp_dtype_t dtype,
+                                  int n_stages, const int* order, const dsp_attn_weights_t* attn,
+                                  const dsp_mlp_weights_t* mlp, float eps, int shard_dim, const void* x, void* y,
+                                  dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!d || !order || !attn || !mlp || !x || !y) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  if (nd < 3 || nd > DSP_ND_MAX_DIMS) return fail(ctx, DSP_ERR_SHAPE, "ndim %d outside [3, %d]", nd, DSP_ND_MAX_DIMS);
+  if (dtype != DSP_BF16 && dtype != DSP_F32) return fail(ctx, DSP_ERR_SHAPE, "unknown dtype");
+  for (int i = 0; i < nd; ++i)
+    if (d[i] < 1) return fail(ctx, DSP_ERR_SHAPE, "extent %d is %lld", i, (long long)d[i]);
+  const int N = ctx->world;
+  const int64_t C = d[nd - 1], e = elem_bytes(dtype);
+  if (num_heads < 1 || C % num_heads) return fail(ctx, DSP_ERR_SHAPE, "C=%lld not divisible by num_heads=%d", (long long)C, num_heads);
+  if (n_stages < 1 || n_stages > nd - 1) return fail(ctx, DSP_ERR_SHAPE, "n_stages %d outside [1, %d]", n_stages, nd - 1);
+  if (shard_dim < 0 || shard_dim > nd - 2) return fail(ctx, DSP_ERR_BAD_DIM, "shard_dim %d outside [0, %d]", shard_dim, nd - 2);
+  int alt = -1;  // the dim the activation is switched to before the stage along shard_dim
+  for (int i = 0; i < n_stages; ++i) {
+    if (order[i] < 0 || order[i] > nd - 2) return fail(ctx, DSP_ERR_BAD_DIM, "attention dim %d outside [0, %d]", order[i], nd - 2);
+    for (int j = 0; j < i; ++j)
+      if (order[j] == order[i]) return fail(ctx, DSP_ERR_BAD_DIM, "attention dim %d repeated", order[i]);
+    if (order[i] == shard_dim) {
+      if (i == 0) return fail(ctx, DSP_ERR_BAD_DIM, "the first attended dim cannot be the sharded one");
+      alt = order[i - 1];
+    }
+  }
+  if (d[shard_dim] % N || (alt >= 0 && d[alt] % N))
+    return fail(ctx, DSP_ERR_DIVISIBILITY, "world %d does not divide the sharded dims", N);
+  {
+    const dsp_shape_t hs{1, 1, 1, C, num_heads, dtype};
+    for (int i = 0; i < n_stages; ++i) DSP_TRY(check_bf16_attn(ctx, &hs, d[order[i]]));
+  }
+  const void* wp[4] = {mlp->ln_w, mlp->ln_b, mlp->w_fc1, mlp->w_fc2};
+  for (int i = 0; i < 4; ++i)
+    if (!wp[i] || !aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "MLP weight %d NULL or not 16-B aligned", i);
+  for (int i = 0; i < n_stages; ++i) {
+    const void* a[4] = {attn[i].ln_w, attn[i].ln_b, attn[i].w_qkv, attn[i].w_o};
+    for (int j = 0; j < 4; ++j)
+      if (!a[j] || !aligned16(a[j])) return fail(ctx, DSP_ERR_ALIGNMENT, "stage %d weight %d NULL or not 16-B aligned", i, j);
+  }
+  if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  int64_t tok = 1;
+  for (int i = 0; i < nd - 1; ++i) tok *= d[i];
+  tok /= N;
+  const int64_t act = tok * C * e;
+  const size_t need = dsp_nd_workspace_bytes(d, nd, dtype, N);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "N-D block needs %zu bytes of workspace", need);
+  if (x != y && overlap(x, act, y, act)) return fail(ctx, DSP_ERR_ALIAS, "x_local partially overlaps y_local");
+  if (overlap(ctx->ws, need, x, act) || overlap(ctx->ws, need, y, act)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y");
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  void* h = ws;
+  uint8_t* big = ws + act;          // qkv [tok, 3C] + o [tok, C] | MLP hidden [tok, 4C] | switch scratch
+  void* qkv = big;
+  void* o = big + 3 * act;
+  void* ys = ws + 5 * act;          // the activation while it is sharded on `alt`
+  if (N > 1 && impl == DSP_SWITCH_P2P) {
+    if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P block without dsp_ctx_set_peer_buffers");
+    void* base = ctx->peer_base.p[ctx->rank];
+    if (!in_region(ys, act, base, ctx->peer_bytes) || !in_region(y, act, base, ctx->peer_bytes))
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P block needs the workspace and y_local inside the symmetric buffer");
+  } else if (N > 1 && impl != DSP_SWITCH_NCCL) {
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "the N-D block supports the NCCL and P2P switch transports");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  auto nd_switch = [&](const void* src, void* dst, int from, int to) -> dsp_status_t {
+    dsp_switch_nd_plan_t p;
+    DSP_TRY(make_plan_nd(ctx, d, nd, (int)e, N, ctx->rank, from, to, &p));
+    RunCopy rc;
+    for (int i = 0; i < 4; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
+    rc.run_bytes = p.run_bytes;
+    return do_switch_plan(ctx, rc, p.dst_peer_off, p.pack_is_identity, p.unpack_is_identity, act, src, dst, impl, st,
+                          big, big + act);
+  };
+  int64_t ld[DSP_ND_MAX_DIMS];
+  for (int i = 0; i < nd; ++i) ld[i] = d[i];
+  int cur = shard_dim;
+  ld[cur] /= N;
+  const void* in = x;
+  void* buf = nullptr;  // the buffer the activation lives in after the first stage (y or ys)
+  for (int i = 0; i < n_stages; ++i) {
+    const int k = order[i];
+    if (k == cur && N > 1) {  // switch before the stage along the sharded dim
+      DSP_TRY(nd_switch(in, ys, cur, alt));
+      ld[cur] = d[cur];
+      cur = alt;
+      ld[cur] = d[cur] / N;
+      in = ys;
+      buf = ys;
+    }
+    int64_t before = 1, after = 1;
+    for (int j = 0; j < k; ++j) before *= ld[j];
+    for (int j = k + 1; j < nd - 1; ++j) after *= ld[j];
+    const int64_t L = ld[k];
+    void* out = buf ? buf : y;
+    DSP_CUDA(ctx, launch_layer_norm(dtype, tok, C, in, attn[i].ln_w, attn[i].ln_b, eps, h, st), "N-D block LN");
+    ctx->launches += 1;
+    // attention along k: sequences of length L at a stride of `after` rows, `before` outer groups
+    const dsp_shape_t s2{after == 1 ? 1 : before, 1, 1, C, num_heads, dtype};
+    if (after == 1) DSP_TRY(attn_stage(ctx, &s2, before, L, DSP_DIM_S, h, attn[i].w_qkv, attn[i].w_o, in, out, qkv, o, st));
+    else DSP_TRY(attn_stage(ctx, &s2, L, after, DSP_DIM_T, h, attn[i].w_qkv, attn[i].w_o, in, out, qkv, o, st));
+    in = out;
+    buf = out;
+  }
+  void* cur_buf = buf;  // n_stages >= 1, so the activation is in y or ys
+  DSP_CUDA(ctx, launch_layer_norm(dtype, tok, C, cur_buf, mlp->ln_w, mlp->ln_b, eps, h, st), "N-D block LN (MLP)");
+  ctx->launches += 1;
+  DSP_TRY(linear(ctx, dtype, tok, 4 * C, C, h, mlp->w_fc1, nullptr, DSP_EPI_GELU, big, st));
+  DSP_TRY(linear(ctx, dtype, tok, C, 4 * C, big, mlp->w_fc2, cur_buf, DSP_EPI_RESIDUAL, cur_buf, st));
+  if (cur != shard_dim && N > 1) DSP_TRY(nd_switch(cur_buf, y, cur, shard_dim));
+  return DSP_OK;
+}
+
 size_t dsp_block_prepared_bytes(const dsp_shape_t* s) {
   if (!s || s->C < 1 || s->dtype != DSP_BF16) return 0;
   return (size_t)prep_layout(s->C).total;

@@ -282,3 +282,103 @@ def test_switch_nd_p2p_virtual_ranks_bitexact(N):
             grp.run(lambda r: grp.ctx[r].switch_nd(dims, b, a, ys[r], xin[r], impl="p2p"))
             for r in range(N):
                 assert np.array_equal(xin[r].cpu().numpy(), sh[r].reshape(-1)), ("back", a, b, r)
+
+
+# ------------------------------------------------------------------ N-D block
+def _nd_weights(C, nstages, seed, dtype="bf16"):
+    """Seeded stage / MLP weights (bf16-representable) as host f64 and device tensors."""
+    rng = np.random.default_rng(seed)
+    def mk(shape, sc):
+        v = rng.uniform(-1, 1, size=shape) * sc
+        bits = synth.round_to_bf16_bits(v)
+        return synth.bf16_bits_to_f64(bits), to_dev(bits, "bf16")
+    st_h, st_d = [], []
+    for _ in range(nstages):
+        parts = dict(ln_w=mk((C,), 0.1), ln_b=mk((C,), 0.1), w_qkv=mk((3 * C, C), np.sqrt(3 / C)),
+                     w_o=mk((C, C), np.sqrt(3 / C)))
+        parts["ln_w"] = (parts["ln_w"][0] + 1.0, to_dev(synth.round_to_bf16_bits(parts["ln_w"][0] + 1.0), "bf16"))
+        st_h.append({k: v[0] for k, v in parts.items()})
+        st_d.append({k: v[1] for k, v in parts.items()})
+    m = dict(ln_w=mk((C,), 0.1), ln_b=mk((C,), 0.1), w_fc1=mk((4 * C, C), np.sqrt(3 / C)),
+             w_fc2=mk((C, 4 * C), 0.5 * np.sqrt(3 / (4 * C))))
+    m["ln_w"] = (m["ln_w"][0] + 1.0, to_dev(synth.round_to_bf16_bits(m["ln_w"][0] + 1.0), "bf16"))
+    return st_h, st_d, {k: v[0] for k, v in m.items()}, {k: v[1] for k, v in m.items()}
+
+
+def test_nd_block_4d_equals_st_block():
+    """[B, T, S, C] with attention along S then T, sharded on T: dsp_nd_block_forward is the ST block
+    (raw weights), bitwise."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, Ws = _setup(sh)
+    ref = bits16(_run_block_n1(sh, xs, Ws))
+    W = weights_dev(Ws, "bf16")
+    stages = [dict(ln_w=W["ln1_w"], ln_b=W["ln1_b"], w_qkv=W["w_qkv_s"], w_o=W["w_o_s"]),
+              dict(ln_w=W["ln2_w"], ln_b=W["ln2_b"], w_qkv=W["w_qkv_t"], w_o=W["w_o_t"])]
+    mlp = dict(ln_w=W["ln3_w"], ln_b=W["ln3_b"], w_fc1=W["w_fc1"], w_fc2=W["w_fc2"])
+    dims = (sh.B, sh.T, sh.S, sh.C)
+    ctx = m.Context()
+    ctx.ensure_workspace(m.nd_workspace_bytes(dims, "bf16", 1))
+    X = to_dev(xs, "bf16")
+    Y = torch.empty_like(X)
+    ctx.nd_block_forward(dims, sh.NH, (2, 1), stages, mlp, 1, X, Y)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits16(Y), ref)
+
+
+@pytest.mark.parametrize("axis", [3, 2, 1])
+def test_nd_block_5d_single_stage_vs_oracle(axis):
+    """[B, T, H, W, C] = [1, 8, 16, 32, 256]: one attention stage along W (spatial-mode packing,
+    4 sequences per tile), H (strided, 8 per tile) or T (strided, 16 per tile) + MLP, against
+    the float64 oracle at the block gate (R22)."""
+    from oracle import block_nd as obn
+    m = dsp()
+    dims, NH = (1, 8, 16, 32, 256), 4
+    st_h, st_d, mlp_h, mlp_d = _nd_weights(dims[-1], 1, 20 + axis)
+    xbits = synth.round_to_bf16_bits(np.random.default_rng(axis).uniform(-1, 1, size=dims))
+    ctx = m.Context()
+    ctx.ensure_workspace(m.nd_workspace_bytes(dims, "bf16", 1))
+    X = to_dev(xbits, "bf16")
+    Y = torch.empty_like(X)
+    ctx.nd_block_forward(dims, NH, (axis,), st_d, mlp_d, 0 if axis != 0 else 1, X, Y)
+    torch.cuda.synchronize()
+    ref = obn.nd_block(synth.bf16_bits_to_f64(xbits), (axis,), st_h, mlp_h, NH)
+    print(assert_block_close(to_f64(Y), ref))
+
+
+def test_nd_block_5d_vs_oracle_and_virtual_ranks():
+    """[B, T, H, W, C] = [1, 8, 16, 32, 256], attention along W, H, T (3 stages), sharded on T:
+    N = 1 against the float64 oracle (rel-L2 gate: four residual-stream roundings instead of the
+    ST block's three, R32); N = 2, 4 virtual ranks (P2P N-D switches) bitwise equal to N = 1."""
+    from oracle import block_nd as obn
+    m = dsp()
+    dims, NH, order, shard = (1, 8, 16, 32, 256), 4, (3, 2, 1), 1
+    C = dims[-1]
+    st_h, st_d, mlp_h, mlp_d = _nd_weights(C, 3, 11)
+    rng = np.random.default_rng(12)
+    xbits = synth.round_to_bf16_bits(rng.uniform(-1, 1, size=dims))
+    x64 = synth.bf16_bits_to_f64(xbits)
+    ctx = m.Context()
+    ctx.ensure_workspace(m.nd_workspace_bytes(dims, "bf16", 1))
+    X = to_dev(xbits, "bf16")
+    Y = torch.empty_like(X)
+    ctx.nd_block_forward(dims, NH, order, st_d, mlp_d, shard, X, Y)
+    torch.cuda.synchronize()
+    ref = obn.nd_block(x64, order, st_h, mlp_h, NH)
+    g = to_f64(Y)
+    l2 = np.linalg.norm(g - ref) / np.linalg.norm(ref)
+    print(f"3-stage N-D block vs oracle: rel-L2 {l2:.3e}, max-abs {np.abs(g - ref).max():.3e}")
+    assert l2 <= 1e-2
+    y1 = bits16(Y).reshape(dims)
+    for N in (2, 4):
+        ws = (m.nd_workspace_bytes(dims, "bf16", N) + 1023) // 1024 * 1024
+        act = X.numel() * 2 // N
+        g = VirtualGroup(N, ws + act)
+        xsh = osw.split_nd(xbits.view(np.int16).reshape(dims), shard, N)
+        Xr = [torch.from_numpy(np.ascontiguousarray(xsh[r]).reshape(-1)).cuda().view(torch.bfloat16) for r in range(N)]
+        Yr = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+        for r in range(N):
+            g.ctx[r].set_workspace(g.region[r][:ws])
+        g.run(lambda r: g.ctx[r].nd_block_forward(dims, NH, order, st_d, mlp_d, shard, Xr[r], Yr[r], impl="p2p"))
+        got = np.concatenate([bits16(Yr[r]).reshape(osw.split_nd(y1, shard, N)[0].shape) for r in range(N)], axis=shard)
+        assert np.array_equal(got, y1), N
