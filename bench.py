@@ -543,13 +543,100 @@ def run_model(args):
         dist.destroy_process_group()
 
 
+def run_nd(args):
+    """Multi-dimensional block (DSP schedule P:93): [B, T, H, W, C] = [1, 16, 32, 32, 1152]
+    (the single-block config with S = 32 x 32 factored), attention along W, H, T, sharded on T,
+    16 heads, bf16, raw weights; one dsp_nd_block_forward per step, CUDA-graph replay."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_10266_b200 as dsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    N = world
+    dims, NH, order, shard = (1, 16, 32, 32, 1152), 16, (3, 2, 1), 1
+    C = dims[-1]
+    ctx = dsp.Context(pg=pg, device=dev)
+    g = torch.Generator(device="cpu").manual_seed(args.seed)
+    u = lambda *sh, sc=1.0: ((torch.rand(*sh, generator=g) * 2 - 1) * sc).to(torch.bfloat16).to(dev)
+    stages = [dict(ln_w=1 + u(C, sc=0.1), ln_b=u(C, sc=0.1), w_qkv=u(3 * C, C, sc=(3 / C) ** 0.5),
+                   w_o=u(C, C, sc=(3 / C) ** 0.5)) for _ in order]
+    mlp = dict(ln_w=1 + u(C, sc=0.1), ln_b=u(C, sc=0.1), w_fc1=u(4 * C, C, sc=(3 / C) ** 0.5),
+               w_fc2=u(C, 4 * C, sc=0.5 * (3 / (4 * C)) ** 0.5))
+    for st_ in stages:
+        st_["ln_w"] = st_["ln_w"].contiguous()
+    mlp["ln_w"] = mlp["ln_w"].contiguous()
+    loc = list(dims)
+    loc[shard] //= N
+    X = u(*loc)
+    ws_bytes = dsp.nd_workspace_bytes(dims, "bf16", N)
+    ctx.ensure_workspace(ws_bytes)
+    Y = torch.empty_like(X)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    step = lambda: ctx.nd_block_forward(dims, NH, order, stages, mlp, shard, X, Y, impl="nccl")
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(torch.cuda.current_stream())
+    gr = torch.cuda.CUDAGraph()
+    l0 = ctx.launch_count()
+    with torch.cuda.stream(cap), torch.cuda.graph(gr, stream=cap):
+        step()
+    per_step = ctx.launch_count() - l0
+    torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+        for a, b in ev:
+            flush.zero_()
+            a.record()
+            gr.replay()
+            b.record()
+        torch.cuda.synchronize()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    tokens = int(np.prod(dims[:-1]))
+    P, _ = peaks()
+    flops = 40 * tokens * C * C + 4 * tokens * C * sum(dims[k] for k in order)
+    t_roof = flops / N / (P["bf16_tflops"] * 1e12) * 1e6
+    if rank == 0:
+        print(json.dumps({"metric": "N-D block fwd tokens/s", "value": tokens * K / (t_ms / 1e3), "unit": "tokens/s",
+                          "n_gpus": N, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic",
+                          "config": {"workload": "multi-dimensional block [B,T,H,W,C]=[1,16,32,32,1152], attention "
+                                                 "along W, H, T, 16 heads, sharded on T (P:44-46, P:93)",
+                                     "l2": "flushed between timed steps", "launch": "cuda graph replay"},
+                          "roofline": {"t_roofline_us": round(t_roof, 1), "frac": round(t_roof / (t_ms / K * 1e3), 3),
+                                       "basis": "block FLOPs / N / measured bf16 peak"},
+                          "gpu_launches": per_step * K, "clocks": clocks.summary()}), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
-    ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28"])
+    ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28", "nd"])
     ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p", "fused"])
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -562,9 +649,13 @@ def main():
     if args.impl == "reference":
         if args.config == "model28":  # 28 blocks of the blk shape: the oracle's block cost x 28
             args.config, args.layers = "blk", 28
+        elif args.config == "nd":
+            return print(json.dumps({"impl": "reference", "unavailable": "no oracle timing leg for the N-D block"}))
         run_reference(args)
     elif args.config == "model28":
         run_model(args)
+    elif args.config == "nd":
+        run_nd(args)
     else:
         run_dsp(args)
 
