@@ -36,20 +36,14 @@
 // 107-112; split + ping-pong: 107-112) and therefore off by default.  The exp loop itself is
 // the bound: scripts/micro/exp_loop.cu measures 3.8 exps/clk/SMSP with two warps per SMSP and
 // 4.8 with four, against 32768 exps per SM per K/V step.
-// fmha_kv1_kernel (3-stage Q|K|V ring, one CTA per SM) for single-K/V-tile sequences: correct
-// but measured slower than fmha_bf16_tc_kernel at the temporal blk shape (36.3 vs 32.8 us) and
-// equal at T = 128 (467 us), so off by default.
-#ifndef DSP_FMHA_KV1
-#define DSP_FMHA_KV1 0
-#endif
-#ifndef DSP_FMHA_SPLIT
-#define DSP_FMHA_SPLIT 0
-#endif
-#ifndef DSP_FMHA_PINGPONG
-#define DSP_FMHA_PINGPONG 0
-#endif
+// Schedules measured SLOWER on B200 at the blk shapes and removed (git history has them):
+// rows split over two softmax threads (4 warps/SMSP, max exchanged through smem): 107-112 us;
+// ping-pong of the two query tiles' exp phases: 105-109 us; a 3-stage Q|K|V ring for
+// single-K/V-tile sequences (temporal): 36.3 vs 32.8 us.  The pair kernel (lock-step): 100-105 us.
 #ifndef DSP_POLY_NUM
 #define DSP_POLY_NUM 6  // with tensor-core row sums: 4/16 104.0 us, 5/16 105.8, 6/16 99.8, 7/16 100.4 (same box)
+#endif
+#ifndef DSP_POLY_DEN
 #define DSP_POLY_DEN 16
 #endif
 
@@ -295,8 +289,7 @@ template <int DP, bool ONES = false>
 __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
                                                   float& m, float& l, uint64_t* o_done, uint32_t& no,
                                                   unsigned long long* tr = nullptr, uint64_t* s_free = nullptr,
-                                                  int* store_pending = nullptr, uint32_t bar_id = 0,
-                                                  int pp_sync = -1, int pp_arrive = -1) {
+                                                  int* store_pending = nullptr, uint32_t bar_id = 0) {
   const int row = G.row;
   const uint32_t lane_off = G.lane_off;
   const float sl2 = G.sl2;
@@ -321,9 +314,6 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
   float2 rs4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   uint32_t pk[64];
   const float2 sl2x2 = make_float2(sl2, sl2), mx2n = make_float2(-m_new, -m_new);
-  // ping-pong: the exponential phase of the two query tiles sharing an SMSP alternates, so
-  // each runs alone on the MUFU while the other does its loads / max / P store / waits
-  if (pp_sync >= 0) named_bar_sync(pp_sync, 64);
   FMHA_STAMP(tr, 10);
 #pragma unroll
   for (int i = 0; i < 64; ++i) {
@@ -341,7 +331,6 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
     pk[i] = pack_bf16x2(e.x, e.y);
   }
   FMHA_STAMP(tr, 11);
-  if (pp_arrive >= 0) named_bar_arrive(pp_arrive, 64);
   if (!ONES) {
     const float2 rsa = fadd2(fadd2(rs4[0], rs4[1]), fadd2(rs4[2], rs4[3]));
     l = l * alpha + (rsa.x + rsa.y);
@@ -950,15 +939,6 @@ __global__ void __launch_bounds__(384, 1)
     const bool store_leader = (threadIdx.x & 127) == 0;
     int store_pending = 0;
     uint32_t ns = 0, no = 0;
-#if DSP_FMHA_PINGPONG
-    // per-SMSP ping-pong barriers (warps 4+q and 8+q share SMSP q): slot 0 waits on 3+q and
-    // releases 7+q; slot 1 the reverse; slot 1 pre-releases slot 0's first phase
-    const int q4 = warp & 3;
-    const int pp_sync = slot == 0 ? 3 + q4 : 7 + q4, pp_arrive = slot == 0 ? 7 + q4 : 3 + q4;
-    if (slot == 1) named_bar_arrive(3 + q4, 64);
-#else
-    const int pp_sync = -1, pp_arrive = -1;
-#endif
     for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
@@ -969,7 +949,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         FMHA_STAMP(tr, 3);
         softmax_tile_full<Cfg::DP, ONES>(G, tS, tO, sPs, j, m, l, &o_done[slot], no, tr, &s_free[slot], &store_pending,
-                                         bar_id, pp_sync, pp_arrive);
+                                         bar_id);
         FMHA_STAMP(tr, 4);
         mbar_arrive(&p_full[slot]);
       }
@@ -984,667 +964,6 @@ __global__ void __launch_bounds__(384, 1)
       FMHA_STAMP(te, 7);
     }
     if (store_leader) bulk_wait_group_read0();
-#if DSP_FMHA_PINGPONG
-    if (slot == 0) named_bar_sync(3 + q4, 64);  // consume slot 1's last release
-#endif
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ---------------------------------------------------------------------------------
-// Long sequences, head dims with a free padding column (Dh <= DP - 8): the pair kernel with
-// every query row split over TWO softmax threads (key columns 0-63 and 64-127), so four
-// softmax warps share each SMSP.  The exp2 / FFMA work of one warp is latency-limited
-// (measured: ~1100 clk for 128 exps with one warp per SMSP vs a ~640 clk MUFU floor); two
-// warps per tile per SMSP hide that latency.  The row sum comes from the tensor core (ones
-// column of V, see softmax_tile_full), so the only exchange between the two halves of a
-// row is the row max: one shared-memory word per thread and a 256-thread named barrier per
-// tile per step.  TMEM as in the pair kernel.
-//   warp 0 TMA    warp 1 MMA    warp 2 V patcher    warp 3 idle
-//   warps 4-11   slot 0: 4-7 key half 0, 8-11 key half 1   (warp & 3 = TMEM lane quadrant)
-//   warps 12-19  slot 1: 12-15 half 0, 16-19 half 1
-template <int NA, int RB>
-struct SplitCfg {
-  using Base = FmhaCfg<NA, RB>;
-  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP, P_BYTES = Base::P_BYTES;
-  static constexpr int RED_BYTES = 2 * 2 * 2 * 128 * 4;   // [step parity][slot][half][row] row maxima
-  static constexpr int SMEM = 1024 + 6 * TILE + 2 * P_BYTES + RED_BYTES + 256;
-  static constexpr bool OK = SMEM <= 227 * 1024 && RB > 0;
-  static constexpr int THREADS = 640;
-  static constexpr int LCOL = DP - 8;   // ones column of V / row-sum column of O
-};
-
-template <int DP>
-__device__ __forceinline__ void softmax_half(uint32_t tS, uint32_t tO, uint32_t lane_off, int row, int half,
-                                             uint8_t* sP, float* red_mine, const float* red_other, int j,
-                                             float sl2, float& m, uint64_t* o_done, uint32_t& no, uint64_t* s_free,
-                                             int* store_pending, uint32_t slot_bar, int pp_sync, int pp_arrive,
-                                             unsigned long long* tr) {
-  uint32_t v[64];
-  tmem_ld32(tS + lane_off + half * 64, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
-  tmem_ld32(tS + lane_off + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-  tmem_ld_wait();
-  FMHA_STAMP(tr, 8);
-  tc_fence_before();
-  mbar_arrive(s_free);  // this half of the S row is in registers
-  const float mx_h = max_tree3<64>(reinterpret_cast<const float*>(v));
-  red_mine[row] = mx_h;
-  named_bar_sync(slot_bar, 256);
-  const float mx = fmaxf(mx_h, red_other[row]);
-  FMHA_STAMP(tr, 9);
-  const float mx2 = mx * sl2;
-  const bool bump = (j == 0) || (mx2 > m + 8.f);
-  const float m_new = bump ? mx2 : m;
-  const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
-  m = m_new;
-  uint32_t pk[32];
-  const float2 sl2x2 = make_float2(sl2, sl2), mx2n = make_float2(-m_new, -m_new);
-  if (pp_sync >= 0) named_bar_sync(pp_sync, 128);
-  FMHA_STAMP(tr, 10);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2, mx2n);
-    float2 e;
-    if ((i % DSP_POLY_DEN) < DSP_POLY_NUM) {
-      e = poly_exp2_x2(x);
-    } else {
-      e.x = fast_exp2(x.x);
-      e.y = fast_exp2(x.y);
-    }
-    pk[i] = pack_bf16x2(e.x, e.y);
-  }
-  FMHA_STAMP(tr, 11);
-  if (pp_arrive >= 0) named_bar_arrive(pp_arrive, 128);
-  if (j > 0) {
-    mbar_wait(o_done, no & 1);  // PV_{j-1} done: O stable, P buffer free
-    ++no;
-    tc_fence_after();
-    FMHA_STAMP(tr, 2);
-    if (__any_sync(0xffffffffu, bump)) {  // lazy rescale; half 0 owns O chunks 0-2, half 1 chunks 3..
-      const float a = bump ? alpha : 1.f;
-      constexpr int NC = DP / 16, C0 = 3;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if ((c < C0) == (half == 0)) {
-          uint32_t o[16];
-          tmem_ld16(tO + lane_off + c * 16, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
-          tmem_st16(tO + lane_off + c * 16, o);
-        }
-      }
-      tmem_st_wait();
-    }
-  }
-  if (*store_pending) {  // previous item's O TMA store must have read the P buffer
-    if ((threadIdx.x & 255) == 0) bulk_wait_group_read0();
-    named_bar_sync(slot_bar, 256);
-    *store_pending = 0;
-  }
-  // P (bf16) -> smem, SW128 K-major chunk `half` (keys half*64 .. +63)
-  const uint32_t prow = smem_u32(sP) + half * 16384 + row * 128;
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-    st_shared_v4(prow + ((c ^ (row & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-  fence_proxy_async_smem();
-  FMHA_STAMP(tr, 12);
-  tc_fence_before();
-}
-
-// O / l -> bf16 -> staging -> TMA store, split over the two halves of the tile's rows: half 0
-// writes the SW128 64-column chunk(s), half 1 the remainder chunk; l is O's column LCOL.
-__host__ __device__ constexpr int half_split_chunks(int na) { return na * 4; }
-template <int NA, int RB, int LCOL, int half>
-__device__ __forceinline__ void epilogue_split(const CUtensorMap* to_a, const CUtensorMap* to_b, uint8_t* stage,
-                                               uint32_t tO, uint32_t lane_off, int row, uint32_t slot_bar,
-                                               const TileCoord& t, uint64_t* o_free, int& store_pending) {
-  constexpr int DP = NA * 64 + RB;
-  constexpr int C0 = half_split_chunks(NA);  // 16-column chunks of half 0 (the SW128 part)
-  const uint32_t st0 = smem_u32(stage);
-  // half 0: chunks [0, NA*4), half 1: the remainder chunk(s), which hold the l column
-  uint32_t lv[16];
-  tmem_ld16(tO + lane_off + (LCOL / 16) * 16, lv);
-  uint32_t ov[4 * 16];
-  if constexpr (half == 0) {
-#pragma unroll
-    for (int c = 0; c < C0; ++c) tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16));
-  } else {
-#pragma unroll
-    for (int c = C0; c < DP / 16; ++c)
-      tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + (c - C0) * 16));
-  }
-  tmem_ld_wait();
-  tc_fence_before();
-  mbar_arrive(o_free);
-  const float inv_l = 1.f / __uint_as_float(lv[LCOL % 16]);
-#pragma unroll
-  for (int c = 0; c < DP / 16; ++c) {
-    if ((c < C0) != (half == 0)) continue;
-#pragma unroll
-    for (int h8 = 0; h8 < 2; ++h8) {
-      const int d = c * 16 + h8 * 8;
-      const uint32_t* w = ov + (c < C0 ? c : c - C0) * 16 + h8 * 8;
-      const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
-      const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
-      const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
-      const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
-      uint32_t addr;
-      if (d < NA * 64) {
-        const int blk = d >> 6, ch = (d & 63) >> 3;
-        addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
-      } else {
-        const int ch = (d - NA * 64) >> 3;
-        addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
-                        : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
-      }
-      st_shared_v4(addr, a0, a1, a2, a3);
-    }
-  }
-  fence_proxy_async_smem();
-  named_bar_sync(slot_bar, 256);
-  if ((threadIdx.x & 255) == 0) {
-#pragma unroll
-    for (int i = 0; i < NA; ++i) tma_store_5d(to_a, stage + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
-    if (RB) tma_store_5d(to_b, stage + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
-    bulk_commit_group();
-  }
-  store_pending = 1;
-}
-
-template <int NA, int RB>
-__global__ void __launch_bounds__(640, 1)
-    fmha_split_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
-                      const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
-                      const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
-                      const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
-                      const FmhaParams p) {
-  using Cfg = SplitCfg<NA, RB>;
-  using Base = FmhaCfg<NA, RB>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + 2 * Cfg::TILE;
-  uint8_t* sV = sK + 2 * Cfg::TILE;
-  uint8_t* sP = sV + 2 * Cfg::TILE;
-  float* red = reinterpret_cast<float*>(sP + 2 * Cfg::P_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * Cfg::P_BYTES + Cfg::RED_BYTES);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = bars + 4;
-  uint64_t* v_full = bars + 6;
-  uint64_t* v_empty = bars + 8;
-  uint64_t* s_full = bars + 10;
-  uint64_t* p_full = bars + 12;
-  uint64_t* o_done = bars + 14;
-  uint64_t* o_free = bars + 16;
-  uint64_t* s_free = bars + 18;
-  uint64_t* v_ready = bars + 20;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 22);
-
-  const int warp = warp_id();
-  const int n = p.n_kv;
-  const int npairs = p.items / 2;
-
-  if (warp == 0 && lane_id() == 0) {
-    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
-    tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b);
-    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], 1);
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&p_full[t], 256);
-      mbar_init(&o_done[t], 1);
-      mbar_init(&o_free[t], 256);
-      mbar_init(&s_free[t], 256);
-      mbar_init(&v_ready[t], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(tmem_holder, 512);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-  griddep_launch_dependents();
-  griddep_wait();
-
-  // launch allocation 96 regs x 640 threads = 61440; 56 x 128 + 104 x 512 = 60416
-  if (warp == 0) {
-    setmaxnreg_dec<56>();
-    if (elect_one()) {
-      uint32_t nq = 0, kv = 0;
-      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
-        mbar_wait_sleep(q_empty, (nq & 1) ^ 1);
-        ++nq;
-        mbar_arrive_expect_tx(q_full, 2 * Cfg::TX);
-        load_tile<NA, RB>(sQ, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip, -1));
-        load_tile<NA, RB>(sQ + Cfg::TILE, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip + 1, -1));
-        for (int j = 0; j < n; ++j, ++kv) {
-          const int st = kv & 1;
-          const uint32_t ph = (kv >> 1) & 1;
-          const TileCoord t = tile_coord(p, 2 * ip, j);
-          mbar_wait_sleep(&k_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&k_full[st], Cfg::TX);
-          load_tile<NA, RB>(sK + st * Cfg::TILE, &tk_a, &tk_b, &k_full[st], t);
-          mbar_wait_sleep(&v_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&v_full[st], Cfg::TX);
-          load_tile<NA, RB>(sV + st * Cfg::TILE, &tv_a, &tv_b, &v_full[st], t);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    setmaxnreg_dec<56>();
-    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
-    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
-    constexpr uint32_t idPVb = make_idesc_bf16(128, RB, 0, 1);
-    const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
-    auto issue_s = [&](int slot, int st) {
-      if (elect_one()) {
-        const uint32_t qa = q0 + slot * Cfg::TILE, ka = k0 + st * Cfg::TILE, d = tmem + slot * 128;
-        int step = 0;
-#pragma unroll
-        for (int i = 0; i < NA; ++i)
-#pragma unroll
-          for (int k = 0; k < 4; ++k, ++step)
-            umma_bf16_ss(d, make_sdesc(qa + i * 16384 + k * 32, 16, 1024, SW_128B),
-                         make_sdesc(ka + i * 16384 + k * 32, 16, 1024, SW_128B), idS, step != 0);
-#pragma unroll
-        for (int k = 0; k < RB / 16; ++k, ++step)
-          umma_bf16_ss(d, make_sdesc(qa + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
-                       make_sdesc(ka + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
-        umma_commit(&s_full[slot]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int slot, int st, bool acc0) {
-      if (elect_one()) {
-        const uint32_t pa = p0 + slot * Cfg::P_BYTES, va = v0 + st * Cfg::TILE, o = tmem + 256 + slot * 128;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint64_t ad = make_sdesc(pa + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SW_128B);
-#pragma unroll
-          for (int i = 0; i < NA; ++i)
-            umma_bf16_ss(o + 64 * i, ad, make_sdesc(va + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
-                         acc0 || k != 0);
-          umma_bf16_ss(o + 64 * NA, ad,
-                       make_sdesc(va + NA * 16384 + k * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
-                       idPVb, acc0 || k != 0);
-        }
-        umma_commit(&o_done[slot]);
-      }
-      __syncwarp();
-    };
-    auto commit = [&](uint64_t* bar) {
-      if (elect_one()) umma_commit(bar);
-      __syncwarp();
-    };
-    uint32_t nq = 0, np0 = 0, np1 = 0, nf0 = 0, nf1 = 0, nit = 0, kvbase = 0;
-    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x, ++nit, kvbase += n) {
-      mbar_wait(q_full, nq & 1);
-      ++nq;
-      const uint32_t kv0 = kvbase;
-      mbar_wait(&k_full[kv0 & 1], (kv0 >> 1) & 1);
-      tc_fence_after();
-      issue_s(0, kv0 & 1);
-      issue_s(1, kv0 & 1);
-      commit(&k_empty[kv0 & 1]);
-      if (n == 1) commit(q_empty);
-      for (int j = 0; j < n; ++j) {
-        const uint32_t kj = kvbase + j, kn = kj + 1;
-        if (j + 1 < n) {
-          mbar_wait(&s_free[0], nf0 & 1);
-          mbar_wait(&k_full[kn & 1], (kn >> 1) & 1);
-          tc_fence_after();
-          issue_s(0, kn & 1);
-          mbar_wait(&s_free[1], nf1 & 1);
-          tc_fence_after();
-          issue_s(1, kn & 1);
-          commit(&k_empty[kn & 1]);
-          if (j + 2 == n) commit(q_empty);
-        }
-        ++nf0;
-        ++nf1;
-        mbar_wait(&p_full[0], np0 & 1);
-        ++np0;
-        mbar_wait(&v_ready[kj & 1], (kj >> 1) & 1);
-        if (j == 0) mbar_wait(&o_free[0], (nit & 1) ^ 1);
-        tc_fence_after();
-        issue_pv(0, kj & 1, j > 0);
-        mbar_wait(&p_full[1], np1 & 1);
-        ++np1;
-        if (j == 0) mbar_wait(&o_free[1], (nit & 1) ^ 1);
-        tc_fence_after();
-        issue_pv(1, kj & 1, j > 0);
-        commit(&v_empty[kj & 1]);
-      }
-    }
-  } else if (warp < 4) {
-    setmaxnreg_dec<56>();
-    if (warp == 2) {  // V patcher: ones column at LCOL (see fmha_pair_kernel)
-      constexpr int CB = (RB - 8) * 2;
-      uint32_t kv = 0;
-      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
-        for (int j = 0; j < n; ++j, ++kv) {
-          const int st = kv & 1;
-          mbar_wait(&v_full[st], (kv >> 1) & 1);
-          const uint32_t vb = smem_u32(sV + st * Cfg::TILE) + NA * 16384;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int r = lane_id() + 32 * i;
-            const uint32_t ch = RB == 16 ? ((CB >> 4) ^ ((r >> 2) & 1)) : ((CB >> 4) ^ ((r >> 1) & 3));
-            st_shared_u16(vb + r * Base::RB_ROW + (ch << 4) + (CB & 15), 0x3F80);
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane_id() == 0) mbar_arrive(&v_ready[st]);
-        }
-      }
-    }
-  } else {
-    setmaxnreg_inc<104>();
-    const int slot = (warp - 4) >> 3, half = ((warp - 4) >> 2) & 1, q4 = warp & 3;
-    const int row = q4 * 32 + lane_id();
-    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128;
-    uint8_t* sPs = sP + slot * Cfg::P_BYTES;
-    const uint32_t slot_bar = 1 + slot;
-#if DSP_FMHA_PINGPONG
-    const int pp_sync = slot == 0 ? 3 + q4 : 7 + q4, pp_arrive = slot == 0 ? 7 + q4 : 3 + q4;
-    if (slot == 1) named_bar_arrive(3 + q4, 128);
-#else
-    const int pp_sync = -1, pp_arrive = -1;
-#endif
-    int store_pending = 0;
-    uint32_t ns = 0, no = 0;
-    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
-      float m = -INFINITY;
-      for (int j = 0; j < n; ++j) {
-        unsigned long long* tr =
-            (p.trace && half == 0) ? p.trace + ((size_t)(slot * 64 + (ns & 63)) * 16) : nullptr;
-        FMHA_STAMP(tr, 0);
-        float* rm = red + ((ns & 1) * 2 + slot) * 256;
-        mbar_wait(&s_full[slot], ns & 1);
-        ++ns;
-        tc_fence_after();
-        FMHA_STAMP(tr, 3);
-        softmax_half<Cfg::DP>(tS, tO, lane_off, row, half, sPs, rm + half * 128, rm + (half ^ 1) * 128, j,
-                              p.scale_log2, m, &o_done[slot], no, &s_free[slot], &store_pending, slot_bar, pp_sync,
-                              pp_arrive, tr);
-        FMHA_STAMP(tr, 4);
-        mbar_arrive(&p_full[slot]);
-      }
-      mbar_wait(&o_done[slot], no & 1);
-      ++no;
-      tc_fence_after();
-      if (half == 0)
-        epilogue_split<NA, RB, Cfg::LCOL, 0>(&to_a, &to_b, sPs, tO, lane_off, row, slot_bar,
-                                             tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
-      else
-        epilogue_split<NA, RB, Cfg::LCOL, 1>(&to_a, &to_b, sPs, tO, lane_off, row, slot_bar,
-                                             tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
-    }
-    if ((threadIdx.x & 255) == 0 && store_pending) bulk_wait_group_read0();
-#if DSP_FMHA_PINGPONG
-    if (slot == 0) named_bar_sync(3 + q4, 128);
-#endif
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// O / l -> bf16 -> a staging tile in the TMA box layout (the SW128 64-column chunks, then the
-// SW32 / SW64 remainder), fenced for the async proxy; `o_free` is arrived once O is in
-// registers.  The caller signals the thread that issues the TMA store.
-template <int NA, int RB>
-__device__ __forceinline__ void stage_o(uint8_t* stage, uint32_t tO, uint32_t lane_off, int row, float l,
-                                        uint64_t* o_free) {
-  constexpr int DP = NA * 64 + RB;
-  const float inv_l = 1.f / l;
-  const uint32_t st0 = smem_u32(stage);
-  uint32_t ov[DP];
-#pragma unroll
-  for (int c = 0; c < DP / 16; ++c) tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16));
-  tmem_ld_wait();
-  tc_fence_before();
-  mbar_arrive(o_free);
-#pragma unroll
-  for (int c = 0; c < DP / 16; ++c) {
-#pragma unroll
-    for (int h8 = 0; h8 < 2; ++h8) {
-      const int d = c * 16 + h8 * 8;
-      const uint32_t* w = ov + d;
-      const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * inv_l, __uint_as_float(w[1]) * inv_l);
-      const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * inv_l, __uint_as_float(w[3]) * inv_l);
-      const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * inv_l, __uint_as_float(w[5]) * inv_l);
-      const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * inv_l, __uint_as_float(w[7]) * inv_l);
-      uint32_t addr;
-      if (d < NA * 64) {
-        const int blk = d >> 6, ch = (d & 63) >> 3;
-        addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
-      } else {
-        const int ch = (d - NA * 64) >> 3;
-        addr = RB == 16 ? st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4)
-                        : st0 + NA * 16384 + row * 64 + ((ch ^ ((row >> 1) & 3)) << 4);
-      }
-      st_shared_v4(addr, a0, a1, a2, a3);
-    }
-  }
-  fence_proxy_async_smem();
-}
-
-// ---------------------------------------------------------------------------------
-// Sequences that fit one K/V tile (n_kv == 1: temporal T = 16 packed 8 per tile, or L = 128):
-// HBM-bound (q, k, v read once, o written once), so the design goal is bytes in flight.
-// One CTA per SM keeps a ring of NS = 3 stages, each holding the Q, K and V tiles of one
-// work item (3 x 20 KB at Dh = 72), so up to three items' loads are in flight per SM while
-// two are computed: S and O of the two compute slots fill the 512 TMEM columns.  After
-// S = Q K^T the stage's Q/K bytes are dead and hold P (SW128, 32 KB); after P V they hold
-// the O staging tile for the TMA store.  A store warp issues that store and frees the stage
-// once the store has read it.
-//   warp 0 TMA producer   warp 1 MMA (S_{k+1} before P_k V_k)   warp 2 O store   warp 3 idle
-//   warps 4-7 softmax + epilogue of even items, warps 8-11 odd items (thread = query row)
-template <int NA, int RB>
-struct Kv1Cfg {
-  using Base = FmhaCfg<NA, RB>;
-  static constexpr int NS = 3;
-  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP;
-  static constexpr int STAGE = 3 * TILE;  // Q | K | V; P and the O staging tile alias Q|K
-  static constexpr int SMEM = 1024 + NS * STAGE + 256;
-  static constexpr bool OK = SMEM <= 227 * 1024 && 2 * TILE >= Base::P_BYTES;
-};
-
-template <int NA, int RB>
-__global__ void __launch_bounds__(384, 1)
-    fmha_kv1_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
-                    const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
-                    const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
-                    const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
-                    const FmhaParams p) {
-  using Cfg = Kv1Cfg<NA, RB>;
-  using Base = FmhaCfg<NA, RB>;
-  constexpr int NS = Cfg::NS;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * Cfg::STAGE);
-  uint64_t* full = bars;              // [NS] Q, K, V of the stage landed
-  uint64_t* stage_free = bars + 3;    // [NS] the stage's O store has read the staging tile
-  uint64_t* o_staged = bars + 6;      // [NS] O staging tile written (128 softmax threads)
-  uint64_t* s_full = bars + 9;        // [2] per slot
-  uint64_t* p_full = bars + 11;       // [2]
-  uint64_t* o_done = bars + 13;       // [2]
-  uint64_t* o_free = bars + 15;       // [2] O read out of TMEM
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
-  const int warp = warp_id();
-  auto stage_ptr = [&](int st) { return smem + st * Cfg::STAGE; };
-
-  if (warp == 0 && lane_id() == 0) {
-    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a); tma_prefetch(&to_a);
-    if (RB) { tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b); tma_prefetch(&to_b); }
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&stage_free[i], 1);
-      mbar_init(&o_staged[i], 128);
-    }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
-      mbar_init(&o_done[t], 1);
-      mbar_init(&o_free[t], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(tmem_holder, 512);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-  griddep_launch_dependents();
-  griddep_wait();
-
-  if (warp == 0) {
-    setmaxnreg_dec<56>();
-    if (elect_one()) {
-      int k = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
-        const int st = k % NS;
-        mbar_wait_sleep(&stage_free[st], ((k / NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[st], 3 * Cfg::TX);
-        uint8_t* sb = stage_ptr(st);
-        const TileCoord t = tile_coord(p, item, 0);
-        load_tile<NA, RB>(sb, &tq_a, &tq_b, &full[st], tile_coord(p, item, -1));
-        load_tile<NA, RB>(sb + Cfg::TILE, &tk_a, &tk_b, &full[st], t);
-        load_tile<NA, RB>(sb + 2 * Cfg::TILE, &tv_a, &tv_b, &full[st], t);
-      }
-    }
-  } else if (warp == 1) {
-    setmaxnreg_dec<56>();
-    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
-    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
-    constexpr uint32_t idPVb = make_idesc_bf16(128, RB == 0 ? 16 : RB, 0, 1);
-    auto issue_s = [&](int k) {  // full[k % NS] observed complete by the caller
-      const int st = k % NS, sl = k & 1;
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t q0 = smem_u32(stage_ptr(st)), k0 = q0 + Cfg::TILE, d = tmem + sl * 256;
-        int step = 0;
-#pragma unroll
-        for (int i = 0; i < NA; ++i)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk, ++step)
-            umma_bf16_ss(d, make_sdesc(q0 + i * 16384 + kk * 32, 16, 1024, SW_128B),
-                         make_sdesc(k0 + i * 16384 + kk * 32, 16, 1024, SW_128B), idS, step != 0);
-#pragma unroll
-        for (int kk = 0; kk < RB / 16; ++kk, ++step)
-          umma_bf16_ss(d, make_sdesc(q0 + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
-                       make_sdesc(k0 + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
-        umma_commit(&s_full[sl]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int k) {  // p_full / o_free observed by the caller
-      const int st = k % NS, sl = k & 1;
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t p0 = smem_u32(stage_ptr(st)), vb = p0 + 2 * Cfg::TILE, o = tmem + sl * 256 + 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t ad = make_sdesc(p0 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B);
-#pragma unroll
-          for (int i = 0; i < NA; ++i)
-            umma_bf16_ss(o + 64 * i, ad, make_sdesc(vb + i * 16384 + kk * 2048, 16384, 1024, SW_128B), idPVa, kk != 0);
-          if (RB)
-            umma_bf16_ss(o + 64 * NA, ad,
-                         make_sdesc(vb + NA * 16384 + kk * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
-                         idPVb, kk != 0);
-        }
-        umma_commit(&o_done[sl]);
-      }
-      __syncwarp();
-    };
-    int nmine = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) ++nmine;
-    // Event loop: S_j may run once its stage has landed and slot j & 1's previous S was consumed
-    // (PV_{j-2} issued, i.e. j <= npv + 1); PV_k once P_k is written and O of the slot is free.
-    // Neither waits for the other's unrelated condition (an item whose load is late does not
-    // hold back the P.V of an item that is ready).
-    int ns = 0, npv = 0;
-    while (npv < nmine) {
-      if (ns < nmine && ns <= npv + 1 && mbar_test(&full[ns % NS], (ns / NS) & 1)) {
-        issue_s(ns);
-        ++ns;
-        continue;
-      }
-      if (npv < ns && mbar_test(&p_full[npv & 1], (npv >> 1) & 1) &&
-          (npv < 2 || mbar_test(&o_free[npv & 1], ((npv >> 1) & 1) ^ 1))) {
-        issue_pv(npv);
-        ++npv;
-        continue;
-      }
-      __nanosleep(40);  // nothing ready: do not steal issue slots from the softmax warps on this SMSP
-    }
-  } else if (warp == 2) {
-    setmaxnreg_dec<56>();
-    if (elect_one()) {  // O store: staging tile -> global, then the stage may be refilled
-      int k = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
-        const int st = k % NS;
-        mbar_wait(&o_staged[st], (k / NS) & 1);
-        const TileCoord t = tile_coord(p, item, -1);
-        uint8_t* sb = stage_ptr(st);
-#pragma unroll
-        for (int i = 0; i < NA; ++i) tma_store_5d(&to_a, sb + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
-        if (RB) tma_store_5d(&to_b, sb + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
-        bulk_commit_group();
-        bulk_wait_group_read0();
-        mbar_arrive(&stage_free[st]);
-      }
-      bulk_wait_group_read0();
-    }
-  } else if (warp == 3) {
-    setmaxnreg_dec<56>();
-  } else {
-    setmaxnreg_inc<224>();
-    const int sl = (warp - 4) >> 2;
-    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
-    const uint32_t tS = tmem + sl * 256, tO = tmem + sl * 256 + 128;
-    uint32_t no_dummy = 0;
-    int k = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
-      if ((k & 1) != sl) continue;
-      const int st = k % NS;
-      uint8_t* sb = stage_ptr(st);
-      float m = -INFINITY, l = 0.f;
-      mbar_wait(&s_full[sl], (k >> 1) & 1);
-      tc_fence_after();
-      if (G.diag) {
-        if (G.nhalf * G.hcols > 32) softmax_tile_diag<64>(G, tS, sb, m, l, nullptr, 0);
-        else softmax_tile_diag<32>(G, tS, sb, m, l, nullptr, 0);
-      } else {
-        softmax_tile<Cfg::DP>(G, tS, tO, sb, 0, m, l, nullptr, no_dummy, nullptr, 0);
-      }
-      mbar_arrive(&p_full[sl]);
-      mbar_wait(&o_done[sl], (k >> 1) & 1);
-      tc_fence_after();
-      stage_o<NA, RB>(sb, tO, G.lane_off, G.row, l, &o_free[sl]);
-      mbar_arrive(&o_staged[st]);
-    }
   }
 
   tc_fence_before();
@@ -1690,21 +1009,6 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       mo[1] = mo[0];
     }
   }
-  if constexpr (SplitCfg<NA, RB>::OK) {
-    if (DSP_FMHA_SPLIT && p.G == 1 && p.n_qt % 2 == 0 && p.Dh <= SplitCfg<NA, RB>::LCOL) {
-      auto ks = fmha_split_kernel<NA, RB>;
-      static bool attr_s = false;
-      if (!attr_s) {
-        cudaError_t e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, SplitCfg<NA, RB>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_s = true;
-      }
-      const int npairs = p.items / 2;
-      const int grid = npairs < num_sms ? npairs : num_sms;
-      return launch_k(ks, dim3(grid), dim3(SplitCfg<NA, RB>::THREADS), SplitCfg<NA, RB>::SMEM, st, 1, m[0], m[1],
-                      m[2], m[3], m[4], m[5], mo[0], mo[1], p);
-    }
-  }
   if constexpr (PairCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0) {
       // row sums by the tensor core when the padded head dim leaves a free column for the ones
@@ -1720,20 +1024,6 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       const int grid = npairs < num_sms ? npairs : num_sms;
       return launch_k(kp, dim3(grid), dim3(PairCfg<NA, RB>::THREADS), PairCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2],
                       m[3], m[4], m[5], mo[0], mo[1], p);
-    }
-  }
-  if constexpr (Kv1Cfg<NA, RB>::OK) {
-    if (DSP_FMHA_KV1 && p.n_kv == 1) {
-      auto k1 = fmha_kv1_kernel<NA, RB>;
-      static bool attr_1 = false;
-      if (!attr_1) {
-        cudaError_t e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, Kv1Cfg<NA, RB>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_1 = true;
-      }
-      const int grid = p.items < num_sms ? p.items : num_sms;
-      return launch_k(k1, dim3(grid), dim3(384), Kv1Cfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2], m[3], m[4], m[5],
-                      mo[0], mo[1], p);
     }
   }
   auto kern = fmha_bf16_tc_kernel<NA, RB>;
