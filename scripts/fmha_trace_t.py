@@ -11,11 +11,13 @@ ctx = dsp.Context()
 for _ in range(3):
     ctx.attention_core(1, 16, 1024, C, 16, "T", QKV, O)
 torch.cuda.synchronize()
-buf = np.zeros(2 * 64 * 8, dtype=np.uint64)
+buf = np.zeros(2 * 64 * 16, dtype=np.uint64)
 ctypes.CDLL("libcudart.so.12").cudaMemcpy(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(L.dsp_debug_fmha_trace()), ctypes.c_size_t(buf.nbytes), 2)
-t = buf.reshape(128, 8).astype(np.int64)
+t = buf.reshape(128, 16).astype(np.int64)
 base = t[t > 0].min()
 print("item | start  S_ready  P_done  O_ready  stored")
 for k in range(10):
     r = t[k]
-    if r[0]: print(k, *[int(x - base) for x in r[:5]])
+    if r[0]:
+        v = [int(x - base) for x in r[:5]]
+        print(k, *v, "  deltas", *[v[i + 1] - v[i] for i in range(4)])
