@@ -39,7 +39,9 @@
 // Schedules measured SLOWER on B200 at the blk shapes and removed (git history has them):
 // rows split over two softmax threads (4 warps/SMSP, max exchanged through smem): 107-112 us;
 // ping-pong of the two query tiles' exp phases: 105-109 us; a 3-stage Q|K|V ring for
-// single-K/V-tile sequences (temporal): 36.3 vs 32.8 us.  The pair kernel (lock-step): 100-105 us.
+// single-K/V-tile sequences (temporal): 36.3 vs 32.8 us; a dedicated epilogue warpgroup (512
+// threads, own O staging; the 128-register launch cap spills the softmax): 125 vs 102 us.
+// The pair kernel (lock-step): 100-105 us.
 #ifndef DSP_POLY_NUM
 #define DSP_POLY_NUM 6  // with tensor-core row sums: 4/16 104.0 us, 5/16 105.8, 6/16 99.8, 7/16 100.4 (same box)
 #endif

@@ -1,12 +1,15 @@
-# One gpurun call: GPU tests, smoke, bench (prepared + raw), ncu launch list of the bench command.
+# One gpurun call: GPU tests, smoke, bench (default + other configs), ncu launch list of the bench command.
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -q -x --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; tail -5 gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 400 > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
-timeout 600 python bench.py --no-prepare --no-cpu-baseline > gpurun_out/bench_raw.json 2>&1; cat gpurun_out/bench_raw.json | cut -c1-400
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cut -c1-300 gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout 600 python bench.py --no-prepare --no-cpu-baseline > gpurun_out/bench_raw.json 2>&1
+timeout 600 python bench.py --config long --steps 5 > gpurun_out/bench_long.json 2>&1
+timeout 600 python bench.py --config model28 --steps 5 > gpurun_out/bench_model28.json 2>&1
+timeout 600 python bench.py --config nd --steps 20 > gpurun_out/bench_nd.json 2>&1
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; cat gpurun_out/bench_ref.json | cut -c1-300
 ls -la gpurun_out
