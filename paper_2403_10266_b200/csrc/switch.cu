@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __res
 
 // Signal-pad barrier across `world` ranks (one block, one thread per peer):
 // release-store `epoch` into slot [rank] of every peer's pad, then acquire-spin until
-// every peer has written >= epoch into our own pad.  Bounded spin (no infinite hang).
+// every peer has written >= epoch into our own pad.  Bounded spin: a peer that never
+// arrives (dead rank, mismatched collective sequence) traps the kernel -- a CUDA error on
+// the stream instead of a hang or a switch that silently proceeds without the peer's data.
 __global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64_t epoch) {
   griddep_wait();
   const int i = threadIdx.x;
@@ -74,6 +76,7 @@ __global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64
       if (v >= epoch) break;
       __nanosleep(64);
     }
+    if (v < epoch) __trap();
   }
   __syncthreads();
 }

@@ -27,6 +27,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # virtual ranks spin on each other (see tests/conftest.py)
 
 import torch  # noqa: E402
 

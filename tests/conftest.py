@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# The GPU tests drive N "virtual ranks" from ONE process on N streams whose switch barriers
+# spin on each other.  With CUDA lazy module loading, the first launch of a kernel on one
+# stream can wait for kernels running on the others -- a spinning barrier among them -- so
+# load every kernel up front (separate processes per rank, as under torchrun, are unaffected).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -173,14 +173,16 @@ def test_switch_p2p_virtual_ranks_bitexact(N, B):
         assert np.array_equal(bits16(xin[r]), tsh[r].view(np.int16).reshape(-1)), f"S->T rank {r}"
 
 
-@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("N", [2, 4, 8])
 @pytest.mark.parametrize("impl", ["p2p", "fused"])
-def test_block_p2p_virtual_ranks_n_invariant(N, impl):
+@pytest.mark.parametrize("sh", [synth.BlockShape(1, 16, 256, 1152, 16, "bf16"),
+                                synth.BlockShape(2, 8, 128, 256, 4, "bf16")])
+def test_block_p2p_virtual_ranks_n_invariant(N, impl, sh):
     """DSP block over N virtual ranks == N=1 block bitwise (no reductions cross ranks,
     no split-K: each output's reduction order is independent of N).  `fused`: the switch is
-    done by the out-projection / FC2 epilogues storing rows at their owner rank."""
+    done by the out-projection / FC2 epilogues storing rows at their owner rank.  B = 2
+    exercises the strided (non-identity) row runs of the switch."""
     m = dsp()
-    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
     xs, Ws = _setup(sh)
     ref1 = bits16(_run_block_n1(sh, xs, Ws))
     shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
@@ -199,7 +201,7 @@ def test_block_p2p_virtual_ranks_n_invariant(N, impl):
     assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
 
 
-@pytest.mark.parametrize("N", [2, 4])
+@pytest.mark.parametrize("N", [2, 4, 8])
 @pytest.mark.parametrize("impl", ["p2p", "fused"])
 def test_block_prepared_virtual_ranks_vs_oracle(N, impl):
     """Prepared (LayerNorm-folded) block over N virtual ranks: LN2 statistics are recomputed
@@ -370,7 +372,7 @@ def test_nd_block_5d_vs_oracle_and_virtual_ranks():
     print(f"3-stage N-D block vs oracle: rel-L2 {l2:.3e}, max-abs {np.abs(g - ref).max():.3e}")
     assert l2 <= 1e-2
     y1 = bits16(Y).reshape(dims)
-    for N in (2, 4):
+    for N in (2, 4, 8):
         ws = (m.nd_workspace_bytes(dims, "bf16", N) + 1023) // 1024 * 1024
         act = X.numel() * 2 // N
         g = VirtualGroup(N, ws + act)

@@ -165,3 +165,37 @@ def test_model_forward_chained_layernorm():
     l2 = np.linalg.norm(g - ref) / np.linalg.norm(ref)
     print(f"3 layers vs oracle: rel-L2 {l2:.3e}, max-abs {np.abs(g - ref).max():.3e}")
     assert l2 <= 1e-2
+
+
+def test_block_long_video_virtual_ranks_n_invariant():
+    """configs[3] at full size (T=128, S=4096, 1.2 GB activation) over N = 2 virtual ranks with the
+    fused switch: bitwise equal to the N = 1 block (the long-video shapes through every kernel,
+    incl. the 32-tile spatial sequences and one-tile temporal sequences)."""
+    from tests.test_gpu_block import VirtualGroup
+    from oracle import switch as osw
+    m = dsp()
+    sh = synth.CONFIGS["long"]
+    xs = synth.make_x(sh, 7)
+    W = weights_dev(synth.make_block_weights(sh, 7), "bf16")
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx = m.Context()
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, "bf16")
+    Y1 = torch.empty_like(X)
+    ctx.st_block_forward(shape, W, X, Y1)
+    torch.cuda.synchronize()
+    ref1 = bits16(Y1).reshape(-1)
+    del ctx, X, Y1
+    torch.cuda.empty_cache()
+    N = 2
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    xsh = osw.split(xs, osw.DIM_T, N)
+    Xr = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Yr = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, Xr[r], Yr[r], impl="fused"))
+    got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref1)
