@@ -116,3 +116,32 @@ def mlp_stage(y2, W):
 def st_block(x: np.ndarray, W: dict, num_heads: int) -> np.ndarray:
     """The unsharded ST block on global x [B, T, S, C] (float64)."""
     return mlp_stage(temporal_stage(spatial_stage(x, W, num_heads), W, num_heads), W)
+
+
+# --------------------------------------------------------------- cross-attention (P:137)
+def cross_attention(h: np.ndarray, ctx: np.ndarray, w_q, w_kv, w_o, num_heads: int) -> np.ndarray:
+    """Multi-head cross-attention of ONE sample's tokens h [L, C] to its context tokens ctx [Lc, C]
+    (ST-DiT "uses spatial-temporal and cross attention"; Latte/PixArt-style text
+    conditioning).  q = h w_q^T, [k | v] = ctx w_kv^T (w_kv rows [k | v], head j owns rows
+    j*Dh..(j+1)*Dh-1 of each, R8); O_j = softmax(q_j k_j^T / sqrt(Dh)) v_j; heads concatenated;
+    return O w_o^T.  No mask, no bias (R4, R7)."""
+    L, C = h.shape
+    dh = C // num_heads
+    q = linear(h, w_q).reshape(L, num_heads, dh).transpose(1, 0, 2)
+    kv = linear(ctx, w_kv)
+    Lc = ctx.shape[0]
+    k = kv[:, :C].reshape(Lc, num_heads, dh).transpose(1, 0, 2)
+    v = kv[:, C:].reshape(Lc, num_heads, dh).transpose(1, 0, 2)
+    o = attention_core(q, k, v)                        # [NH, L, Dh]
+    return linear(o.transpose(1, 0, 2).reshape(L, C), w_o)
+
+
+def cross_stage(x: np.ndarray, ctx: np.ndarray, Wc: dict, num_heads: int) -> np.ndarray:
+    """y = x + CA(LN(x), ctx) on x [B, ..., C] with ctx [B, Lc, C]: every token of sample b attends
+    to sample b's context (position-independent: any sharding of the tokens is local)."""
+    out = np.empty_like(x)
+    for b in range(x.shape[0]):
+        hb = layer_norm(x[b], Wc["ln_w"], Wc["ln_b"]).reshape(-1, x.shape[-1])
+        out[b] = (x[b].reshape(-1, x.shape[-1]) +
+                  cross_attention(hb, ctx[b], Wc["w_q"], Wc["w_kv"], Wc["w_o"], num_heads)).reshape(x[b].shape)
+    return out
