@@ -277,6 +277,22 @@ dsp_status_t dsp_switch_nd_plan(const int64_t* dims, int ndim, int elem_bytes, i
 dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int elem_bytes, int from_dim,
                            int to_dim, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
 
+/* ---------------------------------------------------------------- cross-attention
+ * ST-DiT's conditioning layer ("spatial-temporal and cross attention"): every local
+ * token of sample b attends to sample b's Lc context tokens (e.g. caption embeddings), which
+ * every rank holds in full -- position-independent, so it is local under any DSP sharding.
+ *   out = (residual ? residual : 0) + CA(h),  CA(h) = softmax(q k^T / sqrt(Dh)) v  per head, w_o
+ *   q = h w_q^T,  [k | v] = ctx_tokens w_kv^T  (w_kv [2C, C] rows [k | v], head j rows j*Dh.., R8)
+ * h, residual, out: [B, T_loc, S_loc, C] local tokens (either sharding; LN applied by the caller);
+ * ctx_tokens: [B, Lc, C] (already projected to C); bf16 only.  Keys beyond Lc in the last
+ * 128-key tile are masked.  Needs (B*T*S/world)/B % 256 == 0 local tokens per sample and
+ * workspace >= dsp_cross_workspace_bytes.  Not collective.  Errors: NULL, SHAPE, DIVISIBILITY,
+ * UNSUPPORTED, ALIGNMENT, ALIAS (out overlaps h; out == residual is allowed), WORKSPACE, CUDA. */
+size_t dsp_cross_workspace_bytes(const dsp_shape_t* shape, int world, int64_t Lc);  /* host-only */
+dsp_status_t dsp_cross_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local, const void* ctx_tokens,
+                            int64_t Lc, const void* w_q, const void* w_kv, const void* w_o, const void* residual,
+                            void* out, void* stream);
+
 /* ---------------------------------------------------------------- N-D block
  * Multi-dimensional transformer block on x [d_0, ..., d_{n-2}, C] with attention
  * along each of the dims attn_dims[0..n_stages-1] in that order (pre-LN + residual, R1-R8),

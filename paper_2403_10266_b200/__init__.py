@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
             "dsp_nd_block_forward": [vp, P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      P(ctypes.c_int), P(AttnWeights), P(MlpWeights), ctypes.c_float, ctypes.c_int, vp,
                                      vp, ctypes.c_int, vp],
+            "dsp_cross_attn": [vp, P(Shape), vp, vp, i64, vp, vp, vp, vp, vp, vp],
             "dsp_spatial_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_temporal_attn": [vp, P(Shape), vp, vp, vp, vp, vp, vp],
             "dsp_st_block_forward": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
@@ -122,6 +123,8 @@ def lib() -> ctypes.CDLL:
             f.restype = ctypes.c_int
         L.dsp_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
         L.dsp_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_cross_workspace_bytes.argtypes = [P(Shape), ctypes.c_int, i64]
+        L.dsp_cross_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_nd_workspace_bytes.argtypes = [P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.dsp_nd_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_block_prepared_bytes.argtypes = [P(Shape)]
@@ -192,6 +195,10 @@ def switch_plan(shape: Shape, world: int, rank: int, from_dim, to_dim) -> Switch
     _check(lib().dsp_switch_plan(ctypes.byref(shape), int(world), int(rank), DIMS[from_dim], DIMS[to_dim],
                                  ctypes.byref(p)))
     return p
+
+
+def cross_workspace_bytes(shape: Shape, world: int, Lc: int) -> int:
+    return int(lib().dsp_cross_workspace_bytes(ctypes.byref(shape), int(world), int(Lc)))
 
 
 def nd_workspace_bytes(dims, dtype, world: int) -> int:
@@ -326,6 +333,12 @@ class Context:
     def spatial_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):
         self._call("dsp_spatial_attn", ctypes.byref(shape), _ptr(h), _ptr(w_qkv), _ptr(w_o), _ptr(residual),
                    _ptr(out), _stream(stream))
+
+    def cross_attn(self, shape, h, ctx_tokens, w_q, w_kv, w_o, residual, out, stream=None):
+        """dsp_cross_attn: out = residual + CA(h, ctx_tokens) (ctx_tokens [B, Lc, C])."""
+        Lc = ctx_tokens.numel() // (shape.B * shape.C)
+        self._call("dsp_cross_attn", ctypes.byref(shape), _ptr(h), _ptr(ctx_tokens), int(Lc), _ptr(w_q), _ptr(w_kv),
+                   _ptr(w_o), _ptr(residual), _ptr(out), _stream(stream))
 
     def temporal_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):
         self._call("dsp_temporal_attn", ctypes.byref(shape), _ptr(h), _ptr(w_qkv), _ptr(w_o), _ptr(residual),

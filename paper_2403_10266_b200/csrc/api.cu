@@ -845,6 +845,53 @@ dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   return DSP_OK;
 }
 
+size_t dsp_cross_workspace_bytes(const dsp_shape_t* s, int world, int64_t Lc) {
+  if (!s || world < 1 || s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1 || Lc < 1) return 0;
+  const int64_t tok = s->B * s->T * s->S / world;
+  return (size_t)((2 * tok + 2 * s->B * Lc) * s->C * elem_bytes(s->dtype) + 512);  // q | o | kv
+}
+
+dsp_status_t dsp_cross_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* h, const void* ctx_tokens, int64_t Lc,
+                            const void* w_q, const void* w_kv, const void* w_o, const void* residual, void* out,
+                            void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!h || !ctx_tokens || !w_q || !w_kv || !w_o || !out) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "cross attention runs on the bf16 path");
+  if (Lc < 1) return fail(ctx, DSP_ERR_SHAPE, "context length %lld < 1", (long long)Lc);
+  const int64_t C = s->C, N = ctx->world, tok = s->B * s->T * s->S / N, Lq = tok / s->B;
+  {
+    const dsp_shape_t hs{1, 1, 1, C, s->num_heads, s->dtype};
+    DSP_TRY(check_bf16_attn(ctx, &hs, 128));
+  }
+  if (Lq % 256) return fail(ctx, DSP_ERR_UNSUPPORTED, "cross attention needs the local tokens per sample (%lld) %% 256 == 0", (long long)Lq);
+  const void* bufs[8] = {h, ctx_tokens, w_q, w_kv, w_o, residual, out, ctx->ws};
+  for (int i = 0; i < 8; ++i)
+    if (bufs[i] && !aligned16(bufs[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const size_t need = dsp_cross_workspace_bytes(s, (int)N, Lc);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "cross attention needs %zu bytes of workspace", need);
+  const int64_t act = tok * C * 2;
+  if (overlap(out, act, h, act)) return fail(ctx, DSP_ERR_ALIAS, "out overlaps h");
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  void* q = ws;
+  void* o = ws + act;
+  void* kv = ws + 2 * act;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::string why;
+  cudaError_t e = launch_gemm_bf16(h, w_q, nullptr, q, tok, C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cross q projection", why);
+  e = launch_gemm_bf16(ctx_tokens, w_kv, nullptr, kv, s->B * Lc, 2 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cross kv projection", why);
+  e = launch_fmha_cross_bf16(q, kv, o, s->B, Lq, Lc, C, s->num_heads, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cross attention core", why);
+  e = launch_gemm_bf16(o, w_o, residual, out, tok, C, C, residual ? DSP_EPI_RESIDUAL : DSP_EPI_NONE, ctx->num_sms, st,
+                       &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cross output projection", why);
+  ctx->launches += 4;
+  return DSP_OK;
+}
+
 size_t dsp_nd_workspace_bytes(const int64_t* dims, int ndim, dsp_dtype_t dtype, int world) {
   if (!dims || ndim < 3 || ndim > DSP_ND_MAX_DIMS || world < 1) return 0;
   int64_t tok = 1;

@@ -49,6 +49,9 @@ cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* 
                              int epi, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
                              int dim, int num_sms, cudaStream_t st, std::string* why);
+// cross-attention: queries q [B*Lq, C], context keys / values kv [B*Lc, 2C] ([k | v])
+cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64_t B, int64_t Lq, int64_t Lc,
+                                   int64_t C, int NH, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_gemm_f32(const float* A, const float* W, const float* R, float* D, int64_t M, int64_t N, int64_t K,
                             int epi, cudaStream_t st);
 cudaError_t launch_attn_f32(const float* qkv, float* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,

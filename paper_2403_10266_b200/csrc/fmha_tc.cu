@@ -62,6 +62,7 @@ struct FmhaParams {
   int NH, Dh, C;
   int S_loc, T_loc, B;
   int items;     // n_outer * NH * n_qt
+  int kv_last;   // valid keys in the last K/V tile (128 unless the key length is ragged: cross-attention)
   float scale_log2;
   __nv_bfloat16* o;
   unsigned long long* trace;  // DSP_FMHA_TRACE builds only: per-phase clock64 stamps of CTA 0
@@ -291,7 +292,8 @@ template <int DP, bool ONES = false>
 __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
                                                   float& m, float& l, uint64_t* o_done, uint32_t& no,
                                                   unsigned long long* tr = nullptr, uint64_t* s_free = nullptr,
-                                                  int* store_pending = nullptr, uint32_t bar_id = 0) {
+                                                  int* store_pending = nullptr, uint32_t bar_id = 0,
+                                                  int valid = 128) {
   const int row = G.row;
   const uint32_t lane_off = G.lane_off;
   const float sl2 = G.sl2;
@@ -305,6 +307,11 @@ __device__ __forceinline__ void softmax_tile_full(const SoftmaxGeom& G, uint32_t
   if (s_free) {  // the whole S row is in registers: the MMA may overwrite S with S_{j+1}
     tc_fence_before();
     mbar_arrive(s_free);
+  }
+  if (valid < 128) {  // ragged key length: keys >= valid of this tile are padding (TMA zero fill)
+#pragma unroll
+    for (int i = 0; i < 128; ++i)
+      if (i >= valid) v[i] = __float_as_uint(-INFINITY);
   }
   const float mx = max_tree3<128>(reinterpret_cast<const float*>(v));
   FMHA_STAMP(tr, 9);
@@ -951,7 +958,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         FMHA_STAMP(tr, 3);
         softmax_tile_full<Cfg::DP, ONES>(G, tS, tO, sPs, j, m, l, &o_done[slot], no, tr, &s_free[slot], &store_pending,
-                                         bar_id);
+                                         bar_id, j + 1 == n ? p.kv_last : 128);
         FMHA_STAMP(tr, 4);
         mbar_arrive(&p_full[slot]);
       }
@@ -976,14 +983,22 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// 5-D tile views {Dh, NH, position, outer, outer2} of q, k, v (one per part) and of o
+struct FmhaViews {
+  const void* base[3];
+  uint64_t dims[3][5], strides[3][4];
+  uint64_t odims[5], ostr[4];
+};
+
 template <int NA, int RB>
-cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims, const uint64_t* strides,
-                     const uint32_t* box_rows, int num_sms, cudaStream_t st, std::string* why) {
+cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* box_rows, int num_sms,
+                     cudaStream_t st, std::string* why) {
   using Cfg = FmhaCfg<NA, RB>;
   CUtensorMap m[6];
-  const auto* base = static_cast<const __nv_bfloat16*>(qkv);
   for (int part = 0; part < 3; ++part) {
-    const void* b = base + part * p.C;
+    const void* b = vw.base[part];
+    const uint64_t* dims = vw.dims[part];
+    const uint64_t* strides = vw.strides[part];
     uint32_t boxa[5] = {64, 1, box_rows[0], box_rows[1], 1};
     uint32_t boxb[5] = {(uint32_t)(RB ? RB : 16), 1, box_rows[0], box_rows[1], 1};
     if (!make_tmap_bf16(&m[2 * part], b, 5, dims, strides, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why))
@@ -996,10 +1011,11 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
       m[2 * part + 1] = m[2 * part];
     }
   }
-  // output maps: same 5-D view as q/k/v but over o [tok, C] (row pitch C instead of 3C)
+  // output maps: the query-side tile view over o [tok, C]
   CUtensorMap mo[2];
   {
-    uint64_t ostr[4] = {strides[0], strides[1] / 3, strides[2] / 3, strides[3] / 3};
+    const uint64_t* dims = vw.odims;
+    const uint64_t* ostr = vw.ostr;
     uint32_t boxa[5] = {64, 1, box_rows[0], box_rows[1], 1};
     uint32_t boxb[5] = {(uint32_t)(RB ? RB : 16), 1, box_rows[0], box_rows[1], 1};
     if (!make_tmap_bf16(&mo[0], p.o, 5, dims, ostr, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why)) return cudaErrorInvalidValue;
@@ -1041,6 +1057,9 @@ cudaError_t run_fmha(const void* qkv, const FmhaParams& p, const uint64_t* dims,
 }
 
 }  // namespace
+
+static cudaError_t dispatch_dh(const FmhaViews& vw, const FmhaParams& p, const uint32_t* box_rows, int num_sms,
+                               cudaStream_t st, std::string* why);
 
 #ifdef DSP_FMHA_TRACE
 unsigned long long* g_fmha_trace = nullptr;
@@ -1097,16 +1116,79 @@ cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc,
   }
   uint32_t box_rows[2] = {(uint32_t)(p.G == 1 ? 128 : p.L), (uint32_t)p.G};
   p.items = p.n_outer * NH * p.n_qt;
+  p.kv_last = 128;
   if (p.items == 0) return cudaSuccess;
+  FmhaViews vw;
+  const auto* base = static_cast<const __nv_bfloat16*>(qkv);
+  for (int part = 0; part < 3; ++part) {  // q, k, v: column blocks [part*C, (part+1)*C) of qkv
+    vw.base[part] = base + part * C;
+    for (int i = 0; i < 5; ++i) vw.dims[part][i] = dims[i];
+    for (int i = 0; i < 4; ++i) vw.strides[part][i] = strides[i];
+  }
+  for (int i = 0; i < 5; ++i) vw.odims[i] = dims[i];
+  for (int i = 0; i < 4; ++i) vw.ostr[i] = i == 0 ? strides[0] : strides[i] / 3;  // o [tok, C]: row pitch C
+  return dispatch_dh(vw, p, box_rows, num_sms, st, why);
+}
+
+cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64_t B, int64_t Lq, int64_t Lc,
+                                   int64_t C, int NH, int num_sms, cudaStream_t st, std::string* why) {
+  FmhaParams p{};
+  p.NH = NH;
+  p.Dh = (int)(C / NH);
+  p.C = (int)C;
+  p.B = (int)B;
+  p.S_loc = (int)Lq;
+  p.T_loc = 1;
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.trace = nullptr;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
+  p.spatial = 1;  // queries of sample b = rows [b*Lq, (b+1)*Lq) of q; keys / values = rows of kv
+  p.L = (int)Lq;
+  p.G = 1;
+  p.n_qt = (int)(Lq / 128);
+  p.n_kv = (int)((Lc + 127) / 128);
+  p.kv_last = (int)(Lc - 128 * (p.n_kv - 1));
+  p.n_outer = (int)B;
+  p.items = p.n_outer * NH * p.n_qt;
+  if (Lq % 256 || Lc < 1) {
+    if (why) *why = "cross attention needs tokens per sample % 256 == 0 and at least one context token";
+    return cudaErrorNotSupported;
+  }
+  if (p.items == 0) return cudaSuccess;
+  const uint64_t e = 2;
+  FmhaViews vw;
+  vw.base[0] = q;
+  vw.base[1] = kv;
+  vw.base[2] = static_cast<const __nv_bfloat16*>(kv) + C;
+  const uint64_t qd[5] = {(uint64_t)p.Dh, (uint64_t)NH, (uint64_t)Lq, (uint64_t)B, 1};
+  const uint64_t qs[4] = {p.Dh * e, C * e, Lq * C * e, B * Lq * C * e};
+  const uint64_t kd[5] = {(uint64_t)p.Dh, (uint64_t)NH, (uint64_t)Lc, (uint64_t)B, 1};
+  const uint64_t ks[4] = {p.Dh * e, 2 * C * e, Lc * 2 * C * e, B * Lc * 2 * C * e};
+  for (int i = 0; i < 5; ++i) {
+    vw.dims[0][i] = qd[i];
+    vw.dims[1][i] = vw.dims[2][i] = kd[i];
+    vw.odims[i] = qd[i];
+  }
+  for (int i = 0; i < 4; ++i) {
+    vw.strides[0][i] = qs[i];
+    vw.strides[1][i] = vw.strides[2][i] = ks[i];
+    vw.ostr[i] = qs[i];
+  }
+  const uint32_t box_rows[2] = {128, 1};
+  return dispatch_dh(vw, p, box_rows, num_sms, st, why);
+}
+
+static cudaError_t dispatch_dh(const FmhaViews& vw, const FmhaParams& p, const uint32_t* box_rows, int num_sms,
+                               cudaStream_t st, std::string* why) {
   const int dp = ((p.Dh + 15) / 16) * 16;
   int na = dp / 64, rb = dp % 64;
   if (rb == 48) { na += 1; rb = 0; }
-  if (na == 1 && rb == 16) return run_fmha<1, 16>(qkv, p, dims, strides, box_rows, num_sms, st, why);  // Dh 72, 80
-  if (na == 0 && rb == 16) return run_fmha<0, 16>(qkv, p, dims, strides, box_rows, num_sms, st, why);  // Dh 8, 16
-  if (na == 0 && rb == 32) return run_fmha<0, 32>(qkv, p, dims, strides, box_rows, num_sms, st, why);  // Dh 24, 32
-  if (na == 1 && rb == 0) return run_fmha<1, 0>(qkv, p, dims, strides, box_rows, num_sms, st, why);    // Dh 40..64
-  if (na == 1 && rb == 32) return run_fmha<1, 32>(qkv, p, dims, strides, box_rows, num_sms, st, why);  // Dh 88, 96
-  if (na == 2 && rb == 0) return run_fmha<2, 0>(qkv, p, dims, strides, box_rows, num_sms, st, why);    // Dh 104..128
+  if (na == 1 && rb == 16) return run_fmha<1, 16>(vw, p, box_rows, num_sms, st, why);  // Dh 72, 80
+  if (na == 0 && rb == 16) return run_fmha<0, 16>(vw, p, box_rows, num_sms, st, why);  // Dh 8, 16
+  if (na == 0 && rb == 32) return run_fmha<0, 32>(vw, p, box_rows, num_sms, st, why);  // Dh 24, 32
+  if (na == 1 && rb == 0) return run_fmha<1, 0>(vw, p, box_rows, num_sms, st, why);    // Dh 40..64
+  if (na == 1 && rb == 32) return run_fmha<1, 32>(vw, p, box_rows, num_sms, st, why);  // Dh 88, 96
+  if (na == 2 && rb == 0) return run_fmha<2, 0>(vw, p, box_rows, num_sms, st, why);    // Dh 104..128
   if (why) *why = "bf16 attention supports head dims up to 128";
   return cudaErrorNotSupported;
 }

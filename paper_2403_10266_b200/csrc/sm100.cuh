@@ -341,9 +341,11 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 // 2^x on the FMA pipe (offloads the MUFU): Cody-Waite split x = j + r, r in [-0.5, 0.5],
 // degree-3 fit of 2^r (max relative error 7.7e-5, far below the bf16 rounding of P),
-// exponent j added to the bit pattern.  x <= 128; -inf/very negative clamps to ~2^-127.
+// exponent j added to the bit pattern.  x <= 128; -inf / very negative inputs clamp to -126,
+// giving ~2^-126 (clamping at -127 would underflow the exponent add below zero: p < 1 at r = 0,
+// so p_bits - (127 << 23) wraps to a negative NaN pattern).
 __device__ __forceinline__ float poly_exp2(float x) {
-  x = fmaxf(x, -127.f);
+  x = fmaxf(x, -126.f);
   const float t = x + 12582912.f;        // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
   const float r = x - (t - 12582912.f);
   const float p = fmaf(fmaf(fmaf(0.05508868f, r, 0.24260405f), r, 0.69327623f), r, 0.99992895f);
@@ -372,8 +374,8 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 }
 // poly_exp2 on a pair, FFMA2/FADD2 for the arithmetic
 __device__ __forceinline__ float2 poly_exp2_x2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -126.f);  // see poly_exp2: -127 would wrap to NaN
+  x.y = fmaxf(x.y, -126.f);
   const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 u = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 r = ffma2(u, make_float2(-1.f, -1.f), x);

@@ -119,6 +119,7 @@ def _attn_ref(qkv, B, T, S, C, NH, dim):
 @pytest.mark.parametrize("B,T,S,C,NH,dim,kappa", [
     (1, 2, 1024, 1152, 16, "S", 1.0),     # spatial blk frame, 8 kv tiles
     (1, 1, 256, 1152, 16, "S", 4.0),      # peaky softmax, lazy rescale path
+    (1, 1, 256, 1152, 16, "S", 300.0),    # extreme logits: exp2 arguments far below -126 (poly clamp)
     (2, 3, 128, 256, 4, "S", 1.0),        # Dh=64, one tile
     (1, 5, 16, 128, 8, "S", 1.0),         # S<128: 8 frames per tile, ragged frame count
     (1, 16, 64, 1152, 16, "T", 1.0),      # temporal T=16, 8 columns per tile
@@ -146,3 +147,33 @@ def test_attention_core_f32(ctx, dim):
     ctx.attention_core(B, T, S, C, NH, dim, Q, O)
     torch.cuda.synchronize()
     np.testing.assert_allclose(to_f64(O), _attn_ref(qkv.astype(np.float64), B, T, S, C, NH, dim), rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("B,T,S,Lc,kappa", [(2, 4, 128, 120, 1.0), (1, 2, 256, 77, 1.0), (2, 2, 128, 128, 4.0),
+                                             (1, 4, 64, 300, 1.0), (1, 1, 256, 1, 1.0)])
+def test_cross_attention_bf16(ctx, B, T, S, Lc, kappa):
+    """dsp_cross_attn vs the oracle: caption-like context lengths 120 / 77 (masked tail
+    keys), exactly one tile, three tiles with a ragged last one, a single context token; peaky
+    scores at kappa = 4."""
+    import paper_2403_10266_b200 as dsp
+    C, NH = 1152, 16
+    tok = B * T * S
+    h_bits, h = _rand_bf16((tok, C), 31, 1.0, 1)
+    c_bits, cx = _rand_bf16((B * Lc, C), 32, 1.0, 2)
+    wq_bits, wq = _rand_bf16((C, C), 33, math.sqrt(3.0 * kappa / C), 3)
+    wkv_bits, wkv = _rand_bf16((2 * C, C), 34, math.sqrt(3.0 / C), 4)
+    wkv[:C] *= 1.0  # k rows carry the kappa scale through q
+    wo_bits, wo = _rand_bf16((C, C), 35, math.sqrt(3.0 / C), 5)
+    r_bits, r = _rand_bf16((tok, C), 36, 1.0, 6)
+    shape = dsp.make_shape(B, T, S, C, NH, "bf16")
+    ctx.ensure_workspace(dsp.cross_workspace_bytes(shape, 1, Lc))
+    H, CX, R = to_dev(h_bits, "bf16"), to_dev(c_bits, "bf16"), to_dev(r_bits, "bf16")
+    WQ, WKV, WO = to_dev(wq_bits, "bf16"), to_dev(wkv_bits, "bf16"), to_dev(wo_bits, "bf16")
+    OUT = torch.empty_like(H)
+    ctx.cross_attn(shape, H, CX.view(B, Lc, C), WQ, WKV, WO, R, OUT)
+    torch.cuda.synchronize()
+    Lq = T * S
+    ref = r.copy()
+    for b in range(B):
+        ref[b * Lq:(b + 1) * Lq] += ob.cross_attention(h[b * Lq:(b + 1) * Lq], cx[b * Lc:(b + 1) * Lc], wq, wkv, wo, NH)
+    print(assert_block_close(to_f64(OUT), ref))
