@@ -113,9 +113,15 @@ def mlp_stage(y2, W):
     return y2 + mlp(layer_norm(y2, W["ln3_w"], W["ln3_b"]), W["w_fc1"], W["w_fc2"])
 
 
-def st_block(x: np.ndarray, W: dict, num_heads: int) -> np.ndarray:
-    """The unsharded ST block on global x [B, T, S, C] (float64)."""
-    return mlp_stage(temporal_stage(spatial_stage(x, W, num_heads), W, num_heads), W)
+def st_block(x: np.ndarray, W: dict, num_heads: int, ctx: np.ndarray | None = None) -> np.ndarray:
+    """The unsharded ST block on global x [B, T, S, C] (float64).  With `ctx` [B, Lc, C] and the
+    cross weights in W (ln_c_w, ln_c_b, w_q_c, w_kv_c, w_o_c), the ST-DiT block of P:137: a cross
+    stage y2' = y2 + CA(LN_c(y2), ctx) between the temporal stage and the MLP."""
+    y2 = temporal_stage(spatial_stage(x, W, num_heads), W, num_heads)
+    if ctx is not None:
+        Wc = dict(ln_w=W["ln_c_w"], ln_b=W["ln_c_b"], w_q=W["w_q_c"], w_kv=W["w_kv_c"], w_o=W["w_o_c"])
+        y2 = cross_stage(y2, ctx, Wc, num_heads)
+    return mlp_stage(y2, W)
 
 
 # --------------------------------------------------------------- cross-attention (P:137)

@@ -18,7 +18,7 @@ from .switch import DIM_S, DIM_T, Ledger, gather, split, switch
 
 def simulate_sharded(x: np.ndarray, W: dict, num_heads: int, world: int,
                      ledger: Ledger | None = None, elem_bytes: int = 2, tag: str = "block0",
-                     mlp_before_switch: bool = True):
+                     mlp_before_switch: bool = True, ctx: np.ndarray | None = None):
     """split -> per-rank stages -> message-passing switches -> gather.
 
     Returns (gathered output, list of per-rank T-sharded outputs).
@@ -29,6 +29,9 @@ def simulate_sharded(x: np.ndarray, W: dict, num_heads: int, world: int,
     y1 = [block.spatial_stage(s, W, num_heads) for s in shards]      # a1-a4
     y1s = switch(y1, DIM_T, DIM_S, ledger, f"{tag}.switch_T2S", elem_bytes)   # a5
     y2 = [block.temporal_stage(s, W, num_heads) for s in y1s]        # a6-a9
+    if ctx is not None:  # ST-DiT cross stage: position-independent, local on S-shards
+        Wc = dict(ln_w=W["ln_c_w"], ln_b=W["ln_c_b"], w_q=W["w_q_c"], w_kv=W["w_kv_c"], w_o=W["w_o_c"])
+        y2 = [block.cross_stage(s, ctx, Wc, num_heads) for s in y2]
     if mlp_before_switch:
         y = [block.mlp_stage(s, W) for s in y2]                      # a10
         out = switch(y, DIM_S, DIM_T, ledger, f"{tag}.switch_S2T", elem_bytes)  # a11

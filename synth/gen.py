@@ -149,6 +149,36 @@ def make_block_weights(shape: BlockShape, seed: int, layer: int = 0, kappa: floa
     return {k: _store(v, shape.dtype) for k, v in out.items()}
 
 
+CROSS_NAMES = ("ln_c_w", "ln_c_b", "w_q_c", "w_kv_c", "w_o_c")
+
+
+def make_cross_weights(shape: BlockShape, seed: int, layer: int = 0, kappa: float = 1.0) -> dict:
+    """Cross-attention weights of one block (ST-DiT's text conditioning): LN_c gamma/beta,
+    w_q_c [C, C], w_kv_c [2C, C] ([k | v] rows), w_o_c [C, C].  Tensor ids 3000 + 8*layer + k
+    (disjoint from the 16*layer + k self-attention / MLP ids).  Scales as for self-attention."""
+    C = shape.C
+
+    def u(k, n):
+        return uniform_pm1(seed, 3000 + 8 * layer + k, np.arange(n, dtype=np.uint64))
+
+    out = {"ln_c_w": 1.0 + 0.1 * u(0, C), "ln_c_b": 0.1 * u(1, C),
+           "w_q_c": u(2, C * C).reshape(C, C) * math.sqrt(3.0 * kappa / C)}
+    kv = u(3, 2 * C * C).reshape(2 * C, C)
+    kv[:C] *= math.sqrt(3.0 * kappa / C)
+    kv[C:] *= math.sqrt(3.0 / C)
+    out["w_kv_c"] = kv
+    out["w_o_c"] = u(4, C * C).reshape(C, C) * math.sqrt(3.0 / C)
+    return {k: _store(v, shape.dtype) for k, v in out.items()}
+
+
+def make_context(shape: BlockShape, seed: int, ctx_len: int) -> np.ndarray:
+    """Synthetic caption embeddings [B, ctx_len, C] (already projected to C; tensor id 4000),
+    uniform in [-1, 1) like x -- the paper's text encoder and captions are out of scope."""
+    n = shape.B * ctx_len * shape.C
+    return _store(uniform_pm1(seed, 4000, np.arange(n, dtype=np.uint64)).reshape(shape.B, ctx_len, shape.C),
+                  shape.dtype)
+
+
 def zero_block_weights(shape: BlockShape) -> dict:
     C = shape.C
     dims = {"ln1_w": (C,), "ln1_b": (C,), "ln2_w": (C,), "ln2_b": (C,), "ln3_w": (C,), "ln3_b": (C,),

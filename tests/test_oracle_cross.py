@@ -87,3 +87,20 @@ def test_cross_stage_is_per_sample_and_position_independent():
     xs = x[0].reshape(12, C)[p].reshape(3, 4, C)
     ys = ob.cross_stage(xs[None], ctx[:1], Wc, NH)[0].reshape(12, C)
     np.testing.assert_allclose(ys, y[0].reshape(12, C)[p], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4])
+def test_st_block_with_cross_sharded_equals_unsharded(N):
+    """The ST-DiT block with its cross stage under the DSP schedule (cross stage on S-shards, the
+    context replicated) equals the unsharded block; without ctx it is the plain ST block."""
+    import synth
+    from oracle import sharded
+    sh = synth.BlockShape(1, 4, 16, 32, 4, "f32")
+    x = synth.to_f64(synth.make_x(sh, 3), "f32")
+    W = {k: synth.to_f64(v, "f32") for k, v in synth.make_block_weights(sh, 3).items()}
+    W.update({k: synth.to_f64(v, "f32") for k, v in synth.make_cross_weights(sh, 3).items()})
+    ctx = synth.to_f64(synth.make_context(sh, 3, 7), "f32")
+    want = ob.st_block(x, W, sh.NH, ctx)
+    got, _ = sharded.simulate_sharded(x, W, sh.NH, N, ctx=ctx)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-12)
+    assert not np.allclose(want, ob.st_block(x, W, sh.NH))
