@@ -99,6 +99,14 @@ typedef struct {
    * dsp_st_block_prepare() from THESE weights (bf16 only): every LayerNorm is folded into
    * the GEMM that consumes it (R30).  Stale if the weights change after preparing. */
   const void* prepared;
+  /* Optional cross-attention stage of the ST-DiT block (NULL ln_c_w = none):
+   *   y2 <- y2 + CA(LN_c(y2), ctx_tokens)   between the temporal stage and the MLP,
+   * local on the S-shards (every rank holds the full context).  Weights as dsp_cross_attn
+   * (w_q_c [C, C], w_kv_c [2C, C] rows [k | v], w_o_c [C, C]); ctx_tokens [B, ctx_len, C];
+   * bf16 only; needs T * S / world % 256 == 0. */
+  const void *ln_c_w, *ln_c_b, *w_q_c, *w_kv_c, *w_o_c;
+  const void* ctx_tokens;
+  int64_t ctx_len;
 } dsp_block_weights_t;
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -150,7 +158,7 @@ int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
-#define DSP_ABI_VERSION 2  /* 2: dsp_block_weights_t.prepared, block preparation */
+#define DSP_ABI_VERSION 3  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage */
 
 /* ----------------------------------------------------------- layout (bytes) */
 

@@ -44,10 +44,14 @@ class Shape(ctypes.Structure):
                 ("num_heads", ctypes.c_int32), ("dtype", ctypes.c_int)]
 
 
+CROSS_NAMES = ("ln_c_w", "ln_c_b", "w_q_c", "w_kv_c", "w_o_c")
+
+
 class BlockWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("ln1_w", "ln1_b", "w_qkv_s", "w_o_s", "ln2_w", "ln2_b", "w_qkv_t",
                                                "w_o_t", "ln3_w", "ln3_b", "w_fc1", "w_fc2")] + [
-        ("ln_eps", ctypes.c_float), ("prepared", ctypes.c_void_p)]
+        ("ln_eps", ctypes.c_float), ("prepared", ctypes.c_void_p)] + [
+        (n, ctypes.c_void_p) for n in CROSS_NAMES] + [("ctx_tokens", ctypes.c_void_p), ("ctx_len", ctypes.c_int64)]
 
 
 class SwitchPlan(ctypes.Structure):
@@ -346,10 +350,15 @@ class Context:
 
     @staticmethod
     def block_weights(W: dict, eps: float = 1e-5) -> BlockWeights:
-        """W: the 12 weight tensors by name, plus optionally "prepared" (from prepare_block)."""
+        """W: the 12 weight tensors by name, plus optionally "prepared" (from prepare_block) and the
+        cross stage (CROSS_NAMES + "ctx_tokens" [B, Lc, C])."""
         prep = W.get("prepared")
+        cross = [None] * 5 + [None, 0]
+        if W.get("ln_c_w") is not None:
+            ctxt = W["ctx_tokens"]
+            cross = [_ptr(W[n]) for n in CROSS_NAMES] + [_ptr(ctxt), int(ctxt.shape[-2])]
         return BlockWeights(*[_ptr(W[n]) for n in WEIGHT_NAMES], ctypes.c_float(eps),
-                            None if prep is None else _ptr(prep))
+                            None if prep is None else _ptr(prep), *cross)
 
     def prepare_block(self, shape, W: dict, prepared=None, stream=None) -> torch.Tensor:
         """dsp_st_block_prepare: fold the three LayerNorms into their GEMMs' weights once.

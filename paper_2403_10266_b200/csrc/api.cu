@@ -675,6 +675,17 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     if (!aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d not 16-B aligned", i);
   }
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const bool cross = w->ln_c_w != nullptr;
+  if (cross) {
+    const void* cp[6] = {w->ln_c_w, w->ln_c_b, w->w_q_c, w->w_kv_c, w->w_o_c, w->ctx_tokens};
+    for (int i = 0; i < 6; ++i)
+      if (!cp[i] || !aligned16(cp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "cross weight %d NULL or not 16-B aligned", i);
+    if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "the cross stage runs on the bf16 path");
+    if (w->ctx_len < 1) return fail(ctx, DSP_ERR_SHAPE, "ctx_len %lld < 1", (long long)w->ctx_len);
+    if ((s->T * s->S / ctx->world) % 256) return fail(ctx, DSP_ERR_UNSUPPORTED, "the cross stage needs T*S/world %% 256 == 0");
+    if (s->B * w->ctx_len > s->B * s->T * s->S / ctx->world)
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "context longer than the local tokens per sample");
+  }
   if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
   if (w->prepared && (s->C % 8 || s->C > 1280 || s->C / gemm_bn_for(s->C) > kMaxParts))
     return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= 1280 and C / BN <= %d", kMaxParts);
@@ -780,6 +791,24 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   mark(ctx, DSP_STAGE_LN2, 1, st);
   DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, fold ? cur : h, fold ? wf_t : w->w_qkv_t, w->w_o_t, cur, cur, qkv,
                      o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr, nullptr, fold ? parts : nullptr));
+  if (cross) {  // ST-DiT cross stage: y2 += CA(LN_c(y2), ctx) on the S-shards, in place
+    const int64_t Lq = s->T * (s->S / N), Lc = w->ctx_len;
+    uint8_t* q = big;
+    uint8_t* oc = big + act;
+    uint8_t* kvb = big + 2 * act;  // B * Lc <= tok rows of [k | v]
+    std::string why;
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln_c_w, w->ln_c_b, eps, h, st), "LN_c");
+    cudaError_t e2 = launch_gemm_bf16(h, w->w_q_c, nullptr, q, tok, C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    if (e2 == cudaSuccess)
+      e2 = launch_gemm_bf16(w->ctx_tokens, w->w_kv_c, nullptr, kvb, s->B * Lc, 2 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    if (e2 == cudaSuccess) e2 = launch_fmha_cross_bf16(q, kvb, oc, s->B, Lq, Lc, C, s->num_heads, ctx->num_sms, st, &why);
+    // the cross output projection rewrites the rows LN3 normalises: it writes their partials (R30)
+    if (e2 == cudaSuccess)
+      e2 = fold ? launch_gemm_bf16_res_stats(oc, w->w_o_c, cur, cur, tok, C, C, parts, ctx->num_sms, st, &why)
+                : launch_gemm_bf16(oc, w->w_o_c, cur, cur, tok, C, C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cross stage", why);
+    ctx->launches += 5;
+  }
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
   mark(ctx, DSP_STAGE_LN3, 0, st);
   if (!fold) {

@@ -384,3 +384,65 @@ def test_nd_block_5d_vs_oracle_and_virtual_ranks():
         g.run(lambda r: g.ctx[r].nd_block_forward(dims, NH, order, st_d, mlp_d, shard, Xr[r], Yr[r], impl="p2p"))
         got = np.concatenate([bits16(Yr[r]).reshape(osw.split_nd(y1, shard, N)[0].shape) for r in range(N)], axis=shard)
         assert np.array_equal(got, y1), N
+
+
+# ------------------------------------------------------------------ ST-DiT cross stage
+def _cross_setup(sh, Lc, seed=7):
+    xs, Ws = _setup(sh, seed)
+    Wc = synth.make_cross_weights(sh, seed)
+    cx = synth.make_context(sh, seed, Lc)
+    W = weights_dev(Ws, "bf16")
+    W.update(weights_dev(Wc, "bf16"))
+    W["ctx_tokens"] = to_dev(cx, "bf16").view(sh.B, Lc, sh.C)
+    Wf = weights_f64(Ws, "bf16")
+    Wf.update(weights_f64(Wc, "bf16"))
+    return xs, W, Wf, synth.to_f64(cx, "bf16")
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+@pytest.mark.parametrize("Lc", [120, 77])
+def test_block_with_cross_stage_vs_oracle(prepared, Lc):
+    """The ST-DiT block (SA -> switch -> TA -> cross attention to Lc caption tokens -> MLP -> switch,
+    P:137) at N = 1 against the float64 oracle, raw and LayerNorm-folded weights."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, W, Wf, cx = _cross_setup(sh, Lc)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    if prepared:
+        W["prepared"] = ctx.prepare_block(shape, W)
+    X = to_dev(xs, "bf16")
+    Y = torch.empty_like(X)
+    ctx.st_block_forward(shape, W, X, Y)
+    torch.cuda.synchronize()
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), Wf, sh.NH, cx)
+    print(assert_block_close(to_f64(Y), ref))
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_block_with_cross_stage_virtual_ranks_n_invariant(N):
+    """Cross stage under DSP sharding (local on the S-shards, context replicated): N virtual ranks
+    with the fused switch == N = 1, bitwise."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    xs, W, _, _ = _cross_setup(sh, 120)
+    ctx1 = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx1.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, "bf16")
+    Y = torch.empty_like(X)
+    ctx1.st_block_forward(shape, W, X, Y)
+    torch.cuda.synchronize()
+    ref1 = bits16(Y)
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    xsh = osw.split(xs, osw.DIM_T, N)
+    Xr = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Yr = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, Xr[r], Yr[r], impl="fused"))
+    got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
