@@ -365,7 +365,7 @@ class Context:
         Returns the prepared buffer; pass it as W["prepared"] to st_block_forward."""
         if prepared is None:  # f32 shapes: 0 bytes -> the C call reports DSP_ERR_UNSUPPORTED
             prepared = torch.empty(max(prepared_bytes(shape), 256), dtype=torch.uint8, device=self.device)
-        bw = self.block_weights({k: W[k] for k in WEIGHT_NAMES})
+        bw = self.block_weights({k: v for k, v in W.items() if k != "prepared"})  # incl. the cross stage
         self._call("dsp_st_block_prepare", ctypes.byref(shape), ctypes.byref(bw), _ptr(prepared),
                    prepared.numel() * prepared.element_size(), _stream(stream))
         return prepared

@@ -116,7 +116,7 @@ BlockWs block_ws(const dsp_shape_t* s, int world) {
 // Prepared (LayerNorm-folded) weights of one bf16 block: W o gamma for the three
 // LayerNorm -> linear pairs and their per-output-column u = (W o gamma) 1, v = W beta.
 struct PrepLayout {
-  int64_t wf_s, wf_t, wf_1, uv, total;
+  int64_t wf_s, wf_t, wf_1, uv, wf_c, uv_c, total;
 };
 PrepLayout prep_layout(int64_t C) {
   PrepLayout p{};
@@ -124,7 +124,9 @@ PrepLayout prep_layout(int64_t C) {
   p.wf_t = align256(3 * C * C * 2);
   p.wf_1 = p.wf_t + align256(3 * C * C * 2);
   p.uv = p.wf_1 + align256(4 * C * C * 2);
-  p.total = p.uv + align256(20 * C * 4);
+  p.wf_c = p.uv + align256(20 * C * 4);     // cross stage q projection (filled when ln_c_w is set)
+  p.uv_c = p.wf_c + align256(C * C * 2);
+  p.total = p.uv_c + align256(2 * C * 4);
   return p;
 }
 
@@ -797,8 +799,17 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     uint8_t* oc = big + act;
     uint8_t* kvb = big + 2 * act;  // B * Lc <= tok rows of [k | v]
     std::string why;
-    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln_c_w, w->ln_c_b, eps, h, st), "LN_c");
-    cudaError_t e2 = launch_gemm_bf16(h, w->w_q_c, nullptr, q, tok, C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    cudaError_t e2;
+    if (fold) {  // LN_c folded into the q projection; its statistics from PROJ_T's partials (R30)
+      EpiVec evc{};
+      const float* uvc = reinterpret_cast<const float*>(prep + P.uv_c);
+      evc.col_u = uvc; evc.col_v = uvc + C;
+      evc.part_in = parts; evc.nparts_in = nparts; evc.part_cnt = (int)(C / nparts); evc.eps = eps;
+      e2 = launch_gemm_bf16_ln(cur, prep + P.wf_c, evc, q, tok, C, C, false, ctx->num_sms, st, &why);
+    } else {
+      DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln_c_w, w->ln_c_b, eps, h, st), "LN_c");
+      e2 = launch_gemm_bf16(h, w->w_q_c, nullptr, q, tok, C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    }
     if (e2 == cudaSuccess)
       e2 = launch_gemm_bf16(w->ctx_tokens, w->w_kv_c, nullptr, kvb, s->B * Lc, 2 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
     if (e2 == cudaSuccess) e2 = launch_fmha_cross_bf16(q, kvb, oc, s->B, Lq, Lc, C, s->num_heads, ctx->num_sms, st, &why);
@@ -807,7 +818,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       e2 = fold ? launch_gemm_bf16_res_stats(oc, w->w_o_c, cur, cur, tok, C, C, parts, ctx->num_sms, st, &why)
                 : launch_gemm_bf16(oc, w->w_o_c, cur, cur, tok, C, C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
     if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cross stage", why);
-    ctx->launches += 5;
+    ctx->launches += fold ? 4 : 5;
   }
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
   mark(ctx, DSP_STAGE_LN3, 0, st);
@@ -1064,10 +1075,13 @@ dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     if (!wp[i]) return fail(ctx, DSP_ERR_NULL, "weight %d is NULL", i);
   uint8_t* p = static_cast<uint8_t*>(prep);
   float* uv = reinterpret_cast<float*>(p + P.uv);
-  LnFold jobs[3] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, p + P.wf_s, uv, uv + 3 * C, 3 * C},
+  float* uvc = reinterpret_cast<float*>(p + P.uv_c);
+  LnFold jobs[4] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, p + P.wf_s, uv, uv + 3 * C, 3 * C},
                     {w->w_qkv_t, w->ln2_w, w->ln2_b, p + P.wf_t, uv + 6 * C, uv + 9 * C, 3 * C},
-                    {w->w_fc1, w->ln3_w, w->ln3_b, p + P.wf_1, uv + 12 * C, uv + 16 * C, 4 * C}};
-  DSP_CUDA(ctx, launch_fold_ln_weights(3, jobs, C, (cudaStream_t)stream), "fold LN weights");
+                    {w->w_fc1, w->ln3_w, w->ln3_b, p + P.wf_1, uv + 12 * C, uv + 16 * C, 4 * C},
+                    {w->w_q_c, w->ln_c_w, w->ln_c_b, p + P.wf_c, uvc, uvc + C, C}};
+  const bool cross = w->ln_c_w && w->ln_c_b && w->w_q_c;
+  DSP_CUDA(ctx, launch_fold_ln_weights(cross ? 4 : 3, jobs, C, (cudaStream_t)stream), "fold LN weights");
   ctx->launches += 1;
   return DSP_OK;
 }

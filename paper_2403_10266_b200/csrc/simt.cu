@@ -269,7 +269,7 @@ struct FoldJob {
   int N;
 };
 struct FoldJobs {
-  FoldJob j[3];
+  FoldJob j[4];
 };
 __global__ void fold_ln_weights_kernel(FoldJobs jobs, int K) {
   griddep_wait();
