@@ -199,3 +199,38 @@ def test_block_long_video_virtual_ranks_n_invariant():
     g.run(lambda r: g.ctx[r].st_block_forward(shape, W, Xr[r], Yr[r], impl="fused"))
     got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     assert np.array_equal(got.reshape(-1), ref1)
+
+
+@pytest.mark.parametrize("N,impl", [(8, "fused"), (8, "p2p"), (4, "fused")])
+def test_blk_full_shape_virtual_ranks_n_invariant(N, impl):
+    """configs[1] (the bench's single block, S = 1024) at the N = 4 / 8 shard shapes the north star
+    targets (tok_r = 4096 / 2048), N virtual ranks, prepared weights, against the N = 1 prepared
+    block: LN2 statistics are recomputed after the switch at N > 1 (partials at N = 1), so the
+    comparison is within the block gate (measured rel-L2 8.6e-4) rather than bitwise; the raw
+    path's bitwise N-invariance is covered at S = 256 in test_gpu_block.py."""
+    from tests.test_gpu_block import VirtualGroup
+    from oracle import switch as osw
+    m = dsp()
+    sh = synth.CONFIGS["blk"]
+    xs = synth.make_x(sh, 7)
+    W = weights_dev(synth.make_block_weights(sh, 7), "bf16")
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx = m.Context()
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    W["prepared"] = ctx.prepare_block(shape, W)
+    X = to_dev(xs, "bf16")
+    Y1 = torch.empty_like(X)
+    ctx.st_block_forward(shape, W, X, Y1)
+    torch.cuda.synchronize()
+    ref = to_f64(Y1)
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    xsh = osw.split(xs, osw.DIM_T, N)
+    Xr = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Yr = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, Xr[r], Yr[r], impl=impl))
+    got = np.concatenate([to_f64(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    print(assert_block_close(got, ref.reshape(got.shape), atol=2e-2, rtol=1e-2, rel_l2=5e-3))
