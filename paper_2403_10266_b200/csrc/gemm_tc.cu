@@ -51,6 +51,7 @@ struct GemmCfg {
   static constexpr int EB = BN % 64 == 0 ? 64 : BN % 32 == 0 ? 32 : 16;
   static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
+  static constexpr int NBOX = BN / EB;  // staging boxes per tile (stored / reloaded one by one)
   static constexpr int STAGES = (216 * 1024 - E_BYTES) / STAGE_BYTES > 8 ? 8 : (216 * 1024 - E_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int EPI_VEC_BYTES = 2 * 2 * BN * 4;  // per-accumulator copies of u, v (LN-folded epilogue)
@@ -79,8 +80,9 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* r_full = tempty + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(r_full + 1);
+  uint64_t* r_full = tempty + 2;  // [NBOX]: residual box b of the current tile landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(r_full + Cfg::NBOX);
+  static_assert((2 * STAGES + 4 + Cfg::NBOX) * 8 + 4 <= 256, "barrier region");
   float* evec = reinterpret_cast<float*>(sE + Cfg::E_BYTES + 256);  // [2 acc][u | v][BN]
 
   const int warp = warp_id();
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * 128);  // both CTAs' epilogue threads
     }
-    mbar_init(r_full, 1);
+    for (int b = 0; b < Cfg::NBOX; ++b) mbar_init(&r_full[b], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -172,10 +174,12 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4 && EPI != EPI_RES_REMOTE) {
-    // Bulk-tensor epilogue: the residual tile arrives by TMA into the staging tile sE (issued
-    // by this warpgroup as soon as the previous tile's store has been read out of sE), each
-    // thread adds its accumulator row in place (SW128 layout: 16-B chunk c of row r at
-    // c ^ (r & 7)), and one thread TMA-stores the tile (rows >= M are clipped).
+    // Bulk-tensor epilogue: the staging tile sE holds the tile as NBOX column boxes.  Each
+    // thread adds its accumulator row into box b in place (SW128 layout: 16-B chunk c of row r
+    // at c ^ (r & 7)), and as soon as the warpgroup has finished box b one thread TMA-stores it
+    // (rows >= M are clipped) and, once the previous box's store has been read out of sE,
+    // brings in that box of the NEXT tile's residual -- so the residual loads of tile i+1
+    // overlap the epilogue of tile i instead of following its last store.
     constexpr bool kRes = EPI == DSP_EPI_RESIDUAL;
     constexpr bool kLn = EPI == EPI_LN || EPI == EPI_LN_GELU;
     const int q = warp & 3;
@@ -183,13 +187,13 @@ __global__ void __launch_bounds__(256, 1)
     const bool elected = threadIdx.x == 128;
     const uint32_t e0 = smem_u32(sE);
     int it = 0;
-    auto load_res = [&](int tile) {
+    auto load_res_box = [&](int tile, int b) {
       const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM, n0 = (tile % tiles_n) * BN;
-      mbar_arrive_expect_tx(r_full, Cfg::E_BYTES);
-#pragma unroll
-      for (int b = 0; b < BN / Cfg::EB; ++b) tma_load_2d(sE + b * Cfg::E_BOX, &tmR, r_full, n0 + Cfg::EB * b, m0);
+      mbar_arrive_expect_tx(&r_full[b], Cfg::E_BOX);
+      tma_load_2d(sE + b * Cfg::E_BOX, &tmR, &r_full[b], n0 + Cfg::EB * b, m0);
     };
-    if (kRes && elected && pair < num_tiles) load_res(pair);
+    if (kRes && elected && pair < num_tiles)
+      for (int b = 0; b < Cfg::NBOX; ++b) load_res_box(pair, b);
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
       const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
@@ -226,9 +230,8 @@ __global__ void __launch_bounds__(256, 1)
           st_shared_f32(smem_u32(eu + BN + i), ev.col_v[n0 + i]);
         }
       }
-      if (kRes) {
-        mbar_wait(r_full, it & 1);
-      } else if (it > 0 || kLn) {  // the previous tile's store must have been read out of sE
+      const bool has_next = tile + num_pairs < num_tiles;
+      if (!kRes && (it > 0 || kLn)) {  // the previous tile's store must have been read out of sE
         if (elected && it > 0) bulk_wait_group_read0();
         named_bar_sync(1, 128);
       }
@@ -246,6 +249,7 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
         // chunk c (CW columns = CW/8 x 16 B) of this row inside box (c * CW) / EB
         const int col0 = c * CW;
+        if (kRes && col0 % Cfg::EB == 0) mbar_wait(&r_full[col0 / Cfg::EB], it & 1);
         const uint32_t line = e0 + (col0 / Cfg::EB) * Cfg::E_BOX + row * (Cfg::EB * 2);
 #pragma unroll
         for (int u = 0; u < CW / 8; ++u) {
@@ -295,6 +299,19 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
         }
+        if ((col0 + CW) % Cfg::EB == 0) {  // box b of this tile complete in every row: store it
+          const int b = col0 / Cfg::EB;
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (elected) {
+            tma_store_2d(&tmD, sE + b * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
+            bulk_commit_group();
+            if (kRes && has_next && b > 0) {
+              bulk_wait_group_read1();  // box b-1 read out of sE: reload it for the next tile
+              load_res_box(tile + num_pairs, b - 1);
+            }
+          }
+        }
       }
       if (kStats && m0 + row < M) {
         const float a = s1.x + s1.y, mp = a * (1.f / BN);
@@ -304,16 +321,9 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next
       else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (elected) {
-#pragma unroll
-        for (int b = 0; b < BN / Cfg::EB; ++b) tma_store_2d(&tmD, sE + b * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
-        bulk_commit_group();
-        if (kRes && tile + num_pairs < num_tiles) {
-          bulk_wait_group_read0();  // sE read out: bring in the next tile's residual
-          load_res(tile + num_pairs);
-        }
+      if (kRes && elected && has_next) {
+        bulk_wait_group_read0();
+        load_res_box(tile + num_pairs, Cfg::NBOX - 1);
       }
     }
     if (elected) bulk_wait_group_read0();
