@@ -446,7 +446,9 @@ __device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CU
 // thread's keys are the columns [lo, lo + L) of its diagonal block, inside the warp's 32-
 // or 64-column window.  Single pass from registers, range-compare mask (no division), the
 // full P row is written (zeros outside the block) so the buffer can stage O afterwards.
-template <int W>  // window width: 32 or 64 columns
+// PT: P goes to tensor memory instead (columns [0, 64) of this lane's S row, two bf16 per
+// column: the A operand of a TS-form P.V), so the shared tile only stages O.
+template <int W, bool PT>  // window width: 32 or 64 columns
 __device__ __forceinline__ void softmax_tile_diag(const SoftmaxGeom& G, uint32_t tS, uint8_t* sP, float& m, float& l,
                                                   int* store_pending, uint32_t bar_id) {
   const int row = G.row;
@@ -477,6 +479,18 @@ __device__ __forceinline__ void softmax_tile_diag(const SoftmaxGeom& G, uint32_t
   }
   m = m_new;
   l = rs;
+  if (PT) {  // packed column c holds keys 2c, 2c+1; 32-key chunks outside the window are zero
+    const int wch = G.wc0 >> 5;
+    const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch)
+      if (ch < wch || ch >= wch + W / 32) tmem_st16(tS + G.lane_off + ch * 16, z);
+    tmem_st16(tS + G.lane_off + wch * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+    if (W == 64) tmem_st16(tS + G.lane_off + wch * 16 + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
+    tmem_st_wait();
+    tc_fence_before();
+    return;
+  }
   if (store_pending && *store_pending) {  // previous item's O TMA store must have read the P buffer
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
     named_bar_sync(bar_id, 128);
@@ -528,6 +542,12 @@ __device__ __forceinline__ void store_o(const FmhaParams& p, const TileCoord& t,
     }
   }
 }
+
+#ifdef DSP_FMHA_P_SMEM
+constexpr bool kFmhaPTmem = false;  // A/B: block-diagonal P through shared memory (SS-form P.V)
+#else
+constexpr bool kFmhaPTmem = true;
+#endif
 
 template <int NA, int RB>
 __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
@@ -614,6 +634,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
     constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
     constexpr uint32_t idPVb = make_idesc_bf16(128, RB == 0 ? 16 : RB, 0, 1);
     const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV), p0 = smem_u32(sP);
+    const bool p_tmem = kFmhaPTmem && p.G > 1;  // block-diagonal tiles (n == 1): P in TMEM
     uint32_t nq = 0, nk = 0, nv = 0, np = 0, nit = 0;
     auto issue_s = [&]() {
       mbar_wait(k_full, nk & 1);
@@ -661,15 +682,21 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
           const uint32_t vb = v0 + vs * Cfg::TILE;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {  // 128 keys in steps of 16
-            const uint64_t ad = make_sdesc(p0 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SW_128B);
+            const uint64_t bdr = make_sdesc(vb + NA * 16384 + k * 16 * Cfg::RB_ROW, 16384, 8 * Cfg::RB_ROW, Cfg::RB_SW);
+            if (p_tmem) {  // P_j in TMEM (S columns [0, 64)): 8 packed columns per 16 keys
 #pragma unroll
-            for (int i = 0; i < NA; ++i)
-              umma_bf16_ss(tO + 64 * i, ad, make_sdesc(vb + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
-                           (j | k) != 0);
-            if (RB)
-              umma_bf16_ss(tO + 64 * NA, ad,
-                           make_sdesc(vb + NA * 16384 + k * 16 * Cfg::RB_ROW, 16384, 8 * Cfg::RB_ROW, Cfg::RB_SW),
-                           idPVb, (j | k) != 0);
+              for (int i = 0; i < NA; ++i)
+                umma_bf16_ts(tO + 64 * i, tS + 8 * k, make_sdesc(vb + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+                             (j | k) != 0);
+              if (RB) umma_bf16_ts(tO + 64 * NA, tS + 8 * k, bdr, idPVb, (j | k) != 0);
+            } else {
+              const uint64_t ad = make_sdesc(p0 + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, SW_128B);
+#pragma unroll
+              for (int i = 0; i < NA; ++i)
+                umma_bf16_ss(tO + 64 * i, ad, make_sdesc(vb + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+                             (j | k) != 0);
+              if (RB) umma_bf16_ss(tO + 64 * NA, ad, bdr, idPVb, (j | k) != 0);
+            }
           }
           umma_commit(o_done);
           umma_commit(&v_empty[vs]);
@@ -691,13 +718,18 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
         tc_fence_after();
         FMHA_STAMP(tr, 1);
         if (G.diag) {  // n == 1 in this mode
-          if (G.nhalf * G.hcols > 32) softmax_tile_diag<64>(G, tS, sP, m, l, &store_pending, 1);
-          else softmax_tile_diag<32>(G, tS, sP, m, l, &store_pending, 1);
+          if (G.nhalf * G.hcols > 32) softmax_tile_diag<64, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
+          else softmax_tile_diag<32, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
         } else {
           softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
         }
         FMHA_STAMP(tr, 2);
         mbar_arrive(p_full);
+      }
+      if (kFmhaPTmem && G.diag && store_pending) {  // the staging tile only holds O: free it here
+        if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+        named_bar_sync(1, 128);
+        store_pending = 0;
       }
       mbar_wait(o_done, no & 1);
       ++no;

@@ -126,6 +126,10 @@ def _attn_ref(qkv, B, T, S, C, NH, dim):
     (2, 16, 12, 1152, 16, "T", 4.0),      # ragged column tail, B=2, peaky
     (1, 128, 8, 1152, 16, "T", 1.0),      # long-video T=128, one sequence per tile
     (1, 4, 32, 64, 4, "T", 1.0),          # Dh=16, T=4 -> 32 columns per tile
+    (1, 64, 8, 1152, 16, "T", 1.0),       # T=64: two sequences per tile, 64-key windows (two P stores)
+    (1, 32, 9, 256, 4, "T", 4.0),         # T=32: four per tile, ragged column tail, peaky
+    (1, 3, 64, 256, 4, "S", 1.0),         # S=64 spatial: two frames per tile
+    (1, 2, 70, 128, 2, "T", 1.0),         # T=2: 64 sequences per tile (window 32 keys, 2 valid)
 ])
 def test_attention_core_bf16(ctx, B, T, S, C, NH, dim, kappa):
     bits, qkv = _qkv_case(B, T, S, C, NH, kappa)
