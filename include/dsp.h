@@ -225,8 +225,10 @@ dsp_status_t dsp_switch_plan(const dsp_shape_t* shape, int world, int rank,
  * (R6-R8).  No LayerNorm inside.  Local (no communication).  Uses the workspace for
  * qkv and O (tok_r * 4C * elem bytes).  out may equal residual; out must not overlap h.
  * bf16: tcgen05 QKV GEMM -> tcgen05 FMHA -> tcgen05 out-proj GEMM (+residual epilogue).
- * Errors: SHAPE (C % num_heads), UNSUPPORTED (bf16 needs Dh % 16 == 0 or Dh in {72}
- * ... see dsp_last_error; C % 64 == 0), ALIAS, WORKSPACE, DIVISIBILITY. */
+ * Any sequence length >= 1 (lengths that neither divide nor are a multiple of 128 run with a
+ * masked last key tile, DESIGN R34).
+ * Errors: SHAPE (C % num_heads), UNSUPPORTED (bf16 needs Dh % 8 == 0, Dh <= 128 and
+ * C % 32 == 0; see dsp_last_error), ALIAS, WORKSPACE, DIVISIBILITY. */
 dsp_status_t dsp_spatial_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local,
                               const void* w_qkv, const void* w_o, const void* residual,
                               void* out, void* stream);

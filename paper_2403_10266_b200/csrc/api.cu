@@ -140,8 +140,7 @@ dsp_status_t check_bf16_attn(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t L) {
   }
   if (Dh % 8 || Dh > 128) return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 attention needs Dh %% 8 == 0 and Dh <= 128 (Dh=%lld)", (long long)Dh);
   if (s->C % 32) return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 path needs C %% 32 == 0 (C=%lld)", (long long)s->C);
-  if (!(L % 128 == 0 || 128 % L == 0))
-    return fail(ctx, DSP_ERR_UNSUPPORTED, "bf16 attention needs the sequence length (%lld) to divide 128 or be a multiple of 128", (long long)L);
+  (void)L;  // any length: divisors of 128 are packed per tile, others masked in the last key tile
   return DSP_OK;
 }
 

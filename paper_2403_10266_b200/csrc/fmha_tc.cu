@@ -168,10 +168,12 @@ __device__ __forceinline__ SoftmaxGeom make_geom(const FmhaParams& p, int warp, 
 // One online-softmax step on S_j (in TMEM at tS): row max, lazy O rescale (after PV_{j-1}
 // completed, signalled on o_done), P_j = exp2(S*scale - m) as bf16 into the SW128 smem tile
 // sP, running sum l.  Returns after the P stores are fenced for the async proxy.
+// valid < 128 (non-diagonal tiles only): keys >= valid of this tile are padding of a ragged
+// sequence (TMA zero fill) and are excluded (-inf) in both passes.
 template <int DP>
 __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, uint8_t* sP, int j,
                                              float& m, float& l, uint64_t* o_done, uint32_t& no,
-                                             int* store_pending = nullptr, uint32_t bar_id = 0) {
+                                             int* store_pending = nullptr, uint32_t bar_id = 0, int valid = 128) {
   const int row = G.row;
   const uint32_t lane_off = G.lane_off;
   const bool diag = G.diag;
@@ -199,6 +201,10 @@ __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, 
 #pragma unroll
       for (int i = 0; i < 64; ++i)
         if ((wc0 + hf * 64 + i) / G.L != my_blk) s[i] = -INFINITY;
+    } else if (valid < 128) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (hf * 64 + i >= valid) s[i] = -INFINITY;
     }
     float t8[8];
 #pragma unroll
@@ -259,7 +265,7 @@ __device__ __forceinline__ void softmax_tile(const SoftmaxGeom& G, uint32_t tS, 
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           float x = __uint_as_float(v[i]);
-          if (diag && (col0 + c * 32 + i) / G.L != my_blk) x = -INFINITY;
+          if (diag ? (col0 + c * 32 + i) / G.L != my_blk : col0 + c * 32 + i >= valid) x = -INFINITY;
           e[i] = fast_exp2(fmaf(x, sl2, -m_new));
           rs8[i & 7] += e[i];
         }
@@ -721,7 +727,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
           if (G.nhalf * G.hcols > 32) softmax_tile_diag<64, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
           else softmax_tile_diag<32, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
         } else {
-          softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1);
+          softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1, j + 1 == n ? p.kv_last : 128);
         }
         FMHA_STAMP(tr, 2);
         mbar_arrive(p_full);
@@ -1129,9 +1135,11 @@ cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc,
     p.G = 128 / p.L;
     p.n_kv = 1;
     p.n_qt = 1;
-  } else {
-    if (why) *why = "bf16 attention needs the sequence length to divide 128 or be a multiple of 128";
-    return cudaErrorNotSupported;
+  } else {  // ragged length: one sequence per tile row block, last query tile clipped by the
+            // TMA store, keys >= L of the last key tile masked
+    p.G = 1;
+    p.n_kv = (p.L + 127) / 128;
+    p.n_qt = p.n_kv;
   }
   const uint64_t e = 2, rowb = 3 * (uint64_t)C * e;
   uint64_t dims[5], strides[4];
@@ -1148,7 +1156,7 @@ cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc,
   }
   uint32_t box_rows[2] = {(uint32_t)(p.G == 1 ? 128 : p.L), (uint32_t)p.G};
   p.items = p.n_outer * NH * p.n_qt;
-  p.kv_last = 128;
+  p.kv_last = p.G == 1 ? p.L - 128 * (p.n_kv - 1) : 128;
   if (p.items == 0) return cudaSuccess;
   FmhaViews vw;
   const auto* base = static_cast<const __nv_bfloat16*>(qkv);
