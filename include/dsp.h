@@ -103,7 +103,7 @@ typedef struct {
    *   y2 <- y2 + CA(LN_c(y2), ctx_tokens)   between the temporal stage and the MLP,
    * local on the S-shards (every rank holds the full context).  Weights as dsp_cross_attn
    * (w_q_c [C, C], w_kv_c [2C, C] rows [k | v], w_o_c [C, C]); ctx_tokens [B, ctx_len, C];
-   * bf16 only; needs T * S / world % 256 == 0. */
+   * bf16 only. */
   const void *ln_c_w, *ln_c_b, *w_q_c, *w_kv_c, *w_o_c;
   const void* ctx_tokens;
   int64_t ctx_len;
@@ -295,8 +295,8 @@ dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int ele
  *   q = h w_q^T,  [k | v] = ctx_tokens w_kv^T  (w_kv [2C, C] rows [k | v], head j rows j*Dh.., R8)
  * h, residual, out: [B, T_loc, S_loc, C] local tokens (either sharding; LN applied by the caller);
  * ctx_tokens: [B, Lc, C] (already projected to C); bf16 only.  Keys beyond Lc in the last
- * 128-key tile are masked.  Needs (B*T*S/world)/B % 256 == 0 local tokens per sample and
- * workspace >= dsp_cross_workspace_bytes.  Not collective.  Errors: NULL, SHAPE, DIVISIBILITY,
+ * 128-key tile are masked; any number of local tokens per sample (a ragged last query tile is
+ * clipped).  Needs workspace >= dsp_cross_workspace_bytes.  Not collective.  Errors: NULL, SHAPE, DIVISIBILITY,
  * UNSUPPORTED, ALIGNMENT, ALIAS (out overlaps h; out == residual is allowed), WORKSPACE, CUDA. */
 size_t dsp_cross_workspace_bytes(const dsp_shape_t* shape, int world, int64_t Lc);  /* host-only */
 dsp_status_t dsp_cross_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local, const void* ctx_tokens,

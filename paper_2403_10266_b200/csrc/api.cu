@@ -683,7 +683,6 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       if (!cp[i] || !aligned16(cp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "cross weight %d NULL or not 16-B aligned", i);
     if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "the cross stage runs on the bf16 path");
     if (w->ctx_len < 1) return fail(ctx, DSP_ERR_SHAPE, "ctx_len %lld < 1", (long long)w->ctx_len);
-    if ((s->T * s->S / ctx->world) % 256) return fail(ctx, DSP_ERR_UNSUPPORTED, "the cross stage needs T*S/world %% 256 == 0");
     if (s->B * w->ctx_len > s->B * s->T * s->S / ctx->world)
       return fail(ctx, DSP_ERR_UNSUPPORTED, "context longer than the local tokens per sample");
   }
@@ -904,7 +903,6 @@ dsp_status_t dsp_cross_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* h, 
     const dsp_shape_t hs{1, 1, 1, C, s->num_heads, s->dtype};
     DSP_TRY(check_bf16_attn(ctx, &hs, 128));
   }
-  if (Lq % 256) return fail(ctx, DSP_ERR_UNSUPPORTED, "cross attention needs the local tokens per sample (%lld) %% 256 == 0", (long long)Lq);
   const void* bufs[8] = {h, ctx_tokens, w_q, w_kv, w_o, residual, out, ctx->ws};
   for (int i = 0; i < 8; ++i)
     if (bufs[i] && !aligned16(bufs[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");

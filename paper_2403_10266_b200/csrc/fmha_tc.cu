@@ -1185,13 +1185,13 @@ cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64
   p.spatial = 1;  // queries of sample b = rows [b*Lq, (b+1)*Lq) of q; keys / values = rows of kv
   p.L = (int)Lq;
   p.G = 1;
-  p.n_qt = (int)(Lq / 128);
+  p.n_qt = (int)((Lq + 127) / 128);  // a ragged last query tile is clipped by the TMA store
   p.n_kv = (int)((Lc + 127) / 128);
   p.kv_last = (int)(Lc - 128 * (p.n_kv - 1));
   p.n_outer = (int)B;
   p.items = p.n_outer * NH * p.n_qt;
-  if (Lq % 256 || Lc < 1) {
-    if (why) *why = "cross attention needs tokens per sample % 256 == 0 and at least one context token";
+  if (Lc < 1) {
+    if (why) *why = "cross attention needs at least one context token";
     return cudaErrorNotSupported;
   }
   if (p.items == 0) return cudaSuccess;

@@ -420,6 +420,26 @@ def test_block_with_cross_stage_vs_oracle(prepared, Lc):
     print(assert_block_close(to_f64(Y), ref))
 
 
+@pytest.mark.parametrize("prepared", [False, True])
+def test_block_with_cross_stage_ragged_lengths(prepared):
+    """Block with S = 200 (ragged spatial tiles, R34) and a cross stage whose T * S = 3200
+    queries per sample are 25 query tiles (odd: the single-tile kernel on separate views)."""
+    m = dsp()
+    sh = synth.BlockShape(1, 16, 200, 256, 4, "bf16")
+    xs, W, Wf, cx = _cross_setup(sh, 77)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    if prepared:
+        W["prepared"] = ctx.prepare_block(shape, W)
+    X = to_dev(xs, "bf16")
+    Y = torch.empty_like(X)
+    ctx.st_block_forward(shape, W, X, Y)
+    torch.cuda.synchronize()
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), Wf, sh.NH, cx)
+    print(assert_block_close(to_f64(Y), ref))
+
+
 @pytest.mark.parametrize("N", [2, 4])
 def test_block_with_cross_stage_virtual_ranks_n_invariant(N):
     """Cross stage under DSP sharding (local on the S-shards, context replicated): N virtual ranks

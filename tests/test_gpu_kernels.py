@@ -154,11 +154,13 @@ def test_attention_core_f32(ctx, dim):
 
 
 @pytest.mark.parametrize("B,T,S,Lc,kappa", [(2, 4, 128, 120, 1.0), (1, 2, 256, 77, 1.0), (2, 2, 128, 128, 4.0),
-                                             (1, 4, 64, 300, 1.0), (1, 1, 256, 1, 1.0)])
+                                             (1, 4, 64, 300, 1.0), (1, 1, 256, 1, 1.0),
+                                             (2, 1, 200, 120, 1.0), (1, 3, 128, 77, 1.0), (1, 1, 40, 50, 4.0)])
 def test_cross_attention_bf16(ctx, B, T, S, Lc, kappa):
     """dsp_cross_attn vs the oracle: caption-like context lengths 120 / 77 (masked tail
     keys), exactly one tile, three tiles with a ragged last one, a single context token; peaky
-    scores at kappa = 4."""
+    scores at kappa = 4; query counts per sample that are not a multiple of 256 (200: a
+    clipped second query tile; 384: an odd tile count, single-tile kernel; 40)."""
     import paper_2403_10266_b200 as dsp
     C, NH = 1152, 16
     tok = B * T * S
