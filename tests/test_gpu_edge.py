@@ -112,3 +112,41 @@ def test_block_degenerate_extent(sh, prepared):
     torch.cuda.synchronize()
     ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
     print(assert_block_close(to_f64(Y), ref))
+
+
+@pytest.mark.parametrize("sh,prepared", [
+    (synth.BlockShape(1, 4, 128, 2048, 16, "bf16"), False),   # Dh = 128 (two 64-column TMA boxes)
+    (synth.BlockShape(1, 8, 128, 1024, 16, "bf16"), False),   # Dh = 64
+    (synth.BlockShape(1, 8, 128, 1024, 16, "bf16"), True),
+    (synth.BlockShape(2, 4, 64, 768, 12, "bf16"), True),      # Dh = 64, C = 768 (DiT-B width)
+])
+def test_block_other_widths(sh, prepared):
+    """Model widths other than the paper's 1152 / Dh = 72 against the oracle block."""
+    m = _dsp()
+    Ws = synth.make_block_weights(sh, 7)
+    xs = synth.make_x(sh, 7)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    ctx.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, sh.dtype)
+    Y = torch.empty_like(X)
+    W = weights_dev(Ws, sh.dtype)
+    if prepared:
+        W["prepared"] = ctx.prepare_block(shape, W)
+    ctx.st_block_forward(shape, W, X, Y)
+    torch.cuda.synchronize()
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
+    print(assert_block_close(to_f64(Y), ref))
+
+
+def test_prepared_path_rejects_wide_rows():
+    """C > 1280 on the prepared (LayerNorm-folded) path is a documented UNSUPPORTED, not a
+    wrong answer; the raw-weights path covers it (test_block_other_widths)."""
+    m = _dsp()
+    sh = synth.BlockShape(1, 4, 128, 2048, 16, "bf16")
+    Ws = synth.make_block_weights(sh, 7)
+    ctx = m.Context()
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    W = weights_dev(Ws, sh.dtype)
+    with pytest.raises(m.DSPError, match="UNSUPPORTED"):
+        ctx.prepare_block(shape, W)
