@@ -347,7 +347,8 @@ size_t dsp_block_prepared_bytes(const dsp_shape_t* shape);
  *   (each 256-B aligned) | f32 u_s[3C] v_s[3C] u_t[3C] v_t[3C] u_1[4C] v_1[4C] | with a cross
  *   stage (ln_c_w set): [C, C] bf16 w_q_c o ln_c_w | f32 u_c[C] v_c[C] (LN_c statistics then come
  *   from the temporal out-projection's partials).
- * Enqueued on `stream`.  Errors: NULL, UNSUPPORTED (f32, C % 8 != 0, C > 1280),
+ * Enqueued on `stream`.  Errors: NULL, UNSUPPORTED (f32, C % 8 != 0, C > 3072, or more than 12
+ * LayerNorm partials per row: C / BN > 12 with BN the out-projection tile width),
  * WORKSPACE (prepared_bytes too small), ALIGNMENT, CUDA. */
 dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* w,
                                   void* prepared, size_t prepared_bytes, void* stream);

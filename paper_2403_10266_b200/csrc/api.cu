@@ -687,8 +687,9 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       return fail(ctx, DSP_ERR_UNSUPPORTED, "context longer than the local tokens per sample");
   }
   if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
-  if (w->prepared && (s->C % 8 || s->C > 1280 || s->C / gemm_bn_for(s->C) > kMaxParts))
-    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= 1280 and C / BN <= %d", kMaxParts);
+  if (w->prepared && (s->C % 8 || s->C > 256 * kRowStatsMaxV || s->C / gemm_bn_for(s->C) > kMaxParts))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= %d and C / BN <= %d",
+                256 * kRowStatsMaxV, kMaxParts);
   const int N = ctx->world;
   if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P && impl != DSP_SWITCH_FUSED)
     return fail(ctx, DSP_ERR_UNSUPPORTED, "unknown switch impl %d", (int)impl);
@@ -1063,7 +1064,9 @@ dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   if (!w || !prep) return fail(ctx, DSP_ERR_NULL, "NULL argument");
   if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
   const int64_t C = s->C;
-  if (C % 8 || C > 1280) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0 and C <= 1280 (C=%lld)", (long long)C);
+  if (C % 8 || C > 256 * kRowStatsMaxV || C / gemm_bn_for(C) > kMaxParts)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= %d and C / BN <= %d (C=%lld)",
+                256 * kRowStatsMaxV, kMaxParts, (long long)C);
   const PrepLayout P = prep_layout(C);
   if (prep_bytes < (size_t)P.total) return fail(ctx, DSP_ERR_WORKSPACE, "prepared buffer needs %lld bytes", (long long)P.total);
   if (reinterpret_cast<uintptr_t>(prep) % 256) return fail(ctx, DSP_ERR_ALIGNMENT, "prepared buffer must be 256-B aligned");

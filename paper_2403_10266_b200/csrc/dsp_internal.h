@@ -105,6 +105,7 @@ struct EpiVec {
 int gemm_bn_for(int64_t N);
 // most per-row LayerNorm partials (one per BN-column tile of the producing GEMM) an LN epilogue combines
 constexpr int kMaxParts = 12;
+constexpr int kRowStatsMaxV = 12;  // row statistics kernel: C <= 256 * 12 = 3072
 cudaError_t launch_gemm_bf16_res_stats(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
                                        int64_t K, float2* part_out, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev, void* D, int64_t M, int64_t N,

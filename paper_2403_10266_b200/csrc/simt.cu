@@ -209,12 +209,13 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
 // Per-row LayerNorm statistics (mean, rstd) of a bf16 [rows, C] activation, two-pass in
 // registers like the LayerNorm kernel; 8 bytes out per row.  Used to fold LN into the GEMM
 // that consumes it (LN(x) W^T = rstd (x (W o gamma)^T - mean u) + W beta).
-__global__ void __launch_bounds__(256, 4) row_stats_bf16_kernel(const __nv_bfloat16* __restrict__ x, float eps,
+template <int kMaxV>  // 16-B vectors per lane: C <= 256 * kMaxV
+__global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel(const __nv_bfloat16* __restrict__ x, float eps,
                                                                 float2* __restrict__ stats, long rows, int C) {
   griddep_wait();
   griddep_launch_dependents();
   // DSP_ROWSTATS_R rows per warp (32 warps resident per SM), all loads issued before any reduction
-  constexpr int R = DSP_ROWSTATS_R, kMaxV = 5;  // C <= 1280
+  constexpr int R = DSP_ROWSTATS_R;
   const long r0 = (((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R;
   const int lane = threadIdx.x & 31;
   const int nv = C / 8;
@@ -366,9 +367,12 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
   const int threads = 256;
   const long warps = (rows + DSP_ROWSTATS_R - 1) / DSP_ROWSTATS_R;
   const unsigned blocks = (unsigned)((warps * 32 + threads - 1) / threads);
-  if (C % 8 || C > 1280) return cudaErrorNotSupported;
-  return launch_k(row_stats_bf16_kernel, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, eps,
-                  (float2*)stats, rows, (int)C);
+  if (C % 8 || C > 256 * kRowStatsMaxV) return cudaErrorNotSupported;
+  if (C <= 1280)  // the model widths of the paper (1152): 5 vectors per lane
+    return launch_k(row_stats_bf16_kernel<5>, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, eps,
+                    (float2*)stats, rows, (int)C);
+  return launch_k(row_stats_bf16_kernel<kRowStatsMaxV>, dim3(blocks), dim3(threads), 0, st, 1,
+                  (const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C);
 }
 
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {

@@ -116,6 +116,7 @@ def test_block_degenerate_extent(sh, prepared):
 
 @pytest.mark.parametrize("sh,prepared", [
     (synth.BlockShape(1, 4, 128, 2048, 16, "bf16"), False),   # Dh = 128 (two 64-column TMA boxes)
+    (synth.BlockShape(1, 4, 128, 2048, 16, "bf16"), True),    # 12-vector row statistics, 8 LN partials
     (synth.BlockShape(1, 8, 128, 1024, 16, "bf16"), False),   # Dh = 64
     (synth.BlockShape(1, 8, 128, 1024, 16, "bf16"), True),
     (synth.BlockShape(2, 4, 64, 768, 12, "bf16"), True),      # Dh = 64, C = 768 (DiT-B width)
@@ -140,10 +141,10 @@ def test_block_other_widths(sh, prepared):
 
 
 def test_prepared_path_rejects_wide_rows():
-    """C > 1280 on the prepared (LayerNorm-folded) path is a documented UNSUPPORTED, not a
-    wrong answer; the raw-weights path covers it (test_block_other_widths)."""
+    """C > 3072 on the prepared (LayerNorm-folded) path is a documented UNSUPPORTED, not a
+    wrong answer; the raw-weights path covers any width."""
     m = _dsp()
-    sh = synth.BlockShape(1, 4, 128, 2048, 16, "bf16")
+    sh = synth.BlockShape(1, 2, 16, 4096, 32, "bf16")
     Ws = synth.make_block_weights(sh, 7)
     ctx = m.Context()
     shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
