@@ -226,7 +226,7 @@ dsp_status_t dsp_switch_plan(const dsp_shape_t* shape, int world, int rank,
  * qkv and O (tok_r * 4C * elem bytes).  out may equal residual; out must not overlap h.
  * bf16: tcgen05 QKV GEMM -> tcgen05 FMHA -> tcgen05 out-proj GEMM (+residual epilogue).
  * Any sequence length >= 1 (lengths that neither divide nor are a multiple of 128 run with a
- * masked last key tile, DESIGN R34).
+ * masked last key tile, DESIGN R33).
  * Errors: SHAPE (C % num_heads), UNSUPPORTED (bf16 needs Dh % 8 == 0, Dh <= 128 and
  * C % 32 == 0; see dsp_last_error), ALIAS, WORKSPACE, DIVISIBILITY. */
 dsp_status_t dsp_spatial_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const void* h_local,

@@ -422,7 +422,7 @@ def test_block_with_cross_stage_vs_oracle(prepared, Lc):
 
 @pytest.mark.parametrize("prepared", [False, True])
 def test_block_with_cross_stage_ragged_lengths(prepared):
-    """Block with S = 200 (ragged spatial tiles, R34) and a cross stage whose T * S = 3200
+    """Block with S = 200 (ragged spatial tiles, R33) and a cross stage whose T * S = 3200
     queries per sample are 25 query tiles (odd: the single-tile kernel on separate views)."""
     m = dsp()
     sh = synth.BlockShape(1, 16, 200, 256, 4, "bf16")

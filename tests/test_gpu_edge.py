@@ -4,7 +4,7 @@
   over one key is exactly 1, so each head's output is its value row -- a closed form the
   kernels must hit bit for bit (P = exp2(0) = 1 in bf16, O = V / 1);
 * blocks whose temporal or spatial extent is 1 (one stage reduces to V·Wo), raw and prepared;
-* sequence lengths that are neither a multiple nor a divisor of the 128-row tile (R34): the
+* sequence lengths that are neither a multiple nor a divisor of the 128-row tile (R33): the
   last query tile is clipped by the TMA store, keys past the end of the last key tile are
   masked before the row max.
 """
@@ -61,7 +61,7 @@ def test_length_one_attention_is_v(B, T, S, C, NH, dim):
     (1, 200, 6, 256, 4, "T", 1.0),     # T = 200: two tiles per column (pair kernel)
 ])
 def test_ragged_sequences(B, T, S, C, NH, dim, kappa):
-    """Sequence lengths that neither divide 128 nor are a multiple of it (R34)."""
+    """Sequence lengths that neither divide 128 nor are a multiple of it (R33)."""
     m = _dsp()
     ctx = m.Context()
     ctx.ensure_workspace(1 << 20)
