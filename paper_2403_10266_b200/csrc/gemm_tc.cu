@@ -40,15 +40,19 @@ namespace {
 constexpr int BM = 128;  // rows per CTA (256 per pair)
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SW128 atom row
 
-template <int BN>
+template <int BN, int EPI>
 struct GemmCfg {
   static constexpr int BNH = BN / 2;                    // W rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int E_BYTES = BN * 256;  // epilogue staging: 128 rows x BN bf16 as BN/EB boxes
   // store/residual box width (columns): SW128 at 64, SW64 at 32, SW32 at 16 (BN = 144)
   static constexpr int EB = BN % 64 == 0 ? 64 : BN % 32 == 0 ? 32 : 16;
+  // epilogue staging: the residual epilogue stages the whole 128 x BN tile (the residual tile
+  // lands there by TMA); the others use a ring of two boxes (store of box i overlaps box i+1),
+  // which leaves room for one more mainloop stage at BN = 256
+  static constexpr bool RING = EPI != DSP_EPI_RESIDUAL && EPI != EPI_RES_REMOTE;
+  static constexpr int E_BYTES = RING ? 2 * 128 * EB * 2 : BN * 256;
   static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
   static constexpr int NBOX = BN / EB;  // staging boxes per tile (stored / reloaded one by one)
@@ -69,7 +73,7 @@ __global__ void __launch_bounds__(256, 1)
                         const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
                         const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
                         const EpiVec ev, const RemoteMap rm) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -231,10 +235,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       const bool has_next = tile + num_pairs < num_tiles;
-      if (!kRes && (it > 0 || kLn)) {  // the previous tile's store must have been read out of sE
-        if (elected && it > 0) bulk_wait_group_read0();
-        named_bar_sync(1, 128);
-      }
+      if (kLn) named_bar_sync(1, 128);  // u, v staged
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       // row statistics of the stored (bf16-rounded) values, shifted by the first one
@@ -250,7 +251,13 @@ __global__ void __launch_bounds__(256, 1)
         // chunk c (CW columns = CW/8 x 16 B) of this row inside box (c * CW) / EB
         const int col0 = c * CW;
         if (kRes && col0 % Cfg::EB == 0) mbar_wait(&r_full[col0 / Cfg::EB], it & 1);
-        const uint32_t line = e0 + (col0 / Cfg::EB) * Cfg::E_BOX + row * (Cfg::EB * 2);
+        // ring slot of this box: boxes alternate between the two slots across tiles too
+        const int slot = Cfg::RING ? ((it * Cfg::NBOX + col0 / Cfg::EB) & 1) : col0 / Cfg::EB;
+        if (Cfg::RING && col0 % Cfg::EB == 0) {  // the store that last used this slot has been read
+          if (elected) bulk_wait_group_read1();
+          named_bar_sync(1, 128);
+        }
+        const uint32_t line = e0 + slot * Cfg::E_BOX + row * (Cfg::EB * 2);
 #pragma unroll
         for (int u = 0; u < CW / 8; ++u) {
           const int j = (col0 % Cfg::EB) / 8 + u;
@@ -304,7 +311,7 @@ __global__ void __launch_bounds__(256, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
           if (elected) {
-            tma_store_2d(&tmD, sE + b * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
+            tma_store_2d(&tmD, sE + slot * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
             bulk_commit_group();
             if (kRes && has_next && b > 0) {
               bulk_wait_group_read1();  // box b-1 read out of sE: reload it for the next tile
@@ -480,7 +487,7 @@ template <int BN, int EPI>
 static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
                             int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{},
                             const RemoteMap& rm = RemoteMap{}) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   CUtensorMap ta, tw, td, tr;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
