@@ -348,6 +348,25 @@ def test_nd_block_5d_single_stage_vs_oracle(axis):
     print(assert_block_close(to_f64(Y), ref))
 
 
+@pytest.mark.parametrize("dims,axis", [((1, 6, 12, 20, 256), 3), ((1, 6, 12, 20, 256), 2), ((2, 51, 4, 4, 256), 1)])
+def test_nd_block_ragged_axes_vs_oracle(dims, axis):
+    """N-D block stages along axes whose lengths neither divide nor are a multiple of 128
+    (W = 20, H = 12, T = 51; R33) + MLP, against the float64 oracle at the block gate."""
+    from oracle import block_nd as obn
+    m = dsp()
+    NH = 4
+    st_h, st_d, mlp_h, mlp_d = _nd_weights(dims[-1], 1, 40 + axis)
+    xbits = synth.round_to_bf16_bits(np.random.default_rng(axis + 7).uniform(-1, 1, size=dims))
+    ctx = m.Context()
+    ctx.ensure_workspace(m.nd_workspace_bytes(dims, "bf16", 1))
+    X = to_dev(xbits, "bf16")
+    Y = torch.empty_like(X)
+    ctx.nd_block_forward(dims, NH, (axis,), st_d, mlp_d, 1 if axis != 1 else 2, X, Y)
+    torch.cuda.synchronize()
+    ref = obn.nd_block(synth.bf16_bits_to_f64(xbits), (axis,), st_h, mlp_h, NH)
+    print(assert_block_close(to_f64(Y), ref))
+
+
 def test_nd_block_5d_vs_oracle_and_virtual_ranks():
     """[B, T, H, W, C] = [1, 8, 16, 32, 256], attention along W, H, T (3 stages), sharded on T:
     N = 1 against the float64 oracle (rel-L2 gate: four residual-stream roundings instead of the
