@@ -613,7 +613,10 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   const uint32_t tS = tmem;        // 128 columns
   const uint32_t tO = tmem + 128;  // DP columns
 
+  // two CTAs per SM: launch allocation 128 regs x 256 threads; 56 x 128 + 200 x 128 == 128 x 256
+  // (the softmax warps hold a whole 128-key S row in registers on the non-diagonal path)
   if (warp == 0) {
+    if constexpr (Cfg::CTAS_PER_SM == 2) setmaxnreg_dec<56>();
     if (elect_one()) {
       uint32_t nq = 0, nk = 0, nv = 0;
       for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
@@ -636,6 +639,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
       }
     }
   } else if (warp == 1) {
+    if constexpr (Cfg::CTAS_PER_SM == 2) setmaxnreg_dec<56>();
     constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
     constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
     constexpr uint32_t idPVb = make_idesc_bf16(128, RB == 0 ? 16 : RB, 0, 1);
@@ -710,7 +714,10 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    if constexpr (Cfg::CTAS_PER_SM == 2) setmaxnreg_dec<56>();
+  } else {
+    if constexpr (Cfg::CTAS_PER_SM == 2) setmaxnreg_inc<200>();
     const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
     uint32_t ns = 0, no = 0;
     int store_pending = 0;
@@ -727,7 +734,9 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
           if (G.nhalf * G.hcols > 32) softmax_tile_diag<64, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
           else softmax_tile_diag<32, kFmhaPTmem>(G, tS, sP, m, l, &store_pending, 1);
         } else {
-          softmax_tile<Cfg::DP>(G, tS, tO, sP, j, m, l, o_done, no, &store_pending, 1, j + 1 == n ? p.kv_last : 128);
+          // whole S row in registers, MUFU + FMA-pipe exp2 (the pair kernel's softmax)
+          softmax_tile_full<Cfg::DP, false>(G, tS, tO, sP, j, m, l, o_done, no, nullptr, nullptr, &store_pending, 1,
+                                            j + 1 == n ? p.kv_last : 128);
         }
         FMHA_STAMP(tr, 2);
         mbar_arrive(p_full);
