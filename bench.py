@@ -107,8 +107,8 @@ def run_reference(args):
            "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": desc, "global_tokens": sh.B * sh.T * sh.S},
-           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
-                            "sample": sample},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "cpu_model": cpu_model(),
+                            "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -165,8 +165,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ GPU arm
-def stage_work(name, sh, N):
-    """(algorithmic amount, unit, bound) per rank per launch of a block stage."""
+def stage_work(name, sh, N, prepared=True):
+    """(algorithmic amount, unit, bound) per rank per launch of a block stage.
+
+    Prepared weights (R30): LN1 is a row-statistics pass that only READS the activation
+    (tok*C*elem); LN2 at N > 1 likewise; LN2 at N = 1 and LN3 are folded into the consuming GEMM
+    epilogues (no kernel, no traffic: None).  Raw weights: each LN reads and writes the activation.
+    """
     B, T, S, C = sh.B, sh.T, sh.S, sh.C
     tok = B * T * S // N
     e = sh.elem_bytes
@@ -178,10 +183,26 @@ def stage_work(name, sh, N):
     if name == "ATTN_T":
         return 4 * tok * C * e, "byte", "hbm"  # q, k, v read + o write, once each
     if name.startswith("LN"):
-        return 2 * tok * C * e, "byte", "hbm"
+        if not prepared:
+            return 2 * tok * C * e, "byte", "hbm"
+        if name == "LN1" or (name == "LN2" and N > 1):
+            return tok * C * e, "byte", "hbm"
+        return None, "folded", ""
     if name.startswith("SWITCH"):
         return (N - 1) * B * (T // N) * (S // N) * C * e, "byte", "nvlink"
     return 0, "", ""
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def run_dsp(args):
@@ -293,31 +314,57 @@ def run_dsp(args):
     tokens = sh.B * sh.T * sh.S
     value = tokens * K / (t_ms / 1e3)
 
-    # per-stage timing (same kernels and launch configuration, eager launches): one pass per
-    # stage with events recorded only around that stage on the library's launch stream, so
-    # only that stage's two boundaries lose their programmatic-dependent-launch overlap
+    # per-stage timing: the block is captured once per stage with a pair of CUDA events around
+    # that stage only (event-record nodes inside the graph, on the library's launch stream), and
+    # each graph is replayed KP times with L2 flushed before every replay.  Only the two stage
+    # boundaries lose their programmatic-dependent-launch overlap, so a stage time is the full
+    # duration of its kernel(s) from first CTA to last, launch ramp and tail included.
     KP = max(3, min(K, 10))
-    acc = np.zeros(len(dsp.STAGES))
+    prepared = args.prepare and sh.dtype == "bf16"
+    stage_ms = np.zeros(len(dsp.STAGES))
     for i in range(len(dsp.STAGES)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         stage_ev = [None] * (2 * len(dsp.STAGES))
-        stage_ev[2 * i], stage_ev[2 * i + 1] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stage_ev[2 * i], stage_ev[2 * i + 1] = e0, e1
         ctx.set_stage_events(stage_ev)
+        run, gi = step_eager, None
+        if args.graph and step is not step_eager:
+            cap = torch.cuda.Stream(device=dev)
+            cap.wait_stream(torch.cuda.current_stream())
+            gi = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap), torch.cuda.graph(gi, stream=cap):
+                step_eager()
+            torch.cuda.synchronize()
+            run = gi.replay
+        ctx.set_stage_events(None)
+        barrier()
+        acc = 0.0
         for _ in range(KP):
             flush.zero_()
-            step_eager()
+            run()
             torch.cuda.synchronize()
-            acc[i] += stage_ev[2 * i].elapsed_time(stage_ev[2 * i + 1])
-    ctx.set_stage_events(None)
-    stage_ms = acc / KP
+            acc += e0.elapsed_time(e1)
+        stage_ms[i] = acc / KP
+        del gi
     if world > 1:
         st = torch.tensor(stage_ms, dtype=torch.float64, device=dev)
         dist.all_reduce(st, op=dist.ReduceOp.MAX)
         stage_ms = st.cpu().numpy()
     P, peak_src = peaks()
+    traffic = {}
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}) if N == 1 else {}
+        except Exception:
+            traffic = {}
     stages = {}
     for i, name in enumerate(dsp.STAGES):
-        amt, unit, bound = stage_work(name, sh, N)
+        amt, unit, bound = stage_work(name, sh, N, prepared)
         us = stage_ms[i] * 1e3
+        if amt is None:
+            stages[name] = {"us": round(us, 2), "folded": "into the consuming GEMM epilogue (R30): no kernel"}
+            continue
         if amt == 0 or us <= 0.05:
             stages[name] = {"us": round(us, 2)}
             continue
@@ -328,54 +375,31 @@ def run_dsp(args):
         else:
             ach, pk, u = amt / (us * 1e-6) / 1e9, 900.0, "GB/s"
         stages[name] = {"us": round(us, 2), "achieved": round(ach, 1), "unit": u, "frac": round(ach / pk, 3),
-                        "bound": bound}
-    # dominant kernel: FC2, gemm_bf16_tc_kernel<192, +residual> -- the kernel with the largest
-    # share of the step in the ncu launch list (PROJ_S, PROJ_T, FC2: ~31 %) and FC2 its largest
-    # launch.  Its average launch duration is measured with CUDA events over KP launches of the
-    # same kernel and launch configuration at the rank's FC2 shape (A = [tok_r, 4C] hidden,
-    # W2 [C, 4C], residual = the activation), through dsp_linear, back to back: its A operand
-    # (tok_r x 4C bf16, 151 MB at N=1) is larger than L2, so no flush is needed between launches
-    # (at N > 1 it fits and L2 is flushed before each launch).
-    # (Stage events inside the block add launch latency and break the programmatic-dependent-
-    # launch overlap at the stage boundary, so stage times overstate kernel durations.)
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if sh.dtype == "bf16":
-        dom, tok_r, C = "FC2", tokens // N, sh.C
-        hid = (torch.randn(tok_r, 4 * C, device=dev) * 0.05).to(torch.bfloat16)
-        dfc2 = torch.empty_like(X)
-        for _ in range(3):
-            ctx.linear(hid, W["w_fc2"], dfc2, X, dsp.DSP_EPI_RESIDUAL)
-        evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(KP)]
-        cold = hid.numel() * hid.element_size() < (128 << 20)  # A fits in L2 (N > 1): flush between launches
-        for a, b in evk:
-            if cold:
-                flush.zero_()
-            a.record()
-            ctx.linear(hid, W["w_fc2"], dfc2, X, dsp.DSP_EPI_RESIDUAL)
-            b.record()
-        torch.cuda.synchronize()
-        us_k = float(np.mean([a.elapsed_time(b) for a, b in evk])) * 1e3
-        amt, unit, bound = stage_work(dom, sh, N)
-        ach = amt / (us_k * 1e-6) / 1e12
-        del hid, dfc2
-        roof = {"kernel": "FC2 gemm_bf16_tc_kernel<192,+residual>", "bound": bound, "achieved": round(ach, 1),
-                "peak": P["bf16_tflops"], "unit": "TFLOP/s", "frac": round(ach / P["bf16_tflops"], 3),
-                "traffic": None, "peak_source": peak_src + ", burst (kernel timed alone)",
-                "algorithmic_per_launch": amt, "algorithmic_unit": unit, "launch_us": round(us_k, 2),
-                "launches_timed": KP}
-    else:
-        dom = max((n for n in stages if "frac" in stages[n]), key=lambda n: stages[n]["us"])
-        amt, unit, bound = stage_work(dom, sh, N)
-        roof = {"kernel": dom, "bound": bound, "achieved": stages[dom]["achieved"],
-                "peak": P["bf16_tflops"] if unit == "flop" else P["hbm_gbs"], "unit": stages[dom]["unit"],
-                "frac": stages[dom]["frac"], "traffic": None, "peak_source": peak_src + ", burst",
-                "algorithmic_per_launch": amt, "algorithmic_unit": unit}
-    if os.path.exists(tf):
-        try:
-            roof["traffic"] = json.load(open(tf)).get(args.config, {}).get(dom)
-        except Exception:
-            pass
+                        "bound": bound, "algorithmic_per_launch": amt, "algorithmic_unit": unit + "s",
+                        "traffic": traffic.get(name)}
+    # dominant kernel = the compute stage with the largest measured time (one kernel per stage)
+    KERNELS = {"QKV_S": "gemm_bf16_tc_kernel<192, LN-folded> (spatial QKV)",
+               "ATTN_S": "fmha_pair_kernel (spatial FMHA)",
+               "PROJ_S": "gemm_bf16_tc_kernel<192, +residual +LN partials> (spatial out-proj)",
+               "QKV_T": "gemm_bf16_tc_kernel<192, LN-folded> (temporal QKV)",
+               "ATTN_T": "fmha_bf16_tc_kernel (temporal FMHA, block-diagonal packed)",
+               "PROJ_T": "gemm_bf16_tc_kernel<192, +residual +LN partials> (temporal out-proj)",
+               "FC1": "gemm_bf16_tc_kernel<256, LN-folded +GELU> (FC1)",
+               "FC2": "gemm_bf16_tc_kernel<192, +residual> (FC2)",
+               "LN1": "row_stats_bf16_kernel (LN1 statistics)", "LN2": "row_stats_bf16_kernel (LN2 statistics)"}
+    cands = [n for n in stages if "frac" in stages[n] and stages[n]["bound"] in ("tensor", "hbm")]
+    dom = max(cands, key=lambda n: stages[n]["us"])
+    d = stages[dom]
+    roof = {"kernel": KERNELS.get(dom, dom), "stage": dom, "bound": d["bound"], "achieved": d["achieved"],
+            "peak": P["bf16_tflops"] if d["bound"] == "tensor" else P["hbm_gbs"], "unit": d["unit"],
+            "frac": d["frac"], "traffic": traffic.get(dom),
+            "peak_source": peak_src + ", burst figure (conservative: the kernel runs inside a sub-ms step)",
+            "algorithmic_per_launch": d["algorithmic_per_launch"], "algorithmic_unit": d["algorithmic_unit"],
+            "launch_us": d["us"], "launches_timed": KP,
+            "timing": "CUDA events around this stage only, inside a captured graph of the block, replayed "
+                      f"{KP}x with L2 flushed; dominant = the longest compute stage"}
+    kernels = {n: {"kernel": KERNELS[n], **{k: stages[n][k] for k in ("us", "achieved", "unit", "frac", "bound")}}
+               for n in KERNELS if n in stages and "frac" in stages[n]}
     flops_block = 32 * tokens * sh.C ** 2 + 4 * sh.B * sh.T * sh.S ** 2 * sh.C + 4 * sh.B * sh.S * sh.T ** 2 * sh.C
     t_roof_us = flops_block / N / (P["bf16_tflops"] * 1e12) * 1e6
     nvl_us = 2 * (N - 1) * sh.M // (N * N) * sh.elem_bytes / 900e9 * 1e6
@@ -439,7 +463,7 @@ def run_dsp(args):
         if world == 1 and not args.no_cpu_baseline:
             frames, cols, toks = sample_sizes(sh, "baseline")
             v, secs = oracle_sample(sh, args.seed, frames, cols, toks)
-            cpu = {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "kind": "oracle",
+            cpu = {"value": v, "unit": "tokens/s", "cores": oracle_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                    "sample": f"float64 numpy oracle, stage-sampled: spatial stage on {frames} frames, temporal stage "
                              f"on {cols} columns, MLP stage on {toks} tokens ({secs:.1f} s); tokens/s = 1 / sum of "
                              f"per-token stage costs"}
@@ -450,7 +474,7 @@ def run_dsp(args):
                           "global_tokens": tokens, "switch_impl": impl if N > 1 else "none (N=1)",
                           "l2": "flushed between timed steps (256 MiB memset outside the events)",
                           "launch": graph_note, "weights": prep_note},
-               "roofline": roof, "block_roofline": block_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roof, "kernels": kernels, "block_roofline": block_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launches_per_step": launches / K, "clocks": clocks.summary()}
         if switch:
             out["switch"] = switch
@@ -637,6 +661,41 @@ def run_nd(args):
         dist.destroy_process_group()
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(gpus: int, argv: list) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-launch this script as N ranks through
+    torch.distributed.run on 127.0.0.1 (one process per GPU, RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_* set by the launcher); rank 0's JSON line reaches our stdout.  Returns the exit code."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+def launcher_check(args):
+    """CPU check of the multi-rank launch (no GPU): every rank joins a gloo group and rank 0
+    prints the ranks it saw."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = torch.zeros(world, dtype=torch.int64)
+    t[rank] = rank + 1
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "world": world, "gpus": args.gpus,
+                          "ranks": [int(v) - 1 for v in t.tolist()],
+                          "local_ranks_env": os.environ.get("LOCAL_RANK")}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -650,9 +709,15 @@ def main():
     ap.add_argument("--no-prepare", dest="prepare", action="store_false",
                     help="raw weights: LayerNorm kernels inside the block instead of the folded path")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of graph replay")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="CPU-only: spawn --gpus ranks, join a gloo group, print the ranks (tests the launcher)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "RANK" not in os.environ and args.impl != "reference":
+        raise SystemExit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if args.launcher_check:
+        return launcher_check(args)
     if args.impl == "reference":
         if args.config == "model28":  # 28 blocks of the blk shape: the oracle's block cost x 28
             args.config, args.layers = "blk", 28

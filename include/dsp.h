@@ -65,7 +65,8 @@ typedef enum {
   DSP_ERR_WORKSPACE = 9,     /* workspace missing or smaller than dsp_workspace_bytes() */
   DSP_ERR_CUDA = 10,         /* CUDA runtime / launch failure */
   DSP_ERR_NCCL = 11,         /* NCCL failure or NCCL not available for world > 1 */
-  DSP_ERR_STATE = 12         /* context misuse (wrong device, peer buffers not set, ...) */
+  DSP_ERR_STATE = 12,        /* context misuse (wrong device, peer buffers not set, ...) */
+  DSP_ERR_PEER_TIMEOUT = 13  /* a P2P barrier gave up waiting for a peer (dsp_ctx_check_errors) */
 } dsp_status_t;
 
 typedef enum { DSP_DIM_T = 1, DSP_DIM_S = 2 } dsp_dim_t;   /* axis index in [B,T,S,C] */
@@ -132,12 +133,30 @@ dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* workspace_dev, size_t by
  * device pointers, copied into the context) are rank i's symmetric data buffer and
  * signal pad as mapped in THIS process (torch symmetric memory buffer_ptrs /
  * signal_pad_ptrs, or cudaIpc mappings).  Every rank's data buffer has `bytes` bytes at
- * the same offsets; signal pads need >= 2*world*8 bytes, zero-initialised.
+ * the same offsets; signal pads need >= DSP_SIGNAL_PAD_BYTES bytes, zero-initialised, used
+ * by nothing else.  Pad layout (uint64 slots): [0, 8) the barrier epoch peer i last arrived
+ * at, [8] this rank's own barrier counter (device-resident and advanced by the barrier kernel,
+ * so barriers captured in a CUDA graph stay correct on every replay), [9] the first timeout
+ * record (see dsp_ctx_check_errors).
  * The switch destination (or the block's internal buffers) must lie inside the local
  * data buffer peer_base_dev[rank].  For tests, several "virtual ranks" may share one
  * device: pass one context per virtual rank. */
+#define DSP_SIGNAL_PAD_BYTES 128
 dsp_status_t dsp_ctx_set_peer_buffers(dsp_ctx_t ctx, void* const* peer_base_dev,
                                       void* const* peer_signal_dev, size_t bytes);
+
+/* Wall-clock bound of every P2P signal-pad barrier wait (default 120 s, or
+ * $DSP_BARRIER_TIMEOUT_S at context creation; <= 0 waits forever).  A barrier that times out
+ * records (epoch, peer) in its pad and lets the stream continue -- the switch's data is then
+ * invalid and dsp_ctx_check_errors() reports it; nothing traps, so the CUDA context survives a
+ * slow peer (checkpointing, GC) as long as it arrives within the bound.  HOST-ONLY. */
+dsp_status_t dsp_ctx_set_barrier_timeout(dsp_ctx_t ctx, double seconds);
+
+/* Health check.  SYNCHRONOUS (reads 8 bytes from the device; call between steps, off the
+ * hot path).  Returns PEER_TIMEOUT if any P2P barrier of this rank timed out (detail names
+ * the barrier epoch and the peer), NCCL if the borrowed communicator reports an asynchronous
+ * error (ncclCommGetAsyncError), else OK. */
+dsp_status_t dsp_ctx_check_errors(dsp_ctx_t ctx);
 
 /* Instrumentation (off the hot path).  Stage ids of dsp_st_block_forward, in order. */
 typedef enum {
@@ -151,6 +170,17 @@ typedef enum {
  * NULL entries are skipped, so a caller can time one stage per pass: every event record
  * is a point where the next kernel's programmatic dependent launch cannot overlap. */
 dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n_events);
+/* Instrumentation taps (test infrastructure; off by default): when set, dsp_st_block_forward
+ * copies an intermediate of the block into `dst` (device, >= the local shard bytes) with a
+ * stream-ordered D2D copy (also captured into CUDA graphs):
+ *   DSP_TAP_Y1: y1 = x + MHA_S(LN1 x) after the T->S switch, S-sharded [B, T, S/N, C];
+ *   DSP_TAP_Y2: y2 (after the temporal stage, and the cross stage if any), [B, T, S/N, C].
+ * Slice independence then lets a test check each stage of the production launch
+ * against the oracle on sampled frames / columns.  dst NULL switches a tap off.
+ * Errors: NULL, SHAPE (unknown point), ALIGNMENT; a too-small buffer fails the block call
+ * with WORKSPACE. */
+typedef enum { DSP_TAP_Y1 = 0, DSP_TAP_Y2 = 1, DSP_NUM_TAPS = 2 } dsp_tap_t;
+dsp_status_t dsp_ctx_set_tap(dsp_ctx_t ctx, dsp_tap_t point, void* dst, size_t bytes);
 /* Number of this library's own kernels launched through ctx since creation (NCCL kernels
  * and cudaMemcpy excluded).  HOST-ONLY. */
 int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
@@ -158,7 +188,9 @@ int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
-#define DSP_ABI_VERSION 3  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage */
+#define DSP_ABI_VERSION 4  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage;
+                              4: device-resident barrier epochs, barrier timeout + error check,
+                              exported switch pack / unpack and gather unpack */
 
 /* ----------------------------------------------------------- layout (bytes) */
 
@@ -327,9 +359,9 @@ dsp_status_t dsp_nd_block_forward(dsp_ctx_t ctx, const int64_t* dims, int ndim, 
 /* Forward of a stack of L ST blocks, y = block_{L-1}( ... block_0(x)) (BASELINE configs[2]:
  * the 28-layer ST-DiT-XL/2-shaped model), x and y T-sharded as for one block (x may
  * equal y; blocks 1.. run in place on y).  w: HOST array of L block-weight structs.  With
- * prepared weights (R30) at N == 1, block l's FC2 epilogue also writes the per-row LayerNorm
- * partials of its output and block l + 1 folds LN1 from them (no statistics pass between
- * blocks).  Workspace as for one block (reused by every layer).  COLLECTIVE (2 switches per
+ * prepared weights (R30), block l + 1 folds LN1 from per-row LayerNorm partials of its input: at
+ * N == 1 those block l's FC2 epilogue wrote (no statistics pass between blocks), at N > 1 the
+ * same bits recomputed after the switch -- the output is bitwise independent of N.  Workspace as for one block (reused by every layer).  COLLECTIVE (2 switches per
  * layer).  Errors: as dsp_st_block_forward; SHAPE (L < 1); NULL. */
 dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* const* w,
                                   int L, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);

@@ -49,6 +49,30 @@ dsp_status_t dsp_attention_core(dsp_ctx_t ctx, dsp_dtype_t dtype, int64_t B, int
                                 int64_t S_loc, int64_t C, int32_t num_heads, dsp_dim_t dim,
                                 const void* qkv, void* o, void* stream);
 
+/* ---- the NCCL transport of the dynamic switch, piece by piece (§3.1; SURVEY §8a "The
+ * switch as an exact index map").  dsp_switch(impl = NCCL) is exactly
+ *   dsp_switch_pack -> ncclAlltoAll(send, recv, chunk bytes per peer) -> dsp_switch_unpack
+ * (each copy skipped there when it is an identity).  Chunk order of send / recv: one chunk
+ * of B*(T/N)*(S/N)*C*elem bytes per peer, peers in rank order, each chunk [b][t'][s'][c]:
+ *   T->S pack:   send[q][b][t'][s'][c] = x_local[b][t'][q*S/N + s'][c]     (x_local [B,T/N,S,C])
+ *   T->S unpack: y_local[b][r*T/N + t'][s'][c] = recv[r][b][t'][s'][c]     (y_local [B,T,S/N,C])
+ *   S->T pack:   send[r][b][t'][s'][c] = x_local[b][r*T/N + t'][s'][c]     (x_local [B,T,S/N,C])
+ *   S->T unpack: y_local[b][t'][q*S/N + s'][c] = recv[q][b][t'][s'][c]     (y_local [B,T/N,S,C])
+ * where recv on rank q holds, in slot r, the chunk rank r packed for q.  Local (no
+ * communication), always launch one strided-run copy kernel.  Buffers: shard size
+ * B*T*S*C*elem/N bytes each, device, 16-B aligned, non-overlapping.
+ * Errors: as dsp_switch (SAME_DIM, BAD_DIM, DIVISIBILITY, ALIGNMENT, ALIAS), NULL, CUDA. */
+dsp_status_t dsp_switch_pack(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t from_dim, dsp_dim_t to_dim,
+                             const void* x_local, void* send, void* stream);
+dsp_status_t dsp_switch_unpack(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t from_dim, dsp_dim_t to_dim,
+                               const void* recv, void* y_local, void* stream);
+
+/* The unpack of dsp_gather: `gathered` is the rank-major [N][local shard] buffer an
+ * all-gather of the shards produces; x_global [B,T,S,C] receives shard r at its place along
+ * `dim`.  Local, one strided-run copy kernel (always launched).  Errors: as dsp_split. */
+dsp_status_t dsp_gather_unpack(dsp_ctx_t ctx, const dsp_shape_t* shape, dsp_dim_t dim, const void* gathered,
+                               void* x_global, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,9 @@ DIMS = {"T": DSP_DIM_T, "S": DSP_DIM_S, DSP_DIM_T: DSP_DIM_T, DSP_DIM_S: DSP_DIM
 
 STATUS = {0: "DSP_OK", 1: "DSP_ERR_NULL", 2: "DSP_ERR_SHAPE", 3: "DSP_ERR_DIVISIBILITY", 4: "DSP_ERR_SAME_DIM",
           5: "DSP_ERR_BAD_DIM", 6: "DSP_ERR_UNSUPPORTED", 7: "DSP_ERR_ALIGNMENT", 8: "DSP_ERR_ALIAS",
-          9: "DSP_ERR_WORKSPACE", 10: "DSP_ERR_CUDA", 11: "DSP_ERR_NCCL", 12: "DSP_ERR_STATE"}
+          9: "DSP_ERR_WORKSPACE", 10: "DSP_ERR_CUDA", 11: "DSP_ERR_NCCL", 12: "DSP_ERR_STATE",
+          13: "DSP_ERR_PEER_TIMEOUT"}
+SIGNAL_PAD_BYTES = 128  # DSP_SIGNAL_PAD_BYTES (include/dsp.h)
 
 
 class DSPError(RuntimeError):
@@ -120,6 +122,12 @@ def lib() -> ctypes.CDLL:
             "dsp_linear": [vp, ctypes.c_int, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp, vp],
             "dsp_attention_core": [vp, ctypes.c_int, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp],
             "dsp_ctx_set_stage_events": [vp, P(vp), ctypes.c_int],
+            "dsp_switch_pack": [vp, P(Shape), ctypes.c_int, ctypes.c_int, vp, vp, vp],
+            "dsp_switch_unpack": [vp, P(Shape), ctypes.c_int, ctypes.c_int, vp, vp, vp],
+            "dsp_gather_unpack": [vp, P(Shape), ctypes.c_int, vp, vp, vp],
+            "dsp_ctx_set_barrier_timeout": [vp, ctypes.c_double],
+            "dsp_ctx_check_errors": [vp],
+            "dsp_ctx_set_tap": [vp, ctypes.c_int, vp, ctypes.c_size_t],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -285,7 +293,23 @@ class Context:
         S = (ctypes.c_void_p * n)(*signal_ptrs)
         _check(lib().dsp_ctx_set_peer_buffers(self.handle, B, S, int(nbytes)), self.handle)
 
+    def set_barrier_timeout(self, seconds: float):
+        """dsp_ctx_set_barrier_timeout: wall-clock bound of a P2P barrier wait (<= 0: forever)."""
+        _check(lib().dsp_ctx_set_barrier_timeout(self.handle, float(seconds)), self.handle)
+
+    def check_errors(self):
+        """dsp_ctx_check_errors (synchronous): raise DSPError on a timed-out P2P barrier or an
+        asynchronous NCCL error of the borrowed communicator."""
+        self._call("dsp_ctx_check_errors")
+
     # ---- instrumentation
+    TAPS = {"y1": 0, "y2": 1}
+
+    def set_tap(self, point: str, dst=None):
+        """dsp_ctx_set_tap: copy the block's y1 / y2 (S-sharded) into dst on every block call."""
+        _check(lib().dsp_ctx_set_tap(self.handle, self.TAPS[point], _ptr(dst),
+                                     0 if dst is None else dst.numel() * dst.element_size()), self.handle)
+
     def launch_count(self) -> int:
         return int(lib().dsp_ctx_launch_count(self.handle))
 
@@ -313,6 +337,21 @@ class Context:
     def switch(self, shape, from_dim, to_dim, x_local, y_local, impl="nccl", stream=None):
         self._call("dsp_switch", ctypes.byref(shape), DIMS[from_dim], DIMS[to_dim], _ptr(x_local), _ptr(y_local),
                    IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def switch_pack(self, shape, from_dim, to_dim, x_local, send, stream=None):
+        """dsp_switch_pack: x_local -> per-peer chunks [peer][b][t'][s'][c] (NCCL transport, step 1)."""
+        self._call("dsp_switch_pack", ctypes.byref(shape), DIMS[from_dim], DIMS[to_dim], _ptr(x_local), _ptr(send),
+                   _stream(stream))
+
+    def switch_unpack(self, shape, from_dim, to_dim, recv, y_local, stream=None):
+        """dsp_switch_unpack: received chunks [source rank][b][t'][s'][c] -> y_local (step 3)."""
+        self._call("dsp_switch_unpack", ctypes.byref(shape), DIMS[from_dim], DIMS[to_dim], _ptr(recv), _ptr(y_local),
+                   _stream(stream))
+
+    def gather_unpack(self, shape, dim, gathered, x_global, stream=None):
+        """dsp_gather_unpack: all-gathered [N][local] shards -> the global [B,T,S,C] layout."""
+        self._call("dsp_gather_unpack", ctypes.byref(shape), DIMS[dim], _ptr(gathered), _ptr(x_global),
+                   _stream(stream))
 
     def switch_nd(self, dims, from_dim: int, to_dim: int, x_local, y_local, impl="nccl", stream=None):
         """dsp_switch_nd: N-D dynamic switch of the global [dims] tensor (channel last) between two dims."""

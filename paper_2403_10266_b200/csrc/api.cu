@@ -47,6 +47,8 @@ dsp_status_t cuda_fail(dsp_ctx_t ctx, cudaError_t e, const char* what, const std
     if (_s != DSP_OK) return _s;      \
   } while (0)
 
+constexpr double kDefaultBarrierTimeoutS = 120.0;
+
 int64_t elem_bytes(dsp_dtype_t d) { return d == DSP_BF16 ? 2 : 4; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -177,7 +179,32 @@ bool in_region(const void* p, int64_t n, const void* base, size_t bytes) {
   return a >= b && a + (uintptr_t)n <= b + bytes;
 }
 
-// Execute a switch with explicit scratch (send/recv each >= shard bytes when needed).
+// NCCL transport layouts: send / recv hold one chunk per peer, [peer][i1][i2][i3][run bytes].
+// pack: x_local -> send (level 0 = destination peer); unpack: recv (level 0 = source rank) ->
+// y_local at that rank's slot.  The plan's strides are identical on every rank, so the same
+// dst strides place a received chunk.
+struct ChunkCopies {
+  RunCopy pack, unpack;
+  int64_t chunk;  // bytes per peer
+};
+ChunkCopies chunk_copies(const RunCopy& rc) {
+  ChunkCopies c;
+  c.chunk = rc.n[1] * rc.n[2] * rc.n[3] * rc.run_bytes;
+  c.pack = rc;
+  c.unpack = rc;
+  c.pack.ds[0] = c.chunk; c.pack.ds[1] = rc.n[2] * rc.n[3] * rc.run_bytes; c.pack.ds[2] = rc.n[3] * rc.run_bytes;
+  c.pack.ds[3] = rc.run_bytes;
+  for (int i = 0; i < 4; ++i) c.unpack.ss[i] = c.pack.ds[i];
+  return c;
+}
+
+RunCopy plan_runs(const dsp_switch_plan_t& p) {
+  RunCopy rc;
+  for (int i = 0; i < 3; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
+  rc.run_bytes = p.run_bytes;
+  return rc;
+}
+
 // Execute a switch plan (4-level strided runs, level 0 = peer): P2P = entry barrier, direct
 // stores of every run at its final address in the peer's buffer, exit barrier; NCCL = pack into
 // per-peer chunks (skipped when identity) -> ncclAlltoAll (bytes) -> unpack (skipped when identity).
@@ -191,22 +218,19 @@ dsp_status_t do_switch_plan(dsp_ctx_t ctx, const RunCopy& rc, int64_t dst_peer_o
     if (!in_region(y, bytes, base, ctx->peer_bytes))
       return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P switch destination is not inside the registered symmetric buffer");
     const int64_t y_off = static_cast<uint8_t*>(y) - static_cast<uint8_t*>(base);
-    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p entry barrier");
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "p2p entry barrier");
     DSP_CUDA(ctx, launch_p2p_put(x, ctx->peer_base, y_off + dst_peer_off, rc, ctx->num_sms, st), "p2p put");
-    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "p2p exit barrier");
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "p2p exit barrier");
     ctx->launches += 3;
     return DSP_OK;
   }
   if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
-  const int64_t chunk = rc.n[1] * rc.n[2] * rc.n[3] * rc.run_bytes;  // bytes per peer
-  RunCopy pack = rc, unpack = rc;
-  pack.ds[0] = chunk; pack.ds[1] = rc.n[2] * rc.n[3] * rc.run_bytes; pack.ds[2] = rc.n[3] * rc.run_bytes;
-  pack.ds[3] = rc.run_bytes;
-  for (int i = 0; i < 4; ++i) unpack.ss[i] = pack.ds[i];
+  const ChunkCopies cc = chunk_copies(rc);
+  const int64_t chunk = cc.chunk;
   const void* send = x;
   void* recv = y;
   if (!pack_identity) {
-    DSP_CUDA(ctx, launch_run_copy(x, scratch_send, pack, ctx->num_sms, st), "switch pack");
+    DSP_CUDA(ctx, launch_run_copy(x, scratch_send, cc.pack, ctx->num_sms, st), "switch pack");
     ctx->launches += 1;
     send = scratch_send;
   }
@@ -225,7 +249,7 @@ dsp_status_t do_switch_plan(dsp_ctx_t ctx, const RunCopy& rc, int64_t dst_peer_o
   }
   if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAlltoAll: %s", ctx->nccl.GetErrorString(r));
   if (!unpack_identity) {
-    DSP_CUDA(ctx, launch_run_copy(recv, y, unpack, ctx->num_sms, st), "switch unpack");
+    DSP_CUDA(ctx, launch_run_copy(recv, y, cc.unpack, ctx->num_sms, st), "switch unpack");
     ctx->launches += 1;
   }
   return DSP_OK;
@@ -241,10 +265,7 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
   }
   dsp_switch_plan_t p;
   make_plan(s, N, ctx->rank, from, &p);
-  RunCopy rc;
-  for (int i = 0; i < 3; ++i) { rc.n[i] = p.n[i]; rc.ss[i] = p.src_stride[i]; rc.ds[i] = p.dst_stride[i]; }
-  rc.run_bytes = p.run_bytes;
-  return do_switch_plan(ctx, rc, p.dst_peer_off, p.pack_is_identity, p.unpack_is_identity, bytes, x, y, impl, st,
+  return do_switch_plan(ctx, plan_runs(p), p.dst_peer_off, p.pack_is_identity, p.unpack_is_identity, bytes, x, y, impl, st,
                         scratch_send, scratch_recv);
 }
 
@@ -336,6 +357,7 @@ const char* dsp_status_str(dsp_status_t s) {
     case DSP_ERR_CUDA: return "DSP_ERR_CUDA";
     case DSP_ERR_NCCL: return "DSP_ERR_NCCL";
     case DSP_ERR_STATE: return "DSP_ERR_STATE";
+    case DSP_ERR_PEER_TIMEOUT: return "DSP_ERR_PEER_TIMEOUT";
   }
   return "DSP_ERR_UNKNOWN";
 }
@@ -348,6 +370,11 @@ dsp_status_t dsp_ctx_create(void* nccl_comm, int rank, int world, int device, ds
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, DSP_ERR_SHAPE, "bad rank %d / world %d", rank, world);
   dsp_ctx* c = new dsp_ctx();
   c->rank = rank; c->world = world; c->device = device; c->comm = nccl_comm;
+  {
+    const char* t = std::getenv("DSP_BARRIER_TIMEOUT_S");
+    const double sec = t ? std::atof(t) : kDefaultBarrierTimeoutS;
+    c->barrier_timeout_ns = sec > 0 ? (uint64_t)(sec * 1e9) : 0;
+  }
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
@@ -395,6 +422,15 @@ dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n)
   if (n != 2 * DSP_NUM_STAGES) return fail(ctx, DSP_ERR_SHAPE, "need %d events", 2 * DSP_NUM_STAGES);
   for (int i = 0; i < n; ++i) ctx->stage_events[i] = events[i];
   ctx->has_stage_events = true;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_ctx_set_tap(dsp_ctx_t ctx, dsp_tap_t point, void* dst, size_t bytes) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (point < 0 || point >= DSP_NUM_TAPS) return fail(ctx, DSP_ERR_SHAPE, "unknown tap %d", (int)point);
+  if (dst && !aligned16(dst)) return fail(ctx, DSP_ERR_ALIGNMENT, "tap buffer not 16-B aligned");
+  ctx->tap[point] = dst;
+  ctx->tap_bytes[point] = dst ? bytes : 0;
   return DSP_OK;
 }
 
@@ -467,16 +503,36 @@ dsp_status_t dsp_split(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const
   return DSP_OK;
 }
 
-dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const void* xl, void* xg, void* stream) {
+// Unpack of the all-gathered [N][local] rank-major buffer into the global layout.
+static RunCopy gather_runs(const dsp_shape_t* s, int N, int dim) {
+  const int64_t e = elem_bytes(s->dtype), row = s->C * e, B = s->B, T = s->T, S = s->S, Tn = T / N, Sn = S / N;
+  const int64_t local = B * T * S * row / N;
+  RunCopy rc{};
+  if (dim == DSP_DIM_T) {
+    rc.n[0] = N; rc.n[1] = B; rc.n[2] = 1; rc.run_bytes = Tn * S * row;
+    rc.ss[0] = local; rc.ss[1] = Tn * S * row; rc.ds[0] = Tn * S * row; rc.ds[1] = T * S * row;
+  } else {
+    rc.n[0] = N; rc.n[1] = B; rc.n[2] = T; rc.run_bytes = Sn * row;
+    rc.ss[0] = local; rc.ss[1] = T * Sn * row; rc.ss[2] = Sn * row;
+    rc.ds[0] = Sn * row; rc.ds[1] = T * S * row; rc.ds[2] = S * row;
+  }
+  return rc;
+}
+
+static dsp_status_t check_layout_call(dsp_ctx_t ctx, const dsp_shape_t* s, int dim, const void* a, const void* b) {
   DSP_TRY(check_ctx(ctx));
   DSP_TRY(check_shape(ctx, s));
   DSP_TRY(check_dim(ctx, dim));
   DSP_TRY(check_div(ctx, s, ctx->world));
-  if (!xg || !xl) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
-  if (!aligned16(xg) || !aligned16(xl)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  if (!a || !b) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(a) || !aligned16(b)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  return DSP_OK;
+}
+
+dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const void* xl, void* xg, void* stream) {
+  DSP_TRY(check_layout_call(ctx, s, dim, xl, xg));
   const int N = ctx->world;
-  const int64_t e = elem_bytes(s->dtype), row = s->C * e, B = s->B, T = s->T, S = s->S, Tn = T / N, Sn = S / N;
-  const int64_t local = B * T * S * row / N;
+  const int64_t local = shard_bytes(s, N);
   cudaStream_t st = (cudaStream_t)stream;
   if (overlap(xg, local * N, xl, local)) return fail(ctx, DSP_ERR_ALIAS, "x_local overlaps x_global");
   if (N == 1) {
@@ -484,26 +540,84 @@ dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, cons
     return DSP_OK;
   }
   if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "gather without a communicator");
-  const bool identity = (dim == DSP_DIM_T) ? (B == 1) : (B * T == 1);
+  const bool identity = (dim == DSP_DIM_T) ? (s->B == 1) : (s->B * s->T == 1);
   void* stage = xg;
   if (!identity) {
     if (!ctx->ws || ctx->ws_bytes < (size_t)(local * N)) return fail(ctx, DSP_ERR_WORKSPACE, "gather needs %lld bytes of workspace", (long long)(local * N));
+    if (overlap(ctx->ws, local * N, xl, local) || overlap(ctx->ws, local * N, xg, local * N))
+      return fail(ctx, DSP_ERR_ALIAS, "x_local / x_global overlap the workspace the gather stages through");
     stage = ctx->ws;
   }
   int r = ctx->nccl.AllGather(xl, stage, (size_t)local, kNcclUint8, ctx->comm, st);
   if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAllGather: %s", ctx->nccl.GetErrorString(r));
   if (!identity) {
-    RunCopy rc{};
-    if (dim == DSP_DIM_T) {
-      rc.n[0] = N; rc.n[1] = B; rc.n[2] = 1; rc.run_bytes = Tn * S * row;
-      rc.ss[0] = local; rc.ss[1] = Tn * S * row; rc.ds[0] = Tn * S * row; rc.ds[1] = T * S * row;
-    } else {
-      rc.n[0] = N; rc.n[1] = B; rc.n[2] = T; rc.run_bytes = Sn * row;
-      rc.ss[0] = local; rc.ss[1] = T * Sn * row; rc.ss[2] = Sn * row;
-      rc.ds[0] = Sn * row; rc.ds[1] = T * S * row; rc.ds[2] = S * row;
-    }
-    DSP_CUDA(ctx, launch_run_copy(stage, xg, rc, ctx->num_sms, st), "gather unpack");
+    DSP_CUDA(ctx, launch_run_copy(stage, xg, gather_runs(s, N, dim), ctx->num_sms, st), "gather unpack");
     ctx->launches += 1;
+  }
+  return DSP_OK;
+}
+
+dsp_status_t dsp_gather_unpack(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, const void* gathered, void* xg,
+                               void* stream) {
+  DSP_TRY(check_layout_call(ctx, s, dim, gathered, xg));
+  const int64_t total = shard_bytes(s, 1);
+  if (overlap(gathered, total, xg, total)) return fail(ctx, DSP_ERR_ALIAS, "gathered overlaps x_global");
+  DSP_CUDA(ctx, launch_run_copy(gathered, xg, gather_runs(s, ctx->world, dim), ctx->num_sms, (cudaStream_t)stream),
+           "gather unpack");
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
+// Building blocks of the NCCL transport (include/dsp_kernels.h): the pack / unpack kernels of
+// dsp_switch, always launched (an identity side is a contiguous copy here).
+static dsp_status_t switch_chunk_call(dsp_ctx_t ctx, const dsp_shape_t* s, int from, int to, const void* a, void* b,
+                                      bool pack, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(validate_switch(ctx, s, ctx->world, from, to));
+  if (!a || !b) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(a) || !aligned16(b)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int64_t bytes = shard_bytes(s, ctx->world);
+  if (overlap(a, bytes, b, bytes)) return fail(ctx, DSP_ERR_ALIAS, "source and destination overlap");
+  dsp_switch_plan_t p;
+  make_plan(s, ctx->world, ctx->rank, from, &p);
+  const ChunkCopies cc = chunk_copies(plan_runs(p));
+  DSP_CUDA(ctx, launch_run_copy(a, b, pack ? cc.pack : cc.unpack, ctx->num_sms, (cudaStream_t)stream),
+           pack ? "switch pack" : "switch unpack");
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_switch_pack(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp_dim_t to, const void* x_local,
+                             void* send, void* stream) {
+  return switch_chunk_call(ctx, s, from, to, x_local, send, true, stream);
+}
+
+dsp_status_t dsp_switch_unpack(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp_dim_t to, const void* recv,
+                               void* y_local, void* stream) {
+  return switch_chunk_call(ctx, s, from, to, recv, y_local, false, stream);
+}
+
+dsp_status_t dsp_ctx_set_barrier_timeout(dsp_ctx_t ctx, double seconds) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  ctx->barrier_timeout_ns = seconds > 0 ? (uint64_t)(seconds * 1e9) : 0;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_ctx_check_errors(dsp_ctx_t ctx) {
+  DSP_TRY(check_ctx(ctx));
+  if (ctx->has_peers) {
+    uint64_t rec = 0;
+    const uint64_t* slot = static_cast<const uint64_t*>(ctx->peer_signal.p[ctx->rank]) + kPadError;
+    DSP_CUDA(ctx, cudaMemcpy(&rec, slot, sizeof(rec), cudaMemcpyDeviceToHost), "read barrier error record");
+    if (rec)
+      return fail(ctx, DSP_ERR_PEER_TIMEOUT, "P2P barrier %llu timed out waiting for rank %u (timeout %.1f s)",
+                  (unsigned long long)(rec >> 16), (unsigned)(rec & 0xff), ctx->barrier_timeout_ns * 1e-9);
+  }
+  if (ctx->comm && ctx->nccl.CommGetAsyncError) {
+    int async = 0;
+    int r = ctx->nccl.CommGetAsyncError(ctx->comm, &async);
+    if (r) return fail(ctx, DSP_ERR_NCCL, "ncclCommGetAsyncError: %s", ctx->nccl.GetErrorString(r));
+    if (async) return fail(ctx, DSP_ERR_NCCL, "communicator async error: %s", ctx->nccl.GetErrorString(async));
   }
   return DSP_OK;
 }
@@ -593,6 +707,8 @@ dsp_status_t dsp_switch_nd(dsp_ctx_t ctx, const int64_t* dims, int ndim, int ele
     const int64_t need = (p.pack_is_identity ? 0 : bytes) + (p.unpack_is_identity ? 0 : bytes);
     if (need && (!ctx->ws || ctx->ws_bytes < (size_t)need))
       return fail(ctx, DSP_ERR_WORKSPACE, "switch needs %lld bytes of workspace", (long long)need);
+    if (need && (overlap(ctx->ws, need, x, bytes) || overlap(ctx->ws, need, y, bytes)))
+      return fail(ctx, DSP_ERR_ALIAS, "x_local / y_local overlap the workspace the NCCL switch stages through");
     send = ctx->ws;
     recv = static_cast<uint8_t*>(ctx->ws) + (p.pack_is_identity ? 0 : bytes);
   }
@@ -622,6 +738,8 @@ dsp_status_t dsp_switch(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp
     const int64_t need = (p.pack_is_identity ? 0 : bytes) + (p.unpack_is_identity ? 0 : bytes);
     if (need && (!ctx->ws || ctx->ws_bytes < (size_t)need))
       return fail(ctx, DSP_ERR_WORKSPACE, "switch needs %lld bytes of workspace", (long long)need);
+    if (need && (overlap(ctx->ws, need, x, bytes) || overlap(ctx->ws, need, y, bytes)))
+      return fail(ctx, DSP_ERR_ALIAS, "x_local / y_local overlap the workspace the NCCL switch stages through");
     send = ctx->ws;
     recv = static_cast<uint8_t*>(ctx->ws) + (p.pack_is_identity ? 0 : bytes);
   }
@@ -658,10 +776,12 @@ dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* s, const void* 
   return attn_public(ctx, s, DSP_DIM_T, h, wqkv, wo, res, out, stream);
 }
 
-// One block.  Chaining flags of dsp_st_model_forward (prepared weights, N == 1 only):
-//   ln1_from_parts: the LN1 statistics of x are combined from per-row partials already in the
-//                   workspace (written by the previous block's FC2 epilogue) -- no stats pass;
-//   emit_parts:     the FC2 epilogue writes the per-row partials of y for the next block's LN1.
+// One block.  Chaining flags of dsp_st_model_forward (prepared weights):
+//   ln1_from_parts: the LN1 statistics of x are combined from per-row partials: at N == 1 those
+//                   the previous block's FC2 epilogue left in the workspace (no pass at all), at
+//                   N > 1 recomputed bitwise by launch_row_partials (the rows crossed a switch);
+//   emit_parts:     the FC2 epilogue writes the per-row partials of y for the next block's LN1
+//                   (N == 1).
 static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
                                   void* y, dsp_switch_impl_t impl, void* stream, bool ln1_from_parts,
                                   bool emit_parts) {
@@ -700,6 +820,8 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "block needs %zu bytes of workspace", need);
   if (x != y && overlap(x, act, y, act)) return fail(ctx, DSP_ERR_ALIAS, "x_local partially overlaps y_local");
   if (overlap(ctx->ws, need, x, act) || overlap(ctx->ws, need, y, act)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y");
+  for (int t = 0; t < DSP_NUM_TAPS; ++t)
+    if (ctx->tap[t] && ctx->tap_bytes[t] < (size_t)act) return fail(ctx, DSP_ERR_WORKSPACE, "tap %d needs %lld bytes", t, (long long)act);
   const BlockWs L = block_ws(s, N);
   uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
   void* h = ws + L.h;                // [tok, C]
@@ -737,28 +859,31 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   float2* parts = reinterpret_cast<float2*>(ws + L.parts);
   const int nparts = (int)(C / gemm_bn_for(C));
   EpiVec ev1{}, ev2{}, ev3{};
-  const bool chain_in = fold && N == 1 && ln1_from_parts, chain_out = fold && N == 1 && emit_parts;
+  // LN statistics from per-row partials are the same bits at every N: at N > 1 the rows reach
+  // their consumer through a switch without their producer's partials, so launch_row_partials
+  // recomputes them bitwise (SURVEY §8c.4 (i) N-invariance).
+  const bool chain_in = fold && ln1_from_parts, chain_out = fold && N == 1 && emit_parts;
+  const int part_cnt = (int)(C / nparts);
   if (fold) {
     ev1.row_stats = stats; ev1.col_u = uv; ev1.col_v = uv + 3 * C;
     if (chain_in) {
       ev1.row_stats = nullptr;
-      ev1.part_in = parts; ev1.nparts_in = nparts; ev1.part_cnt = (int)(C / nparts); ev1.eps = eps;
+      ev1.part_in = parts; ev1.nparts_in = nparts; ev1.part_cnt = part_cnt; ev1.eps = eps;
     }
     ev2.col_u = uv + 6 * C; ev2.col_v = uv + 9 * C;
     ev3.col_u = uv + 12 * C; ev3.col_v = uv + 16 * C;
-    ev3.part_in = parts; ev3.nparts_in = nparts; ev3.part_cnt = (int)(C / nparts); ev3.eps = eps;
-    if (N == 1) {
-      ev2.part_in = parts; ev2.nparts_in = nparts; ev2.part_cnt = (int)(C / nparts); ev2.eps = eps;
-    } else {
-      ev2.row_stats = stats;
-    }
+    ev3.part_in = parts; ev3.nparts_in = nparts; ev3.part_cnt = part_cnt; ev3.eps = eps;
+    ev2.part_in = parts; ev2.nparts_in = nparts; ev2.part_cnt = part_cnt; ev2.eps = eps;
   }
   const void* wf_s = fold ? prep + P.wf_s : nullptr;
   const void* wf_t = fold ? prep + P.wf_t : nullptr;
   const void* wf_1 = fold ? prep + P.wf_1 : nullptr;
   // a1: LN1 (prepared: row statistics of x only)
   mark(ctx, DSP_STAGE_LN1, 0, st);
-  if (!chain_in) {
+  if (chain_in && N > 1) {  // the previous block's FC2 partials stayed on the other side of its switch
+    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, x, parts, st), "LN1 partials");
+    ctx->launches += 1;
+  } else if (!chain_in) {
     if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
     else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
     ctx->launches += 1;
@@ -772,7 +897,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
   if (fused) {
-    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "fused switch barrier");
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "fused switch barrier");
     ctx->launches += 1;
     cur = ys;
   } else if (N > 1) {
@@ -780,13 +905,14 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     cur = ys;
   }
   mark(ctx, DSP_STAGE_SWITCH_TS, 1, st);
+  if (ctx->tap[DSP_TAP_Y1]) DSP_CUDA(ctx, cudaMemcpyAsync(ctx->tap[DSP_TAP_Y1], cur, act, cudaMemcpyDeviceToDevice, st), "tap y1");
   // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place; prepared: + LN3 partials)
   mark(ctx, DSP_STAGE_LN2, 0, st);
   if (!fold) {
     DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
     ctx->launches += 1;
   } else if (N > 1) {
-    DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN2 stats");
+    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, cur, parts, st), "LN2 partials");
     ctx->launches += 1;
   }
   mark(ctx, DSP_STAGE_LN2, 1, st);
@@ -819,6 +945,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "cross stage", why);
     ctx->launches += fold ? 4 : 5;
   }
+  if (ctx->tap[DSP_TAP_Y2]) DSP_CUDA(ctx, cudaMemcpyAsync(ctx->tap[DSP_TAP_Y2], cur, act, cudaMemcpyDeviceToDevice, st), "tap y2");
   // a10: y = y2 + W2 gelu(W1 LN3 y2) (in place)
   mark(ctx, DSP_STAGE_LN3, 0, st);
   if (!fold) {
@@ -854,7 +981,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   // a11: switch S -> T back into y
   mark(ctx, DSP_STAGE_SWITCH_ST, 0, st);
   if (fused) {
-    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ++ctx->epoch, st), "fused switch barrier");
+    DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "fused switch barrier");
     ctx->launches += 1;
   } else if (N > 1) {
     DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));

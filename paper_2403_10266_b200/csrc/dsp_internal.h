@@ -16,6 +16,9 @@
 namespace dsp {
 
 constexpr int kMaxPeers = 8;  // one NVLink/NVSwitch box
+// signal pad slots (uint64) of the P2P barrier (switch.cu): [0, kMaxPeers) peer arrivals,
+// kPadEpoch own barrier counter, kPadError first timeout record; DSP_SIGNAL_PAD_BYTES in dsp.h
+constexpr int kPadEpoch = kMaxPeers, kPadError = kMaxPeers + 1;
 
 // ---- NCCL, resolved at run time from the libnccl.so.2 torch already loaded ----
 struct NcclApi {
@@ -27,6 +30,7 @@ struct NcclApi {
   int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
+  int (*CommGetAsyncError)(void*, int*) = nullptr;
 };
 bool nccl_load(NcclApi* api, std::string* err);
 constexpr int kNcclUint8 = 1;  // ncclUint8 in nccl.h
@@ -62,7 +66,7 @@ cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int n
 // P2P: run (i0=peer,i1,i2) stored to peer_base.p[i0] + dst_off + i1*ds[1] + i2*ds[2]
 cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t dst_off, const RunCopy& rc,
                            int num_sms, cudaStream_t st);
-cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st);
+cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t timeout_ns, cudaStream_t st);
 
 // LayerNorm folded into the following GEMM (bf16 path)
 struct LnFold {
@@ -75,6 +79,8 @@ struct LnFold {
   int64_t N;
 };
 cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
+// per-row LayerNorm partials over `seg`-column segments, bitwise = the residual epilogue's (R30)
+cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st);
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
 // GEMM epilogue codes beyond the public dsp_epilogue_t
 enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5 };
@@ -165,7 +171,9 @@ struct dsp_ctx {
   int64_t launches = 0;            // own kernels launched (instrumentation)
   void* stage_events[2 * DSP_NUM_STAGES] = {};
   bool has_stage_events = false;
-  uint64_t epoch = 0;  // P2P barrier epoch (monotonic, identical sequence on all ranks)
+  void* tap[DSP_NUM_TAPS] = {};    // instrumentation: copies of intermediates (dsp_ctx_set_tap)
+  size_t tap_bytes[DSP_NUM_TAPS] = {};
+  uint64_t barrier_timeout_ns = 0;  // P2P barrier wall-clock timeout (0 = none); DSP_BARRIER_TIMEOUT_S
   // pipelined host path (dsp_st_block_forward_host_pipelined): copy-in / copy-out streams and
   // per-staging-buffer events, created on first use, destroyed with the context
   void* h2d_stream = nullptr;

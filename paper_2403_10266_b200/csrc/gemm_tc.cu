@@ -321,9 +321,10 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (kStats && m0 + row < M) {
-        const float a = s1.x + s1.y, mp = a * (1.f / BN);
+        // explicit rounding steps: launch_row_partials (simt.cu) reproduces these bits after a switch
+        const float a = __fadd_rn(s1.x, s1.y), mp = __fmul_rn(a, 1.f / BN);
         ev.part_out[(size_t)(m0 + row) * tiles_n + (tile % tiles_n)] =
-            make_float2(mp - sh.x, fmaxf(s2.x + s2.y - a * mp, 0.f));
+            make_float2(__fsub_rn(mp, sh.x), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2.x, s2.y)), 0.f));
       }
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next

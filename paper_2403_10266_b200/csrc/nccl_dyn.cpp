@@ -38,6 +38,7 @@ bool nccl_load(NcclApi* api, std::string* err) {
          sym(h, "ncclGroupEnd", &api->GroupEnd) && sym(h, "ncclSend", &api->Send) && sym(h, "ncclRecv", &api->Recv) &&
          sym(h, "ncclGetErrorString", &api->GetErrorString);
   }
+  if (ok) sym(h, "ncclCommGetAsyncError", &api->CommGetAsyncError);  // optional: health check only
   if (!ok && err) *err = "libnccl.so.2 lacks the collectives dsp needs";
   api->ok = ok;
   return ok;

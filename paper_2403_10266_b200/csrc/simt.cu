@@ -257,6 +257,44 @@ __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel
   }
 }
 
+// Per-row LayerNorm partials (mean_p, M2_p) of a bf16 [rows, C] activation over column segments
+// of `seg` values, BITWISE identical to the partials the residual GEMM epilogue writes for the
+// rows it stores (gemm_tc.cu, kStats; R30): per segment, values shifted by the segment's first
+// value, even / odd columns summed in two lanes in column order (s1, s2 = sum d, sum d*d),
+// a = s1e + s1o, mp = a * (1/seg), partial = (mp + x0, max(s2e + s2o - a*mp, 0)), every step
+// with explicit round-to-nearest intrinsics (no contraction differences).  Used after a switch
+// (N > 1), where the rows arrive without the partials their producer computed, so the LN
+// statistics the consuming GEMM combines are the same bits at every N.
+// One thread per (row, segment).
+__global__ void __launch_bounds__(256) row_partials_bf16_kernel(const __nv_bfloat16* __restrict__ x, long rows, int C,
+                                                                int seg, float2* __restrict__ parts) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int nseg = C / seg;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * nseg) return;
+  const long row = idx / nseg;
+  const int sg = (int)(idx % nseg);
+  const uint4* p = reinterpret_cast<const uint4*>(x + row * C + (long)sg * seg);
+  float x0 = 0.f, s1e = 0.f, s1o = 0.f, s2e = 0.f, s2o = 0.f;
+  for (int j = 0; j < seg / 8; ++j) {
+    const uint4 v = p[j];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float lo = __uint_as_float(w[t] << 16), hi = __uint_as_float(w[t] & 0xFFFF0000u);
+      if (j == 0 && t == 0) x0 = lo;
+      const float de = __fadd_rn(lo, -x0), dd = __fadd_rn(hi, -x0);
+      s1e = __fadd_rn(s1e, de);
+      s1o = __fadd_rn(s1o, dd);
+      s2e = __fmaf_rn(de, de, s2e);
+      s2o = __fmaf_rn(dd, dd, s2o);
+    }
+  }
+  const float a = __fadd_rn(s1e, s1o), mp = __fmul_rn(a, __frcp_rn((float)seg));
+  parts[idx] = make_float2(__fadd_rn(mp, x0), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2e, s2o)), 0.f));
+}
+
 // Fold a LayerNorm's affine parameters into the weight of the following linear layer:
 //   W'[n, c] = bf16(W[n, c] * gamma[c]),  u[n] = sum_c W'[n, c],  v[n] = sum_c W[n, c] * beta[c]
 // One warp per output row n; up to 3 matrices per launch (blockIdx.y).
@@ -373,6 +411,14 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
                     (float2*)stats, rows, (int)C);
   return launch_k(row_stats_bf16_kernel<kRowStatsMaxV>, dim3(blocks), dim3(threads), 0, st, 1,
                   (const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C);
+}
+
+cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  if (seg % 8 || C % seg) return cudaErrorNotSupported;
+  const long n = rows * (C / seg);
+  return launch_k(row_partials_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
+                  (const __nv_bfloat16*)x, (long)rows, (int)C, seg, parts);
 }
 
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {

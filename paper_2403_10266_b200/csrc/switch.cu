@@ -57,28 +57,48 @@ __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __res
   }
 }
 
-// Signal-pad barrier across `world` ranks (one block, one thread per peer):
-// release-store `epoch` into slot [rank] of every peer's pad, then acquire-spin until
-// every peer has written >= epoch into our own pad.  Bounded spin: a peer that never
-// arrives (dead rank, mismatched collective sequence) traps the kernel -- a CUDA error on
-// the stream instead of a hang or a switch that silently proceeds without the peer's data.
-__global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64_t epoch) {
+// Signal-pad barrier across `world` ranks (one block, one thread per peer).  Pad layout
+// (uint64 slots of every rank's pad): [0, kMaxPeers) = the epoch peer i last arrived at;
+// kPadEpoch = this rank's own barrier counter; kPadError = first timeout record.  The epoch
+// lives in DEVICE memory and is advanced by the kernel itself, so a captured CUDA graph
+// replays a fresh epoch every time (a host-side counter would be frozen into the graph and
+// every replayed barrier would pass at once).  Thread i release-stores the new epoch into
+// slot [rank] of peer i's pad, then acquire-spins until peer i has written >= epoch into our
+// slot [i].  Timeout (wall clock, %globaltimer; 0 = wait forever): the waiting thread records
+// (epoch << 16 | 1 << 8 | peer) in kPadError and returns instead of trapping -- a trap would
+// kill the whole CUDA context; dsp_ctx_check_errors() reports the record to the host.
+__global__ void p2p_barrier_kernel(PeerPtrs signals, int rank, int world, uint64_t timeout_ns) {
   griddep_wait();
+  __shared__ uint64_t s_epoch;
+  uint64_t* pad = static_cast<uint64_t*>(signals.p[rank]);
+  if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(pad + kPadEpoch) + 1;
+  __syncthreads();
+  const uint64_t epoch = s_epoch;
   const int i = threadIdx.x;
   if (i < world) {
     __threadfence_system();
     uint64_t* remote = static_cast<uint64_t*>(signals.p[i]) + rank;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote), "l"(epoch) : "memory");
-    const uint64_t* mine = static_cast<const uint64_t*>(signals.p[rank]) + i;
-    uint64_t v = 0;
-    for (long spin = 0; spin < (1L << 26); ++spin) {
+    const uint64_t* mine = pad + i;
+    uint64_t v = 0, t0 = 0;
+    if (timeout_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
       if (v >= epoch) break;
+      if (timeout_ns) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+          atomicCAS(reinterpret_cast<unsigned long long*>(pad + kPadError), 0ull,
+                    (unsigned long long)((epoch << 16) | (1u << 8) | (unsigned)i));
+          break;
+        }
+      }
       __nanosleep(64);
     }
-    if (v < epoch) __trap();
   }
   __syncthreads();
+  if (threadIdx.x == 0) pad[kPadEpoch] = epoch;  // read by the next barrier in stream order
 }
 
 }  // namespace
@@ -110,8 +130,8 @@ cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t d
   return launch_copy(src, nullptr, rc, peer_base, 1, dst_off, num_sms, st);
 }
 
-cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t epoch, cudaStream_t st) {
-  return launch_k(p2p_barrier_kernel, dim3(1), dim3(32), 0, st, 1, signals, rank, world, epoch);
+cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t timeout_ns, cudaStream_t st) {
+  return launch_k(p2p_barrier_kernel, dim3(1), dim3(32), 0, st, 1, signals, rank, world, timeout_ns);
 }
 
 }  // namespace dsp

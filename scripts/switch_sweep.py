@@ -145,7 +145,7 @@ def run_virtual(args):
         Tn, Sn = T // N, S // N
         shard = B * Tn * S * C * 2
         region = [torch.empty(2 * shard, dtype=torch.uint8, device=dev) for _ in range(N)]
-        sig = [torch.zeros(2 * N, dtype=torch.int64, device=dev) for _ in range(N)]
+        sig = [torch.zeros(dsp.SIGNAL_PAD_BYTES // 8, dtype=torch.int64, device=dev) for _ in range(N)]
         for c in ctxs:
             c.set_peer_buffers([t.data_ptr() for t in region], [t.data_ptr() for t in sig], 2 * shard)
         xT = [region[r][:shard].view(torch.bfloat16) for r in range(N)]

@@ -7,6 +7,8 @@ plan's chunk order [peer][b][t'][s'][c], exchanges them with a real gloo all_to_
 strides, and checks the result against the oracle's S-shard bit-exactly; then back.
 """
 import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import socket
 
 import numpy as np
@@ -91,3 +93,22 @@ def test_switch_world2_gloo(B):
         assert ok1 is True, (rank, ok1)
         assert ok2 is True
         assert sent == (world - 1) * B * (8 // world) * (16 // world) * 16 * 2
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_self_spawns_n_ranks(n):
+    """`python bench.py --gpus N` started WITHOUT torchrun re-launches itself as N ranks (one
+    process per GPU on a GPU box) through torch.distributed.run on 127.0.0.1; here every rank
+    joins a gloo group and rank 0 alone prints the ranks it saw."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--launcher-check"],
+                       capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 only
+    out = json.loads(lines[0])
+    assert out["world"] == n and out["ranks"] == list(range(n))

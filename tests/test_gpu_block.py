@@ -127,7 +127,7 @@ class VirtualGroup:
         self.N = N
         self.ctx = [m.Context(rank=r, world=N) for r in range(N)]
         self.region = [torch.zeros(region_bytes, dtype=torch.uint8, device="cuda") for _ in range(N)]
-        self.sig = [torch.zeros(2 * N, dtype=torch.int64, device="cuda") for _ in range(N)]
+        self.sig = [torch.zeros(m.SIGNAL_PAD_BYTES // 8, dtype=torch.int64, device="cuda") for _ in range(N)]
         base = [t.data_ptr() for t in self.region]
         sigp = [t.data_ptr() for t in self.sig]
         for c in self.ctx:
@@ -485,3 +485,43 @@ def test_block_with_cross_stage_virtual_ranks_n_invariant(N):
     g.run(lambda r: g.ctx[r].st_block_forward(shape, W, Xr[r], Yr[r], impl="fused"))
     got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
+
+
+@pytest.mark.parametrize("impl", ["p2p", "fused"])
+def test_model_prepared_cross_virtual_ranks_n_invariant(impl):
+    """dsp_st_model_forward (prepared weights + cross stage, 3 layers) over 2 virtual ranks equals
+    the N = 1 model bitwise: at N = 1 LN1 of layers 1.. is folded from the previous FC2 epilogue's
+    partials, at N = 2 the same partial bits are recomputed after the S->T switch."""
+    m = dsp()
+    N, L, Lc = 2, 3, 120
+    sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    prep_ctx = m.Context()
+    ctxt = to_dev(synth.make_context(sh, 7, Lc), "bf16").view(sh.B, Lc, sh.C)
+    layers = []
+    for layer in range(L):
+        Ws = synth.make_block_weights(sh, 7, layer=layer)
+        Ws.update(synth.make_cross_weights(sh, 7, layer=layer))
+        W = weights_dev(Ws, "bf16")
+        W["ctx_tokens"] = ctxt
+        W["prepared"] = prep_ctx.prepare_block(shape, W)
+        layers.append(W)
+    xs = synth.make_x(sh, 7)
+    c1 = m.Context()
+    c1.ensure_workspace(m.workspace_bytes(shape, 1))
+    X = to_dev(xs, "bf16")
+    Y1 = torch.empty_like(X)
+    c1.st_model_forward(shape, layers, X, Y1)
+    torch.cuda.synchronize()
+    ref = bits16(Y1)
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    xsh = osw.split(xs, osw.DIM_T, N)
+    Xr = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Yr = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_model_forward(shape, layers, Xr[r], Yr[r], impl=impl))
+    got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref.reshape(-1))
