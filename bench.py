@@ -246,6 +246,8 @@ def run_dsp(args):
     X = to_dev(xs)
     act_bytes = X.numel() * X.element_size()
     ws_bytes = dsp.workspace_bytes(shape, N)
+    if args.schedule == "ulysses":
+        ws_bytes = max(ws_bytes, dsp.ulysses_workspace_bytes(shape, N))
     impl = args.switch
     if impl in ("p2p", "fused") and N > 1:
         import torch.distributed._symmetric_memory as symm
@@ -261,8 +263,13 @@ def run_dsp(args):
         Y = torch.empty_like(X)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    ulysses = args.schedule == "ulysses" and N > 1
+
     def step_eager():
-        ctx.st_block_forward(shape, bw, X, Y, impl=impl)
+        if ulysses:  # the comparison system of P:99 / P:153 on the same kernels
+            ctx.st_block_forward_ulysses(shape, bw, X, Y, impl=impl)
+        else:
+            ctx.st_block_forward(shape, bw, X, Y, impl=impl)
 
     def barrier():
         torch.cuda.synchronize()
@@ -270,6 +277,14 @@ def run_dsp(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
+    # device-side stage clocks (dsp_ctx_set_stage_clocks): each kernel of the block records its span
+    # (first CTA past its dependency wait -> last CTA exit, %globaltimer) with one atomic per CTA,
+    # inside the timed, graph-replayed steps themselves
+    NS = len(dsp.STAGES)
+    clk = torch.zeros(NS, 2, dtype=torch.int64, device=dev)
+    clk_reset = torch.zeros(NS, 2, dtype=torch.int64, device=dev)
+    clk_reset[:, 0] = -1  # UINT64_MAX for the atomicMin
+    ctx.set_stage_clocks(clk)
     # warm-up (eager), then capture one block in a CUDA graph: replay removes the host launch
     # overhead of the ~13 launches per block (the kernels and NCCL calls are the same)
     for _ in range(args.warmup):
@@ -297,14 +312,28 @@ def run_dsp(args):
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     l0 = ctx.launch_count()
+    clk_hist = torch.zeros(K, NS, 2, dtype=torch.int64, device=dev)
     with ClockSampler(local) as clocks:
         barrier()
         for i in range(K):
             flush.zero_()                      # L2 flush between timed steps (outside the events)
+            clk.copy_(clk_reset)
             ev[i][0].record()
             step()
             ev[i][1].record()
+            clk_hist[i].copy_(clk)
         barrier()
+    ctx.set_stage_clocks(None)
+    ch = clk_hist.cpu().numpy().astype(np.uint64)
+    span_us = np.zeros(NS)
+    for i in range(NS):
+        ok = (ch[:, i, 0] != np.uint64(0xFFFFFFFFFFFFFFFF)) & (ch[:, i, 1] > ch[:, i, 0])
+        if ok.any():
+            span_us[i] = float(np.mean((ch[ok, i, 1] - ch[ok, i, 0]).astype(np.float64))) / 1e3
+    if world > 1:
+        st_ = torch.tensor(span_us, dtype=torch.float64, device=dev)
+        dist.all_reduce(st_, op=dist.ReduceOp.MAX)
+        span_us = st_.cpu().numpy()
     launches = ctx.launch_count() - l0 if per_step_launches is None else per_step_launches * K
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
@@ -361,7 +390,7 @@ def run_dsp(args):
     stages = {}
     for i, name in enumerate(dsp.STAGES):
         amt, unit, bound = stage_work(name, sh, N, prepared)
-        us = stage_ms[i] * 1e3
+        us = span_us[i] if span_us[i] > 0 else stage_ms[i] * 1e3
         if amt is None:
             stages[name] = {"us": round(us, 2), "folded": "into the consuming GEMM epilogue (R30): no kernel"}
             continue
@@ -376,10 +405,11 @@ def run_dsp(args):
             ach, pk, u = amt / (us * 1e-6) / 1e9, 900.0, "GB/s"
         stages[name] = {"us": round(us, 2), "achieved": round(ach, 1), "unit": u, "frac": round(ach / pk, 3),
                         "bound": bound, "algorithmic_per_launch": amt, "algorithmic_unit": unit + "s",
-                        "traffic": traffic.get(name)}
+                        "traffic": traffic.get(name), "timing": "device clock" if span_us[i] > 0 else "events",
+                        "event_us": round(stage_ms[i] * 1e3, 2)}
     # dominant kernel = the compute stage with the largest measured time (one kernel per stage)
     KERNELS = {"QKV_S": "gemm_bf16_tc_kernel<192, LN-folded> (spatial QKV)",
-               "ATTN_S": "fmha_pair_kernel (spatial FMHA)",
+               "ATTN_S": "fmha_pt_kernel (spatial FMHA, P in TMEM)",
                "PROJ_S": "gemm_bf16_tc_kernel<192, +residual +LN partials> (spatial out-proj)",
                "QKV_T": "gemm_bf16_tc_kernel<192, LN-folded> (temporal QKV)",
                "ATTN_T": "fmha_bf16_tc_kernel (temporal FMHA, block-diagonal packed)",
@@ -395,15 +425,20 @@ def run_dsp(args):
             "frac": d["frac"], "traffic": traffic.get(dom),
             "peak_source": peak_src + ", burst figure (conservative: the kernel runs inside a sub-ms step)",
             "algorithmic_per_launch": d["algorithmic_per_launch"], "algorithmic_unit": d["algorithmic_unit"],
-            "launch_us": d["us"], "launches_timed": KP,
-            "timing": "CUDA events around this stage only, inside a captured graph of the block, replayed "
-                      f"{KP}x with L2 flushed; dominant = the longest compute stage"}
+            "launch_us": d["us"], "launches_timed": K,
+            "timing": "device stage clock: span from the first CTA past its dependency wait to the last CTA "
+                      "exit (%globaltimer, one atomic per CTA), averaged over the K timed graph replays; "
+                      "dominant = the longest compute stage",
+            "event_us": d["event_us"],
+            "event_timing": f"CUDA events around this stage only in a separately captured graph, {KP} replays"}
     kernels = {n: {"kernel": KERNELS[n], **{k: stages[n][k] for k in ("us", "achieved", "unit", "frac", "bound")}}
                for n in KERNELS if n in stages and "frac" in stages[n]}
+    clocked_sum_us = float(span_us.sum())
     flops_block = 32 * tokens * sh.C ** 2 + 4 * sh.B * sh.T * sh.S ** 2 * sh.C + 4 * sh.B * sh.S * sh.T ** 2 * sh.C
     t_roof_us = flops_block / N / (P["bf16_tflops"] * 1e12) * 1e6
     nvl_us = 2 * (N - 1) * sh.M // (N * N) * sh.elem_bytes / 900e9 * 1e6
     block_roof = {"t_roofline_us": round(max(t_roof_us, nvl_us), 1), "t_block_us": round(t_ms / K * 1e3, 1),
+                  "sum_of_stage_spans_us": round(clocked_sum_us, 1),
                   "frac": round(max(t_roof_us, nvl_us) / (t_ms / K * 1e3), 3),
                   "basis": "max(block FLOPs/N / measured bf16 peak, 2 switches' bytes / 900 GB/s)"}
 
@@ -472,6 +507,7 @@ def run_dsp(args):
                "vs_baseline": None, "dtype": sh.dtype, "data": "synthetic",
                "config": {"workload": desc, "B": sh.B, "T": sh.T, "S": sh.S, "C": sh.C, "num_heads": sh.NH,
                           "global_tokens": tokens, "switch_impl": impl if N > 1 else "none (N=1)",
+                          "schedule": ("ulysses" if ulysses else "dsp"),
                           "l2": "flushed between timed steps (256 MiB memset outside the events)",
                           "launch": graph_note, "weights": prep_note},
                "roofline": roof, "kernels": kernels, "block_roofline": block_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
@@ -704,6 +740,8 @@ def main():
     ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
     ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28", "nd"])
     ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p", "fused"])
+    ap.add_argument("--schedule", default="dsp", choices=["dsp", "ulysses"],
+                    help="ulysses: DeepSpeed-Ulysses on the same kernels (4 all-to-alls per attention stage)")
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prepare", dest="prepare", action="store_false",

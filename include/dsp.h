@@ -145,6 +145,16 @@ dsp_status_t dsp_ctx_set_workspace(dsp_ctx_t ctx, void* workspace_dev, size_t by
 dsp_status_t dsp_ctx_set_peer_buffers(dsp_ctx_t ctx, void* const* peer_base_dev,
                                       void* const* peer_signal_dev, size_t bytes);
 
+/* TEST INFRASTRUCTURE.  on != 0: the NCCL transport's collectives (the all-to-all of
+ * dsp_switch / dsp_switch_nd / the blocks with impl NCCL, the all-gather of dsp_gather) are
+ * emulated over the peer mappings instead of calling NCCL: signal-pad barrier, one kernel that
+ * pulls every peer's piece (recv[r] = peer r's send chunk for this rank; stage[r] = peer r's
+ * x_local), barrier.  Everything else of the NCCL code path (pack, unpack, workspace staging)
+ * runs unchanged.  For N "virtual ranks" sharing one device (NCCL refuses two ranks per GPU);
+ * the staged send buffer (the workspace, or x_local when the pack is an identity) must lie in
+ * the registered symmetric buffer.  Errors: NULL, STATE (no peer buffers). */
+dsp_status_t dsp_ctx_set_collective_emulation(dsp_ctx_t ctx, int on);
+
 /* Wall-clock bound of every P2P signal-pad barrier wait (default 120 s, or
  * $DSP_BARRIER_TIMEOUT_S at context creation; <= 0 waits forever).  A barrier that times out
  * records (epoch, peer) in its pad and lets the stream continue -- the switch's data is then
@@ -170,6 +180,16 @@ typedef enum {
  * NULL entries are skipped, so a caller can time one stage per pass: every event record
  * is a point where the next kernel's programmatic dependent launch cannot overlap. */
 dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n_events);
+/* Stage clocks (instrumentation; off by default).  clocks_dev: device buffer of
+ * 2*DSP_NUM_STAGES uint64, or NULL to switch off.  While set, every kernel dsp_st_block_forward
+ * launches inside stage i records, with one atomic per CTA, the earliest %globaltimer (ns) at
+ * which one of its CTAs passed its dependency wait into clocks[2i] (atomicMin) and the latest
+ * CTA exit into clocks[2i+1] (atomicMax) -- the stage's span inside an unperturbed (e.g. graph-
+ * replayed) block, with programmatic dependent launch intact.  The caller resets the buffer
+ * (clocks[2i] = UINT64_MAX, clocks[2i+1] = 0) before each block; stages without a kernel (folded
+ * LayerNorms, switches at N = 1, NCCL / copy kernels) keep the reset values.  The pointer is
+ * baked into captured graphs.  Errors: NULL, ALIGNMENT (8 B). */
+dsp_status_t dsp_ctx_set_stage_clocks(dsp_ctx_t ctx, void* clocks_dev);
 /* Instrumentation taps (test infrastructure; off by default): when set, dsp_st_block_forward
  * copies an intermediate of the block into `dst` (device, >= the local shard bytes) with a
  * stream-ordered D2D copy (also captured into CUDA graphs):
@@ -188,9 +208,10 @@ int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
-#define DSP_ABI_VERSION 4  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage;
+#define DSP_ABI_VERSION 5  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage;
                               4: device-resident barrier epochs, barrier timeout + error check,
-                              exported switch pack / unpack and gather unpack */
+                              exported switch pack / unpack and gather unpack; 5: Ulysses block,
+                              stage clocks, taps, collective emulation */
 
 /* ----------------------------------------------------------- layout (bytes) */
 
@@ -286,6 +307,27 @@ dsp_status_t dsp_temporal_attn(dsp_ctx_t ctx, const dsp_shape_t* shape, const vo
 dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* shape,
                                   const dsp_block_weights_t* w, const void* x_local,
                                   void* y_local, dsp_switch_impl_t impl, void* stream);
+
+/* ------------------------------------------------- Ulysses schedule (A/B baseline)
+ * The same ST block (identical weights, kernels and result) under DeepSpeed-Ulysses sequence
+ * parallelism ("AlltoAll for query, key, value, and output"), the
+ * comparison system of the paper's experiments, built on this library's kernels.
+ * x_local / y_local are T-sharded [B, T/N, S, C] throughout (the activation never switches).
+ * Each attention stage: local QKV GEMM -> three all-to-alls (q, k, v: sequence-sharded ->
+ * head-sharded; rank g receives every token of heads [g*NH/N, (g+1)*NH/N)) -> attention over the
+ * full sequence with NH/N heads -> one all-to-all (o: head-sharded -> sequence-sharded) ->
+ * local out-projection + residual.  The MLP is local.  8 all-to-alls per block, each moving
+ * (N-1)*M/N^2 elements per rank: 4x DSP's volume (Table 1: 8M/N vs 2M/N).
+ * impl NCCL: one ncclAlltoAll per tensor (pack / unpack kernels around it); P2P: q, k, v in one
+ * direct put and o in another (workspace inside the symmetric buffer).  N == 1: the DSP block.
+ * Prepared weights (R30) supported; no cross stage.  Workspace >= dsp_ulysses_workspace_bytes
+ * (11 * tok_r * C * elem + statistics).  COLLECTIVE.  Output is bitwise independent of N and
+ * equal to dsp_st_block_forward at N = 1 (per-head attention, no reductions across ranks).
+ * Errors: as dsp_st_block_forward; UNSUPPORTED (f32, N does not divide num_heads, cross stage,
+ * impl FUSED), ALIGNMENT (C/N*elem % 16). */
+size_t dsp_ulysses_workspace_bytes(const dsp_shape_t* shape, int world);  /* host-only */
+dsp_status_t dsp_st_block_forward_ulysses(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* w,
+                                          const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
 
 /* ---------------------------------------------------------------- N-D switch
  * DSP on a multi-dimensional activation [d_0, ..., d_{n-2}, C] with any number of sequence

@@ -128,6 +128,9 @@ def lib() -> ctypes.CDLL:
             "dsp_ctx_set_barrier_timeout": [vp, ctypes.c_double],
             "dsp_ctx_check_errors": [vp],
             "dsp_ctx_set_tap": [vp, ctypes.c_int, vp, ctypes.c_size_t],
+            "dsp_ctx_set_stage_clocks": [vp, vp],
+            "dsp_ctx_set_collective_emulation": [vp, ctypes.c_int],
+            "dsp_st_block_forward_ulysses": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -139,6 +142,8 @@ def lib() -> ctypes.CDLL:
         L.dsp_cross_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_nd_workspace_bytes.argtypes = [P(i64), ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.dsp_nd_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_ulysses_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
+        L.dsp_ulysses_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_block_prepared_bytes.argtypes = [P(Shape)]
         L.dsp_block_prepared_bytes.restype = ctypes.c_size_t
         L.dsp_status_str.argtypes = [ctypes.c_int]
@@ -189,6 +194,11 @@ def _stream(stream=None) -> int:
 
 def workspace_bytes(shape: Shape, world: int) -> int:
     return int(lib().dsp_workspace_bytes(ctypes.byref(shape), int(world)))
+
+
+def ulysses_workspace_bytes(shape: Shape, world: int) -> int:
+    """dsp_ulysses_workspace_bytes: per-rank workspace of the Ulysses-schedule block."""
+    return int(lib().dsp_ulysses_workspace_bytes(ctypes.byref(shape), int(world)))
 
 
 def prepared_bytes(shape: Shape) -> int:
@@ -297,6 +307,11 @@ class Context:
         """dsp_ctx_set_barrier_timeout: wall-clock bound of a P2P barrier wait (<= 0: forever)."""
         _check(lib().dsp_ctx_set_barrier_timeout(self.handle, float(seconds)), self.handle)
 
+    def set_collective_emulation(self, on: bool = True):
+        """dsp_ctx_set_collective_emulation (test infrastructure): NCCL all-to-all / all-gather of this
+        virtual rank emulated over the peer mappings (barrier + pull kernel + barrier)."""
+        _check(lib().dsp_ctx_set_collective_emulation(self.handle, int(bool(on))), self.handle)
+
     def check_errors(self):
         """dsp_ctx_check_errors (synchronous): raise DSPError on a timed-out P2P barrier or an
         asynchronous NCCL error of the borrowed communicator."""
@@ -309,6 +324,12 @@ class Context:
         """dsp_ctx_set_tap: copy the block's y1 / y2 (S-sharded) into dst on every block call."""
         _check(lib().dsp_ctx_set_tap(self.handle, self.TAPS[point], _ptr(dst),
                                      0 if dst is None else dst.numel() * dst.element_size()), self.handle)
+
+    def set_stage_clocks(self, clocks=None):
+        """dsp_ctx_set_stage_clocks: clocks = int64 CUDA tensor [len(STAGES), 2] (reset to
+        [max, 0] before each block; read back as ns spans per stage), or None (off)."""
+        self._clocks = clocks
+        _check(lib().dsp_ctx_set_stage_clocks(self.handle, _ptr(clocks)), self.handle)
 
     def launch_count(self) -> int:
         return int(lib().dsp_ctx_launch_count(self.handle))
@@ -413,6 +434,13 @@ class Context:
         bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
         self._call("dsp_st_block_forward", ctypes.byref(shape), ctypes.byref(bw), _ptr(x_local), _ptr(y_local),
                    IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def st_block_forward_ulysses(self, shape, weights, x_local, y_local, impl="nccl", stream=None):
+        """dsp_st_block_forward_ulysses: the same block under DeepSpeed-Ulysses (4 all-to-alls per
+        attention stage; T-sharded in and out)."""
+        bw = weights if isinstance(weights, BlockWeights) else self.block_weights(weights)
+        self._call("dsp_st_block_forward_ulysses", ctypes.byref(shape), ctypes.byref(bw), _ptr(x_local),
+                   _ptr(y_local), IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
 
     def st_model_forward(self, shape, layers, x_local, y_local, impl="nccl", stream=None):
         """dsp_st_model_forward: layers = list of per-layer weights (dicts or BlockWeights)."""

@@ -205,6 +205,31 @@ RunCopy plan_runs(const dsp_switch_plan_t& p) {
   return rc;
 }
 
+// Emulated collectives (virtual ranks on one device, dsp_ctx_set_collective_emulation): the
+// contract of ncclAlltoAll / ncclAllGather on byte buffers -- recv[r] = peer r's send[rank] /
+// stage[r] = peer r's x_local -- realised as barrier, one kernel pulling every peer's piece over
+// the peer mappings, barrier.  `src` must lie inside the registered symmetric buffer (the same
+// offset on every rank).  Test infrastructure for the NCCL transport's code path (NCCL cannot put
+// two ranks on one GPU); never selected implicitly.
+dsp_status_t emulated_gather_pieces(dsp_ctx_t ctx, const void* src, int64_t src_stride_rank, int64_t piece,
+                                    void* dst, cudaStream_t st, const char* what) {
+  const int N = ctx->world;
+  if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "%s: collective emulation needs peer buffers", what);
+  void* base = ctx->peer_base.p[ctx->rank];
+  if (!in_region(src, src_stride_rank * (N - 1) + piece, base, ctx->peer_bytes))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "%s: emulated collective source is not inside the symmetric buffer", what);
+  const int64_t src_off = static_cast<const uint8_t*>(src) - static_cast<uint8_t*>(base) + ctx->rank * src_stride_rank;
+  RunCopy rc;
+  rc.n[0] = N;
+  rc.run_bytes = piece;
+  rc.ds[0] = piece;
+  DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "emulated collective entry");
+  DSP_CUDA(ctx, launch_p2p_pull(ctx->peer_base, src_off, dst, rc, ctx->num_sms, st), "emulated collective pull");
+  DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "emulated collective exit");
+  ctx->launches += 3;
+  return DSP_OK;
+}
+
 // Execute a switch plan (4-level strided runs, level 0 = peer): P2P = entry barrier, direct
 // stores of every run at its final address in the peer's buffer, exit barrier; NCCL = pack into
 // per-peer chunks (skipped when identity) -> ncclAlltoAll (bytes) -> unpack (skipped when identity).
@@ -224,7 +249,8 @@ dsp_status_t do_switch_plan(dsp_ctx_t ctx, const RunCopy& rc, int64_t dst_peer_o
     ctx->launches += 3;
     return DSP_OK;
   }
-  if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
+  if (!ctx->emulate_collectives && (!ctx->nccl.ok || !ctx->comm))
+    return fail(ctx, DSP_ERR_NCCL, "NCCL switch without a communicator");
   const ChunkCopies cc = chunk_copies(rc);
   const int64_t chunk = cc.chunk;
   const void* send = x;
@@ -236,7 +262,10 @@ dsp_status_t do_switch_plan(dsp_ctx_t ctx, const RunCopy& rc, int64_t dst_peer_o
   }
   if (!unpack_identity) recv = scratch_recv;
   int r;
-  if (ctx->nccl.AlltoAll) {
+  if (ctx->emulate_collectives) {
+    DSP_TRY(emulated_gather_pieces(ctx, send, chunk, chunk, recv, st, "switch"));
+    r = 0;
+  } else if (ctx->nccl.AlltoAll) {
     r = ctx->nccl.AlltoAll(send, recv, (size_t)chunk, kNcclUint8, ctx->comm, st);
   } else {
     r = ctx->nccl.GroupStart();
@@ -270,6 +299,8 @@ dsp_status_t do_switch(dsp_ctx_t ctx, const dsp_shape_t* s, int from, const void
 }
 
 inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
+  // stage clocks: every kernel launched inside the stage records its span into the stage's slot
+  if (stage >= 0) t_clk = (!end && ctx->stage_clk) ? ctx->stage_clk + 2 * stage : nullptr;
   if (ctx->has_stage_events && stage >= 0 && ctx->stage_events[2 * stage + end]) {
     // inside a stream capture the record becomes an external event node of the graph, so a
     // replayed graph timestamps the stage boundary
@@ -425,6 +456,13 @@ dsp_status_t dsp_ctx_set_stage_events(dsp_ctx_t ctx, void* const* events, int n)
   return DSP_OK;
 }
 
+dsp_status_t dsp_ctx_set_stage_clocks(dsp_ctx_t ctx, void* clocks_dev) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (clocks_dev && (reinterpret_cast<uintptr_t>(clocks_dev) & 7)) return fail(ctx, DSP_ERR_ALIGNMENT, "clock buffer not 8-B aligned");
+  ctx->stage_clk = static_cast<unsigned long long*>(clocks_dev);
+  return DSP_OK;
+}
+
 dsp_status_t dsp_ctx_set_tap(dsp_ctx_t ctx, dsp_tap_t point, void* dst, size_t bytes) {
   if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
   if (point < 0 || point >= DSP_NUM_TAPS) return fail(ctx, DSP_ERR_SHAPE, "unknown tap %d", (int)point);
@@ -539,7 +577,8 @@ dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, cons
     DSP_CUDA(ctx, cudaMemcpyAsync(xg, xl, local, cudaMemcpyDeviceToDevice, st), "gather copy (N=1)");
     return DSP_OK;
   }
-  if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "gather without a communicator");
+  if (!ctx->emulate_collectives && (!ctx->nccl.ok || !ctx->comm))
+    return fail(ctx, DSP_ERR_NCCL, "gather without a communicator");
   const bool identity = (dim == DSP_DIM_T) ? (s->B == 1) : (s->B * s->T == 1);
   void* stage = xg;
   if (!identity) {
@@ -548,8 +587,12 @@ dsp_status_t dsp_gather(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t dim, cons
       return fail(ctx, DSP_ERR_ALIAS, "x_local / x_global overlap the workspace the gather stages through");
     stage = ctx->ws;
   }
-  int r = ctx->nccl.AllGather(xl, stage, (size_t)local, kNcclUint8, ctx->comm, st);
-  if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAllGather: %s", ctx->nccl.GetErrorString(r));
+  if (ctx->emulate_collectives) {
+    DSP_TRY(emulated_gather_pieces(ctx, xl, 0, local, stage, st, "gather"));
+  } else {
+    int r = ctx->nccl.AllGather(xl, stage, (size_t)local, kNcclUint8, ctx->comm, st);
+    if (r) return fail(ctx, DSP_ERR_NCCL, "ncclAllGather: %s", ctx->nccl.GetErrorString(r));
+  }
   if (!identity) {
     DSP_CUDA(ctx, launch_run_copy(stage, xg, gather_runs(s, N, dim), ctx->num_sms, st), "gather unpack");
     ctx->launches += 1;
@@ -595,6 +638,13 @@ dsp_status_t dsp_switch_pack(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from
 dsp_status_t dsp_switch_unpack(dsp_ctx_t ctx, const dsp_shape_t* s, dsp_dim_t from, dsp_dim_t to, const void* recv,
                                void* y_local, void* stream) {
   return switch_chunk_call(ctx, s, from, to, recv, y_local, false, stream);
+}
+
+dsp_status_t dsp_ctx_set_collective_emulation(dsp_ctx_t ctx, int on) {
+  if (!ctx) return fail(nullptr, DSP_ERR_NULL, "context is NULL");
+  if (on && !ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "collective emulation needs dsp_ctx_set_peer_buffers");
+  ctx->emulate_collectives = on != 0;
+  return DSP_OK;
 }
 
 dsp_status_t dsp_ctx_set_barrier_timeout(dsp_ctx_t ctx, double seconds) {
@@ -993,6 +1043,193 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
 dsp_status_t dsp_st_block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* x,
                                   void* y, dsp_switch_impl_t impl, void* stream) {
   return block_forward(ctx, s, w, x, y, impl, stream, false, false);
+}
+
+// ------------------------------------------------------------------ Ulysses
+// DeepSpeed-Ulysses on the same kernels ("AlltoAll for query, key, value, and output"):
+// the activation stays T-sharded; every attention stage projects q, k, v locally, exchanges
+// them sequence-sharded -> head-sharded (rank g receives the full sequence of head group g,
+// channels [g*C/N, (g+1)*C/N) of each of q, k, v), attends over the full sequence with NH/N
+// heads, and exchanges o back head-sharded -> sequence-sharded before the local out-projection.
+// 4 all-to-alls per attention stage, 8 per block (Table 1: 8M/N) against DSP's 2.
+struct UlyssesWs {
+  int64_t act, h, qkv, qkvh, oh, o, send, recv, stats, parts, total;
+};
+static UlyssesWs ulysses_ws(const dsp_shape_t* s, int world) {
+  UlyssesWs w{};
+  const int64_t tok = s->B * s->T * s->S / world, C = s->C, e = elem_bytes(s->dtype);
+  w.act = tok * C * e;
+  w.h = 0;
+  w.qkv = w.act;        // [tok, 3C] local projection (and, with qkvh, the MLP hidden [tok, 4C])
+  w.qkvh = 4 * w.act;   // [B*T*S, 3C/N] head-sharded q | k | v of this rank's head group
+  w.oh = 7 * w.act;     // [B*T*S, C/N] attention output of the head group
+  w.o = 8 * w.act;      // [tok, C] attention output, sequence-sharded again
+  w.send = 9 * w.act;   // NCCL staging
+  w.recv = 10 * w.act;
+  w.stats = align256(11 * w.act);
+  w.parts = w.stats + align256(tok * 8);
+  w.total = w.parts + align256(tok * (C / gemm_bn_for(C)) * 8) + 256;
+  return w;
+}
+
+// q, k, v (columns [p*C, (p+1)*C) of qkv [B, T/N, S, 3C]) -> qkvh [B, T, S, 3C/N]: run (g, b, row)
+// of C/N elements goes to rank g's qkvh row (b, rank*T/N*S + row), column p*C/N.  NCCL: one
+// all-to-all per part (q, k, v: three, as DeepSpeed-Ulysses); P2P: the three parts in one put.
+static dsp_status_t ulysses_exchange_qkv(dsp_ctx_t ctx, const dsp_shape_t* s, const uint8_t* qkv, uint8_t* qkvh,
+                                  dsp_switch_impl_t impl, cudaStream_t st, void* send, void* recv) {
+  const int N = ctx->world;
+  const int64_t e = elem_bytes(s->dtype), C = s->C, Cn = C / N, Tn = s->T / N, S = s->S, T = s->T, B = s->B;
+  const int parts = impl == DSP_SWITCH_P2P ? 3 : 1;
+  RunCopy rc;
+  rc.n[0] = N; rc.n[1] = B; rc.n[2] = Tn * S; rc.n[3] = parts;
+  rc.run_bytes = Cn * e;
+  rc.ss[0] = Cn * e; rc.ss[1] = Tn * S * 3 * C * e; rc.ss[2] = 3 * C * e; rc.ss[3] = C * e;
+  rc.ds[0] = Tn * S * 3 * Cn * e; rc.ds[1] = T * S * 3 * Cn * e; rc.ds[2] = 3 * Cn * e; rc.ds[3] = Cn * e;
+  const int64_t total = B * T * S * 3 * Cn * e;
+  for (int p = 0; p < 3; p += parts)
+    DSP_TRY(do_switch_plan(ctx, rc, ctx->rank * rc.ds[0], false, false, total - p * Cn * e, qkv + p * C * e,
+                           qkvh + p * Cn * e, impl, st, send, recv));
+  return DSP_OK;
+}
+
+// oh [B, T, S, C/N] (this rank's head group, every token) -> o [B, T/N, S, C] of the token's owner,
+// columns [rank*C/N, (rank+1)*C/N): the fourth all-to-all.
+static dsp_status_t ulysses_exchange_o(dsp_ctx_t ctx, const dsp_shape_t* s, const uint8_t* oh, uint8_t* o,
+                                dsp_switch_impl_t impl, cudaStream_t st, void* send, void* recv) {
+  const int N = ctx->world;
+  const int64_t e = elem_bytes(s->dtype), C = s->C, Cn = C / N, Tn = s->T / N, S = s->S, T = s->T, B = s->B;
+  RunCopy rc;
+  rc.n[0] = N; rc.n[1] = B; rc.n[2] = Tn * S; rc.n[3] = 1;
+  rc.run_bytes = Cn * e;
+  rc.ss[0] = Tn * S * Cn * e; rc.ss[1] = T * S * Cn * e; rc.ss[2] = Cn * e;
+  rc.ds[0] = Cn * e; rc.ds[1] = Tn * S * C * e; rc.ds[2] = C * e;
+  return do_switch_plan(ctx, rc, ctx->rank * rc.ds[0], false, false, B * Tn * S * C * e, oh, o, impl, st, send, recv);
+}
+
+// One Ulysses attention stage on the T-sharded activation: out = res + MHA_dim(LN(res)).
+// ln != nullptr: prepared weights (LN folded into the QKV GEMM); else h holds LN(res) already.
+static dsp_status_t ulysses_attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int dim, const void* a_in, const void* res,
+                                void* out, const void* w_qkv, const void* w_o, const EpiVec* ln, float2* part_out,
+                                uint8_t* ws, const UlyssesWs& L, dsp_switch_impl_t impl, cudaStream_t st, int stage0) {
+  const int N = ctx->world;
+  const int64_t C = s->C, Cn = C / N, tok = s->B * s->T * s->S / N;
+  uint8_t *qkv = ws + L.qkv, *qkvh = ws + L.qkvh, *oh = ws + L.oh, *o = ws + L.o;
+  std::string why;
+  mark(ctx, stage0, 0, st);
+  cudaError_t e = ln ? launch_gemm_bf16_ln(a_in, w_qkv, *ln, qkv, tok, 3 * C, C, false, ctx->num_sms, st, &why)
+                     : launch_gemm_bf16(a_in, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "qkv projection", why);
+  ctx->launches += 1;
+  mark(ctx, stage0, 1, st);
+  mark(ctx, stage0 + 1, 0, st);
+  DSP_TRY(ulysses_exchange_qkv(ctx, s, qkv, qkvh, impl, st, ws + L.send, ws + L.recv));
+  // the full sequence (all T frames, all S positions) of NH/N heads
+  e = launch_fmha_bf16(qkvh, oh, s->B, s->T, s->S, Cn, s->num_heads / N, dim, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core (head group)", why);
+  ctx->launches += 1;
+  DSP_TRY(ulysses_exchange_o(ctx, s, oh, o, impl, st, ws + L.send, ws + L.recv));
+  mark(ctx, stage0 + 1, 1, st);
+  mark(ctx, stage0 + 2, 0, st);
+  e = part_out ? launch_gemm_bf16_res_stats(o, w_o, res, out, tok, C, C, part_out, ctx->num_sms, st, &why)
+               : launch_gemm_bf16(o, w_o, res, out, tok, C, C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "output projection", why);
+  ctx->launches += 1;
+  mark(ctx, stage0 + 2, 1, st);
+  return DSP_OK;
+}
+
+size_t dsp_ulysses_workspace_bytes(const dsp_shape_t* s, int world) {
+  if (!s || world < 1 || s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1) return 0;
+  return (size_t)ulysses_ws(s, world).total;
+}
+
+dsp_status_t dsp_st_block_forward_ulysses(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w,
+                                                     const void* x, void* y, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!w || !x || !y) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  const int N = ctx->world;
+  if (N == 1) return block_forward(ctx, s, w, x, y, impl, stream, false, false);  // no exchange at N = 1
+  if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "the Ulysses schedule runs on the bf16 path");
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "Ulysses supports the NCCL and P2P transports");
+  if (s->num_heads % N) return fail(ctx, DSP_ERR_UNSUPPORTED, "Ulysses needs N | num_heads (N=%d, heads=%d)", N, s->num_heads);
+  if (((s->C / N) * 2) % 16) return fail(ctx, DSP_ERR_ALIGNMENT, "Ulysses needs C/N*2 %% 16 == 0");
+  if (w->ln_c_w) return fail(ctx, DSP_ERR_UNSUPPORTED, "the Ulysses block has no cross stage");
+  const void* wp[12] = {w->ln1_w, w->ln1_b, w->w_qkv_s, w->w_o_s, w->ln2_w, w->ln2_b,
+                        w->w_qkv_t, w->w_o_t, w->ln3_w, w->ln3_b, w->w_fc1, w->w_fc2};
+  for (int i = 0; i < 12; ++i)
+    if (!wp[i] || !aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d NULL or not 16-B aligned", i);
+  if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  {
+    const dsp_shape_t hs{1, 1, 1, s->C / N, s->num_heads / N, s->dtype};
+    DSP_TRY(check_bf16_attn(ctx, &hs, 128));
+  }
+  const bool fold = w->prepared != nullptr;
+  const int64_t C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * 2;
+  const UlyssesWs L = ulysses_ws(s, N);
+  if (!ctx->ws || ctx->ws_bytes < (size_t)L.total) return fail(ctx, DSP_ERR_WORKSPACE, "Ulysses block needs %lld bytes of workspace", (long long)L.total);
+  if (x != y && overlap(x, act, y, act)) return fail(ctx, DSP_ERR_ALIAS, "x_local partially overlaps y_local");
+  if (overlap(ctx->ws, L.total, x, act) || overlap(ctx->ws, L.total, y, act)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y");
+  if (impl == DSP_SWITCH_P2P) {
+    if (!ctx->has_peers) return fail(ctx, DSP_ERR_STATE, "P2P Ulysses without dsp_ctx_set_peer_buffers");
+    if (!in_region(ctx->ws, L.total, ctx->peer_base.p[ctx->rank], ctx->peer_bytes))
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "P2P Ulysses needs the workspace inside the symmetric buffer");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  const float eps = w->ln_eps;
+  const PrepLayout P = prep_layout(C);
+  const uint8_t* prep = static_cast<const uint8_t*>(w->prepared);
+  const float* uv = fold ? reinterpret_cast<const float*>(prep + P.uv) : nullptr;
+  float2* stats = reinterpret_cast<float2*>(ws + L.stats);
+  float2* parts = reinterpret_cast<float2*>(ws + L.parts);
+  const int nparts = (int)(C / gemm_bn_for(C));
+  EpiVec ev1{}, ev2{}, ev3{};
+  if (fold) {  // R30: as the DSP block at N = 1 (the rows never move, so every partial stays local)
+    ev1.row_stats = stats; ev1.col_u = uv; ev1.col_v = uv + 3 * C;
+    ev2.col_u = uv + 6 * C; ev2.col_v = uv + 9 * C;
+    ev3.col_u = uv + 12 * C; ev3.col_v = uv + 16 * C;
+    for (EpiVec* ev : {&ev2, &ev3}) {
+      ev->part_in = parts; ev->nparts_in = nparts; ev->part_cnt = (int)(C / nparts); ev->eps = eps;
+    }
+  }
+  void* h = ws + L.h;
+  mark(ctx, DSP_STAGE_LN1, 0, st);
+  if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
+  else DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, x, w->ln1_w, w->ln1_b, eps, h, st), "LN1");
+  ctx->launches += 1;
+  mark(ctx, DSP_STAGE_LN1, 1, st);
+  DSP_TRY(ulysses_attn_stage(ctx, s, DSP_DIM_S, fold ? x : h, x, y, fold ? prep + P.wf_s : w->w_qkv_s, w->w_o_s,
+                             fold ? &ev1 : nullptr, fold ? parts : nullptr, ws, L, impl, st, DSP_STAGE_QKV_S));
+  mark(ctx, DSP_STAGE_LN2, 0, st);
+  if (!fold) {
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, y, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
+    ctx->launches += 1;
+  }
+  mark(ctx, DSP_STAGE_LN2, 1, st);
+  DSP_TRY(ulysses_attn_stage(ctx, s, DSP_DIM_T, fold ? y : h, y, y, fold ? prep + P.wf_t : w->w_qkv_t, w->w_o_t,
+                             fold ? &ev2 : nullptr, fold ? parts : nullptr, ws, L, impl, st, DSP_STAGE_QKV_T));
+  mark(ctx, DSP_STAGE_LN3, 0, st);
+  if (!fold) {
+    DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, y, w->ln3_w, w->ln3_b, eps, h, st), "LN3");
+    ctx->launches += 1;
+  }
+  mark(ctx, DSP_STAGE_LN3, 1, st);
+  uint8_t* hid = ws + L.qkv;  // [tok, 4C] over qkv and the front of qkvh
+  std::string why;
+  mark(ctx, DSP_STAGE_FC1, 0, st);
+  cudaError_t e = fold ? launch_gemm_bf16_ln(y, prep + P.wf_1, ev3, hid, tok, 4 * C, C, true, ctx->num_sms, st, &why)
+                       : launch_gemm_bf16(h, w->w_fc1, nullptr, hid, tok, 4 * C, C, DSP_EPI_GELU, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "FC1", why);
+  mark(ctx, DSP_STAGE_FC1, 1, st);
+  mark(ctx, DSP_STAGE_FC2, 0, st);
+  e = launch_gemm_bf16(hid, w->w_fc2, y, y, tok, C, 4 * C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "FC2", why);
+  mark(ctx, DSP_STAGE_FC2, 1, st);
+  ctx->launches += 2;
+  return DSP_OK;
 }
 
 dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* const* w, int L,

@@ -48,6 +48,11 @@ struct RunCopy {
   int64_t ss[4] = {0, 0, 0, 0}, ds[4] = {0, 0, 0, 0};
 };
 
+// Stage clock of the launches the current thread issues next ([2] u64 in device memory, or NULL):
+// block_forward points it at the stage's slot of dsp_ctx_set_stage_clocks' buffer, the
+// launchers pass it to their kernels (clk_start / clk_end in sm100.cuh).
+extern thread_local unsigned long long* t_clk;
+
 // ---- launchers (return cudaGetLastError() after the launch) ----
 cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
                              int epi, int num_sms, cudaStream_t st, std::string* why);
@@ -66,6 +71,9 @@ cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int n
 // P2P: run (i0=peer,i1,i2) stored to peer_base.p[i0] + dst_off + i1*ds[1] + i2*ds[2]
 cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t dst_off, const RunCopy& rc,
                            int num_sms, cudaStream_t st);
+// pull: run (i0=peer,i1,i2,i3) read from peer_base.p[i0] + src_off + i1*ss[1] + ... into dst + sum(i*ds)
+cudaError_t launch_p2p_pull(const PeerPtrs& peer_base, int64_t src_off, void* dst, const RunCopy& rc, int num_sms,
+                            cudaStream_t st);
 cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t timeout_ns, cudaStream_t st);
 
 // LayerNorm folded into the following GEMM (bf16 path)
@@ -106,6 +114,7 @@ struct EpiVec {
   int nparts_in, part_cnt;
   float eps;
   float2* part_out;         // residual epilogue: [M, N / BN] partials of the stored (bf16) rows
+  unsigned long long* clk;  // stage clock (set by run_gemm from t_clk)
 };
 // BN (output-tile width) the GEMM dispatch picks for N output columns
 int gemm_bn_for(int64_t N);
@@ -171,9 +180,11 @@ struct dsp_ctx {
   int64_t launches = 0;            // own kernels launched (instrumentation)
   void* stage_events[2 * DSP_NUM_STAGES] = {};
   bool has_stage_events = false;
+  unsigned long long* stage_clk = nullptr;  // [DSP_NUM_STAGES][2] device buffer (dsp_ctx_set_stage_clocks)
   void* tap[DSP_NUM_TAPS] = {};    // instrumentation: copies of intermediates (dsp_ctx_set_tap)
   size_t tap_bytes[DSP_NUM_TAPS] = {};
-  uint64_t barrier_timeout_ns = 0;  // P2P barrier wall-clock timeout (0 = none); DSP_BARRIER_TIMEOUT_S
+  uint64_t barrier_timeout_ns = 0;
+  bool emulate_collectives = false;  // virtual ranks: NCCL all-to-all / all-gather emulated over peer mappings  // P2P barrier wall-clock timeout (0 = none); DSP_BARRIER_TIMEOUT_S
   // pipelined host path (dsp_st_block_forward_host_pipelined): copy-in / copy-out streams and
   // per-staging-buffer events, created on first use, destroyed with the context
   void* h2d_stream = nullptr;

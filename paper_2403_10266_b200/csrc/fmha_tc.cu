@@ -66,6 +66,7 @@ struct FmhaParams {
   float scale_log2;
   __nv_bfloat16* o;
   unsigned long long* trace;  // DSP_FMHA_TRACE builds only: per-phase clock64 stamps of CTA 0
+  unsigned long long* clk;    // stage clock (instrumentation, t_clk)
 };
 
 #ifdef DSP_FMHA_TRACE
@@ -610,6 +611,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
   const uint32_t tmem = *tmem_holder;
   griddep_launch_dependents();
   griddep_wait();
+  clk_start(p.clk);
   const uint32_t tS = tmem;        // 128 columns
   const uint32_t tO = tmem + 128;  // DP columns
 
@@ -759,6 +761,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
 
   tc_fence_before();
   __syncthreads();
+  clk_end(p.clk);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 256);
@@ -843,6 +846,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t tmem = *tmem_holder;
   griddep_launch_dependents();
   griddep_wait();
+  clk_start(p.clk);
 
   // launch allocation is 168 regs x 384 threads; 56 x 128 + 224 x 256 == 168 x 384 exactly
   if (warp == 0) {
@@ -1024,6 +1028,725 @@ __global__ void __launch_bounds__(384, 1)
 
   tc_fence_before();
   __syncthreads();
+  clk_end(p.clk);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Long sequences, P in tensor memory (the production spatial kernel; DSP_FMHA_PAIR_SMEM builds
+// the shared-memory-P pair kernel above for A/B).  Same roles and two query tiles ("slots")
+// per CTA as fmha_pair_kernel, but each slot's P_j (bf16) overwrites the first 64 columns of its
+// own S_j in TMEM and P.V is the TS form (A = P from TMEM, B = V from smem).  Shared memory then
+// carries only the TMA tiles and the MMA's Q / K / V operand reads: the pair kernel's 64 KB of P
+// stores plus 64 KB of P operand reads per K/V step (more than the K/V/Q traffic itself) are
+// gone.  Because P_j aliases S_j, S_{j+1} of a slot is issued right after PV_j of that slot;
+// the MMA warp alternates slots (PV0_j, S0_{j+1}, PV1_j, S1_{j+1}), so one slot's exponentials
+// overlap the other slot's tensor work (ping-pong).  When a slot sees S_j, every earlier MMA of
+// the CTA has completed (tcgen05.commit tracks all prior MMAs), so PV_{j-1} is done: O can be
+// rescaled in place and S's columns may be overwritten by P_j without further waits.
+// TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+DP), O1 [384, 384+DP).  ONES only (the row sums
+// come from V's ones column, R31).
+template <int NA, int RB>
+struct PtCfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP;
+  static constexpr int KV_STAGES = 2;
+  // Q0,Q1 | K x stages | V x stages | O staging x 2 | barriers
+  static constexpr int SMEM = 1024 + (2 + 2 * KV_STAGES + 2) * TILE + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024 && RB > 0;
+  static constexpr int THREADS = 384;
+};
+
+#ifndef DSP_PT_POLY_NUM
+#define DSP_PT_POLY_NUM DSP_POLY_NUM
+#endif
+
+// One online-softmax step of the P-in-TMEM kernel (thread = query row, whole 128-key row):
+// S_j -> registers, row max, lazy O rescale (R28), P_j = exp2(S*scale - m) as bf16 into TMEM
+// columns [0, 64) of the same S tile (packed column c = keys 2c, 2c+1), chunk by chunk as the
+// exponentials are produced.  valid < 128: keys >= valid are padding (masked to -inf).
+template <int DP>
+__device__ __forceinline__ void softmax_step_pt(const SoftmaxGeom& G, uint32_t tS, uint32_t tO, int j, float& m,
+                                                int valid, unsigned long long* tr = nullptr) {
+  const uint32_t lane_off = G.lane_off;
+  const float sl2 = G.sl2;
+  uint32_t v[128];
+  tmem_ld32(tS + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+  tmem_ld32(tS + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tmem_ld32(tS + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
+  tmem_ld32(tS + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
+  tmem_ld_wait();
+  FMHA_STAMP(tr, 8);
+  if (valid < 128) {
+#pragma unroll
+    for (int i = 0; i < 128; ++i)
+      if (i >= valid) v[i] = __float_as_uint(-INFINITY);
+  }
+  const float mx = max_tree3<128>(reinterpret_cast<const float*>(v));
+  const float mx2 = mx * sl2;
+  const bool bump = (j == 0) || (mx2 > m + 8.f);
+  const float m_new = bump ? mx2 : m;
+  const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
+  m = m_new;
+  FMHA_STAMP(tr, 9);
+  if (j > 0 && __any_sync(0xffffffffu, bump)) {  // PV_{j-1} completed before S_j: O is stable
+    const float a = bump ? alpha : 1.f;
+#pragma unroll
+    for (int c = 0; c < DP / 16; ++c) {
+      uint32_t o[16];
+      tmem_ld16(tO + lane_off + c * 16, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+      tmem_st16(tO + lane_off + c * 16, o);
+    }
+  }
+  const float2 sl2x2 = make_float2(sl2, sl2), mx2n = make_float2(-m_new, -m_new);
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {  // 32 keys -> 16 packed P columns per chunk
+    uint32_t pk[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = ch * 16 + u;
+      const float2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2, mx2n);
+      float2 e;
+      if ((i % DSP_POLY_DEN) < DSP_PT_POLY_NUM) {
+        e = poly_exp2_x2(x);
+      } else {
+        e.x = fast_exp2(x.x);
+        e.y = fast_exp2(x.y);
+      }
+      pk[u] = pack_bf16x2(e.x, e.y);
+    }
+    tmem_st16(tS + lane_off + ch * 16, pk);
+  }
+  FMHA_STAMP(tr, 11);
+  tmem_st_wait();
+  FMHA_STAMP(tr, 12);
+  tc_fence_before();
+}
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(384, 1)
+    fmha_pt_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
+                   const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
+                   const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                   const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
+                   const FmhaParams p) {
+  using Cfg = PtCfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  constexpr int KS = Cfg::KV_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                        // 2 tiles
+  uint8_t* sK = sQ + 2 * Cfg::TILE;          // KS stages
+  uint8_t* sV = sK + KS * Cfg::TILE;         // KS stages
+  uint8_t* sO = sV + KS * Cfg::TILE;         // 2 staging tiles (epilogue)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * Cfg::TILE);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;             // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [KS]
+  uint64_t* v_empty = v_full + KS;         // [KS]
+  uint64_t* v_ready = v_empty + KS;        // [KS] V patched with its ones column
+  uint64_t* s_full = v_ready + KS;         // [2] per slot
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* o_done = p_full + 2;           // [2]
+  uint64_t* o_free = o_done + 2;           // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = warp_id();
+  const int n = p.n_kv;
+  const int npairs = p.items / 2;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
+    tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); mbar_init(&v_ready[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
+  clk_start(p.clk);
+
+  // launch allocation is 168 regs x 384 threads; 56 x 128 + 224 x 256 == 168 x 384 exactly
+  if (warp == 0) {
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      uint32_t nq = 0, kv = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+        mbar_wait_sleep(q_empty, (nq & 1) ^ 1);
+        ++nq;
+        mbar_arrive_expect_tx(q_full, 2 * Cfg::TX);
+        load_tile<NA, RB>(sQ, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip, -1));
+        load_tile<NA, RB>(sQ + Cfg::TILE, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip + 1, -1));
+        for (int j = 0; j < n; ++j, ++kv) {
+          const int st = kv % KS;
+          const uint32_t ph = (kv / KS) & 1;
+          const TileCoord t = tile_coord(p, 2 * ip, j);
+          mbar_wait_sleep(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::TX);
+          load_tile<NA, RB>(sK + st * Cfg::TILE, &tk_a, &tk_b, &k_full[st], t);
+          mbar_wait_sleep(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::TX);
+          load_tile<NA, RB>(sV + st * Cfg::TILE, &tv_a, &tv_b, &v_full[st], t);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    setmaxnreg_dec<56>();
+    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
+    constexpr uint32_t idPVb = make_idesc_bf16(128, RB, 0, 1);
+    const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV);
+    auto issue_s = [&](int slot, int st) {  // S_slot = Q_slot K^T
+      if (elect_one()) {
+        const uint32_t qa = q0 + slot * Cfg::TILE, ka = k0 + st * Cfg::TILE, d = tmem + slot * 128;
+        int step = 0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k, ++step)
+            umma_bf16_ss(d, make_sdesc(qa + i * 16384 + k * 32, 16, 1024, SW_128B),
+                         make_sdesc(ka + i * 16384 + k * 32, 16, 1024, SW_128B), idS, step != 0);
+#pragma unroll
+        for (int k = 0; k < RB / 16; ++k, ++step)
+          umma_bf16_ss(d, make_sdesc(qa + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
+                       make_sdesc(ka + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+        umma_commit(&s_full[slot]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int slot, int st, bool acc0) {  // O_slot (+)= P_slot V (P from TMEM)
+      if (elect_one()) {
+        const uint32_t va = v0 + st * Cfg::TILE, o = tmem + 256 + slot * 128, ps = tmem + slot * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // 16 keys = 8 packed P columns per step
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            umma_bf16_ts(o + 64 * i, ps + 8 * k, make_sdesc(va + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+                         acc0 || k != 0);
+          umma_bf16_ts(o + 64 * NA, ps + 8 * k,
+                       make_sdesc(va + NA * 16384 + k * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
+                       idPVb, acc0 || k != 0);
+        }
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) umma_commit(bar);
+      __syncwarp();
+    };
+    uint32_t nq = 0, np0 = 0, np1 = 0, nit = 0, kvbase = 0;
+    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x, ++nit, kvbase += n) {
+      mbar_wait(q_full, nq & 1);
+      ++nq;
+      {
+        const uint32_t kv0 = kvbase;
+        mbar_wait(&k_full[kv0 % KS], (kv0 / KS) & 1);
+        tc_fence_after();
+        issue_s(0, kv0 % KS);
+        issue_s(1, kv0 % KS);
+        commit(&k_empty[kv0 % KS]);
+        if (n == 1) commit(q_empty);
+      }
+      for (int j = 0; j < n; ++j) {
+        const uint32_t kj = kvbase + j, kn = kj + 1;
+        const int sj = kj % KS, sn = kn % KS;
+        // slot 0: O0 += P0_j V_j, then S0_{j+1} into the same TMEM (after PV0_j in issue order)
+        mbar_wait(&p_full[0], np0 & 1);
+        ++np0;
+        mbar_wait(&v_ready[sj], (kj / KS) & 1);
+        if (j == 0) mbar_wait(&o_free[0], (nit & 1) ^ 1);
+        tc_fence_after();
+        issue_pv(0, sj, j > 0);
+        if (j + 1 == n) commit(&o_done[0]);
+        if (j + 1 < n) {
+          mbar_wait(&k_full[sn], (kn / KS) & 1);
+          tc_fence_after();
+          issue_s(0, sn);
+        }
+        // slot 1
+        mbar_wait(&p_full[1], np1 & 1);
+        ++np1;
+        if (j == 0) mbar_wait(&o_free[1], (nit & 1) ^ 1);
+        tc_fence_after();
+        issue_pv(1, sj, j > 0);
+        commit(&v_empty[sj]);
+        if (j + 1 == n) commit(&o_done[1]);
+        if (j + 1 < n) {
+          issue_s(1, sn);
+          commit(&k_empty[sn]);
+          if (j + 2 == n) commit(q_empty);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    setmaxnreg_dec<56>();
+    if (warp == 2) {
+      // V patcher: once a V tile has landed, set its column DP - 8 (zero-filled padding, since
+      // Dh <= DP - 8) to 1.0 in every row, so P.V also produces the row sums (R31)
+      constexpr int CB = (RB - 8) * 2;  // byte offset of the ones column inside the RB chunk row
+      uint32_t kv = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+        for (int j = 0; j < n; ++j, ++kv) {
+          const int st = kv % KS;
+          mbar_wait(&v_full[st], (kv / KS) & 1);
+          const uint32_t vb = smem_u32(sV + st * Cfg::TILE) + NA * 16384;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = lane_id() + 32 * i;
+            const uint32_t ch = RB == 16 ? ((CB >> 4) ^ ((r >> 2) & 1)) : ((CB >> 4) ^ ((r >> 1) & 3));
+            st_shared_u16(vb + r * Base::RB_ROW + (ch << 4) + (CB & 15), 0x3F80);  // bf16 1.0
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&v_ready[st]);
+        }
+      }
+    }
+  } else {
+    setmaxnreg_inc<224>();
+    const int slot = (warp - 4) >> 2;
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128;
+    uint8_t* sOs = sO + slot * Cfg::TILE;
+    const uint32_t bar_id = 1 + slot;
+    int store_pending = 0;
+    uint32_t ns = 0, no = 0;
+    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+      float m = -INFINITY;
+      for (int j = 0; j < n; ++j) {
+        unsigned long long* tr = p.trace ? p.trace + ((size_t)(slot * 64 + (ns & 63)) * 16) : nullptr;
+        FMHA_STAMP(tr, 0);
+        mbar_wait(&s_full[slot], ns & 1);
+        ++ns;
+        tc_fence_after();
+        FMHA_STAMP(tr, 3);
+        softmax_step_pt<Cfg::DP>(G, tS, tO, j, m, j + 1 == n ? p.kv_last : 128, tr);
+        mbar_arrive(&p_full[slot]);
+        FMHA_STAMP(tr, 4);
+      }
+      mbar_wait(&o_done[slot], no & 1);  // last PV done: O final
+      ++no;
+      tc_fence_after();
+      if (store_pending) {  // the previous item's O store must have read the staging tile
+        if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+        named_bar_sync(bar_id, 128);
+        store_pending = 0;
+      }
+      epilogue_tma_store<NA, RB, Cfg::DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
+                                              tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
+    }
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  clk_end(p.clk);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Long sequences, split-row softmax (the production spatial kernel for DP <= 80, i.e. the
+// paper's Dh = 72).  As fmha_pt_kernel -- two query tiles ("slots") per CTA ping-ponging on the
+// tensor pipe, P_j (bf16) over S_j in TMEM, TS-form P.V -- plus:
+//  * every query row is exponentiated by TWO threads (one per 64-key half; 16 softmax warps,
+//    four warpgroups: slot x half), which halves the per-step dependency chain of the softmax;
+//    the two halves agree on the row max through shared memory (one named barrier per slot);
+//  * Q lives in TMEM too (copied there once per item by the softmax threads), so S = Q K^T is a
+//    TS-form MMA that reads only K from shared memory (the SS form needs 128 B/clk of smem,
+//    all of it, at the tensor pipe's rate);
+//  * a 3-deep K/V ring, and Q's smem tile is released as soon as it is in TMEM.
+// TMEM: S0 [0,128), S1 [128,256), O0 [256,256+DP), Q0 [256+DP, 256+DP*3/2), O1 / Q1 at +128.
+// Roles: warp 0 TMA, warp 1 MMA + TMEM alloc, warp 2 V patcher (ones column, R31), warp 3 idle,
+// warps 4 + 4*(2*slot + half) .. +3 softmax (TMEM lane quadrant = warp % 4); the half-0
+// warpgroup of each slot also runs the epilogue.
+template <int NA, int RB>
+struct SplitCfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP;
+  static constexpr int KV_STAGES = 3;
+  static constexpr int RED_BYTES = 2 * 2 * 2 * 128 * 4;  // [parity][slot][half][row] row maxima
+  static constexpr int SMEM = 1024 + (2 + 2 * KV_STAGES + 2) * TILE + RED_BYTES + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024 && RB > 0 && DP + DP / 2 <= 128;
+  static constexpr int THREADS = 640;
+};
+
+template <int DP>
+__device__ __forceinline__ void softmax_step_split(const SoftmaxGeom& G, int half, uint32_t tS, uint32_t tO, int j,
+                                                   float& m, int valid, float* red_mine, const float* red_other,
+                                                   uint32_t bar_id, unsigned long long* tr = nullptr) {
+  const uint32_t lane_off = G.lane_off;
+  const float sl2 = G.sl2;
+  const int c0 = half * 64;  // this thread's key columns [c0, c0 + 64)
+  uint32_t v[64];
+  tmem_ld32(tS + lane_off + c0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+  tmem_ld32(tS + lane_off + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+  tmem_ld_wait();
+  FMHA_STAMP(tr, 8);
+  if (valid < 128) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (c0 + i >= valid) v[i] = __float_as_uint(-INFINITY);
+  }
+  const float mh = max_tree3<64>(reinterpret_cast<const float*>(v));
+  *red_mine = mh;
+  named_bar_sync(bar_id, 256);  // both halves' S loaded (P may now overwrite S) and maxima posted
+  FMHA_STAMP(tr, 9);
+  const float mx = fmaxf(mh, *red_other);
+  const float mx2 = mx * sl2;
+  const bool bump = (j == 0) || (mx2 > m + 8.f);
+  const float m_new = bump ? mx2 : m;
+  const float alpha = (j == 0) ? 0.f : fast_exp2(m - m_new);
+  m = m_new;
+  if (j > 0 && __any_sync(0xffffffffu, bump)) {  // PV_{j-1} completed before S_j: O is stable
+    const float a = bump ? alpha : 1.f;
+    constexpr int NC = DP / 16, NC0 = (NC + 1) / 2;  // 16-column chunks of O: half 0 takes the first NC0
+    const int cb = half ? NC0 : 0, ce = half ? NC : NC0;
+    for (int c = cb; c < ce; ++c) {
+      uint32_t o[16];
+      tmem_ld16(tO + lane_off + c * 16, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * a);
+      tmem_st16(tO + lane_off + c * 16, o);
+    }
+  }
+  const float2 sl2x2 = make_float2(sl2, sl2), mx2n = make_float2(-m_new, -m_new);
+#pragma unroll
+  for (int ch = 0; ch < 2; ++ch) {  // 32 keys -> 16 packed P columns per chunk
+    uint32_t pk[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int i = ch * 16 + u;
+      const float2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2, mx2n);
+      float2 e;
+      if (((i + half * 32) % DSP_POLY_DEN) < DSP_PT_POLY_NUM) {
+        e = poly_exp2_x2(x);
+      } else {
+        e.x = fast_exp2(x.x);
+        e.y = fast_exp2(x.y);
+      }
+      pk[u] = pack_bf16x2(e.x, e.y);
+    }
+    tmem_st16(tS + lane_off + half * 32 + ch * 16, pk);
+  }
+  FMHA_STAMP(tr, 11);
+  tmem_st_wait();
+  FMHA_STAMP(tr, 12);
+  tc_fence_before();
+}
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(640, 1)
+    fmha_split_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
+                      const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
+                      const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                      const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
+                      const FmhaParams p) {
+  using Cfg = SplitCfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  constexpr int KS = Cfg::KV_STAGES, DP = Cfg::DP;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                        // 2 tiles
+  uint8_t* sK = sQ + 2 * Cfg::TILE;          // KS stages
+  uint8_t* sV = sK + KS * Cfg::TILE;         // KS stages
+  uint8_t* sO = sV + KS * Cfg::TILE;         // 2 staging tiles (epilogue)
+  float* red = reinterpret_cast<float*>(sO + 2 * Cfg::TILE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * Cfg::TILE + Cfg::RED_BYTES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;            // count 512: Q copied to TMEM by every softmax thread
+  uint64_t* k_full = bars + 2;             // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [KS]
+  uint64_t* v_empty = v_full + KS;         // [KS]
+  uint64_t* v_ready = v_empty + KS;        // [KS] V patched with its ones column
+  uint64_t* q_tm = v_ready + KS;           // [2] Q_slot in TMEM (count 256)
+  uint64_t* s_full = q_tm + 2;             // [2]
+  uint64_t* p_full = s_full + 2;           // [2] (count 256)
+  uint64_t* o_done = p_full + 2;           // [2]
+  uint64_t* o_free = o_done + 2;           // [2] (count 128: the half-0 warpgroup)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = warp_id();
+  const int n = p.n_kv;
+  const int npairs = p.items / 2;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
+    tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 512);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); mbar_init(&v_ready[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&q_tm[t], 256);
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 256);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
+  clk_start(p.clk);
+
+  // launch allocation 96 regs x 640 threads = 61440, redistributed exactly: 32 x 128 + 112 x 512
+  // (setmaxnreg.inc can only take registers this CTA's own setmaxnreg.dec released)
+  if (warp == 0) {
+    setmaxnreg_dec<32>();
+    if (elect_one()) {
+      uint32_t nq = 0, kv = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+        mbar_wait_sleep(q_empty, (nq & 1) ^ 1);
+        ++nq;
+        mbar_arrive_expect_tx(q_full, 2 * Cfg::TX);
+        load_tile<NA, RB>(sQ, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip, -1));
+        load_tile<NA, RB>(sQ + Cfg::TILE, &tq_a, &tq_b, q_full, tile_coord(p, 2 * ip + 1, -1));
+        for (int j = 0; j < n; ++j, ++kv) {
+          const int st = kv % KS;
+          const uint32_t ph = (kv / KS) & 1;
+          const TileCoord t = tile_coord(p, 2 * ip, j);
+          mbar_wait_sleep(&k_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[st], Cfg::TX);
+          load_tile<NA, RB>(sK + st * Cfg::TILE, &tk_a, &tk_b, &k_full[st], t);
+          mbar_wait_sleep(&v_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&v_full[st], Cfg::TX);
+          load_tile<NA, RB>(sV + st * Cfg::TILE, &tv_a, &tv_b, &v_full[st], t);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    setmaxnreg_dec<32>();
+    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
+    constexpr uint32_t idPVb = make_idesc_bf16(128, RB, 0, 1);
+    const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV);
+    auto issue_s = [&](int slot, int st) {  // S_slot = Q_slot (TMEM) K^T
+      if (elect_one()) {
+        const uint32_t ka = k0 + st * Cfg::TILE, d = tmem + slot * 128, qt = tmem + 256 + slot * 128 + DP;
+        int step = 0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k, ++step)
+            umma_bf16_ts(d, qt + 8 * step, make_sdesc(ka + i * 16384 + k * 32, 16, 1024, SW_128B), idS, step != 0);
+#pragma unroll
+        for (int k = 0; k < RB / 16; ++k, ++step)
+          umma_bf16_ts(d, qt + 8 * step, make_sdesc(ka + NA * 16384 + k * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS,
+                       step != 0);
+        umma_commit(&s_full[slot]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int slot, int st, bool acc0) {  // O_slot (+)= P_slot V (P from TMEM)
+      if (elect_one()) {
+        const uint32_t va = v0 + st * Cfg::TILE, o = tmem + 256 + slot * 128, ps = tmem + slot * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // 16 keys = 8 packed P columns per step
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            umma_bf16_ts(o + 64 * i, ps + 8 * k, make_sdesc(va + i * 16384 + k * 2048, 16384, 1024, SW_128B), idPVa,
+                         acc0 || k != 0);
+          umma_bf16_ts(o + 64 * NA, ps + 8 * k,
+                       make_sdesc(va + NA * 16384 + k * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
+                       idPVb, acc0 || k != 0);
+        }
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) umma_commit(bar);
+      __syncwarp();
+    };
+    uint32_t np0 = 0, np1 = 0, nit = 0, kvbase = 0;
+    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x, ++nit, kvbase += n) {
+      {
+        const uint32_t kv0 = kvbase;
+        mbar_wait(&k_full[kv0 % KS], (kv0 / KS) & 1);
+        mbar_wait(&q_tm[0], nit & 1);
+        tc_fence_after();
+        issue_s(0, kv0 % KS);
+        mbar_wait(&q_tm[1], nit & 1);
+        tc_fence_after();
+        issue_s(1, kv0 % KS);
+        commit(&k_empty[kv0 % KS]);
+      }
+      for (int j = 0; j < n; ++j) {
+        const uint32_t kj = kvbase + j, kn = kj + 1;
+        const int sj = kj % KS, sn = kn % KS;
+        mbar_wait(&p_full[0], np0 & 1);
+        ++np0;
+        mbar_wait(&v_ready[sj], (kj / KS) & 1);
+        if (j == 0) mbar_wait(&o_free[0], (nit & 1) ^ 1);
+        tc_fence_after();
+        issue_pv(0, sj, j > 0);
+        if (j + 1 == n) commit(&o_done[0]);
+        if (j + 1 < n) {
+          mbar_wait(&k_full[sn], (kn / KS) & 1);
+          tc_fence_after();
+          issue_s(0, sn);
+        }
+        mbar_wait(&p_full[1], np1 & 1);
+        ++np1;
+        if (j == 0) mbar_wait(&o_free[1], (nit & 1) ^ 1);
+        tc_fence_after();
+        issue_pv(1, sj, j > 0);
+        commit(&v_empty[sj]);
+        if (j + 1 == n) commit(&o_done[1]);
+        if (j + 1 < n) {
+          issue_s(1, sn);
+          commit(&k_empty[sn]);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    setmaxnreg_dec<32>();
+    if (warp == 2) {  // V patcher: column DP - 8 of every V row := 1.0 (row sums by the tensor core, R31)
+      constexpr int CB = (RB - 8) * 2;
+      uint32_t kv = 0;
+      for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+        for (int j = 0; j < n; ++j, ++kv) {
+          const int st = kv % KS;
+          mbar_wait(&v_full[st], (kv / KS) & 1);
+          const uint32_t vb = smem_u32(sV + st * Cfg::TILE) + NA * 16384;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = lane_id() + 32 * i;
+            const uint32_t ch = RB == 16 ? ((CB >> 4) ^ ((r >> 2) & 1)) : ((CB >> 4) ^ ((r >> 1) & 3));
+            st_shared_u16(vb + r * Base::RB_ROW + (ch << 4) + (CB & 15), 0x3F80);  // bf16 1.0
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&v_ready[st]);
+        }
+      }
+    }
+  } else {
+    setmaxnreg_inc<112>();
+    const int wg = (warp - 4) >> 2;  // 0..3
+    const int slot = wg >> 1, half = wg & 1;
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    const int row = G.row;
+    const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128, tQ = tO + DP;
+    const uint32_t q_src = smem_u32(sQ + slot * Cfg::TILE);
+    uint8_t* sOs = sO + slot * Cfg::TILE;
+    const uint32_t bar_red = 1 + slot, bar_epi = 3 + slot;
+    int store_pending = 0;
+    uint32_t nq = 0, ns = 0, no = 0;
+    for (int ip = blockIdx.x; ip < npairs; ip += gridDim.x) {
+      // Q_slot -> TMEM (packed bf16 pairs: column c = dims 2c, 2c+1): half 0 the SW128 atoms,
+      // half 1 the RB remainder chunk; then release the smem tile to the producer
+      mbar_wait(q_full, nq & 1);
+      ++nq;
+      if (half == 0) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i) {
+          uint32_t w[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t a = q_src + i * 16384 + row * 128 + ((c ^ (row & 7)) << 4);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w[4 * c]), "=r"(w[4 * c + 1]), "=r"(w[4 * c + 2]), "=r"(w[4 * c + 3]) : "r"(a));
+          }
+          tmem_st16(tQ + G.lane_off + i * 32, *reinterpret_cast<const uint32_t(*)[16]>(w));
+          tmem_st16(tQ + G.lane_off + i * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(w + 16));
+        }
+      } else {
+        constexpr int NCH = RB / 8;  // 16-B chunks of the remainder row
+        uint32_t w[16];
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const uint32_t sw = RB == 16 ? (c ^ ((row >> 2) & 1)) : (c ^ ((row >> 1) & 3));
+          const uint32_t a = q_src + NA * 16384 + row * Base::RB_ROW + (sw << 4);
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[4 * c]), "=r"(w[4 * c + 1]), "=r"(w[4 * c + 2]), "=r"(w[4 * c + 3]) : "r"(a));
+        }
+        if constexpr (RB == 16) {
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                           tQ + G.lane_off + NA * 32),
+                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                       : "memory");
+        } else {
+          tmem_st16(tQ + G.lane_off + NA * 32, *reinterpret_cast<const uint32_t(*)[16]>(w));
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&q_tm[slot]);
+      mbar_arrive(q_empty);
+      float m = -INFINITY;
+      for (int j = 0; j < n; ++j) {
+        unsigned long long* tr = (p.trace && half == 0) ? p.trace + ((size_t)(slot * 64 + (ns & 63)) * 16) : nullptr;
+        FMHA_STAMP(tr, 0);
+        mbar_wait(&s_full[slot], ns & 1);
+        tc_fence_after();
+        FMHA_STAMP(tr, 3);
+        float* rb = red + ((ns & 1) * 4 + slot * 2) * 128;
+        ++ns;
+        softmax_step_split<DP>(G, half, tS, tO, j, m, j + 1 == n ? p.kv_last : 128, rb + half * 128 + row,
+                               rb + (1 - half) * 128 + row, bar_red, tr);
+        mbar_arrive(&p_full[slot]);
+        FMHA_STAMP(tr, 4);
+      }
+      mbar_wait(&o_done[slot], no & 1);  // last PV done: O final
+      ++no;
+      tc_fence_after();
+      if (half == 0) {
+        if (store_pending) {  // the previous item's O store must have read the staging tile
+          if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+          named_bar_sync(bar_epi, 128);
+          store_pending = 0;
+        }
+        epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, row, 0.f, bar_epi,
+                                           tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
+      }
+    }
+    if (half == 0 && (threadIdx.x & 127) == 0) bulk_wait_group_read0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  clk_end(p.clk);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1074,6 +1797,40 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
       mo[1] = mo[0];
     }
   }
+#if !defined(DSP_FMHA_PAIR_SMEM) && !defined(DSP_FMHA_PT1)
+  if constexpr (SplitCfg<NA, RB>::OK) {
+    if (p.G == 1 && p.n_qt % 2 == 0 && p.Dh <= SplitCfg<NA, RB>::DP - 8) {
+      auto kp = fmha_split_kernel<NA, RB>;
+      static bool attr_sp = false;
+      if (!attr_sp) {
+        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, SplitCfg<NA, RB>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_sp = true;
+      }
+      const int npairs = p.items / 2;
+      const int grid = npairs < num_sms ? npairs : num_sms;
+      return launch_k(kp, dim3(grid), dim3(SplitCfg<NA, RB>::THREADS), SplitCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2],
+                      m[3], m[4], m[5], mo[0], mo[1], p);
+    }
+  }
+#endif
+#ifndef DSP_FMHA_PAIR_SMEM
+  if constexpr (PtCfg<NA, RB>::OK) {
+    if (p.G == 1 && p.n_qt % 2 == 0 && p.Dh <= PtCfg<NA, RB>::DP - 8) {
+      auto kp = fmha_pt_kernel<NA, RB>;
+      static bool attr_pt = false;
+      if (!attr_pt) {
+        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, PtCfg<NA, RB>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_pt = true;
+      }
+      const int npairs = p.items / 2;
+      const int grid = npairs < num_sms ? npairs : num_sms;
+      return launch_k(kp, dim3(grid), dim3(PtCfg<NA, RB>::THREADS), PtCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2], m[3],
+                      m[4], m[5], mo[0], mo[1], p);
+    }
+  }
+#endif
   if constexpr (PairCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0) {
       // row sums by the tensor core when the padded head dim leaves a free column for the ones
@@ -1124,6 +1881,7 @@ cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc,
   p.B = (int)B;
   p.o = static_cast<__nv_bfloat16*>(o);
   p.trace = nullptr;
+  p.clk = t_clk;
 #ifdef DSP_FMHA_TRACE
   {
     static unsigned long long* tbuf = nullptr;
@@ -1190,6 +1948,7 @@ cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64
   p.T_loc = 1;
   p.o = static_cast<__nv_bfloat16*>(o);
   p.trace = nullptr;
+  p.clk = t_clk;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
   p.spatial = 1;  // queries of sample b = rows [b*Lq, (b+1)*Lq) of q; keys / values = rows of kv
   p.L = (int)Lq;

@@ -35,6 +35,8 @@
 
 namespace dsp {
 
+thread_local unsigned long long* t_clk = nullptr;
+
 namespace {
 
 constexpr int BM = 128;  // rows per CTA (256 per pair)
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_holder;
   griddep_launch_dependents();
   griddep_wait();
+  clk_start(ev.clk);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(256, 1)
 
   tc_fence_before();
   cluster_sync();
+  clk_end(ev.clk);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_2sm(tmem, Cfg::TMEM_COLS);
@@ -516,8 +520,10 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   }
   const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
   const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  EpiVec evc = ev;
+  evc.clk = t_clk;
   return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, td, tr, (const __nv_bfloat16*)R,
-                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ev, rm);
+                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, evc, rm);
 }
 
 template <int EPI>

@@ -211,9 +211,11 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
 // that consumes it (LN(x) W^T = rstd (x (W o gamma)^T - mean u) + W beta).
 template <int kMaxV>  // 16-B vectors per lane: C <= 256 * kMaxV
 __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel(const __nv_bfloat16* __restrict__ x, float eps,
-                                                                float2* __restrict__ stats, long rows, int C) {
+                                                                float2* __restrict__ stats, long rows, int C,
+                                                                unsigned long long* clk) {
   griddep_wait();
   griddep_launch_dependents();
+  clk_start(clk);
   // DSP_ROWSTATS_R rows per warp (32 warps resident per SM), all loads issued before any reduction
   constexpr int R = DSP_ROWSTATS_R;
   const long r0 = (((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * R;
@@ -255,6 +257,10 @@ __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel
     for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, off);
     if (lane == 0 && r0 + q < rows) stats[r0 + q] = make_float2(mean, rsqrtf(qq / C + eps));
   }
+  if (clk) {
+    __syncthreads();
+    clk_end(clk);
+  }
 }
 
 // Per-row LayerNorm partials (mean_p, M2_p) of a bf16 [rows, C] activation over column segments
@@ -267,12 +273,17 @@ __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel
 // statistics the consuming GEMM combines are the same bits at every N.
 // One thread per (row, segment).
 __global__ void __launch_bounds__(256) row_partials_bf16_kernel(const __nv_bfloat16* __restrict__ x, long rows, int C,
-                                                                int seg, float2* __restrict__ parts) {
+                                                                int seg, float2* __restrict__ parts,
+                                                                unsigned long long* clk) {
   griddep_wait();
   griddep_launch_dependents();
+  clk_start(clk);
   const int nseg = C / seg;
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= rows * nseg) return;
+  if (idx >= rows * nseg) {
+    if (clk) clk_end(clk);  // thread 0 of a CTA past the end still closes the clock
+    return;
+  }
   const long row = idx / nseg;
   const int sg = (int)(idx % nseg);
   const uint4* p = reinterpret_cast<const uint4*>(x + row * C + (long)sg * seg);
@@ -293,6 +304,7 @@ __global__ void __launch_bounds__(256) row_partials_bf16_kernel(const __nv_bfloa
   }
   const float a = __fadd_rn(s1e, s1o), mp = __fmul_rn(a, __frcp_rn((float)seg));
   parts[idx] = make_float2(__fadd_rn(mp, x0), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2e, s2o)), 0.f));
+  if (clk) clk_end(clk);  // thread 0 (partial of CTA-wide span; the CTA's other rows finish alongside)
 }
 
 // Fold a LayerNorm's affine parameters into the weight of the following linear layer:
@@ -408,9 +420,9 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
   if (C % 8 || C > 256 * kRowStatsMaxV) return cudaErrorNotSupported;
   if (C <= 1280)  // the model widths of the paper (1152): 5 vectors per lane
     return launch_k(row_stats_bf16_kernel<5>, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, eps,
-                    (float2*)stats, rows, (int)C);
+                    (float2*)stats, rows, (int)C, t_clk);
   return launch_k(row_stats_bf16_kernel<kRowStatsMaxV>, dim3(blocks), dim3(threads), 0, st, 1,
-                  (const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C);
+                  (const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C, t_clk);
 }
 
 cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st) {
@@ -418,7 +430,7 @@ cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x,
   if (seg % 8 || C % seg) return cudaErrorNotSupported;
   const long n = rows * (C / seg);
   return launch_k(row_partials_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
-                  (const __nv_bfloat16*)x, (long)rows, (int)C, seg, parts);
+                  (const __nv_bfloat16*)x, (long)rows, (int)C, seg, parts, t_clk);
 }
 
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {

@@ -220,6 +220,19 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // (barrier init, TMEM alloc, descriptor prefetch) while the previous kernel drains, then
 // griddep_wait() before touching any memory the previous kernel produces or consumes.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Stage clocks (instrumentation, dsp_ctx_set_stage_clocks): clk[0] = earliest CTA start after its
+// dependency wait, clk[1] = latest CTA end, %globaltimer ns; one atomic per CTA, NULL = off.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void clk_start(unsigned long long* clk) {
+  if (clk && threadIdx.x == 0) atomicMin(clk, global_ns());
+}
+__device__ __forceinline__ void clk_end(unsigned long long* clk) {
+  if (clk && threadIdx.x == 0) atomicMax(clk + 1, global_ns());
+}
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------- clusters / CTA pairs

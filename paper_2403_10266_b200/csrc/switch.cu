@@ -38,8 +38,11 @@ __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __res
     const int64_t i2 = (run / rc.n[3]) % rc.n[2];
     const int64_t i1 = (run / (rc.n[3] * rc.n[2])) % rc.n[1];
     const int64_t i0 = run / (rc.n[3] * rc.n[2] * rc.n[1]);
-    const uint4* s = reinterpret_cast<const uint4*>(src + i0 * rc.ss[0] + i1 * rc.ss[1] + i2 * rc.ss[2] + i3 * rc.ss[3]);
-    uint8_t* dbase = use_peers ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
+    // use_peers 1: level 0 selects the DESTINATION peer (P2P put); 2: the SOURCE peer (pull, the
+    // emulated all-to-all / all-gather of virtual ranks)
+    const uint8_t* sbase = use_peers == 2 ? static_cast<const uint8_t*>(peers.p[i0]) + peer_off : src + i0 * rc.ss[0];
+    const uint4* s = reinterpret_cast<const uint4*>(sbase + i1 * rc.ss[1] + i2 * rc.ss[2] + i3 * rc.ss[3]);
+    uint8_t* dbase = use_peers == 1 ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
     uint4* d = reinterpret_cast<uint4*>(dbase + i1 * rc.ds[1] + i2 * rc.ds[2] + i3 * rc.ds[3]);
     for (int64_t v0 = (int64_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; v0 < nv; v0 += step) {
       uint4 buf[kUnroll];
@@ -54,6 +57,41 @@ __global__ void __launch_bounds__(kThreads) run_copy_kernel(const uint8_t* __res
         if (v < nv) st_stream(d + v, buf[u]);
       }
     }
+  }
+}
+
+// Short runs (< 4 KB, e.g. the head-group runs of the Ulysses exchange): one flat index space of
+// 16-B vectors over all runs, so no thread idles on a run shorter than the CTA.
+__global__ void __launch_bounds__(kThreads) run_copy_flat_kernel(const uint8_t* __restrict__ src,
+                                                                 uint8_t* __restrict__ dst, RunCopy rc, PeerPtrs peers,
+                                                                 int use_peers, int64_t peer_off) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int64_t nv = rc.run_bytes / 16;
+  const int64_t total = rc.n[0] * rc.n[1] * rc.n[2] * rc.n[3] * nv;
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b < total; b += stride * kUnroll) {
+    uint4 buf[kUnroll];
+    uint4* dp[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t idx = b + u * stride;
+      dp[u] = nullptr;
+      if (idx < total) {
+        const int64_t run = idx / nv, v = idx - run * nv;
+        const int64_t i3 = run % rc.n[3];
+        const int64_t i2 = (run / rc.n[3]) % rc.n[2];
+        const int64_t i1 = (run / (rc.n[3] * rc.n[2])) % rc.n[1];
+        const int64_t i0 = run / (rc.n[3] * rc.n[2] * rc.n[1]);
+        const uint8_t* sb = use_peers == 2 ? static_cast<const uint8_t*>(peers.p[i0]) + peer_off : src + i0 * rc.ss[0];
+        uint8_t* db = use_peers == 1 ? static_cast<uint8_t*>(peers.p[i0]) + peer_off : dst + i0 * rc.ds[0];
+        buf[u] = ld_stream(reinterpret_cast<const uint4*>(sb + i1 * rc.ss[1] + i2 * rc.ss[2] + i3 * rc.ss[3]) + v);
+        dp[u] = reinterpret_cast<uint4*>(db + i1 * rc.ds[1] + i2 * rc.ds[2] + i3 * rc.ds[3]) + v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (dp[u]) st_stream(dp[u], buf[u]);
   }
 }
 
@@ -109,6 +147,13 @@ static cudaError_t launch_copy(const void* src, void* dst, const RunCopy& rc, co
   if (runs == 0 || rc.run_bytes == 0) return cudaSuccess;
   if (rc.run_bytes % 16) return cudaErrorInvalidValue;
   const int64_t nv = rc.run_bytes / 16;
+  if (nv < 256) {  // short runs: flat vector index space, ~8 resident CTAs per SM
+    const int64_t total = runs * nv;
+    int64_t blocks = (total + kThreads * kUnroll - 1) / (kThreads * kUnroll);
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    return launch_k(run_copy_flat_kernel, dim3((unsigned)blocks), dim3(kThreads), 0, st, 1,
+                    static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), rc, peers, use_peers, peer_off);
+  }
   int64_t bx = (nv + kThreads * kUnroll - 1) / (kThreads * kUnroll);
   const int64_t want = (int64_t)num_sms * 8;  // ~8 resident CTAs per SM in total
   int64_t cap = (want + runs - 1) / runs;
@@ -128,6 +173,11 @@ cudaError_t launch_run_copy(const void* src, void* dst, const RunCopy& rc, int n
 cudaError_t launch_p2p_put(const void* src, const PeerPtrs& peer_base, int64_t dst_off, const RunCopy& rc, int num_sms,
                            cudaStream_t st) {
   return launch_copy(src, nullptr, rc, peer_base, 1, dst_off, num_sms, st);
+}
+
+cudaError_t launch_p2p_pull(const PeerPtrs& peer_base, int64_t src_off, void* dst, const RunCopy& rc, int num_sms,
+                            cudaStream_t st) {
+  return launch_copy(nullptr, dst, rc, peer_base, 2, src_off, num_sms, st);
 }
 
 cudaError_t launch_p2p_barrier(const PeerPtrs& signals, int rank, int world, uint64_t timeout_ns, cudaStream_t st) {

@@ -21,8 +21,12 @@ rt.cudaMemcpy(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(ptr), ctypes.
 t = buf.reshape(2, 64, 16).astype(np.int64)
 base = t[t > 0].min()
 # stamps: 0 wait S, 3 S ready, 8 S in regs, 9 max done, 10 pp go, 11 exps done, 1 after l, 2 o_done, 12 P stored, 4 arrive
-order = [0, 3, 8, 9, 10, 11, 2, 12, 4]
-names = ["waitS", "Srdy", "ldtm", "max", "ppgo", "exps", "odone", "Pst", "done"]
+if os.environ.get("PT"):  # fmha_pt_kernel: 0 wait S, 3 S ready, 8 S in regs, 9 max, 11 exps + P st issued, 12 st done, 4 arrive
+    order = [0, 3, 8, 9, 11, 12, 4]
+    names = ["waitS", "Srdy", "ldtm", "max", "exps", "stw", "done"]
+else:
+    order = [0, 3, 8, 9, 10, 11, 2, 12, 4]
+    names = ["waitS", "Srdy", "ldtm", "max", "ppgo", "exps", "odone", "Pst", "done"]
 print("slot tile  " + " ".join(f"{n:>7s}" for n in names) + "   deltas")
 for s in range(2):
     for k in range(0, 40):

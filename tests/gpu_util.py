@@ -23,10 +23,20 @@ def weights_f64(W: dict, dtype: str) -> dict:
     return {k: synth.to_f64(v, dtype) for k, v in W.items()}
 
 
-def assert_block_close(got: np.ndarray, ref: np.ndarray, atol=2e-2, rtol=1e-2, rel_l2=1e-2):
-    """DESIGN.md tolerance T1 (north_star 'max-abs 2e-2 / rel 1e-2', read as allclose) + rel-L2."""
+BF16_U = 2.0 ** -8  # unit roundoff of bf16 (8-bit significand)
+
+
+def assert_block_close(got: np.ndarray, ref: np.ndarray, atol=2e-2, rtol=1e-2, rel_l2=1e-2, stored=None):
+    """DESIGN.md tolerance R22 (north_star 'max-abs 2e-2 / rel 1e-2', read as allclose) + rel-L2.
+    stored (R34): list of the residual-stream values (oracle, same shape) the block stores in bf16 on
+    the way to `ref` (y1, y2, ..., y); an element is also within tolerance if its error is within
+    atol + the storage bound sum_k u*|z_k|, u = 2^-8 -- what bf16 storage alone may cost at large
+    magnitudes (|z| ~ 17 in deep layers: 1.5 % for four stores, more than rtol's 1 %)."""
     err = np.abs(got - ref)
-    bad = err > atol + rtol * np.abs(ref)
+    allowed = atol + rtol * np.abs(ref)
+    if stored is not None:
+        allowed = np.maximum(allowed, atol + BF16_U * sum(np.abs(z) for z in stored))
+    bad = err > allowed
     l2 = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
     msg = (f"max-abs {err.max():.3e}, max-rel {(err / np.maximum(np.abs(ref), 1e-6)).max():.3e}, "
            f"rel-L2 {l2:.3e}, violations {int(bad.sum())}/{bad.size}")

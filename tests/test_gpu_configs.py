@@ -390,6 +390,10 @@ def test_model28_prepared_cross_teacher_forced():
         xin, xout = to_f64(prefix(layer)), to_f64(prefix(layer + 1))
         Wf = weights_f64(host[layer], "bf16")
         Wc = dict(ln_w=Wf["ln_c_w"], ln_b=Wf["ln_c_b"], w_q=Wf["w_q_c"], w_kv=Wf["w_kv_c"], w_o=Wf["w_o_c"])
-        y1 = ob.spatial_stage(xin, Wf, sh.NH)
-        y2 = ob.cross_stage(ob.temporal_stage(y1[:, :, cols], Wf, sh.NH), c64, Wc, sh.NH)
-        print(f"layer {layer}:", assert_block_close(xout[:, :, cols], ob.mlp_stage(y2, Wf)))
+        y1 = ob.spatial_stage(xin, Wf, sh.NH)[:, :, cols]
+        y2 = ob.temporal_stage(y1, Wf, sh.NH)
+        y2c = ob.cross_stage(y2, c64, Wc, sh.NH)
+        y = ob.mlp_stage(y2c, Wf)
+        # R34: the layer stores y1, y2, y2' and y in bf16 (|y| ~ 17 by layer 13: ulp 0.125)
+        msg = assert_block_close(xout[:, :, cols], y, stored=[y1, y2, y2c, y])
+        print(f"layer {layer}: max |y| {np.abs(y).max():.2f}:", msg)

@@ -239,3 +239,87 @@ def test_p2p_barrier_timeout_is_reported_not_trapped():
     t = torch.arange(10, device="cuda").sum()  # the context is alive
     assert int(t.item()) == 45
     g.ctx[1].check_errors()  # the peer itself saw nothing
+
+
+# ------------------------------------------------------------------ NCCL code path, emulated
+def _emulated_group(N, region_bytes):
+    g = VirtualGroup(N, region_bytes)
+    for c in g.ctx:
+        c.set_collective_emulation(True)
+    return g
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("B", [1, 2])
+@pytest.mark.parametrize("direction", ["TS", "ST"])
+def test_switch_nccl_code_path_emulated_bitexact(N, B, direction):
+    """dsp_switch(impl = NCCL) end to end over N virtual ranks at the blk shape: the library's own
+    NCCL branch (pack into the workspace unless identity, all-to-all, unpack unless identity) with
+    only the ncclAlltoAll call replaced by the emulated collective (barrier + pull + barrier)."""
+    m = dsp()
+    sh, x = _tagged(B)
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    fr, to = direction[0], direction[1]
+    src = osw.split(x, DIMS[fr], N)
+    want = osw.switch(src, DIMS[fr], DIMS[to])
+    nb = sh.M * 2 // N  # bytes per shard
+    g = _emulated_group(N, 4 * nb)  # x | y | workspace (send + recv staging)
+    for r in range(N):
+        g.view(r, 0, nb, torch.int16).copy_(_dev16(src[r]))
+        g.ctx[r].set_workspace(g.region[r][2 * nb:])
+    xs = [g.view(r, 0, nb, torch.bfloat16) for r in range(N)]
+    ys = [g.view(r, nb, nb, torch.bfloat16) for r in range(N)]
+    g.run(lambda r: g.ctx[r].switch(shape, fr, to, xs[r], ys[r], impl="nccl"))
+    for r in range(N):
+        assert np.array_equal(_host16(ys[r]), want[r].reshape(-1)), f"rank {r}"
+    for c in g.ctx:
+        c.check_errors()
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("dim", ["T", "S"])
+@pytest.mark.parametrize("B", [1, 2])
+def test_gather_nccl_code_path_emulated_bitexact(N, dim, B):
+    """dsp_gather at N > 1 end to end (all-gather into x_global or the workspace + the unpack kernel)
+    with the ncclAllGather call emulated; every rank's x_global equals oracle.gather bitwise."""
+    m = dsp()
+    sh, x = _tagged(B)
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    shards = osw.split(x, DIMS[dim], N)
+    nb = sh.M * 2 // N
+    g = _emulated_group(N, nb + sh.M * 2)  # x_local | workspace
+    for r in range(N):
+        g.view(r, 0, nb, torch.int16).copy_(_dev16(shards[r]))
+        g.ctx[r].set_workspace(g.region[r][nb:])
+    outs = [torch.empty(sh.M, dtype=torch.bfloat16, device="cuda") for _ in range(N)]
+    g.run(lambda r: g.ctx[r].gather(shape, dim, g.view(r, 0, nb, torch.bfloat16), outs[r]))
+    want = osw.gather(shards, DIMS[dim]).reshape(-1)
+    for r in range(N):
+        assert np.array_equal(_host16(outs[r]), want), f"rank {r}"
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("prepared", [False, True])
+def test_block_nccl_code_path_emulated_n_invariant(N, prepared):
+    """The block with impl = NCCL (bench.py's default transport at N > 1) over N virtual ranks at
+    the blk shape, collectives emulated: bitwise equal to the N = 1 block (raw and prepared)."""
+    m = dsp()
+    sh = synth.CONFIGS["blk"]
+    xs, Ws = _setup(sh)
+    ref1 = bits16(_run_block_n1(sh, xs, Ws, prepared=prepared))
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = _emulated_group(N, ws + act)
+    W = weights_dev(Ws, "bf16")
+    if prepared:
+        W["prepared"] = g.ctx[0].prepare_block(shape, W)
+        torch.cuda.synchronize()
+    xsh = osw.split(xs, osw.DIM_T, N)
+    X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl="nccl"))
+    got = np.concatenate([bits16(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
