@@ -1162,10 +1162,9 @@ dsp_status_t dsp_st_block_forward_ulysses(dsp_ctx_t ctx, const dsp_shape_t* s, c
   for (int i = 0; i < 12; ++i)
     if (!wp[i] || !aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d NULL or not 16-B aligned", i);
   if (!aligned16(x) || !aligned16(y)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
-  {
-    const dsp_shape_t hs{1, 1, 1, s->C / N, s->num_heads / N, s->dtype};
-    DSP_TRY(check_bf16_attn(ctx, &hs, 128));
-  }
+  DSP_TRY(check_bf16_attn(ctx, s, 128));  // the projections run at the full width C
+  // the attention core runs on C/N channels (NH/N heads): only its head-dim limits apply
+  // (C/N need not be a GEMM tile multiple: C = 1152 at N = 8 gives 144)
   const bool fold = w->prepared != nullptr;
   const int64_t C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * 2;
   const UlyssesWs L = ulysses_ws(s, N);
