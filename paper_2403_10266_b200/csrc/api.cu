@@ -98,7 +98,7 @@ int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 //   [act, 5 act)      big: qkv [tok,3C] + o [tok,C] | MLP hidden [tok,4C] | switch send/recv
 //   [5 act, 6 act)    ys: S-sharded activation (N > 1)
 //   stats             [tok] float2 (mean, rstd) of a LayerNorm input (prepared path)
-//   parts             [tok, C / BN] float2 per-row partials from the out-projection epilogues
+//   parts             [tok, C / 64] float2 per-row partials from the out-projection epilogues
 struct BlockWs {
   int64_t act, h, big, ys, stats, parts, total;
 };
@@ -111,7 +111,7 @@ BlockWs block_ws(const dsp_shape_t* s, int world) {
   w.ys = 5 * w.act;
   w.stats = align256(6 * w.act);
   w.parts = w.stats + align256(tok * 8);
-  w.total = w.parts + align256(tok * (C / gemm_bn_for(C)) * 8) + 256;
+  w.total = w.parts + align256(tok * (C / gemm_part_cols(C)) * 8) + 256;
   return w;
 }
 
@@ -857,7 +857,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       return fail(ctx, DSP_ERR_UNSUPPORTED, "context longer than the local tokens per sample");
   }
   if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
-  if (w->prepared && (s->C % 8 || s->C > 256 * kRowStatsMaxV || s->C / gemm_bn_for(s->C) > kMaxParts))
+  if (w->prepared && (s->C % 8 || s->C > 256 * kRowStatsMaxV || s->C / gemm_part_cols(s->C) > kMaxParts))
     return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= %d and C / BN <= %d",
                 256 * kRowStatsMaxV, kMaxParts);
   const int N = ctx->world;
@@ -907,7 +907,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   const float* uv = fold ? reinterpret_cast<const float*>(prep + P.uv) : nullptr;
   float2* stats = reinterpret_cast<float2*>(ws + L.stats);
   float2* parts = reinterpret_cast<float2*>(ws + L.parts);
-  const int nparts = (int)(C / gemm_bn_for(C));
+  const int nparts = (int)(C / gemm_part_cols(C));
   EpiVec ev1{}, ev2{}, ev3{};
   // LN statistics from per-row partials are the same bits at every N: at N > 1 the rows reach
   // their consumer through a switch without their producer's partials, so launch_row_partials
@@ -1068,7 +1068,7 @@ static UlyssesWs ulysses_ws(const dsp_shape_t* s, int world) {
   w.recv = 10 * w.act;
   w.stats = align256(11 * w.act);
   w.parts = w.stats + align256(tok * 8);
-  w.total = w.parts + align256(tok * (C / gemm_bn_for(C)) * 8) + 256;
+  w.total = w.parts + align256(tok * (C / gemm_part_cols(C)) * 8) + 256;
   return w;
 }
 
@@ -1184,7 +1184,7 @@ dsp_status_t dsp_st_block_forward_ulysses(dsp_ctx_t ctx, const dsp_shape_t* s, c
   const float* uv = fold ? reinterpret_cast<const float*>(prep + P.uv) : nullptr;
   float2* stats = reinterpret_cast<float2*>(ws + L.stats);
   float2* parts = reinterpret_cast<float2*>(ws + L.parts);
-  const int nparts = (int)(C / gemm_bn_for(C));
+  const int nparts = (int)(C / gemm_part_cols(C));
   EpiVec ev1{}, ev2{}, ev3{};
   if (fold) {  // R30: as the DSP block at N = 1 (the rows never move, so every partial stays local)
     ev1.row_stats = stats; ev1.col_u = uv; ev1.col_v = uv + 3 * C;
@@ -1427,7 +1427,7 @@ dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   if (!w || !prep) return fail(ctx, DSP_ERR_NULL, "NULL argument");
   if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
   const int64_t C = s->C;
-  if (C % 8 || C > 256 * kRowStatsMaxV || C / gemm_bn_for(C) > kMaxParts)
+  if (C % 8 || C > 256 * kRowStatsMaxV || C / gemm_part_cols(C) > kMaxParts)
     return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= %d and C / BN <= %d (C=%lld)",
                 256 * kRowStatsMaxV, kMaxParts, (long long)C);
   const PrepLayout P = prep_layout(C);

@@ -105,7 +105,7 @@ cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R,
 // Epilogue vectors.  LN-folded GEMM (EPI_LN*): per-row statistics either as (mean, rstd) in
 // row_stats, or (row_stats == nullptr) combined in the epilogue from part_in: nparts_in
 // per-row partials (mean_p, M2_p) over part_cnt columns each, written by the residual
-// epilogue of the GEMM that produced the rows (part_out, one partial per BN-column tile).
+// epilogue of the GEMM that produced the rows (part_out, one partial per gemm_part_cols(N) columns).
 struct EpiVec {
   const float2* row_stats;  // [M] (mean, rstd)
   const float* col_u;       // [N]
@@ -113,13 +113,15 @@ struct EpiVec {
   const float2* part_in;    // [M, nparts_in] (mean_p, M2_p)
   int nparts_in, part_cnt;
   float eps;
-  float2* part_out;         // residual epilogue: [M, N / BN] partials of the stored (bf16) rows
+  float2* part_out;         // residual epilogue: [M, N / gemm_part_cols(N)] partials of the stored (bf16) rows
   unsigned long long* clk;  // stage clock (set by run_gemm from t_clk)
 };
 // BN (output-tile width) the GEMM dispatch picks for N output columns
 int gemm_bn_for(int64_t N);
-// most per-row LayerNorm partials (one per BN-column tile of the producing GEMM) an LN epilogue combines
-constexpr int kMaxParts = 12;
+// columns per LayerNorm partial the residual epilogue writes (one per BN-wide tile: 192 at C = 1152)
+int gemm_part_cols(int64_t N);
+// most per-row LayerNorm partials an LN-folded epilogue combines
+constexpr int kMaxParts = 24;
 constexpr int kRowStatsMaxV = 12;  // row statistics kernel: C <= 256 * 12 = 3072
 cudaError_t launch_gemm_bf16_res_stats(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
                                        int64_t K, float2* part_out, int num_sms, cudaStream_t st, std::string* why);

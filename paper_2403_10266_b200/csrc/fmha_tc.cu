@@ -1113,7 +1113,11 @@ __device__ __forceinline__ void softmax_step_pt(const SoftmaxGeom& G, uint32_t t
       const int i = ch * 16 + u;
       const float2 x = ffma2(make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])), sl2x2, mx2n);
       float2 e;
+#ifdef DSP_PT_SPREAD  // A/B: FMA-pipe pairs spread evenly through each group of DEN
+      if ((((i % DSP_POLY_DEN) * DSP_PT_POLY_NUM) % DSP_POLY_DEN) < DSP_PT_POLY_NUM) {
+#else
       if ((i % DSP_POLY_DEN) < DSP_PT_POLY_NUM) {
+#endif
         e = poly_exp2_x2(x);
       } else {
         e.x = fast_exp2(x.x);
@@ -1374,8 +1378,9 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ---------------------------------------------------------------------------------
-// Long sequences, split-row softmax (the production spatial kernel for DP <= 80, i.e. the
-// paper's Dh = 72).  As fmha_pt_kernel -- two query tiles ("slots") per CTA ping-ponging on the
+// Long sequences, split-row softmax (an A/B variant, -DDSP_FMHA_SPLIT: at the blk shape it
+// measured 110-113 us against fmha_pt_kernel's 101-104 us; 640 threads cap it at 96 registers,
+// which spills, and the row max exchange adds a barrier per step).  As fmha_pt_kernel -- two query tiles ("slots") per CTA ping-ponging on the
 // tensor pipe, P_j (bf16) over S_j in TMEM, TS-form P.V -- plus:
 //  * every query row is exponentiated by TWO threads (one per 64-key half; 16 softmax warps,
 //    four warpgroups: slot x half), which halves the per-step dependency chain of the softmax;
@@ -1797,7 +1802,7 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
       mo[1] = mo[0];
     }
   }
-#if !defined(DSP_FMHA_PAIR_SMEM) && !defined(DSP_FMHA_PT1)
+#if defined(DSP_FMHA_SPLIT)  // A/B only: measured slower than fmha_pt_kernel (110-113 vs 101-104 us)
   if constexpr (SplitCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0 && p.Dh <= SplitCfg<NA, RB>::DP - 8) {
       auto kp = fmha_split_kernel<NA, RB>;

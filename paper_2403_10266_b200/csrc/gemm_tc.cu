@@ -39,6 +39,12 @@ thread_local unsigned long long* t_clk = nullptr;
 
 namespace {
 
+#ifndef DSP_GEMM_EPI_WG
+// epilogue warpgroups of the LN-folded + GELU epilogue (FC1): its per-element work keeps one
+// warpgroup behind the MMA (block FC1 135 -> 124 us with two); the lighter epilogues measured
+// 2-3 % slower with two (A/B: -DDSP_GEMM_EPI_WG=1)
+#define DSP_GEMM_EPI_WG 2
+#endif
 constexpr int BM = 128;  // rows per CTA (256 per pair)
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SW128 atom row
 
@@ -58,9 +64,14 @@ struct GemmCfg {
   static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
   static constexpr int NBOX = BN / EB;  // staging boxes per tile (stored / reloaded one by one)
+  static constexpr int SPLIT_MAX = NBOX; // a narrow tail tile is a whole number of EB-column boxes
+  // epilogue warpgroups (TMA epilogues: two, each owning every other box; the remote-row
+  // epilogue of the fused switch: one)
+  static constexpr int EPI_WG = EPI == EPI_LN_GELU ? DSP_GEMM_EPI_WG : 1;
+  static constexpr int THREADS = 128 + 128 * EPI_WG;
   static constexpr int STAGES = (216 * 1024 - E_BYTES) / STAGE_BYTES > 8 ? 8 : (216 * 1024 - E_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int EPI_VEC_BYTES = 2 * 2 * BN * 4;  // per-accumulator copies of u, v (LN-folded epilogue)
+  static constexpr int EPI_VEC_BYTES = 2 * 2 * BN * 4 + 2 * 128 * 8;  // per-accumulator u, v and row stats (LN-folded)
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + E_BYTES + 256 /*barriers*/ + EPI_VEC_BYTES;
 };
 
@@ -69,10 +80,81 @@ __device__ __forceinline__ float gelu_tanh_f(float u) {
   return 0.5f * u * (1.f + fast_tanh(k0 * (u + k1 * u * u * u)));
 }
 
+// Static tile schedule over P pairs: `full` BN-wide tiles; when the last wave is partial (rem =
+// full % P tiles) and its tiles cut into `split` narrower ones (split | BN/EB, so a narrow tile is
+// whole epilogue boxes) fit in one wave (rem * split <= P), tiles [head, num_tiles) are those
+// narrow tiles, split-major per parent tile.  head is a multiple of P, so every pair gets at most
+// one narrow tile, as its last.
+struct TileSched {
+  int head, split, num_tiles;
+};
+// most narrow tiles one BN-wide tile may be cut into; 1 for a residual epilogue that writes
+// LayerNorm partials (one partial per BN-wide tile, R30)
 template <int BN, int EPI>
-__global__ void __launch_bounds__(256, 1)
+__host__ __device__ inline int gemm_split_max(const EpiVec& ev) {
+  return (EPI == DSP_EPI_RESIDUAL && ev.part_out != nullptr) ? 1 : GemmCfg<BN, EPI>::SPLIT_MAX;
+}
+__host__ __device__ inline TileSched make_tile_sched(int full, int P, int smax) {
+  TileSched t{full, 1, full};
+  const int rem = full % P;
+#ifdef DSP_GEMM_NO_SPLIT
+  return t;  // A/B experiments only
+#endif
+  if (rem == 0) return t;
+  for (int sp = smax; sp > 1; --sp) {
+    if (smax % sp || rem * sp > P) continue;
+    t.split = sp;
+    t.head = full - rem;
+    t.num_tiles = t.head + rem * sp;
+    break;
+  }
+  return t;
+}
+
+// LayerNorm statistics (mean, rstd) of row r from its producer's per-row partials (mean_p, M2_p)
+// over part_cnt columns each (R30): Chan et al. combination of equal-count partials, in column
+// order.  The row's partials are contiguous: loaded as 16-B vectors up to 24 partials.
+__device__ __forceinline__ float2 ln_stats_from_parts(const EpiVec& ev, int r) {
+  constexpr int kVec = 12;
+  const int np = ev.nparts_in;
+  const float2* pp = ev.part_in + (size_t)r * np;
+  float mean = 0.f, m2 = 0.f;
+  if ((np & 1) == 0 && np <= 2 * kVec && (reinterpret_cast<uintptr_t>(pp) & 15) == 0) {
+    float4 pv[kVec];
+#pragma unroll
+    for (int i = 0; i < kVec; ++i)
+      if (2 * i < np) pv[i] = __ldg(reinterpret_cast<const float4*>(pp) + i);
+#pragma unroll
+    for (int i = 0; i < kVec; ++i)
+      if (2 * i < np) {
+        mean += pv[i].x;
+        mean += pv[i].z;
+      }
+    mean /= np;
+#pragma unroll
+    for (int i = 0; i < kVec; ++i)
+      if (2 * i < np) {
+        const float d0 = pv[i].x - mean, d1 = pv[i].z - mean;
+        m2 += pv[i].y + ev.part_cnt * d0 * d0;
+        m2 += pv[i].w + ev.part_cnt * d1 * d1;
+      }
+  } else {
+    for (int i = 0; i < np; ++i) mean += pp[i].x;
+    mean /= np;
+    for (int i = 0; i < np; ++i) {
+      const float2 pv = pp[i];
+      const float d = pv.x - mean;
+      m2 += pv.y + ev.part_cnt * d * d;
+    }
+  }
+  return make_float2(mean, rsqrtf(m2 / (float)(np * ev.part_cnt) + ev.eps));
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
-                        const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
+                        const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmD,
+                        const __grid_constant__ CUtensorMap tmR,
                         const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
                         const EpiVec ev, const RemoteMap rm) {
   using Cfg = GemmCfg<BN, EPI>;
@@ -96,9 +178,25 @@ __global__ void __launch_bounds__(256, 1)
   const bool leader = rank == 0;
   const int tiles_m = (M + 2 * BM - 1) / (2 * BM);
   const int tiles_n = N / BN;
-  const int num_tiles = tiles_m * tiles_n;
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+  // Tile schedule (static round robin over the pairs): the last, partial wave of BN-wide tiles
+  // is cut into `split` narrower tiles when they then fit in one wave (gemm_tail_split), so the
+  // idle pairs of that wave share its work.  Every output element is still one tile's K-ordered
+  // accumulation: the bits do not depend on the tile width (N-invariance).
+  const TileSched ts = make_tile_sched(tiles_m * tiles_n, num_pairs, gemm_split_max<BN, EPI>(ev));
+  const int num_tiles = ts.num_tiles;
+  auto geom = [&](int t, int& mrow, int& ncol, int& width) {
+    int p = t, sub = 0;
+    width = BN;
+    if (t >= ts.head) {
+      p = ts.head + (t - ts.head) / ts.split;
+      sub = (t - ts.head) % ts.split;
+      width = BN / ts.split;
+    }
+    mrow = (p / tiles_n) * (2 * BM);
+    ncol = (p % tiles_n) * BN + sub * width;
+  };
 
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch(&tmA);
@@ -110,7 +208,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2 * 128);  // both CTAs' epilogue threads
+      mbar_init(&tempty[i], 2 * 128 * Cfg::EPI_WG);  // both CTAs' epilogue threads
     }
     for (int b = 0; b < Cfg::NBOX; ++b) mbar_init(&r_full[b], 1);
     fence_barrier_init();
@@ -132,13 +230,17 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < num_tiles; tile += num_pairs) {
-        const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
-        const int n0 = (tile % tiles_n) * BN + rank * Cfg::BNH;
+        int mrow, ncol, width;
+        geom(tile, mrow, ncol, width);
+        const int m0 = mrow + rank * BM;
+        const int n0 = ncol + rank * (width / 2);
+        const bool narrow = width != BN;
+        const uint32_t bytes = 2 * (Cfg::A_BYTES + (width / 2) * BK * 2);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_2d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
-          tma_load_2d_2sm(sB + stage * Cfg::B_BYTES, &tmW, &full[stage], kb * BK, n0);
+          tma_load_2d_2sm(sB + stage * Cfg::B_BYTES, narrow ? &tmW2 : &tmW, &full[stage], kb * BK, n0);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -148,12 +250,13 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, 0, 0);
+      constexpr uint32_t idesc_full = make_idesc_bf16(2 * BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
         const int acc = it & 1;
+        const uint32_t idesc = tile < ts.head ? idesc_full : make_idesc_bf16(2 * BM, BN / ts.split, 0, 0);
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
@@ -181,160 +284,170 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4 && EPI != EPI_RES_REMOTE) {
-    // Bulk-tensor epilogue: the staging tile sE holds the tile as NBOX column boxes.  Each
-    // thread adds its accumulator row into box b in place (SW128 layout: 16-B chunk c of row r
-    // at c ^ (r & 7)), and as soon as the warpgroup has finished box b one thread TMA-stores it
-    // (rows >= M are clipped) and, once the previous box's store has been read out of sE,
-    // brings in that box of the NEXT tile's residual -- so the residual loads of tile i+1
-    // overlap the epilogue of tile i instead of following its last store.
+    // Bulk-tensor epilogue, EPI_WG warpgroups: warpgroup h (warps 4+4h .. 7+4h, TMEM lane quadrant
+    // = warp % 4, thread = accumulator row) owns the tile's EB-column boxes b with b % EPI_WG == h.
+    // Each thread adds its accumulator row into its box in place (SW128 layout: 16-B chunk c of
+    // row r at c ^ (r & 7)); as soon as the warpgroup has finished a box, one of its threads
+    // TMA-stores it (rows >= M are clipped).  Residual epilogue: box b's slot first receives the
+    // residual box by TMA (issued while the previous tile's epilogue ran: once that tile's store of
+    // the warpgroup's previous box has been read out of sE, the next tile's copy of that box is
+    // loaded).  Other epilogues stage through one slot per warpgroup.  A LayerNorm partial is one
+    // box of one row, so the partials' arithmetic does not depend on the warpgroup split.
     constexpr bool kRes = EPI == DSP_EPI_RESIDUAL;
     constexpr bool kLn = EPI == EPI_LN || EPI == EPI_LN_GELU;
+    constexpr int WG = Cfg::EPI_WG;
     const int q = warp & 3;
+    const int h = (warp - 4) >> 2;
     const int row = q * 32 + lane_id();
-    const bool elected = threadIdx.x == 128;
+    const int etid = threadIdx.x - 128;
+    const bool elected = (etid & 127) == 0;
+    const uint32_t bar_wg = 2 + h;
     const uint32_t e0 = smem_u32(sE);
-    int it = 0;
+    int it = 0, nbox_done = 0;
+    auto nbox_of = [&](int tile) { return tile < ts.head ? Cfg::NBOX : Cfg::NBOX / ts.split; };
     auto load_res_box = [&](int tile, int b) {
-      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM, n0 = (tile % tiles_n) * BN;
+      if (b >= nbox_of(tile)) return;  // a narrow tail tile has fewer boxes
+      int mrow, ncol, width;
+      geom(tile, mrow, ncol, width);
       mbar_arrive_expect_tx(&r_full[b], Cfg::E_BOX);
-      tma_load_2d(sE + b * Cfg::E_BOX, &tmR, &r_full[b], n0 + Cfg::EB * b, m0);
+      tma_load_2d(sE + b * Cfg::E_BOX, &tmR, &r_full[b], ncol + Cfg::EB * b, mrow + rank * BM);
     };
     if (kRes && elected && pair < num_tiles)
-      for (int b = 0; b < Cfg::NBOX; ++b) load_res_box(pair, b);
+      for (int b = h; b < Cfg::NBOX; b += WG) load_res_box(pair, b);
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
-      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
-      const int n0 = (tile % tiles_n) * BN;
+      int m0, n0, width;
+      geom(tile, m0, n0, width);
+      m0 += rank * BM;
+      const int nb = width / Cfg::EB;
       // LayerNorm folded into this GEMM: per-row (mean, rstd) of the raw input row; the tile's
       // per-column u, v staged in smem (one copy per accumulator: the other copy may still be
       // read by a slower warp of the previous tile)
       float2 rstat = make_float2(0.f, 0.f);
       float* eu = evec + acc * 2 * BN;
+      float2* rsm = reinterpret_cast<float2*>(evec + 2 * 2 * BN) + acc * 128;  // row stats, shared by the WGs
       if (kLn) {
-        if (m0 + row < M) {
-          if (ev.row_stats) {
-            rstat = ev.row_stats[m0 + row];
-          } else {  // Chan et al. combination of equal-count partials (mean_p, M2_p), <= kMaxParts
-            const float2* pp = ev.part_in + (size_t)(m0 + row) * ev.nparts_in;
-            float2 pv[kMaxParts];
-#pragma unroll
-            for (int i = 0; i < kMaxParts; ++i) pv[i] = i < ev.nparts_in ? pp[i] : make_float2(0.f, 0.f);
-            float mean = 0.f;
-#pragma unroll
-            for (int i = 0; i < kMaxParts; ++i) mean += pv[i].x;
-            mean /= ev.nparts_in;
-            float m2 = 0.f;
-#pragma unroll
-            for (int i = 0; i < kMaxParts; ++i) {
-              const float d = pv[i].x - mean;
-              if (i < ev.nparts_in) m2 += pv[i].y + ev.part_cnt * d * d;
-            }
-            rstat = make_float2(mean, rsqrtf(m2 / (float)(ev.nparts_in * ev.part_cnt) + ev.eps));
-          }
+        if (h == 0) {
+          if (m0 + row < M) rstat = ev.row_stats ? ev.row_stats[m0 + row] : ln_stats_from_parts(ev, m0 + row);
+          rsm[row] = rstat;
         }
-        for (int i = threadIdx.x - 128; i < BN; i += 128) {
+        for (int i = etid; i < width; i += 128 * WG) {
           st_shared_f32(smem_u32(eu + i), ev.col_u[n0 + i]);
           st_shared_f32(smem_u32(eu + BN + i), ev.col_v[n0 + i]);
         }
       }
       const bool has_next = tile + num_pairs < num_tiles;
-      if (kLn) named_bar_sync(1, 128);  // u, v staged
+      if (kLn) {
+        named_bar_sync(1, 128 * WG);  // u, v and the row statistics staged
+        rstat = rsm[row];
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      // row statistics of the stored (bf16-rounded) values, shifted by the first one
+      // row statistics of the stored (bf16-rounded) values, shifted by the box's first one
+      // (one LayerNorm partial per row per BN-wide tile; the residual epilogue runs one warpgroup,
+      // so the row's boxes are summed in column order by one thread)
       const bool kStats = kRes && ev.part_out != nullptr;
+      static_assert(!kRes || WG == 1, "the residual epilogue's row partials assume one warpgroup");
       float2 sh = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
       constexpr int CW = Cfg::CW;
-#pragma unroll
-      for (int c = 0; c < BN / CW; ++c) {
-        uint32_t v[CW];
-        if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
-        else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
-        tmem_ld_wait();
-        // chunk c (CW columns = CW/8 x 16 B) of this row inside box (c * CW) / EB
-        const int col0 = c * CW;
-        if (kRes && col0 % Cfg::EB == 0) mbar_wait(&r_full[col0 / Cfg::EB], it & 1);
-        // ring slot of this box: boxes alternate between the two slots across tiles too
-        const int slot = Cfg::RING ? ((it * Cfg::NBOX + col0 / Cfg::EB) & 1) : col0 / Cfg::EB;
-        if (Cfg::RING && col0 % Cfg::EB == 0) {  // the store that last used this slot has been read
-          if (elected) bulk_wait_group_read1();
-          named_bar_sync(1, 128);
-        }
+      for (int b = h; b < nb; b += WG, ++nbox_done) {
+        // staging slot: the residual tile's own box; else a ring of two slots (one warpgroup:
+        // boxes alternate, so a store overlaps the next box) or one slot per warpgroup
+        const int slot = Cfg::RING ? (WG == 1 ? (nbox_done & 1) : h) : b;
         const uint32_t line = e0 + slot * Cfg::E_BOX + row * (Cfg::EB * 2);
 #pragma unroll
-        for (int u = 0; u < CW / 8; ++u) {
-          const int j = (col0 % Cfg::EB) / 8 + u;
-          const uint32_t addr =
-              line + ((Cfg::EB == 64 ? (j ^ (row & 7)) : Cfg::EB == 32 ? (j ^ ((row >> 1) & 3)) : (j ^ ((row >> 2) & 1)))
-                      << 4);
-          float f[8];
+        for (int cb = 0; cb < Cfg::EB / CW; ++cb) {
+          const int col0 = b * Cfg::EB + cb * CW;
+          uint32_t v[CW];
+          if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col0, v);
+          else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col0, v);
+          tmem_ld_wait();
+          if (cb == 0) {
+            if (kRes) mbar_wait(&r_full[b], it & 1);
+            if (Cfg::RING) {  // the warpgroup's previous store out of this slot has been read
+              if (elected) {
+                if (WG == 1) bulk_wait_group_read1();
+                else bulk_wait_group_read0();
+              }
+              named_bar_sync(bar_wg, 128);
+            }
+          }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * u + i]);
-          if (kRes) {
-            uint32_t r0, r1, r2, r3;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-            f[0] += bf16lo(r0); f[1] += bf16hi(r0); f[2] += bf16lo(r1); f[3] += bf16hi(r1);
-            f[4] += bf16lo(r2); f[5] += bf16hi(r2); f[6] += bf16lo(r3); f[7] += bf16hi(r3);
-          } else if (EPI == DSP_EPI_GELU) {
+          for (int u = 0; u < CW / 8; ++u) {
+            const int j = cb * (CW / 8) + u;
+            const uint32_t addr =
+                line + ((Cfg::EB == 64 ? (j ^ (row & 7)) : Cfg::EB == 32 ? (j ^ ((row >> 1) & 3)) : (j ^ ((row >> 2) & 1)))
+                        << 4);
+            float f[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
-          } else if (kLn) {
-            // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, broadcast loads)
-            const uint32_t ua = smem_u32(eu + col0 + 8 * u), va = smem_u32(eu + BN + col0 + 8 * u);
-            const float2 nm = make_float2(-rstat.x, -rstat.x), rs = make_float2(rstat.y, rstat.y);
+            for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * u + i]);
+            if (kRes) {
+              uint32_t r0, r1, r2, r3;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+              f[0] += bf16lo(r0); f[1] += bf16hi(r0); f[2] += bf16lo(r1); f[3] += bf16hi(r1);
+              f[4] += bf16lo(r2); f[5] += bf16hi(r2); f[6] += bf16lo(r3); f[7] += bf16hi(r3);
+            } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const float4 uu = ld_shared_f32x4(ua + 16 * h), vv = ld_shared_f32x4(va + 16 * h);
-              const float2 y0 = ffma2(rs, ffma2(nm, make_float2(uu.x, uu.y), make_float2(f[4 * h], f[4 * h + 1])),
-                                      make_float2(vv.x, vv.y));
-              const float2 y1 = ffma2(rs, ffma2(nm, make_float2(uu.z, uu.w), make_float2(f[4 * h + 2], f[4 * h + 3])),
-                                      make_float2(vv.z, vv.w));
-              f[4 * h] = y0.x; f[4 * h + 1] = y0.y; f[4 * h + 2] = y1.x; f[4 * h + 3] = y1.y;
-              if (EPI == EPI_LN_GELU) {
+              for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
+            } else if (kLn) {
+              // y = rstd * (x.(W o gamma) - mean * u) + W.beta   (u, v: per-column, broadcast loads)
+              const uint32_t ua = smem_u32(eu + col0 + 8 * u), va = smem_u32(eu + BN + col0 + 8 * u);
+              const float2 nm = make_float2(-rstat.x, -rstat.x), rs = make_float2(rstat.y, rstat.y);
 #pragma unroll
-                for (int t = 0; t < 4; ++t) f[4 * h + t] = gelu_tanh_f(f[4 * h + t]);
+              for (int hh = 0; hh < 2; ++hh) {
+                const float4 uu = ld_shared_f32x4(ua + 16 * hh), vv = ld_shared_f32x4(va + 16 * hh);
+                const float2 y0 = ffma2(rs, ffma2(nm, make_float2(uu.x, uu.y), make_float2(f[4 * hh], f[4 * hh + 1])),
+                                        make_float2(vv.x, vv.y));
+                const float2 y1 = ffma2(rs, ffma2(nm, make_float2(uu.z, uu.w), make_float2(f[4 * hh + 2], f[4 * hh + 3])),
+                                        make_float2(vv.z, vv.w));
+                f[4 * hh] = y0.x; f[4 * hh + 1] = y0.y; f[4 * hh + 2] = y1.x; f[4 * hh + 3] = y1.y;
+                if (EPI == EPI_LN_GELU) {
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) f[4 * hh + t] = gelu_tanh_f(f[4 * hh + t]);
+                }
+              }
+            }
+            const uint32_t pk[4] = {pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                    pack_bf16x2(f[6], f[7])};
+            st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
+            if (kStats) {  // shifted sums of the STORED (bf16-rounded) row values (R30), packed pairs
+              if (b == 0 && cb == 0 && u == 0) sh = make_float2(-bf16lo(pk[0]), -bf16lo(pk[0]));
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 d = fadd2(make_float2(bf16lo(pk[i]), bf16hi(pk[i])), sh);
+                s1 = fadd2(s1, d);
+                s2 = ffma2(d, d, s2);
               }
             }
           }
-          const uint32_t pk[4] = {pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                                  pack_bf16x2(f[6], f[7])};
-          st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
-          if (kStats) {  // shifted sums of the STORED (bf16-rounded) row values (R30), packed pairs
-            if (c == 0 && u == 0) sh = make_float2(-bf16lo(pk[0]), -bf16lo(pk[0]));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 d = fadd2(make_float2(bf16lo(pk[i]), bf16hi(pk[i])), sh);
-              s1 = fadd2(s1, d);
-              s2 = ffma2(d, d, s2);
-            }
-          }
         }
-        if ((col0 + CW) % Cfg::EB == 0) {  // box b of this tile complete in every row: store it
-          const int b = col0 / Cfg::EB;
-          fence_proxy_async_smem();
-          named_bar_sync(1, 128);
-          if (elected) {
-            tma_store_2d(&tmD, sE + slot * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
-            bulk_commit_group();
-            if (kRes && has_next && b > 0) {
-              bulk_wait_group_read1();  // box b-1 read out of sE: reload it for the next tile
-              load_res_box(tile + num_pairs, b - 1);
-            }
+        // box b of this tile complete in every row of the warpgroup
+        fence_proxy_async_smem();
+        named_bar_sync(bar_wg, 128);
+        if (elected) {
+          tma_store_2d(&tmD, sE + slot * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
+          bulk_commit_group();
+          if (kRes && has_next && b >= WG) {
+            bulk_wait_group_read1();  // box b-WG read out of sE: reload it for the next tile
+            load_res_box(tile + num_pairs, b - WG);
           }
         }
       }
       if (kStats && m0 + row < M) {
-        // explicit rounding steps: launch_row_partials (simt.cu) reproduces these bits after a switch
+        // explicit rounding steps: launch_row_partials (simt.cu) reproduces these bits for rows
+        // that crossed a switch (a tile with partials is always BN wide: no narrow tail tiles)
         const float a = __fadd_rn(s1.x, s1.y), mp = __fmul_rn(a, 1.f / BN);
-        ev.part_out[(size_t)(m0 + row) * tiles_n + (tile % tiles_n)] =
+        ev.part_out[(size_t)(m0 + row) * tiles_n + n0 / BN] =
             make_float2(__fsub_rn(mp, sh.x), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2.x, s2.y)), 0.f));
       }
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next
       else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
       if (kRes && elected && has_next) {
-        bulk_wait_group_read0();
-        load_res_box(tile + num_pairs, Cfg::NBOX - 1);
+        bulk_wait_group_read0();  // the warpgroup's boxes of the next tile not reloaded yet
+        int last = -1;
+        for (int b = h; b < nb; b += WG) last = b;
+        for (int b = (last >= 0 ? last : h); b < Cfg::NBOX; b += WG) load_res_box(tile + num_pairs, b);
       }
     }
     if (elected) bulk_wait_group_read0();
@@ -344,8 +457,9 @@ __global__ void __launch_bounds__(256, 1)
     int it = 0;
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
-      const int m0 = (tile / tiles_n) * (2 * BM) + rank * BM;
-      const int n0 = (tile % tiles_n) * BN;
+      int m0, n0, width;
+      geom(tile, m0, n0, width);
+      m0 += rank * BM;
       const int grow = m0 + row;
       const bool live = grow < M;
       __nv_bfloat16* drow = D + (size_t)grow * N + n0;
@@ -370,7 +484,8 @@ __global__ void __launch_bounds__(256, 1)
       if (kRes && live) {
         const uint4* rp = reinterpret_cast<const uint4*>(R + (size_t)grow * N + n0);
 #pragma unroll
-        for (int j = 0; j < BN / 8; ++j) rv[j] = rp[j];
+        for (int j = 0; j < BN / 8; ++j)
+          if (j * 8 < width) rv[j] = rp[j];
       }
       // LayerNorm folded into this GEMM: per-row (mean, rstd) of the raw input row; the tile's
       // per-column u, v staged once in smem (one copy per accumulator, so a slow warp of the
@@ -379,7 +494,7 @@ __global__ void __launch_bounds__(256, 1)
       float* eu = evec + acc * 2 * BN;
       if (EPI == EPI_LN || EPI == EPI_LN_GELU) {
         if (live) rstat = ev.row_stats[grow];
-        for (int i = threadIdx.x - 128; i < BN; i += 128) {
+        for (int i = threadIdx.x - 128; i < width; i += 128) {
           eu[i] = ev.col_u[n0 + i];
           eu[BN + i] = ev.col_v[n0 + i];
         }
@@ -390,6 +505,7 @@ __global__ void __launch_bounds__(256, 1)
       constexpr int CW = Cfg::CW;
 #pragma unroll
       for (int c = 0; c < BN / CW; ++c) {
+        if (c * CW >= width) break;  // narrow tail tile
         uint32_t v[CW];
         if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
         else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
@@ -493,7 +609,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
                             int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{},
                             const RemoteMap& rm = RemoteMap{}) {
   using Cfg = GemmCfg<BN, EPI>;
-  CUtensorMap ta, tw, td, tr;
+  CUtensorMap ta, tw, tw2, td, tr;
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
   uint64_t dd[2] = {(uint64_t)N, (uint64_t)M}, sd[1] = {(uint64_t)N * 2};
@@ -504,6 +620,18 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   if (!make_tmap_bf16(&ta, A, 2, da, sa, ba, CU_TENSOR_MAP_SWIZZLE_128B, why) ||
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
+  // grid: one pair per tile up to all pairs; a partial last wave becomes narrow tiles (TileSched)
+  const int64_t full = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int pmax = num_sms / 2;
+  const int smax = gemm_split_max<BN, EPI>(ev);
+  TileSched tsh = make_tile_sched((int)full, pmax, smax);
+  const int64_t pairs = full >= pmax ? pmax : (tsh.num_tiles < pmax ? tsh.num_tiles : pmax);
+  tsh = make_tile_sched((int)full, (int)pairs, smax);  // what the kernel will compute
+  tw2 = tw;
+  if (tsh.split > 1) {
+    uint32_t bw2[2] = {BK, (uint32_t)(Cfg::BNH / tsh.split)};
+    if (!make_tmap_bf16(&tw2, W, 2, dw, sw, bw2, CU_TENSOR_MAP_SWIZZLE_128B, why)) return cudaErrorInvalidValue;
+  }
   td = ta;
   tr = ta;
   if (EPI != EPI_RES_REMOTE) {
@@ -518,11 +646,9 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int64_t tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
-  const int64_t pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   EpiVec evc = ev;
   evc.clk = t_clk;
-  return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(256), Cfg::SMEM, st, 2, ta, tw, td, tr, (const __nv_bfloat16*)R,
+  return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(Cfg::THREADS), Cfg::SMEM, st, 2, ta, tw, tw2, td, tr, (const __nv_bfloat16*)R,
                   (__nv_bfloat16*)D, (int)M, (int)N, (int)K, evc, rm);
 }
 
@@ -553,9 +679,14 @@ cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev,
   return dispatch_bn<EPI_LN>(A, Wf, nullptr, D, M, N, K, num_sms, st, why, ev);
 }
 
+int gemm_part_cols(int64_t N) { return gemm_bn_for(N); }  // one partial per BN-wide tile
+
 int gemm_bn_for(int64_t N) {
 #ifdef DSP_GEMM_BN_1152
   if (N == 1152) return DSP_GEMM_BN_1152;  // A/B experiments only
+#endif
+#ifdef DSP_GEMM_BN_4608
+  if (N == 4608) return DSP_GEMM_BN_4608;  // A/B experiments only
 #endif
   // A function of N only (never of M): the tile width fixes how many LayerNorm partials a
   // residual epilogue writes, and the block must not depend on the shard size (N-invariance).

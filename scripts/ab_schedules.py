@@ -14,7 +14,6 @@ import numpy as np
 import torch
 import paper_2403_10266_b200 as dsp
 import synth
-from oracle import switch as osw
 from tests.gpu_util import to_dev, weights_dev
 
 ap = argparse.ArgumentParser()
@@ -45,7 +44,8 @@ def run(N, schedule, impl):
         c.set_workspace(region[r][:ws])
         if impl == "nccl":
             c.set_collective_emulation(True)
-    xsh = osw.split(xs, osw.DIM_T, N)
+    Tn = sh.T // N
+    xsh = [np.ascontiguousarray(xs[:, r * Tn:(r + 1) * Tn]) for r in range(N)]  # rank r's T-chunk
     X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
     Y = [region[r][ws:ws + act].view(torch.bfloat16) for r in range(N)]
     streams = [torch.cuda.Stream() for _ in range(N)]

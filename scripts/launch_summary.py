@@ -17,7 +17,7 @@ def kind(name):
     m = re.search(r"gemm_bf16_tc_kernel<(\d+), (\d+)>", name)
     if m:
         return f"gemm BN={m.group(1)} {EPI.get(m.group(2), m.group(2))} [{ROLE.get(m.group(2), '?')}]"
-    for k in ("fmha_pair_kernel", "fmha_bf16_tc_kernel", "row_stats", "layer_norm", "run_copy", "p2p_barrier",
+    for k in ("fmha_pt_kernel", "fmha_split_kernel", "fmha_pair_kernel", "fmha_bf16_tc_kernel", "row_partials", "row_stats", "layer_norm", "run_copy", "p2p_barrier",
               "p2p_put", "fold_ln_weights"):
         if k in name:
             return k
