@@ -22,7 +22,7 @@ def t(fn, reps=10, n=8):
 name = os.environ.get("DSP_LIB_OVERRIDE", "libdsp.so")[-22:]
 C = 1152
 for M in (16384, 2048):
-    for K, N, epi, tag in ((C, 3 * C, 0, "QKV"), (C, C, 1, "PROJ+res"), (C, 4 * C, 2, "FC1 gelu"), (C, 4 * C, 0, "FC1 none"),
+    for K, N, epi, tag in ((C, 3 * C, 0, "QKV"), (C, C, 1, "PROJ+res"), (C, C, 0, "PROJ none"), (C, 2 * C, 0, "N=2304"), (C, 4 * C, 2, "FC1 gelu"), (C, 4 * C, 0, "FC1 none"),
                            (4 * C, C, 1, "FC2+res")):
         A = (torch.randn(M, K, device="cuda") * 0.1).to(torch.bfloat16)
         W = (torch.randn(N, K, device="cuda") * 0.03).to(torch.bfloat16)
