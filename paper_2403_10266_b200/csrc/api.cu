@@ -98,7 +98,7 @@ int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 //   [act, 5 act)      big: qkv [tok,3C] + o [tok,C] | MLP hidden [tok,4C] | switch send/recv
 //   [5 act, 6 act)    ys: S-sharded activation (N > 1)
 //   stats             [tok] float2 (mean, rstd) of a LayerNorm input (prepared path)
-//   parts             [tok, C / 64] float2 per-row partials from the out-projection epilogues
+//   parts             [tok, C / BN] float2 per-row partials from the out-projection epilogues
 struct BlockWs {
   int64_t act, h, big, ys, stats, parts, total;
 };
@@ -313,23 +313,34 @@ inline void mark(dsp_ctx_t ctx, int stage, int end, cudaStream_t st) {
 
 // one attention stage: out = (res ? res : 0) + MHA_dim(h); scratch qkv [tok,3C], o [tok,C].
 // stage0 >= 0: record stage events for (QKV, ATTN, PROJ) = stage0, stage0+1, stage0+2.
+// o_tseq != nullptr (temporal stage of the block): when the shape allows (tseq_ok), q | k | v are
+// written sequence-major (TSEQ, dsp_internal.h) into qkv -- which must then hold tseq_bytes --
+// and the attention output goes to o_tseq instead of o.
 dsp_status_t attn_stage(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim, const void* h,
                         const void* w_qkv, const void* w_o, const void* res, void* out, void* qkv, void* o,
                         cudaStream_t st, int stage0 = -1, const EpiVec* ln = nullptr,
-                        const RemoteMap* remote = nullptr, float2* part_out = nullptr) {
+                        const RemoteMap* remote = nullptr, float2* part_out = nullptr, void* o_tseq = nullptr) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
+#ifdef DSP_NO_TSEQ
+  o_tseq = nullptr;  // A/B: token-major q | k | v for the temporal stage too
+#endif
+  const bool tseq = o_tseq && dim == DSP_DIM_T && s->dtype == DSP_BF16 && tseq_ok(s->B, T_loc, S_loc, C, s->num_heads);
+  if (tseq) o = o_tseq;
   const int epi = res ? DSP_EPI_RESIDUAL : DSP_EPI_NONE;
   const int sq = stage0, sa = stage0 < 0 ? -1 : stage0 + 1, sp = stage0 < 0 ? -1 : stage0 + 2;
   if (s->dtype == DSP_BF16) {
     std::string why;
     mark(ctx, sq, 0, st);
     // ln != nullptr: h is the raw (un-normalised) input and w_qkv the LN-folded weight
-    cudaError_t e = ln ? launch_gemm_bf16_ln(h, w_qkv, *ln, qkv, tok, 3 * C, C, false, ctx->num_sms, st, &why)
-                       : launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
+    const TseqShape ts{(int)s->B, (int)T_loc, (int)S_loc, s->num_heads, (int)C};
+    cudaError_t e = tseq ? launch_gemm_bf16_tseq(h, w_qkv, ln, qkv, ts, tok, C, ctx->num_sms, st, &why)
+                    : ln ? launch_gemm_bf16_ln(h, w_qkv, *ln, qkv, tok, 3 * C, C, false, ctx->num_sms, st, &why)
+                         : launch_gemm_bf16(h, w_qkv, nullptr, qkv, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "qkv projection", why);
     mark(ctx, sq, 1, st);
     mark(ctx, sa, 0, st);
-    e = launch_fmha_bf16(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, dim, ctx->num_sms, st, &why);
+    e = tseq ? launch_fmha_bf16_tseq(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, ctx->num_sms, st, &why)
+             : launch_fmha_bf16(qkv, o, s->B, T_loc, S_loc, C, s->num_heads, dim, ctx->num_sms, st, &why);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
     mark(ctx, sa, 1, st);
     mark(ctx, sp, 0, st);
@@ -966,8 +977,9 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     ctx->launches += 1;
   }
   mark(ctx, DSP_STAGE_LN2, 1, st);
+  // (temporal q | k | v sequence-major in big, the attention output in h: both free here)
   DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, fold ? cur : h, fold ? wf_t : w->w_qkv_t, w->w_o_t, cur, cur, qkv,
-                     o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr, nullptr, fold ? parts : nullptr));
+                     o, st, DSP_STAGE_QKV_T, fold ? &ev2 : nullptr, nullptr, fold ? parts : nullptr, h));
   if (cross) {  // ST-DiT cross stage: y2 += CA(LN_c(y2), ctx) on the S-shards, in place
     const int64_t Lq = s->T * (s->S / N), Lc = w->ctx_len;
     uint8_t* q = big;

@@ -58,6 +58,9 @@ cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* 
                              int epi, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
                              int dim, int num_sms, cudaStream_t st, std::string* why);
+// temporal attention reading q | k | v from the TSEQ layout (launch_gemm_bf16_tseq); o [tok, C]
+cudaError_t launch_fmha_bf16_tseq(const void* qkv_tseq, void* o, int64_t B, int64_t T, int64_t S_loc, int64_t C,
+                                  int NH, int num_sms, cudaStream_t st, std::string* why);
 // cross-attention: queries q [B*Lq, C], context keys / values kv [B*Lc, 2C] ([k | v])
 cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64_t B, int64_t Lq, int64_t Lc,
                                    int64_t C, int NH, int num_sms, cudaStream_t st, std::string* why);
@@ -91,7 +94,23 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
 cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st);
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
 // GEMM epilogue codes beyond the public dsp_epilogue_t
-enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5 };
+enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5, EPI_TSEQ = 6, EPI_LN_TSEQ = 7 };
+// Sequence-major temporal layout of q | k | v ("TSEQ", written by the temporal QKV GEMM, read by
+// the temporal FMHA): element (part, b, h, s, t, d) at ((((part*B + b)*NH + h)*S_loc + s)*T + t)*kTseqDP
+// + d, d < Dh = kTseqDh; columns Dh..DP-1 are zero.  Every temporal sequence (b, h, s) is one
+// contiguous block of T rows (T = 128: 20 KB), so the FMHA's tiles are single contiguous reads
+// instead of T token rows S_loc * 3C elements apart (T = 128, S_loc = 4096: a 3.6 GB span per tile,
+// which bounds the token-major gathers at ~2.6 TB/s).  Used for T >= 64 (tseq_ok).
+constexpr int kTseqDh = 72, kTseqDP = 80;
+struct TseqShape {
+  int B, T, S_loc, NH, C;
+};
+int64_t tseq_bytes(const TseqShape& t);  // 3 * B * NH * S_loc * T * DP * 2
+// the shapes the TSEQ path supports: bf16, Dh == kTseqDh, S_loc % 128 == 0, 3C % 144 == 0
+bool tseq_ok(int64_t B, int64_t T, int64_t S_loc, int64_t C, int NH);
+cudaError_t launch_gemm_bf16_tseq(const void* A, const void* W, const struct EpiVec* ln, void* qkv_tseq,
+                                  const TseqShape& ts, int64_t M, int64_t K, int num_sms, cudaStream_t st,
+                                  std::string* why);
 // Residual epilogue whose output rows go straight to their owner rank after a switch
 // (switch fused into the GEMM): mode 1 = T->S (rows of [B,Tn,S] -> peers' [B,T,Sn]),
 // mode 2 = S->T (rows of [B,T,Sn] -> peers' [B,Tn,S]).  Row bytes = C * 2.
@@ -115,6 +134,7 @@ struct EpiVec {
   float eps;
   float2* part_out;         // residual epilogue: [M, N / gemm_part_cols(N)] partials of the stored (bf16) rows
   unsigned long long* clk;  // stage clock (set by run_gemm from t_clk)
+  TseqShape tseq;           // EPI_*TSEQ: the temporal layout's shape
 };
 // BN (output-tile width) the GEMM dispatch picks for N output columns
 int gemm_bn_for(int64_t N);

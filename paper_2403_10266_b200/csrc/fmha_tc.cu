@@ -63,6 +63,8 @@ struct FmhaParams {
   int S_loc, T_loc, B;
   int items;     // n_outer * NH * n_qt
   int kv_last;   // valid keys in the last K/V tile (128 unless the key length is ragged: cross-attention)
+  int cross;     // 1: cross-attention views (queries and keys from different tensors)
+  int colfast;   // 1: item order column-fastest (outer before head), for the head-major TSEQ layout
   float scale_log2;
   __nv_bfloat16* o;
   unsigned long long* trace;  // DSP_FMHA_TRACE builds only: per-phase clock64 stamps of CTA 0
@@ -100,8 +102,8 @@ __device__ __forceinline__ TileCoord tile_coord(const FmhaParams& p, int item, i
   const int qt = item % p.n_qt;
   const int rest = item / p.n_qt;
   TileCoord t;
-  t.h = rest % p.NH;
-  const int outer = rest / p.NH;
+  t.h = p.colfast ? rest / p.n_outer : rest % p.NH;
+  const int outer = p.colfast ? rest % p.n_outer : rest / p.NH;
   if (p.G == 1) {
     t.x2 = (kv >= 0 ? kv : qt) * 128;
     if (p.spatial) { t.x3 = outer; t.x4 = 0; }
@@ -1378,6 +1380,229 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ---------------------------------------------------------------------------------
+// Sequences of one 128-row tile (L <= 128 with one sequence per tile: the long video's T = 128
+// temporal stage, ragged lengths), self-attention.  Each item (sequence, head) needs its own Q,
+// K and V tiles exactly once, gathered by TMA from token rows far apart in HBM (T = 128: 128
+// rows S_loc * 6912 B apart per tile), so the kernel is bound by how many bytes it keeps in
+// flight: one CTA per SM with a KS-deep ring of {Q, K, V} stages (the loads of the next KS - 1
+// items stream in while one is computed), two softmax/epilogue warpgroups ("slots") taking
+// alternate items, and per-slot S and O in TMEM so item i + 1's Q K^T runs during item i's
+// softmax.  P_i (bf16) overwrites the first 64 columns of its S in TMEM, P.V is the TS form,
+// the row sums come from V's ones column (R31).
+// TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+DP), O1 [384, 384+DP).
+//   warp 0 TMA producer   warp 1 MMA issuer + TMEM allocator   warp 2 V patcher   warp 3 idle
+//   warps 4-7 slot 0 (even items)   warps 8-11 slot 1 (odd items)
+template <int NA, int RB>
+struct SeqCfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int TILE = Base::TILE, TX = Base::TX, DP = Base::DP;
+  static constexpr int KS = 3;  // {Q, K, V} stages
+  static constexpr int SMEM = 1024 + (3 * KS + 2) * TILE + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024 && RB > 0;
+  static constexpr int THREADS = 384;
+};
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(384, 1)
+    fmha_seq_kernel(const __grid_constant__ CUtensorMap tq_a, const __grid_constant__ CUtensorMap tq_b,
+                    const __grid_constant__ CUtensorMap tk_a, const __grid_constant__ CUtensorMap tk_b,
+                    const __grid_constant__ CUtensorMap tv_a, const __grid_constant__ CUtensorMap tv_b,
+                    const __grid_constant__ CUtensorMap to_a, const __grid_constant__ CUtensorMap to_b,
+                    const FmhaParams p) {
+  using Cfg = SeqCfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  constexpr int KS = Cfg::KS, DP = Cfg::DP;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQKV = smem;                      // stage st: Q, K, V tiles at (3 * st + part) * TILE
+  uint8_t* sO = smem + 3 * KS * Cfg::TILE;   // 2 staging tiles (epilogue), one per slot
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + 2 * Cfg::TILE);
+  uint64_t* full = bars;                     // [KS] Q, K, V of the stage landed
+  uint64_t* empty = full + KS;               // [KS] the stage's P.V has completed
+  uint64_t* v_ready = empty + KS;            // [KS] V patched with its ones column
+  uint64_t* s_full = v_ready + KS;           // [2] per slot
+  uint64_t* p_full = s_full + 2;             // [2] (count 128)
+  uint64_t* o_done = p_full + 2;             // [2]
+  uint64_t* o_free = o_done + 2;             // [2] (count 128)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = warp_id();
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&tq_a); tma_prefetch(&tk_a); tma_prefetch(&tv_a);
+    tma_prefetch(&tq_b); tma_prefetch(&tk_b); tma_prefetch(&tv_b);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&v_ready[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
+  clk_start(p.clk);
+
+  // launch allocation 168 regs x 384 threads; 56 x 128 + 224 x 256 == 168 x 384
+  if (warp == 0) {
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      uint32_t k = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+        const int st = k % KS;
+        mbar_wait_sleep(&empty[st], ((k / KS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[st], 3 * Cfg::TX);
+        uint8_t* b = sQKV + 3 * st * Cfg::TILE;
+        load_tile<NA, RB>(b, &tq_a, &tq_b, &full[st], tile_coord(p, item, -1));
+        const TileCoord t = tile_coord(p, item, 0);
+        load_tile<NA, RB>(b + Cfg::TILE, &tk_a, &tk_b, &full[st], t);
+        load_tile<NA, RB>(b + 2 * Cfg::TILE, &tv_a, &tv_b, &full[st], t);
+      }
+    }
+  } else if (warp == 1) {
+    setmaxnreg_dec<56>();
+    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idPVa = make_idesc_bf16(128, 64, 0, 1);
+    constexpr uint32_t idPVb = make_idesc_bf16(128, RB, 0, 1);
+    const uint32_t b0 = smem_u32(sQKV);
+    // The tensor pipe serves two independent streams -- S of the next item once its tiles have
+    // landed, P.V of the previous item once its softmax is done -- so the issuer polls both
+    // instead of blocking on one: P.V (which frees a {Q, K, V} stage for the producer) is
+    // never held up behind the loads of a later item.
+    auto issue_s = [&](uint32_t k) {  // S_slot = Q K^T of the k-th local item
+      const int st = k % KS, slot = k & 1;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t qa = b0 + 3 * st * Cfg::TILE, ka = qa + Cfg::TILE, d = tmem + slot * 128;
+        int step = 0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk, ++step)
+            umma_bf16_ss(d, make_sdesc(qa + i * 16384 + kk * 32, 16, 1024, SW_128B),
+                         make_sdesc(ka + i * 16384 + kk * 32, 16, 1024, SW_128B), idS, step != 0);
+#pragma unroll
+        for (int kk = 0; kk < RB / 16; ++kk, ++step)
+          umma_bf16_ss(d, make_sdesc(qa + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
+                       make_sdesc(ka + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+        umma_commit(&s_full[slot]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](uint32_t k) {  // O_slot = P V (P from TMEM), then the stage is free
+      const int st = k % KS, slot = k & 1;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t va = b0 + (3 * st + 2) * Cfg::TILE, o = tmem + 256 + slot * 128, ps = tmem + slot * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // 16 keys = 8 packed P columns per step
+#pragma unroll
+          for (int i = 0; i < NA; ++i)
+            umma_bf16_ts(o + 64 * i, ps + 8 * kk, make_sdesc(va + i * 16384 + kk * 2048, 16384, 1024, SW_128B), idPVa,
+                         kk != 0);
+          umma_bf16_ts(o + 64 * NA, ps + 8 * kk,
+                       make_sdesc(va + NA * 16384 + kk * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW),
+                       idPVb, kk != 0);
+        }
+        umma_commit(&o_done[slot]);
+        umma_commit(&empty[st]);
+      }
+      __syncwarp();
+    };
+    const uint32_t nloc = blockIdx.x < (unsigned)p.items ? (p.items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    uint32_t ks = 0, kp = 0;  // next item to issue S for / P.V for (kp <= ks)
+    while (kp < nloc) {
+      const uint32_t ks0 = ks, kp0 = kp;
+      // S of item ks: its tiles landed, and its slot's previous item (ks - 2) has been stored
+      // (its P.V done, O read), so S and O of the slot may be overwritten
+      if (ks < nloc && ks < kp + 2 && mbar_try_wait(smem_u32(&full[ks % KS]), (ks / KS) & 1) &&
+          mbar_try_wait(smem_u32(&o_free[ks & 1]), ((ks >> 1) & 1) ^ 1)) {
+        issue_s(ks);
+        ++ks;
+      }
+      if (kp < ks && mbar_try_wait(smem_u32(&p_full[kp & 1]), (kp >> 1) & 1) &&
+          mbar_try_wait(smem_u32(&v_ready[kp % KS]), (kp / KS) & 1)) {
+        issue_pv(kp);
+        ++kp;
+      }
+      if (ks == ks0 && kp == kp0) __nanosleep(20);  // nothing ready: leave the issue slots to the softmax warps
+    }
+  } else if (warp < 4) {
+    setmaxnreg_dec<56>();
+    if (warp == 2) {
+      // V patcher: once a V tile has landed, set its column DP - 8 (zero-filled padding, since
+      // Dh <= DP - 8) to 1.0 in every row, so P.V also produces the row sums (R31)
+      constexpr int CB = (RB - 8) * 2;  // byte offset of the ones column inside the RB chunk row
+      uint32_t k = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+        const int st = k % KS;
+        mbar_wait(&full[st], (k / KS) & 1);
+        const uint32_t vb = smem_u32(sQKV + (3 * st + 2) * Cfg::TILE) + NA * 16384;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = lane_id() + 32 * i;
+          const uint32_t ch = RB == 16 ? ((CB >> 4) ^ ((r >> 2) & 1)) : ((CB >> 4) ^ ((r >> 1) & 3));
+          st_shared_u16(vb + r * Base::RB_ROW + (ch << 4) + (CB & 15), 0x3F80);  // bf16 1.0
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&v_ready[st]);
+      }
+    }
+  } else {
+    setmaxnreg_inc<224>();
+    const int slot = (warp - 4) >> 2;
+    const SoftmaxGeom G = make_geom(p, warp, p.scale_log2);
+    const uint32_t tS = tmem + slot * 128, tO = tmem + 256 + slot * 128;
+    uint8_t* sOs = sO + slot * Cfg::TILE;
+    const uint32_t bar_id = 1 + slot;
+    int store_pending = 0;
+    uint32_t n = 0;
+    uint32_t k = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++k) {
+      if ((int)(k & 1) != slot) continue;
+      mbar_wait(&s_full[slot], n & 1);
+      tc_fence_after();
+      float m = -INFINITY;
+      softmax_step_pt<DP>(G, tS, tO, 0, m, p.kv_last);
+      mbar_arrive(&p_full[slot]);
+      mbar_wait(&o_done[slot], n & 1);  // P.V done: O final
+      ++n;
+      tc_fence_after();
+      if (store_pending) {  // the previous item's O store must have read the staging tile
+        if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+        named_bar_sync(bar_id, 128);
+        store_pending = 0;
+      }
+      epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
+                                         tile_coord(p, item, -1), &o_free[slot], store_pending);
+    }
+    if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  clk_end(p.clk);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Long sequences, split-row softmax (an A/B variant, -DDSP_FMHA_SPLIT: at the blk shape it
 // measured 110-113 us against fmha_pt_kernel's 101-104 us; 640 threads cap it at 96 registers,
 // which spills, and the row max exchange adds a barrier per step).  As fmha_pt_kernel -- two query tiles ("slots") per CTA ping-ponging on the
@@ -1819,6 +2044,22 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
     }
   }
 #endif
+#ifndef DSP_FMHA_NO_SEQ
+  if constexpr (SeqCfg<NA, RB>::OK) {
+    if (p.G == 1 && p.n_kv == 1 && !p.cross && p.Dh <= SeqCfg<NA, RB>::DP - 8) {
+      auto kp = fmha_seq_kernel<NA, RB>;
+      static bool attr_sq = false;
+      if (!attr_sq) {
+        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, SeqCfg<NA, RB>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_sq = true;
+      }
+      const int grid = p.items < num_sms ? p.items : num_sms;
+      return launch_k(kp, dim3(grid), dim3(SeqCfg<NA, RB>::THREADS), SeqCfg<NA, RB>::SMEM, st, 1, m[0], m[1], m[2],
+                      m[3], m[4], m[5], mo[0], mo[1], p);
+    }
+  }
+#endif
 #ifndef DSP_FMHA_PAIR_SMEM
   if constexpr (PtCfg<NA, RB>::OK) {
     if (p.G == 1 && p.n_qt % 2 == 0 && p.Dh <= PtCfg<NA, RB>::DP - 8) {
@@ -1956,6 +2197,7 @@ cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64
   p.clk = t_clk;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
   p.spatial = 1;  // queries of sample b = rows [b*Lq, (b+1)*Lq) of q; keys / values = rows of kv
+  p.cross = 1;
   p.L = (int)Lq;
   p.G = 1;
   p.n_qt = (int)((Lq + 127) / 128);  // a ragged last query tile is clipped by the TMA store
@@ -1988,6 +2230,58 @@ cudaError_t launch_fmha_cross_bf16(const void* q, const void* kv, void* o, int64
     vw.ostr[i] = qs[i];
   }
   const uint32_t box_rows[2] = {128, 1};
+  return dispatch_dh(vw, p, box_rows, num_sms, st, why);
+}
+
+cudaError_t launch_fmha_bf16_tseq(const void* qkv_tseq, void* o, int64_t B, int64_t T, int64_t S_loc, int64_t C,
+                                  int NH, int num_sms, cudaStream_t st, std::string* why) {
+  // Same tiles and dims order {Dh, NH, T (pos), S (column), B} as the token-major temporal view,
+  // only the strides differ (layout [part][b][h][s][t][DP]): a tile is one contiguous block.
+  FmhaParams p{};
+  p.NH = NH;
+  p.Dh = (int)(C / NH);
+  p.C = (int)C;
+  p.S_loc = (int)S_loc;
+  p.T_loc = (int)T;
+  p.B = (int)B;
+  p.o = static_cast<__nv_bfloat16*>(o);
+  p.trace = nullptr;
+  p.clk = t_clk;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
+  p.spatial = 0;
+  p.L = (int)T;
+  if (p.Dh != kTseqDh) {
+    if (why) *why = "TSEQ layout needs Dh == 72";
+    return cudaErrorNotSupported;
+  }
+  if (p.L % 128 == 0) {
+    p.G = 1; p.n_kv = p.L / 128; p.n_qt = p.n_kv;
+  } else if (128 % p.L == 0) {
+    p.G = 128 / p.L; p.n_kv = 1; p.n_qt = 1;
+  } else {
+    p.G = 1; p.n_kv = (p.L + 127) / 128; p.n_qt = p.n_kv;
+  }
+  const uint64_t e = 2, row = kTseqDP * e;
+  const uint64_t dims[5] = {(uint64_t)p.Dh, (uint64_t)NH, (uint64_t)T, (uint64_t)S_loc, (uint64_t)B};
+  const uint64_t strides[4] = {S_loc * T * row, row, T * row, NH * S_loc * T * row};
+  p.n_outer = (int)(p.G == 1 ? B * S_loc : B * ((S_loc + p.G - 1) / p.G));
+  uint32_t box_rows[2] = {(uint32_t)(p.G == 1 ? 128 : p.L), (uint32_t)p.G};
+  p.items = p.n_outer * NH * p.n_qt;
+  p.kv_last = p.G == 1 ? p.L - 128 * (p.n_kv - 1) : 128;
+  if (p.items == 0) return cudaSuccess;
+  FmhaViews vw;
+  const auto* base = static_cast<const __nv_bfloat16*>(qkv_tseq);
+  const uint64_t part_elems = (uint64_t)B * NH * S_loc * T * kTseqDP;
+  for (int part = 0; part < 3; ++part) {
+    vw.base[part] = base + part * part_elems;
+    for (int i = 0; i < 5; ++i) vw.dims[part][i] = dims[i];
+    for (int i = 0; i < 4; ++i) vw.strides[part][i] = strides[i];
+  }
+  // o [tok, C] token-major as for the standard view: {Dh, NH, T (stride S_loc rows), S, B}
+  const uint64_t orow = C * e;
+  const uint64_t ostr[4] = {p.Dh * e, S_loc * orow, orow, T * S_loc * orow};
+  for (int i = 0; i < 5; ++i) vw.odims[i] = dims[i];
+  for (int i = 0; i < 4; ++i) vw.ostr[i] = ostr[i];
   return dispatch_dh(vw, p, box_rows, num_sms, st, why);
 }
 

@@ -59,8 +59,9 @@ struct GemmCfg {
   // epilogue staging: the residual epilogue stages the whole 128 x BN tile (the residual tile
   // lands there by TMA); the others use a ring of two boxes (store of box i overlaps box i+1),
   // which leaves room for one more mainloop stage at BN = 256
-  static constexpr bool RING = EPI != DSP_EPI_RESIDUAL && EPI != EPI_RES_REMOTE;
-  static constexpr int E_BYTES = RING ? 2 * 128 * EB * 2 : BN * 256;
+  static constexpr bool TSEQ = EPI == EPI_TSEQ || EPI == EPI_LN_TSEQ;  // temporal q|k|v layout, per-head boxes
+  static constexpr bool RING = EPI != DSP_EPI_RESIDUAL && EPI != EPI_RES_REMOTE && !TSEQ;
+  static constexpr int E_BYTES = TSEQ ? (BN / kTseqDh) * 128 * kTseqDP * 2 : RING ? 2 * 128 * EB * 2 : BN * 256;
   static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
   static constexpr int NBOX = BN / EB;  // staging boxes per tile (stored / reloaded one by one)
@@ -92,7 +93,8 @@ struct TileSched {
 // LayerNorm partials (one partial per BN-wide tile, R30)
 template <int BN, int EPI>
 __host__ __device__ inline int gemm_split_max(const EpiVec& ev) {
-  return (EPI == DSP_EPI_RESIDUAL && ev.part_out != nullptr) ? 1 : GemmCfg<BN, EPI>::SPLIT_MAX;
+  return ((EPI == DSP_EPI_RESIDUAL && ev.part_out != nullptr) || GemmCfg<BN, EPI>::TSEQ) ? 1
+                                                                                        : GemmCfg<BN, EPI>::SPLIT_MAX;
 }
 __host__ __device__ inline TileSched make_tile_sched(int full, int P, int smax) {
   TileSched t{full, 1, full};
@@ -283,6 +285,94 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
         }
       }
     }
+  } else if (warp >= 4 && Cfg::TSEQ) {
+   if constexpr (Cfg::TSEQ) {
+    // Temporal-layout epilogue (EPI_TSEQ / EPI_LN_TSEQ): the tile's BN = HPT * Dh columns are
+    // HPT whole heads of q, k or v; each head's 128 x Dh block is staged in sE as 128 rows of DP
+    // elements (columns Dh..DP-1 zero, so every stored row is whole 32-B sectors) and stored by
+    // one 5-D TMA box {DP, 1 (t), 128 (s), 1 (h), 1 (part*B + b)}: the CTA's 128 rows are 128
+    // consecutive columns s of one (b, t) (S_loc % 128 == 0), T * DP elements apart in the layout
+    // (dsp_internal.h TseqShape).  All BN accumulator columns are read from TMEM before one wait.
+    constexpr bool kLn = EPI == EPI_LN_TSEQ;
+    constexpr int HD = kTseqDh, HPT = BN / HD;
+    static_assert(BN % HD == 0 && Cfg::CW == 16, "TSEQ tiles are whole heads, read 16 columns at a time");
+    const int q = warp & 3;
+    const int row = q * 32 + lane_id();
+    const bool elected = threadIdx.x == 128;
+    const uint32_t e0 = smem_u32(sE);
+    const TseqShape tq = ev.tseq;
+    constexpr int ROWB = kTseqDP * 2;  // staged row pitch (bytes)
+#pragma unroll
+    for (int hh = 0; hh < HPT; ++hh)  // the padding columns Dh..DP-1 of every staged row: zero, once
+      for (int c = HD * 2; c < ROWB; c += 16) st_shared_v4(e0 + hh * (128 * ROWB) + row * ROWB + c, 0u, 0u, 0u, 0u);
+    int it = 0;
+    for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
+      const int acc = it & 1;
+      int m0, n0, width;
+      geom(tile, m0, n0, width);
+      m0 += rank * BM;
+      float2 rstat = make_float2(0.f, 0.f);
+      float* eu = evec + acc * 2 * BN;
+      if (kLn) {
+        if (m0 + row < M) rstat = ev.row_stats ? ev.row_stats[m0 + row] : ln_stats_from_parts(ev, m0 + row);
+        for (int i = threadIdx.x - 128; i < BN; i += 128) {
+          st_shared_f32(smem_u32(eu + i), ev.col_u[n0 + i]);
+          st_shared_f32(smem_u32(eu + BN + i), ev.col_v[n0 + i]);
+        }
+      }
+      if (elected) bulk_wait_group_read0();  // the previous tile's head boxes have left sE
+      named_bar_sync(1, 128);               // (and u, v staged)
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t va[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 16; ++c)
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * 16, *reinterpret_cast<uint32_t(*)[16]>(va + 16 * c));
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < BN / 16; ++c) {
+        const uint32_t* v = va + 16 * c;
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const int col = c * 16 + g * 8, hh = col / HD, d = col - hh * HD;
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * g + i]);
+          if (kLn) {
+            const float2 nm = make_float2(-rstat.x, -rstat.x), rs = make_float2(rstat.y, rstat.y);
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const float4 uu = ld_shared_f32x4(smem_u32(eu + col + 4 * hf)),
+                           vv = ld_shared_f32x4(smem_u32(eu + BN + col + 4 * hf));
+              const float2 y0 = ffma2(rs, ffma2(nm, make_float2(uu.x, uu.y), make_float2(f[4 * hf], f[4 * hf + 1])),
+                                      make_float2(vv.x, vv.y));
+              const float2 y1 = ffma2(rs, ffma2(nm, make_float2(uu.z, uu.w), make_float2(f[4 * hf + 2], f[4 * hf + 3])),
+                                      make_float2(vv.z, vv.w));
+              f[4 * hf] = y0.x; f[4 * hf + 1] = y0.y; f[4 * hf + 2] = y1.x; f[4 * hf + 3] = y1.y;
+            }
+          }
+          st_shared_v4(e0 + hh * (128 * ROWB) + row * ROWB + d * 2, pack_bf16x2(f[0], f[1]),
+                       pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (elected) {
+        const int ts_rows = tq.T * tq.S_loc;
+        const int b = m0 / ts_rows, t = (m0 / tq.S_loc) % tq.T, s0 = m0 % tq.S_loc;
+#pragma unroll
+        for (int hh = 0; hh < HPT; ++hh) {
+          const int gcol = n0 + hh * HD, part = gcol / tq.C, h = (gcol % tq.C) / HD;
+          tma_store_5d(&tmD, sE + hh * (128 * ROWB), 0, t, s0, h, part * tq.B + b);
+        }
+        bulk_commit_group();
+      }
+      tc_fence_before();
+      if (leader) mbar_arrive(&tempty[acc]);
+      else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+    }
+    if (elected) bulk_wait_group_read0();
+   }
   } else if (warp >= 4 && EPI != EPI_RES_REMOTE) {
     // Bulk-tensor epilogue, EPI_WG warpgroups: warpgroup h (warps 4+4h .. 7+4h, TMEM lane quadrant
     // = warp % 4, thread = accumulator row) owns the tile's EB-column boxes b with b % EPI_WG == h.
@@ -634,7 +724,14 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   }
   td = ta;
   tr = ta;
-  if (EPI != EPI_RES_REMOTE) {
+  if (Cfg::TSEQ) {  // 5-D store view of the temporal layout: {DP, T, S_loc, NH, 3B}
+    const TseqShape& q = ev.tseq;
+    const uint64_t row = kTseqDP * 2;
+    uint64_t dt[5] = {(uint64_t)kTseqDP, (uint64_t)q.T, (uint64_t)q.S_loc, (uint64_t)q.NH, (uint64_t)(3 * q.B)};
+    uint64_t st5[4] = {row, (uint64_t)q.T * row, (uint64_t)q.S_loc * q.T * row, (uint64_t)q.NH * q.S_loc * q.T * row};
+    uint32_t bx[5] = {(uint32_t)kTseqDP, 1, BM, 1, 1};
+    if (!make_tmap_bf16(&td, D, 5, dt, st5, bx, CU_TENSOR_MAP_SWIZZLE_NONE, why)) return cudaErrorInvalidValue;
+  } else if (EPI != EPI_RES_REMOTE) {
     if (!make_tmap_bf16(&td, D, 2, dd, sd, bd, esw, why)) return cudaErrorInvalidValue;
     if (EPI == DSP_EPI_RESIDUAL && !make_tmap_bf16(&tr, R, 2, dd, sd, bd, esw, why))
       return cudaErrorInvalidValue;
@@ -664,6 +761,31 @@ static cudaError_t dispatch_bn(const void* A, const void* W, const void* R, void
     case 64: return run_gemm<64, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
     default: return run_gemm<32, EPI>(A, W, R, D, M, N, K, num_sms, st, why, ev, rm);
   }
+}
+
+int64_t tseq_bytes(const TseqShape& t) {
+  return 3 * (int64_t)t.B * t.NH * t.S_loc * t.T * kTseqDP * 2;
+}
+
+bool tseq_ok(int64_t B, int64_t T, int64_t S_loc, int64_t C, int NH) {
+  (void)B;
+  // T >= 64: at T = 16 the token-major gathers already run near the HBM floor (32 us at configs[1])
+  // and the head-at-a-time epilogue costs the QKV GEMM more than the attention gains
+  return T >= 64 && NH > 0 && C % NH == 0 && C / NH == kTseqDh && S_loc % BM == 0 && (3 * C) % (2 * kTseqDh) == 0;
+}
+
+cudaError_t launch_gemm_bf16_tseq(const void* A, const void* W, const EpiVec* ln, void* qkv_tseq, const TseqShape& ts,
+                                  int64_t M, int64_t K, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  if (!tseq_ok(ts.B, ts.T, ts.S_loc, ts.C, ts.NH) || M != (int64_t)ts.B * ts.T * ts.S_loc) {
+    if (why) *why = "TSEQ layout: unsupported shape";
+    return cudaErrorNotSupported;
+  }
+  EpiVec ev = ln ? *ln : EpiVec{};
+  ev.tseq = ts;
+  constexpr int BNT = 2 * kTseqDh;  // two heads per tile
+  if (ln) return run_gemm<BNT, EPI_LN_TSEQ>(A, W, nullptr, qkv_tseq, M, 3 * ts.C, K, num_sms, st, why, ev);
+  return run_gemm<BNT, EPI_TSEQ>(A, W, nullptr, qkv_tseq, M, 3 * ts.C, K, num_sms, st, why, ev);
 }
 
 cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,

@@ -525,3 +525,46 @@ def test_model_prepared_cross_virtual_ranks_n_invariant(impl):
     g.run(lambda r: g.ctx[r].st_model_forward(shape, layers, Xr[r], Yr[r], impl=impl))
     got = np.concatenate([bits16(Yr[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
     assert np.array_equal(got.reshape(-1), ref.reshape(-1))
+
+
+# ---------------------------------------------------------------- temporal TSEQ layout (T >= 64)
+TSEQ_SHAPE = synth.BlockShape(1, 64, 128, 1152, 16, "bf16")  # T >= 64, S_loc % 128 == 0, Dh = 72
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+def test_block_tseq_vs_oracle(prepared):
+    """T = 64, S = 128: the temporal stage runs on the sequence-major q | k | v layout (the
+    temporal QKV GEMM's per-head TMA-box epilogue + contiguous FMHA tiles); full block against
+    the float64 oracle at the block gate (R22)."""
+    sh = TSEQ_SHAPE
+    xs, Ws = _setup(sh)
+    got = to_f64(_run_block_n1(sh, xs, Ws, prepared=prepared))
+    ref = ob.st_block(synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16"), sh.NH)
+    print(assert_block_close(got.reshape(ref.shape), ref))
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+def test_block_tseq_equals_token_major_bitwise(prepared):
+    """The TSEQ temporal stage (N = 1, S_loc = 128) and the token-major one (N = 2 virtual ranks,
+    S_loc = 64 < 128) compute every output with the same arithmetic: the whole blocks are bitwise
+    equal (R35: the QKV tile width does not change any bit; the FMHA tiles hold the same rows)."""
+    m = dsp()
+    sh, N = TSEQ_SHAPE, 2
+    xs, Ws = _setup(sh)
+    ref1 = bits16(_run_block_n1(sh, xs, Ws, prepared=prepared))
+    shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
+    ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
+    act = sh.M * 2 // N
+    g = VirtualGroup(N, ws + act)
+    W = weights_dev(Ws, "bf16")
+    if prepared:
+        W["prepared"] = g.ctx[0].prepare_block(shape, W)
+        torch.cuda.synchronize()
+    xsh = osw.split(xs, osw.DIM_T, N)
+    X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
+    Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
+    for r in range(N):
+        g.ctx[r].set_workspace(g.region[r][:ws])
+    g.run(lambda r: g.ctx[r].st_block_forward(shape, W, X[r], Y[r], impl="p2p"))
+    got = np.concatenate([bits16(Y[r]).reshape(sh.B, sh.T // N, sh.S, sh.C) for r in range(N)], axis=1)
+    assert np.array_equal(got.reshape(-1), ref1.reshape(-1))
