@@ -1392,6 +1392,10 @@ __global__ void __launch_bounds__(384, 1)
 // TMEM: S0 [0,128), S1 [128,256), O0 [256, 256+DP), O1 [384, 384+DP).
 //   warp 0 TMA producer   warp 1 MMA issuer + TMEM allocator   warp 2 V patcher   warp 3 idle
 //   warps 4-7 slot 0 (even items)   warps 8-11 slot 1 (odd items)
+#ifndef DSP_FMHA_SEQ_DIAG
+#define DSP_FMHA_SEQ_DIAG 1  // block-diagonal tiles (T = 16: 8 sequences per tile) on fmha_seq_kernel too
+#endif
+constexpr bool kSeqDiag = DSP_FMHA_SEQ_DIAG != 0;
 template <int NA, int RB>
 struct SeqCfg {
   using Base = FmhaCfg<NA, RB>;
@@ -1576,8 +1580,13 @@ __global__ void __launch_bounds__(384, 1)
       if ((int)(k & 1) != slot) continue;
       mbar_wait(&s_full[slot], n & 1);
       tc_fence_after();
-      float m = -INFINITY;
-      softmax_step_pt<DP>(G, tS, tO, 0, m, p.kv_last);
+      float m = -INFINITY, l = 0.f;
+      if (G.diag) {  // G = 128 / L sequences per tile: each thread only its diagonal block, l in fp32
+        if (G.nhalf * G.hcols > 32) softmax_tile_diag<64, true>(G, tS, nullptr, m, l, nullptr, bar_id);
+        else softmax_tile_diag<32, true>(G, tS, nullptr, m, l, nullptr, bar_id);
+      } else {
+        softmax_step_pt<DP>(G, tS, tO, 0, m, p.kv_last);
+      }
       mbar_arrive(&p_full[slot]);
       mbar_wait(&o_done[slot], n & 1);  // P.V done: O final
       ++n;
@@ -1587,8 +1596,12 @@ __global__ void __launch_bounds__(384, 1)
         named_bar_sync(bar_id, 128);
         store_pending = 0;
       }
-      epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
-                                         tile_coord(p, item, -1), &o_free[slot], store_pending);
+      if (G.diag)
+        epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, l, bar_id, tile_coord(p, item, -1),
+                                   &o_free[slot], store_pending);
+      else
+        epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
+                                           tile_coord(p, item, -1), &o_free[slot], store_pending);
     }
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
   }
@@ -2046,7 +2059,7 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
 #endif
 #ifndef DSP_FMHA_NO_SEQ
   if constexpr (SeqCfg<NA, RB>::OK) {
-    if (p.G == 1 && p.n_kv == 1 && !p.cross && p.Dh <= SeqCfg<NA, RB>::DP - 8) {
+    if (p.n_kv == 1 && !p.cross && p.Dh <= SeqCfg<NA, RB>::DP - 8 && (p.G == 1 || kSeqDiag)) {
       auto kp = fmha_seq_kernel<NA, RB>;
       static bool attr_sq = false;
       if (!attr_sq) {
