@@ -17,4 +17,5 @@ from .gen import (  # noqa: F401
     splitmix64, uniform_pm1, round_to_bf16_bits, bf16_bits_to_f64, to_f64,
     TENSOR_IDS, WEIGHT_NAMES, CONFIGS, BlockShape, make_x, make_block_weights,
     zero_block_weights, make_index_tagged, tensor_id, CROSS_NAMES, make_cross_weights, make_context,
+    LATTE_NAMES, make_latte_weights, make_modulation, make_temporal_pe,
 )

@@ -206,3 +206,47 @@ def make_index_tagged(shape: BlockShape, seed: int, t_range=None, s_range=None) 
     h = (splitmix64(_keys(seed, 0xFFF, idx)) & np.uint64(0xFFFF))
     v = np.where(c == 0, g & np.uint64(0xFFFF), np.where(c == 1, (g >> np.uint64(16)) & np.uint64(0xFFFF), h))
     return v.astype(np.uint16)
+
+
+LATTE_NAMES = ("ln_m_w", "ln_m_b", "w_fc1_s", "w_fc2_s")
+
+
+def make_latte_weights(shape: BlockShape, seed: int, layer: int = 0) -> dict:
+    """The Latte pair's spatial MLP (R38): LN_m gamma / beta, w_fc1_s [4C, C], w_fc2_s
+    [C, 4C]; tensor ids 1000 + 8*layer + k; scales as the block's MLP."""
+    C = shape.C
+
+    def u(k, n):
+        return uniform_pm1(seed, 1000 + 8 * layer + k, np.arange(n, dtype=np.uint64))
+
+    out = {"ln_m_w": 1.0 + 0.1 * u(0, C), "ln_m_b": 0.1 * u(1, C),
+           "w_fc1_s": u(2, 4 * C * C).reshape(4 * C, C) * math.sqrt(3.0 / C),
+           "w_fc2_s": u(3, 4 * C * C).reshape(C, 4 * C) * (0.5 * math.sqrt(3.0 / (4 * C)))}
+    return {k: _store(v, shape.dtype) for k, v in out.items()}
+
+
+def make_modulation(shape: BlockShape, seed: int, layer: int = 0, sublayers=("s", "t", "m")) -> dict:
+    """adaLN-Zero modulation (R36) of sample b: {sublayer: (shift, scale, gate)}, each
+    [B, C] float32 (the per-step conditioning, already through SiLU + Linear): shift = 0.1 v,
+    scale = 0.1 v, gate = 1 + 0.25 v (a trained, non-zero gate).  Tensor ids 1500 + 16*layer + 4*i + j."""
+    B, C = shape.B, shape.C
+    out = {}
+    for i, k in enumerate(sublayers):
+        def u(j):
+            return uniform_pm1(seed, 1500 + 16 * layer + 4 * i + j, np.arange(B * C, dtype=np.uint64)).reshape(B, C)
+        out[k] = ((0.1 * u(0)).astype(np.float32), (0.1 * u(1)).astype(np.float32),
+                  (1.0 + 0.25 * u(2)).astype(np.float32))
+    return out
+
+
+def make_temporal_pe(shape: BlockShape) -> np.ndarray:
+    """Sinusoidal temporal positional embedding [T, C] (R37, Latte / "Attention is all
+    you need" table): pe[t, 2i] = sin(t / 10000^(2i/C)), pe[t, 2i+1] = cos(...), stored dtype."""
+    T, C = shape.T, shape.C
+    t = np.arange(T, dtype=np.float64)[:, None]
+    i = np.arange(C // 2, dtype=np.float64)[None, :]
+    ang = t / np.power(10000.0, 2.0 * i / C)
+    pe = np.empty((T, C))
+    pe[:, 0::2] = np.sin(ang)
+    pe[:, 1::2] = np.cos(ang)
+    return _store(pe, shape.dtype)
