@@ -108,6 +108,16 @@ typedef struct {
   const void *ln_c_w, *ln_c_b, *w_q_c, *w_kv_c, *w_o_c;
   const void* ctx_tokens;
   int64_t ctx_len;
+  /* Optional Latte pair (R38, "basically follows Latte"; NULL w_fc1_s = none):
+   *   y1 <- y1 + W2_s gelu_tanh(W1_s LN_m(y1))   right after the spatial attention, on the
+   * T-shards (position-wise: local).  ln_m_w / ln_m_b [C], w_fc1_s [4C, C], w_fc2_s [C, 4C]; bf16;
+   * not with the FUSED transport. */
+  const void *ln_m_w, *ln_m_b, *w_fc1_s, *w_fc2_s;
+  /* Optional temporal positional embedding (R37; NULL = none): pe_t [T, C] (all T frames, every
+   * rank) added to the residual stream after the spatial part, y1[b,t,s] += pe_t[t], on the
+   * S-shards (each holds all frames of its columns).  Latte adds it before the first temporal
+   * block: set it on the first block of a stack only. */
+  const void* pe_t;
 } dsp_block_weights_t;
 
 /* ---------------------------------------------------------------- lifecycle */
@@ -208,10 +218,11 @@ int64_t dsp_ctx_launch_count(dsp_ctx_t ctx);
 const char* dsp_status_str(dsp_status_t status);
 const char* dsp_last_error(dsp_ctx_t ctx);   /* "" if none; valid until the next call */
 int dsp_abi_version(void);                   /* DSP_ABI_VERSION */
-#define DSP_ABI_VERSION 5  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage;
+#define DSP_ABI_VERSION 6  /* 2: dsp_block_weights_t.prepared, block preparation; 3: optional cross stage;
                               4: device-resident barrier epochs, barrier timeout + error check,
                               exported switch pack / unpack and gather unpack; 5: Ulysses block,
-                              stage clocks, taps, collective emulation */
+                              stage clocks, taps, collective emulation; 6: Latte pair, temporal
+                              positional embedding, dsp_adaln_fold */
 
 /* ----------------------------------------------------------- layout (bytes) */
 
@@ -407,6 +418,22 @@ dsp_status_t dsp_nd_block_forward(dsp_ctx_t ctx, const int64_t* dims, int ndim, 
  * layer).  Errors: as dsp_st_block_forward; SHAPE (L < 1); NULL. */
 dsp_status_t dsp_st_model_forward(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* const* w,
                                   int L, const void* x_local, void* y_local, dsp_switch_impl_t impl, void* stream);
+
+/* adaLN-Zero conditioning of one block for ONE sample (R36, DiT as cited by P:137):
+ *   y = x + gate_k * F_k(LN_k(x) * (1 + scale_k) + shift_k)   for each sublayer k
+ * with k = spatial attention, temporal attention, MLP, and the Latte pair's spatial MLP.  At B = 1
+ * (the paper's batch) this is the plain block with modulated weights:
+ *   gamma_k' = gamma_k (1 + scale_k),  beta_k' = beta_k (1 + scale_k) + shift_k,
+ *   W_out_k' = diag(gate_k) W_out_k    (W_out = w_o_s, w_o_t, w_fc2, w_fc2_s),
+ * which this call writes (bf16) into the buffers `out` points to: out->ln1_w/ln1_b, ln2_w/ln2_b,
+ * ln3_w/ln3_b, w_o_s, w_o_t, w_fc2 (and ln_m_w/ln_m_b, w_fc2_s when w->w_fc1_s is set) -- the
+ * caller owns them (same sizes as the inputs) and copies every other pointer of *w into *out.
+ * The conditioned block is then dsp_st_block_forward(out) (prepare it again when preparing).
+ * mod: device f32 [4][3][C] = (shift, scale, gate) for sublayers (spatial attention, temporal
+ * attention, MLP, spatial MLP).  Once per sampling step per block; enqueued on `stream`.
+ * Errors: NULL, UNSUPPORTED (f32, B != 1), ALIGNMENT, CUDA. */
+dsp_status_t dsp_adaln_fold(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* w, const float* mod,
+                            const dsp_block_weights_t* out, void* stream);
 
 /* Bytes of the prepared-weights buffer for one bf16 block of this shape (0 for f32). */
 size_t dsp_block_prepared_bytes(const dsp_shape_t* shape);

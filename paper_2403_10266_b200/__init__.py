@@ -47,13 +47,16 @@ class Shape(ctypes.Structure):
 
 
 CROSS_NAMES = ("ln_c_w", "ln_c_b", "w_q_c", "w_kv_c", "w_o_c")
+LATTE_NAMES = ("ln_m_w", "ln_m_b", "w_fc1_s", "w_fc2_s")  # the Latte pair's spatial MLP (R38)
+ADALN_SUBLAYERS = ("s", "t", "m", "ms")  # dsp_adaln_fold's mod rows: spatial attn, temporal attn, MLP, spatial MLP
 
 
 class BlockWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("ln1_w", "ln1_b", "w_qkv_s", "w_o_s", "ln2_w", "ln2_b", "w_qkv_t",
                                                "w_o_t", "ln3_w", "ln3_b", "w_fc1", "w_fc2")] + [
         ("ln_eps", ctypes.c_float), ("prepared", ctypes.c_void_p)] + [
-        (n, ctypes.c_void_p) for n in CROSS_NAMES] + [("ctx_tokens", ctypes.c_void_p), ("ctx_len", ctypes.c_int64)]
+        (n, ctypes.c_void_p) for n in CROSS_NAMES] + [("ctx_tokens", ctypes.c_void_p), ("ctx_len", ctypes.c_int64)] + [
+        (n, ctypes.c_void_p) for n in LATTE_NAMES] + [("pe_t", ctypes.c_void_p)]
 
 
 class SwitchPlan(ctypes.Structure):
@@ -116,6 +119,7 @@ def lib() -> ctypes.CDLL:
             "dsp_st_model_forward": [vp, P(Shape), P(P(BlockWeights)), ctypes.c_int, vp, vp, ctypes.c_int, vp],
             "dsp_st_block_forward_host": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, ctypes.c_int, vp],
             "dsp_st_block_prepare": [vp, P(Shape), P(BlockWeights), vp, ctypes.c_size_t, vp],
+            "dsp_adaln_fold": [vp, P(Shape), P(BlockWeights), vp, P(BlockWeights), vp],
             "dsp_st_block_forward_host_pipelined": [vp, P(Shape), P(BlockWeights), ctypes.c_int, P(vp), P(vp),
                                                     P(vp), P(vp), ctypes.c_int, vp],
             "dsp_layer_norm": [vp, ctypes.c_int, i64, i64, vp, vp, vp, ctypes.c_float, vp, vp],
@@ -410,15 +414,34 @@ class Context:
 
     @staticmethod
     def block_weights(W: dict, eps: float = 1e-5) -> BlockWeights:
-        """W: the 12 weight tensors by name, plus optionally "prepared" (from prepare_block) and the
-        cross stage (CROSS_NAMES + "ctx_tokens" [B, Lc, C])."""
+        """W: the 12 weight tensors by name, plus optionally "prepared" (from prepare_block), the
+        cross stage (CROSS_NAMES + "ctx_tokens" [B, Lc, C]), the Latte pair (LATTE_NAMES) and the
+        temporal positional embedding "pe_t" [T, C]."""
         prep = W.get("prepared")
         cross = [None] * 5 + [None, 0]
         if W.get("ln_c_w") is not None:
             ctxt = W["ctx_tokens"]
             cross = [_ptr(W[n]) for n in CROSS_NAMES] + [_ptr(ctxt), int(ctxt.shape[-2])]
+        latte = [_ptr(W[n]) if W.get(n) is not None else None for n in LATTE_NAMES]
+        pe = W.get("pe_t")
         return BlockWeights(*[_ptr(W[n]) for n in WEIGHT_NAMES], ctypes.c_float(eps),
-                            None if prep is None else _ptr(prep), *cross)
+                            None if prep is None else _ptr(prep), *cross, *latte, None if pe is None else _ptr(pe))
+
+    def adaln_fold(self, shape, W: dict, mod: torch.Tensor, stream=None) -> dict:
+        """dsp_adaln_fold (R36, B = 1): returns a copy of W whose LayerNorm parameters and output
+        projections carry sample 0's adaLN-Zero modulation; mod: f32 CUDA tensor [4, 3, C] rows
+        (shift, scale, gate) for ADALN_SUBLAYERS (the spatial-MLP row is read only with a Latte pair)."""
+        out = {k: v for k, v in W.items() if k != "prepared"}
+        names = ["ln1_w", "ln1_b", "w_o_s", "ln2_w", "ln2_b", "w_o_t", "ln3_w", "ln3_b", "w_fc2"]
+        if W.get("w_fc1_s") is not None:
+            names += ["ln_m_w", "ln_m_b", "w_fc2_s"]
+        for n in names:
+            out[n] = torch.empty_like(W[n])
+        bw_in = self.block_weights({k: v for k, v in W.items() if k != "prepared"})
+        bw_out = self.block_weights(out)
+        self._call("dsp_adaln_fold", ctypes.byref(shape), ctypes.byref(bw_in), _ptr(mod.contiguous()),
+                   ctypes.byref(bw_out), _stream(stream))
+        return out
 
     def prepare_block(self, shape, W: dict, prepared=None, stream=None) -> torch.Tensor:
         """dsp_st_block_prepare: fold the three LayerNorms into their GEMMs' weights once.

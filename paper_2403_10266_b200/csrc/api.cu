@@ -118,7 +118,7 @@ BlockWs block_ws(const dsp_shape_t* s, int world) {
 // Prepared (LayerNorm-folded) weights of one bf16 block: W o gamma for the three
 // LayerNorm -> linear pairs and their per-output-column u = (W o gamma) 1, v = W beta.
 struct PrepLayout {
-  int64_t wf_s, wf_t, wf_1, uv, wf_c, uv_c, total;
+  int64_t wf_s, wf_t, wf_1, uv, wf_c, uv_c, wf_1s, uv_1s, total;
 };
 PrepLayout prep_layout(int64_t C) {
   PrepLayout p{};
@@ -128,7 +128,9 @@ PrepLayout prep_layout(int64_t C) {
   p.uv = p.wf_1 + align256(4 * C * C * 2);
   p.wf_c = p.uv + align256(20 * C * 4);     // cross stage q projection (filled when ln_c_w is set)
   p.uv_c = p.wf_c + align256(C * C * 2);
-  p.total = p.uv_c + align256(2 * C * 4);
+  p.wf_1s = p.uv_c + align256(2 * C * 4);   // Latte pair spatial FC1 (filled when w_fc1_s is set, R38)
+  p.uv_1s = p.wf_1s + align256(4 * C * C * 2);
+  p.total = p.uv_1s + align256(8 * C * 4);
   return p;
 }
 
@@ -867,6 +869,17 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     if (s->B * w->ctx_len > s->B * s->T * s->S / ctx->world)
       return fail(ctx, DSP_ERR_UNSUPPORTED, "context longer than the local tokens per sample");
   }
+  const bool latte = w->w_fc1_s != nullptr;
+  if (latte) {
+    const void* lp[4] = {w->ln_m_w, w->ln_m_b, w->w_fc1_s, w->w_fc2_s};
+    for (int i = 0; i < 4; ++i)
+      if (!lp[i] || !aligned16(lp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "Latte weight %d NULL or not 16-B aligned", i);
+    if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "the Latte pair runs on the bf16 path");
+    if (impl == DSP_SWITCH_FUSED && ctx->world > 1)
+      return fail(ctx, DSP_ERR_UNSUPPORTED, "the Latte pair does not run with the fused switch");
+  }
+  if (w->pe_t && (s->dtype != DSP_BF16 || !aligned16(w->pe_t) || s->C % 8))
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "temporal positional embedding: bf16, 16-B aligned, C %% 8 == 0");
   if (w->prepared && s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared weights exist for the bf16 path only");
   if (w->prepared && (s->C % 8 || s->C > 256 * kRowStatsMaxV || s->C / gemm_part_cols(s->C) > kMaxParts))
     return fail(ctx, DSP_ERR_UNSUPPORTED, "prepared path needs C %% 8 == 0, C <= %d and C / BN <= %d",
@@ -953,7 +966,27 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   // a2-a4: y1 = x + MHA_S(LN1 x), local on T-shards, stored in y (N == 1 prepared: + LN2 partials)
   DSP_TRY(attn_stage(ctx, s, Tn, s->S, DSP_DIM_S, fold ? x : h, fold ? wf_s : w->w_qkv_s, w->w_o_s, x, y, qkv, o,
                      st, DSP_STAGE_QKV_S, fold ? &ev1 : nullptr, fused ? &rm_ts : nullptr,
-                     fold && N == 1 ? parts : nullptr));
+                     fold && (N == 1 || latte) ? parts : nullptr));
+  if (latte) {  // R38: y1 += W2_s gelu(W1_s LN_m(y1)), local on the T-shards (LN_m from PROJ_S's partials)
+    std::string why;
+    cudaError_t e2;
+    if (fold) {
+      const float* uv1s = reinterpret_cast<const float*>(prep + P.uv_1s);
+      EpiVec evm{};
+      evm.col_u = uv1s; evm.col_v = uv1s + 4 * C;
+      evm.part_in = parts; evm.nparts_in = nparts; evm.part_cnt = part_cnt; evm.eps = eps;
+      e2 = launch_gemm_bf16_ln(y, prep + P.wf_1s, evm, big, tok, 4 * C, C, true, ctx->num_sms, st, &why);
+    } else {
+      DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, y, w->ln_m_w, w->ln_m_b, eps, h, st), "LN_m");
+      ctx->launches += 1;
+      e2 = launch_gemm_bf16(h, w->w_fc1_s, nullptr, big, tok, 4 * C, C, DSP_EPI_GELU, ctx->num_sms, st, &why);
+    }
+    if (e2 == cudaSuccess)  // (+ the partials LN2 folds at N == 1)
+      e2 = fold && N == 1 ? launch_gemm_bf16_res_stats(big, w->w_fc2_s, y, y, tok, C, 4 * C, parts, ctx->num_sms, st, &why)
+                          : launch_gemm_bf16(big, w->w_fc2_s, y, y, tok, C, 4 * C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
+    if (e2 != cudaSuccess) return cuda_fail(ctx, e2, "Latte spatial MLP", why);
+    ctx->launches += 2;
+  }
   // a5: switch T -> S (fused: the out-projection already stored every row at its owner)
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
@@ -966,13 +999,17 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     cur = ys;
   }
   mark(ctx, DSP_STAGE_SWITCH_TS, 1, st);
+  if (w->pe_t) {  // R37: y1 += pe_t[t] on the S-shards (every frame of the local columns)
+    DSP_CUDA(ctx, launch_add_temporal_pe(cur, w->pe_t, s->B, s->T, Sn, C, st), "temporal positional embedding");
+    ctx->launches += 1;
+  }
   if (ctx->tap[DSP_TAP_Y1]) DSP_CUDA(ctx, cudaMemcpyAsync(ctx->tap[DSP_TAP_Y1], cur, act, cudaMemcpyDeviceToDevice, st), "tap y1");
   // a6-a9: y2 = y1 + MHA_T(LN2 y1), local on S-shards (in place; prepared: + LN3 partials)
   mark(ctx, DSP_STAGE_LN2, 0, st);
   if (!fold) {
     DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
     ctx->launches += 1;
-  } else if (N > 1) {
+  } else if (N > 1 || w->pe_t) {  // the rows moved, or pe changed them: their partials again
     DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, cur, parts, st), "LN2 partials");
     ctx->launches += 1;
   }
@@ -1169,6 +1206,8 @@ dsp_status_t dsp_st_block_forward_ulysses(dsp_ctx_t ctx, const dsp_shape_t* s, c
   if (s->num_heads % N) return fail(ctx, DSP_ERR_UNSUPPORTED, "Ulysses needs N | num_heads (N=%d, heads=%d)", N, s->num_heads);
   if (((s->C / N) * 2) % 16) return fail(ctx, DSP_ERR_ALIGNMENT, "Ulysses needs C/N*2 %% 16 == 0");
   if (w->ln_c_w) return fail(ctx, DSP_ERR_UNSUPPORTED, "the Ulysses block has no cross stage");
+  if (w->w_fc1_s || w->pe_t)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "the Ulysses block has no Latte pair / temporal positional embedding");
   const void* wp[12] = {w->ln1_w, w->ln1_b, w->w_qkv_s, w->w_o_s, w->ln2_w, w->ln2_b,
                         w->w_qkv_t, w->w_o_t, w->ln3_w, w->ln3_b, w->w_fc1, w->w_fc2};
   for (int i = 0; i < 12; ++i)
@@ -1432,6 +1471,32 @@ size_t dsp_block_prepared_bytes(const dsp_shape_t* s) {
   return (size_t)prep_layout(s->C).total;
 }
 
+dsp_status_t dsp_adaln_fold(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const float* mod,
+                            const dsp_block_weights_t* out, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  if (!w || !mod || !out) return fail(ctx, DSP_ERR_NULL, "NULL argument");
+  if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "adaLN fold: bf16 weights only");
+  if (s->B != 1) return fail(ctx, DSP_ERR_UNSUPPORTED, "adaLN fold is per sample: B must be 1 (B = %lld)", (long long)s->B);
+  const int64_t C = s->C;
+  const bool latte = w->w_fc1_s != nullptr;
+  // sublayer k: (LN gamma, beta, output weight [C, K]) and where the modulated copies go (R36)
+  const AdaFold jobs[4] = {
+      {w->ln1_w, w->ln1_b, w->w_o_s, (void*)out->ln1_w, (void*)out->ln1_b, (void*)out->w_o_s, mod, C},
+      {w->ln2_w, w->ln2_b, w->w_o_t, (void*)out->ln2_w, (void*)out->ln2_b, (void*)out->w_o_t, mod + 3 * C, C},
+      {w->ln3_w, w->ln3_b, w->w_fc2, (void*)out->ln3_w, (void*)out->ln3_b, (void*)out->w_fc2, mod + 6 * C, 4 * C},
+      {w->ln_m_w, w->ln_m_b, w->w_fc2_s, (void*)out->ln_m_w, (void*)out->ln_m_b, (void*)out->w_fc2_s, mod + 9 * C, 4 * C}};
+  const int nj = latte ? 4 : 3;
+  for (int j = 0; j < nj; ++j) {
+    const void* ptr[6] = {jobs[j].gamma, jobs[j].beta, jobs[j].W, jobs[j].gamma_out, jobs[j].beta_out, jobs[j].W_out};
+    for (int i = 0; i < 6; ++i)
+      if (!ptr[i]) return fail(ctx, DSP_ERR_NULL, "adaLN fold: sublayer %d tensor %d is NULL", j, i);
+  }
+  DSP_CUDA(ctx, launch_adaln_fold(nj, jobs, C, (cudaStream_t)stream), "adaLN fold");
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
 dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, void* prep,
                                   size_t prep_bytes, void* stream) {
   DSP_TRY(check_ctx(ctx));
@@ -1451,6 +1516,7 @@ dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   uint8_t* p = static_cast<uint8_t*>(prep);
   float* uv = reinterpret_cast<float*>(p + P.uv);
   float* uvc = reinterpret_cast<float*>(p + P.uv_c);
+  float* uv1s = reinterpret_cast<float*>(p + P.uv_1s);
   LnFold jobs[4] = {{w->w_qkv_s, w->ln1_w, w->ln1_b, p + P.wf_s, uv, uv + 3 * C, 3 * C},
                     {w->w_qkv_t, w->ln2_w, w->ln2_b, p + P.wf_t, uv + 6 * C, uv + 9 * C, 3 * C},
                     {w->w_fc1, w->ln3_w, w->ln3_b, p + P.wf_1, uv + 12 * C, uv + 16 * C, 4 * C},
@@ -1458,6 +1524,12 @@ dsp_status_t dsp_st_block_prepare(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   const bool cross = w->ln_c_w && w->ln_c_b && w->w_q_c;
   DSP_CUDA(ctx, launch_fold_ln_weights(cross ? 4 : 3, jobs, C, (cudaStream_t)stream), "fold LN weights");
   ctx->launches += 1;
+  if (w->w_fc1_s) {  // Latte pair: LN_m folded into the spatial FC1 (R38)
+    if (!w->ln_m_w || !w->ln_m_b) return fail(ctx, DSP_ERR_NULL, "Latte pair without ln_m_w / ln_m_b");
+    const LnFold lj = {w->w_fc1_s, w->ln_m_w, w->ln_m_b, p + P.wf_1s, uv1s, uv1s + 4 * C, 4 * C};
+    DSP_CUDA(ctx, launch_fold_ln_weights(1, &lj, C, (cudaStream_t)stream), "fold LN_m weights");
+    ctx->launches += 1;
+  }
   return DSP_OK;
 }
 

@@ -92,6 +92,18 @@ struct LnFold {
 cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
 // per-row LayerNorm partials over `seg`-column segments, bitwise = the residual epilogue's (R30)
 cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st);
+// R37: x [B, T, S_loc, C] += pe [T, C] (bf16, in place)
+cudaError_t launch_add_temporal_pe(void* x, const void* pe, int64_t B, int64_t T, int64_t S_loc, int64_t C,
+                                   cudaStream_t st);
+// R36: one sublayer's adaLN-Zero fold: gamma_out = gamma (1 + scale), beta_out = beta (1 + scale) + shift,
+// W_out = diag(gate) W (W [C, K]); mod = [3][C] f32 (shift, scale, gate)
+struct AdaFold {
+  const void *gamma, *beta, *W;
+  void *gamma_out, *beta_out, *W_out;
+  const float* mod;
+  int64_t K;
+};
+cudaError_t launch_adaln_fold(int njobs, const AdaFold* jobs, int64_t C, cudaStream_t st);
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
 // GEMM epilogue codes beyond the public dsp_epilogue_t
 enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5, EPI_TSEQ = 6, EPI_LN_TSEQ = 7 };

@@ -425,6 +425,84 @@ cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, 
                   (const __nv_bfloat16*)x, eps, (float2*)stats, rows, (int)C, t_clk);
 }
 
+// Temporal positional embedding (R37): x[b, t, s, :] += pe[t, :] on an S-sharded activation
+// [B, T, S_loc, C] (bf16, in place; fp32 add, one rounding).  One thread per 8 channels.
+__global__ void __launch_bounds__(256) add_temporal_pe_kernel(__nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ pe, long rows,
+                                                              int T, int S_loc, int C, unsigned long long* clk) {
+  griddep_wait();
+  griddep_launch_dependents();
+  clk_start(clk);
+  const int cv = C / 8;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < rows * cv) {
+    const long row = idx / cv;
+    const int c8 = (int)(idx % cv);
+    const int t = (int)((row / S_loc) % T);
+    uint4* px = reinterpret_cast<uint4*>(x + row * C) + c8;
+    const uint4 a = *px, b = reinterpret_cast<const uint4*>(pe + (long)t * C)[c8];
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      o[i] = pack_bf16x2(bf16lo(aw[i]) + bf16lo(bw[i]), bf16hi(aw[i]) + bf16hi(bw[i]));
+    *px = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  if (clk) clk_end(clk);
+}
+
+cudaError_t launch_add_temporal_pe(void* x, const void* pe, int64_t B, int64_t T, int64_t S_loc, int64_t C,
+                                   cudaStream_t st) {
+  const long rows = (long)(B * T * S_loc);
+  if (C % 8) return cudaErrorNotSupported;
+  const long n = rows * (C / 8);
+  if (n == 0) return cudaSuccess;
+  return launch_k(add_temporal_pe_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
+                  (__nv_bfloat16*)x, (const __nv_bfloat16*)pe, rows, (int)T, (int)S_loc, (int)C, t_clk);
+}
+
+// adaLN-Zero fold for one sample (R36): per sublayer k, LN affine (1 + scale_k) and shift_k, and
+// the output projection's rows scaled by gate_k.  blockIdx.y = job; grid-stride over elements.
+struct AdaJob {
+  const __nv_bfloat16 *g, *b, *W;  // LN gamma / beta [C], output weight [C, K] (rows = C outputs)
+  __nv_bfloat16 *g_out, *b_out, *W_out;
+  const float* mod;                // [3][C]: shift, scale, gate
+  int K;
+};
+struct AdaJobs {
+  AdaJob j[4];
+};
+__global__ void __launch_bounds__(256) adaln_fold_kernel(AdaJobs jobs, int C) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const AdaJob& J = jobs.j[blockIdx.y];
+  const float* shift = J.mod;
+  const float* scale = J.mod + C;
+  const float* gate = J.mod + 2 * C;
+  const long nW = (long)C * J.K;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nW + C; i += (long)gridDim.x * blockDim.x) {
+    if (i < nW) {
+      const int n = (int)(i / J.K);
+      J.W_out[i] = __float2bfloat16_rn(__bfloat162float(J.W[i]) * gate[n]);
+    } else {
+      const int c = (int)(i - nW);
+      const float sc = 1.f + scale[c];
+      J.g_out[c] = __float2bfloat16_rn(__bfloat162float(J.g[c]) * sc);
+      J.b_out[c] = __float2bfloat16_rn(__fmaf_rn(__bfloat162float(J.b[c]), sc, shift[c]));
+    }
+  }
+}
+
+cudaError_t launch_adaln_fold(int njobs, const AdaFold* jobs, int64_t C, cudaStream_t st) {
+  AdaJobs aj{};
+  for (int i = 0; i < njobs; ++i)
+    aj.j[i] = AdaJob{(const __nv_bfloat16*)jobs[i].gamma, (const __nv_bfloat16*)jobs[i].beta,
+                     (const __nv_bfloat16*)jobs[i].W, (__nv_bfloat16*)jobs[i].gamma_out,
+                     (__nv_bfloat16*)jobs[i].beta_out, (__nv_bfloat16*)jobs[i].W_out, jobs[i].mod, (int)jobs[i].K};
+  if (njobs == 0) return cudaSuccess;
+  return launch_k(adaln_fold_kernel, dim3(148 * 4, njobs), dim3(256), 0, st, 1, aj, (int)C);
+}
+
 cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
   if (seg % 8 || C % seg) return cudaErrorNotSupported;

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_status_strings():
     L = dsp().lib()
-    assert L.dsp_abi_version() == 5
+    assert L.dsp_abi_version() == 6
     for code, name in dsp().STATUS.items():
         assert L.dsp_status_str(code).decode() == name
 
