@@ -1013,6 +1013,12 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, cur, parts, st), "LN2 partials");
     ctx->launches += 1;
   }
+#ifdef DSP_LN2_ROWSTATS  // A/B experiment: LN2 statistics by a row-statistics pass instead of partials
+  if (fold) {
+    DSP_CUDA(ctx, launch_row_stats(tok, C, cur, eps, stats, st), "LN2 stats");
+    ev2.row_stats = stats;
+  }
+#endif
   mark(ctx, DSP_STAGE_LN2, 1, st);
   // (temporal q | k | v sequence-major in big, the attention output in h: both free here)
   DSP_TRY(attn_stage(ctx, s, s->T, Sn, DSP_DIM_T, fold ? cur : h, fold ? wf_t : w->w_qkv_t, w->w_o_t, cur, cur, qkv,

@@ -116,38 +116,55 @@ __host__ __device__ inline TileSched make_tile_sched(int full, int P, int smax) 
 // LayerNorm statistics (mean, rstd) of row r from its producer's per-row partials (mean_p, M2_p)
 // over part_cnt columns each (R30): Chan et al. combination of equal-count partials, in column
 // order.  The row's partials are contiguous: loaded as 16-B vectors up to 24 partials.
+template <int KV>
+__device__ __forceinline__ float2 ln_combine(const EpiVec& ev, const float4 (&pv)[KV]) {
+  const int np = ev.nparts_in;
+  float mean = 0.f, m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < KV; ++i)
+    if (2 * i < np) {
+      mean += pv[i].x;
+      mean += pv[i].z;
+    }
+  mean /= np;
+#pragma unroll
+  for (int i = 0; i < KV; ++i)
+    if (2 * i < np) {
+      const float d0 = pv[i].x - mean, d1 = pv[i].z - mean;
+      m2 += pv[i].y + ev.part_cnt * d0 * d0;
+      m2 += pv[i].w + ev.part_cnt * d1 * d1;
+    }
+  return make_float2(mean, rsqrtf(m2 / (float)(np * ev.part_cnt) + ev.eps));
+}
+__device__ __forceinline__ bool ln_parts_vec(const EpiVec& ev, int kv) {
+  return (ev.nparts_in & 1) == 0 && ev.nparts_in <= 2 * kv && (reinterpret_cast<uintptr_t>(ev.part_in) & 15) == 0;
+}
+template <int KV>
+__device__ __forceinline__ void ln_parts_load(const EpiVec& ev, int r, float4 (&pv)[KV]) {
+  const float4* pp = reinterpret_cast<const float4*>(ev.part_in + (size_t)r * ev.nparts_in);
+#pragma unroll
+  for (int i = 0; i < KV; ++i)
+    if (2 * i < ev.nparts_in) pv[i] = __ldg(pp + i);
+}
+// LayerNorm statistics (mean, rstd) of row r from its producer's per-row partials (mean_p, M2_p)
+// over part_cnt columns each (R30): Chan et al. combination of equal-count partials, in column
+// order.  The row's partials are contiguous: loaded as 16-B vectors up to 24 partials.
 __device__ __forceinline__ float2 ln_stats_from_parts(const EpiVec& ev, int r) {
   constexpr int kVec = 12;
+  if (ln_parts_vec(ev, kVec)) {
+    float4 pv[kVec];
+    ln_parts_load(ev, r, pv);
+    return ln_combine(ev, pv);
+  }
   const int np = ev.nparts_in;
   const float2* pp = ev.part_in + (size_t)r * np;
   float mean = 0.f, m2 = 0.f;
-  if ((np & 1) == 0 && np <= 2 * kVec && (reinterpret_cast<uintptr_t>(pp) & 15) == 0) {
-    float4 pv[kVec];
-#pragma unroll
-    for (int i = 0; i < kVec; ++i)
-      if (2 * i < np) pv[i] = __ldg(reinterpret_cast<const float4*>(pp) + i);
-#pragma unroll
-    for (int i = 0; i < kVec; ++i)
-      if (2 * i < np) {
-        mean += pv[i].x;
-        mean += pv[i].z;
-      }
-    mean /= np;
-#pragma unroll
-    for (int i = 0; i < kVec; ++i)
-      if (2 * i < np) {
-        const float d0 = pv[i].x - mean, d1 = pv[i].z - mean;
-        m2 += pv[i].y + ev.part_cnt * d0 * d0;
-        m2 += pv[i].w + ev.part_cnt * d1 * d1;
-      }
-  } else {
-    for (int i = 0; i < np; ++i) mean += pp[i].x;
-    mean /= np;
-    for (int i = 0; i < np; ++i) {
-      const float2 pv = pp[i];
-      const float d = pv.x - mean;
-      m2 += pv.y + ev.part_cnt * d * d;
-    }
+  for (int i = 0; i < np; ++i) mean += pp[i].x;
+  mean /= np;
+  for (int i = 0; i < np; ++i) {
+    const float2 pv = pp[i];
+    const float d = pv.x - mean;
+    m2 += pv.y + ev.part_cnt * d * d;
   }
   return make_float2(mean, rsqrtf(m2 / (float)(np * ev.part_cnt) + ev.eps));
 }
@@ -404,6 +421,21 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
     };
     if (kRes && elected && pair < num_tiles)
       for (int b = h; b < Cfg::NBOX; b += WG) load_res_box(pair, b);
+    // LayerNorm folded (kLn): the next tile's row statistics (or its rows' partials, up to 8) are
+    // loaded while this tile is processed, so their L2 latency is off the epilogue's critical path
+    constexpr int kPF = 4;
+    const bool pf_parts = kLn && !ev.row_stats && ln_parts_vec(ev, kPF);
+    float4 pfv[kPF];
+    float2 pfrs = make_float2(0.f, 0.f);
+    auto prefetch = [&](int t) {
+      int mr, nc, wd;
+      geom(t, mr, nc, wd);
+      const int r = mr + rank * BM + row;
+      if (r >= M) return;
+      if (ev.row_stats) pfrs = ev.row_stats[r];
+      else if (pf_parts) ln_parts_load(ev, r, pfv);
+    };
+    if (kLn && h == 0 && pair < num_tiles) prefetch(pair);
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
       int m0, n0, width;
@@ -418,8 +450,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       float2* rsm = reinterpret_cast<float2*>(evec + 2 * 2 * BN) + acc * 128;  // row stats, shared by the WGs
       if (kLn) {
         if (h == 0) {
-          if (m0 + row < M) rstat = ev.row_stats ? ev.row_stats[m0 + row] : ln_stats_from_parts(ev, m0 + row);
+          if (m0 + row < M)
+            rstat = ev.row_stats ? pfrs : pf_parts ? ln_combine(ev, pfv) : ln_stats_from_parts(ev, m0 + row);
           rsm[row] = rstat;
+          if (tile + num_pairs < num_tiles) prefetch(tile + num_pairs);
         }
         for (int i = etid; i < width; i += 128 * WG) {
           st_shared_f32(smem_u32(eu + i), ev.col_u[n0 + i]);
