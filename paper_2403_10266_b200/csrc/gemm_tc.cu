@@ -436,6 +436,22 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       else if (pf_parts) ln_parts_load(ev, r, pfv);
     };
     if (kLn && h == 0 && pair < num_tiles) prefetch(pair);
+    // ... and so are the next tile's per-column u, v (at most two columns per thread: BN <= 256)
+    float pu[2] = {0.f, 0.f}, pvv[2] = {0.f, 0.f};
+    auto prefetch_uv = [&](int t) {
+      int mr, nc, wd;
+      geom(t, mr, nc, wd);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int i = etid + k * 128 * WG;
+        if (i < wd) {
+          pu[k] = ev.col_u[nc + i];
+          pvv[k] = ev.col_v[nc + i];
+        }
+      }
+    };
+    static_assert(!kLn || BN <= 2 * 128, "u, v prefetch covers two columns per epilogue thread");
+    if (kLn && pair < num_tiles) prefetch_uv(pair);
     for (int tile = pair; tile < num_tiles; tile += num_pairs, ++it) {
       const int acc = it & 1;
       int m0, n0, width;
@@ -455,10 +471,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
           rsm[row] = rstat;
           if (tile + num_pairs < num_tiles) prefetch(tile + num_pairs);
         }
-        for (int i = etid; i < width; i += 128 * WG) {
-          st_shared_f32(smem_u32(eu + i), ev.col_u[n0 + i]);
-          st_shared_f32(smem_u32(eu + BN + i), ev.col_v[n0 + i]);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int i = etid + k * 128 * WG;
+          if (i < width) {
+            st_shared_f32(smem_u32(eu + i), pu[k]);
+            st_shared_f32(smem_u32(eu + BN + i), pvv[k]);
+          }
         }
+        if (tile + num_pairs < num_tiles) prefetch_uv(tile + num_pairs);
       }
       const bool has_next = tile + num_pairs < num_tiles;
       if (kLn) {
