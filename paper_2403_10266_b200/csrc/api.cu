@@ -916,6 +916,12 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       const int64_t y_off = static_cast<uint8_t*>(y) - static_cast<uint8_t*>(base);
       rm_ts = RemoteMap{ctx->peer_base, ys_off, 1, ctx->rank, (int)s->B, (int)s->T, (int)s->S, (int)(s->T / N), (int)(s->S / N)};
       rm_st = RemoteMap{ctx->peer_base, y_off, 2, ctx->rank, (int)s->B, (int)s->T, (int)s->S, (int)(s->T / N), (int)(s->S / N)};
+      // prepared weights: the T->S barrier is split -- PROJ_S's last CTA arrives, the LN2 partials
+      // pass waits per row for the rank that sent it (f1: no barrier launch, rows consumed as
+      // their sender finishes)
+      rm_ts.signals = ctx->peer_signal;
+      rm_ts.world = N;
+      rm_ts.arrive = w->prepared != nullptr && !w->pe_t;
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -990,7 +996,12 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   // a5: switch T -> S (fused: the out-projection already stored every row at its owner)
   void* cur = y;
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
-  if (fused) {
+  PeerWait ts_wait{};
+  if (fused && rm_ts.arrive) {  // split barrier: the LN2 partials pass below waits per sending rank
+    ts_wait = PeerWait{static_cast<const uint64_t*>(ctx->peer_signal.p[ctx->rank]), (int)s->T, (int)Tn, (int)Sn,
+                       ctx->barrier_timeout_ns};
+    cur = ys;
+  } else if (fused) {
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "fused switch barrier");
     ctx->launches += 1;
     cur = ys;
@@ -1010,7 +1021,7 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
     DSP_CUDA(ctx, launch_layer_norm(s->dtype, tok, C, cur, w->ln2_w, w->ln2_b, eps, h, st), "LN2");
     ctx->launches += 1;
   } else if (N > 1 || w->pe_t) {  // the rows moved, or pe changed them: their partials again
-    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, cur, parts, st), "LN2 partials");
+    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, cur, parts, st, ts_wait, ctx->num_sms), "LN2 partials");
     ctx->launches += 1;
   }
 #ifdef DSP_LN2_ROWSTATS  // A/B experiment: LN2 statistics by a row-statistics pass instead of partials

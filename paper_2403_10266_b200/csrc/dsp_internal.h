@@ -19,6 +19,8 @@ constexpr int kMaxPeers = 8;  // one NVLink/NVSwitch box
 // signal pad slots (uint64) of the P2P barrier (switch.cu): [0, kMaxPeers) peer arrivals,
 // kPadEpoch own barrier counter, kPadError first timeout record; DSP_SIGNAL_PAD_BYTES in dsp.h
 constexpr int kPadEpoch = kMaxPeers, kPadError = kMaxPeers + 1;
+// kPadCount: CTAs of a signalling kernel that have finished (the last one arrives for the rank)
+constexpr int kPadCount = kMaxPeers + 2;
 
 // ---- NCCL, resolved at run time from the libnccl.so.2 torch already loaded ----
 struct NcclApi {
@@ -90,8 +92,17 @@ struct LnFold {
   int64_t N;
 };
 cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
+// per-row wait of a consumer of the S-sharded rows [B, T, S_loc] after a fused T->S switch: row
+// (b, t, s) came from rank t / Tn; wait until that rank's arrival (slot [src] of this rank's pad)
+// reaches this rank's current epoch.  pad == nullptr: no wait.
+struct PeerWait {
+  const uint64_t* pad;
+  int T, Tn, S_loc;
+  uint64_t timeout_ns;
+};
 // per-row LayerNorm partials over `seg`-column segments, bitwise = the residual epilogue's (R30)
-cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st);
+cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st,
+                                const PeerWait& pw = PeerWait{}, int num_sms = 148);
 // R37: x [B, T, S_loc, C] += pe [T, C] (bf16, in place)
 cudaError_t launch_add_temporal_pe(void* x, const void* pe, int64_t B, int64_t T, int64_t S_loc, int64_t C,
                                    cudaStream_t st);
@@ -130,6 +141,12 @@ struct RemoteMap {
   PeerPtrs base;
   int64_t dst_off;  // offset of the destination buffer inside every peer's symmetric buffer
   int mode, rank, B, T, S, Tn, Sn;
+  // arrive != 0: the kernel's last CTA to finish arrives at the signal-pad barrier for this rank
+  // (the first half of p2p_barrier_kernel: epoch + 1, release-stored into every peer's slot
+  // [rank]) once every CTA's rows are stored -- the consumer then waits only for the peers whose
+  // rows it reads (launch_row_partials with a PeerWait) instead of a barrier launch.
+  PeerPtrs signals;
+  int arrive, world;
 };
 cudaError_t launch_gemm_bf16_remote(const void* A, const void* W, const void* R, const RemoteMap& rm, int64_t M,
                                     int64_t N, int64_t K, int num_sms, cudaStream_t st, std::string* why);

@@ -703,10 +703,28 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       if (leader) mbar_arrive(&tempty[acc]);
       else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
     }
+    if (EPI == EPI_RES_REMOTE && rm.arrive) __threadfence_system();  // this thread's peer stores, before the arrival
   }
 
   tc_fence_before();
   cluster_sync();
+  if (EPI == EPI_RES_REMOTE && rm.arrive && threadIdx.x == 0) {
+    // the last CTA to get here arrives at the signal-pad barrier for this rank (RemoteMap): every
+    // CTA's epilogue threads fenced their peer stores at system scope before the cluster barrier
+    uint64_t* pad = static_cast<uint64_t*>(rm.signals.p[rm.rank]);
+    __threadfence_system();
+    const unsigned long long done = atomicAdd(reinterpret_cast<unsigned long long*>(pad + kPadCount), 1ull);
+    if (done == gridDim.x - 1) {
+      __threadfence_system();
+      pad[kPadCount] = 0;
+      const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(pad + kPadEpoch) + 1;
+      pad[kPadEpoch] = epoch;
+      for (int i = 0; i < rm.world; ++i) {
+        uint64_t* remote = static_cast<uint64_t*>(rm.signals.p[i]) + rm.rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote), "l"(epoch) : "memory");
+      }
+    }
+  }
   clk_end(ev.clk);
   if (warp == 1) {
     tc_fence_after();

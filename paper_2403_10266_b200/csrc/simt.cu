@@ -272,38 +272,65 @@ __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel
 // (N > 1), where the rows arrive without the partials their producer computed, so the LN
 // statistics the consuming GEMM combines are the same bits at every N.
 // One thread per (row, segment).
+__device__ __forceinline__ void wait_peer_rows(const PeerWait& pw, uint64_t epoch, long row) {
+  const int src = (int)((row / pw.S_loc) % pw.T) / pw.Tn;
+  const uint64_t* slot = pw.pad + src;
+  uint64_t v = 0, t0 = 0;
+  if (pw.timeout_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+    if (v >= epoch) return;
+    if (pw.timeout_ns) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > pw.timeout_ns) {
+        atomicCAS(reinterpret_cast<unsigned long long*>(const_cast<uint64_t*>(pw.pad) + kPadError), 0ull,
+                  (unsigned long long)((epoch << 16) | (2u << 8) | (unsigned)src));
+        return;
+      }
+    }
+    __nanosleep(64);
+  }
+}
+
 __global__ void __launch_bounds__(256) row_partials_bf16_kernel(const __nv_bfloat16* __restrict__ x, long rows, int C,
                                                                 int seg, float2* __restrict__ parts,
-                                                                unsigned long long* clk) {
+                                                                unsigned long long* clk, PeerWait pw) {
   griddep_wait();
-  griddep_launch_dependents();
+  // a waiting launch lets its dependent (the next, SM-filling GEMM) launch only once its rows are
+  // in: early-resident dependents would hold the SMs the peers' producers need when virtual ranks
+  // share one GPU
+  if (!pw.pad) griddep_launch_dependents();
   clk_start(clk);
   const int nseg = C / seg;
-  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= rows * nseg) {
-    if (clk) clk_end(clk);  // thread 0 of a CTA past the end still closes the clock
-    return;
-  }
-  const long row = idx / nseg;
-  const int sg = (int)(idx % nseg);
-  const uint4* p = reinterpret_cast<const uint4*>(x + row * C + (long)sg * seg);
-  float x0 = 0.f, s1e = 0.f, s1o = 0.f, s2e = 0.f, s2o = 0.f;
-  for (int j = 0; j < seg / 8; ++j) {
-    const uint4 v = p[j];
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  const uint64_t epoch = pw.pad ? *reinterpret_cast<const volatile uint64_t*>(pw.pad + kPadEpoch) : 0;
+  // grid-stride (a waiting launch is capped at one CTA per SM, so it never crowds out the peers'
+  // producers when virtual ranks share one GPU)
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * nseg;
+       idx += (long)gridDim.x * blockDim.x) {
+    const long row = idx / nseg;
+    const int sg = (int)(idx % nseg);
+    if (pw.pad) wait_peer_rows(pw, epoch, row);
+    const uint4* p = reinterpret_cast<const uint4*>(x + row * C + (long)sg * seg);
+    float x0 = 0.f, s1e = 0.f, s1o = 0.f, s2e = 0.f, s2o = 0.f;
+    for (int j = 0; j < seg / 8; ++j) {
+      const uint4 v = p[j];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float lo = __uint_as_float(w[t] << 16), hi = __uint_as_float(w[t] & 0xFFFF0000u);
-      if (j == 0 && t == 0) x0 = lo;
-      const float de = __fadd_rn(lo, -x0), dd = __fadd_rn(hi, -x0);
-      s1e = __fadd_rn(s1e, de);
-      s1o = __fadd_rn(s1o, dd);
-      s2e = __fmaf_rn(de, de, s2e);
-      s2o = __fmaf_rn(dd, dd, s2o);
+      for (int t = 0; t < 4; ++t) {
+        const float lo = __uint_as_float(w[t] << 16), hi = __uint_as_float(w[t] & 0xFFFF0000u);
+        if (j == 0 && t == 0) x0 = lo;
+        const float de = __fadd_rn(lo, -x0), dd = __fadd_rn(hi, -x0);
+        s1e = __fadd_rn(s1e, de);
+        s1o = __fadd_rn(s1o, dd);
+        s2e = __fmaf_rn(de, de, s2e);
+        s2o = __fmaf_rn(dd, dd, s2o);
+      }
     }
+    const float a = __fadd_rn(s1e, s1o), mp = __fmul_rn(a, __frcp_rn((float)seg));
+    parts[idx] = make_float2(__fadd_rn(mp, x0), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2e, s2o)), 0.f));
   }
-  const float a = __fadd_rn(s1e, s1o), mp = __fmul_rn(a, __frcp_rn((float)seg));
-  parts[idx] = make_float2(__fadd_rn(mp, x0), fmaxf(__fmaf_rn(-a, mp, __fadd_rn(s2e, s2o)), 0.f));
+  if (pw.pad) griddep_launch_dependents();
   if (clk) clk_end(clk);  // thread 0 (partial of CTA-wide span; the CTA's other rows finish alongside)
 }
 
@@ -503,12 +530,15 @@ cudaError_t launch_adaln_fold(int njobs, const AdaFold* jobs, int64_t C, cudaStr
   return launch_k(adaln_fold_kernel, dim3(148 * 4, njobs), dim3(256), 0, st, 1, aj, (int)C);
 }
 
-cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st) {
+cudaError_t launch_row_partials(int64_t rows, int64_t C, int seg, const void* x, float2* parts, cudaStream_t st,
+                                const PeerWait& pw, int num_sms) {
   if (rows == 0) return cudaSuccess;
   if (seg % 8 || C % seg) return cudaErrorNotSupported;
   const long n = rows * (C / seg);
-  return launch_k(row_partials_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
-                  (const __nv_bfloat16*)x, (long)rows, (int)C, seg, parts, t_clk);
+  long blocks = (n + 255) / 256;
+  if (pw.pad && blocks > num_sms) blocks = num_sms;
+  return launch_k(row_partials_bf16_kernel, dim3((unsigned)blocks), dim3(256), 0, st, 1, (const __nv_bfloat16*)x,
+                  (long)rows, (int)C, seg, parts, t_clk, pw);
 }
 
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st) {

@@ -180,20 +180,26 @@ def test_p2p_switch_graph_replay_device_epoch():
         c.check_errors()
 
 
+@pytest.mark.parametrize("prepared", [False, True])
 @pytest.mark.parametrize("impl", ["p2p", "fused"])
-def test_block_graph_replay_virtual_ranks_bitwise(impl):
+def test_block_graph_replay_virtual_ranks_bitwise(impl, prepared):
     """The bench's launch mode for P2P / fused at N > 1: each virtual rank's block captured in a
-    CUDA graph and replayed three times equals the N = 1 block bitwise every time."""
+    CUDA graph and replayed three times equals the N = 1 block bitwise every time.  Prepared +
+    fused runs the split T->S barrier (PROJ_S's last CTA arrives, the LN2 partials pass waits per
+    sending rank): its epochs must advance exactly like the barrier kernel's under replay."""
     m = dsp()
     N = 2
     sh = synth.BlockShape(1, 16, 256, 1152, 16, "bf16")
     xs, Ws = _setup(sh)
-    ref1 = bits16(_run_block_n1(sh, xs, Ws))
+    ref1 = bits16(_run_block_n1(sh, xs, Ws, prepared=prepared))
     shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "bf16")
     ws = (m.workspace_bytes(shape, N) + 1023) // 1024 * 1024
     act = sh.M * 2 // N
     g = VirtualGroup(N, ws + act)
     W = weights_dev(Ws, "bf16")
+    if prepared:
+        W["prepared"] = g.ctx[0].prepare_block(shape, W)
+        torch.cuda.synchronize()
     xsh = osw.split(xs, osw.DIM_T, N)
     X = [to_dev(xsh[r], "bf16").reshape(-1) for r in range(N)]
     Y = [g.view(r, ws, act, torch.bfloat16) for r in range(N)]
