@@ -78,8 +78,12 @@ typedef enum { DSP_BF16 = 0, DSP_F32 = 1 } dsp_dtype_t;
  *        epilogue stores every output row directly at its final address in the S-shard
  *        owner's buffer, and the FC2 epilogue stores directly into the T-shard owner's
  *        y_local, over the peer mappings (the NVLink transfer overlaps the GEMM tiles);
- *        one signal-pad barrier after each of the two GEMMs.  Needs the peer buffers of
- *        DSP_SWITCH_P2P; dsp_switch treats FUSED as P2P. */
+ *        one signal-pad barrier after each of the two GEMMs -- with prepared weights split
+ *        into the neighbouring kernels: the GEMM's last CTA arrives (release-stores the epoch
+ *        into every peer's pad) and the next kernel that reads the rows (the LN2 partials pass;
+ *        in dsp_st_model_forward the next block's LN1 partials pass) waits per row only for the
+ *        rank that sent it, so no barrier kernel runs (the last block of a stack keeps its S->T
+ *        barrier).  Needs the peer buffers of DSP_SWITCH_P2P; dsp_switch treats FUSED as P2P. */
 typedef enum { DSP_SWITCH_NCCL = 0, DSP_SWITCH_P2P = 1, DSP_SWITCH_FUSED = 2 } dsp_switch_impl_t;
 
 /* GLOBAL shape of the activation; identical on all ranks. */

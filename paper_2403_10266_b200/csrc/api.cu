@@ -922,6 +922,11 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
       rm_ts.signals = ctx->peer_signal;
       rm_ts.world = N;
       rm_ts.arrive = w->prepared != nullptr && !w->pe_t;
+      // a stack of prepared blocks (dsp_st_model_forward): the S->T barrier is split too -- FC2's last
+      // CTA arrives, the next block's LN1 partials pass waits per row; the last block keeps the barrier
+      rm_st.signals = ctx->peer_signal;
+      rm_st.world = N;
+      rm_st.arrive = w->prepared != nullptr && emit_parts;
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -961,7 +966,11 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   // a1: LN1 (prepared: row statistics of x only)
   mark(ctx, DSP_STAGE_LN1, 0, st);
   if (chain_in && N > 1) {  // the previous block's FC2 partials stayed on the other side of its switch
-    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, x, parts, st), "LN1 partials");
+    // (fused: the previous block's FC2 arrived instead of a barrier; wait per row for its sender)
+    const PeerWait st_wait = fused ? PeerWait{static_cast<const uint64_t*>(ctx->peer_signal.p[ctx->rank]), 2, (int)s->T,
+                                              (int)Tn, (int)Sn, (int)s->S, (int)Sn, ctx->barrier_timeout_ns}
+                                   : PeerWait{};
+    DSP_CUDA(ctx, launch_row_partials(tok, C, part_cnt, x, parts, st, st_wait, ctx->num_sms), "LN1 partials");
     ctx->launches += 1;
   } else if (!chain_in) {
     if (fold) DSP_CUDA(ctx, launch_row_stats(tok, C, x, eps, stats, st), "LN1 stats");
@@ -998,8 +1007,8 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   mark(ctx, DSP_STAGE_SWITCH_TS, 0, st);
   PeerWait ts_wait{};
   if (fused && rm_ts.arrive) {  // split barrier: the LN2 partials pass below waits per sending rank
-    ts_wait = PeerWait{static_cast<const uint64_t*>(ctx->peer_signal.p[ctx->rank]), (int)s->T, (int)Tn, (int)Sn,
-                       ctx->barrier_timeout_ns};
+    ts_wait = PeerWait{static_cast<const uint64_t*>(ctx->peer_signal.p[ctx->rank]), 1, (int)s->T, (int)Tn, (int)Sn,
+                       (int)s->S, (int)Sn, ctx->barrier_timeout_ns};
     cur = ys;
   } else if (fused) {
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "fused switch barrier");
@@ -1096,10 +1105,10 @@ static dsp_status_t block_forward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp
   mark(ctx, DSP_STAGE_FC2, 1, st);
   // a11: switch S -> T back into y
   mark(ctx, DSP_STAGE_SWITCH_ST, 0, st);
-  if (fused) {
+  if (fused && !rm_st.arrive) {
     DSP_CUDA(ctx, launch_p2p_barrier(ctx->peer_signal, ctx->rank, N, ctx->barrier_timeout_ns, st), "fused switch barrier");
     ctx->launches += 1;
-  } else if (N > 1) {
+  } else if (N > 1 && !fused) {
     DSP_TRY(do_switch(ctx, s, DSP_DIM_S, ys, y, impl, st, big, big + act));
   }
   mark(ctx, DSP_STAGE_SWITCH_ST, 1, st);

@@ -92,12 +92,13 @@ struct LnFold {
   int64_t N;
 };
 cudaError_t launch_row_stats(int64_t rows, int64_t C, const void* x, float eps, void* stats, cudaStream_t st);
-// per-row wait of a consumer of the S-sharded rows [B, T, S_loc] after a fused T->S switch: row
-// (b, t, s) came from rank t / Tn; wait until that rank's arrival (slot [src] of this rank's pad)
-// reaches this rank's current epoch.  pad == nullptr: no wait.
+// per-row wait of a consumer of rows that arrived through a fused switch: mode 1 (after T->S):
+// the S-sharded rows [B, T, S_loc], row (b, t, s) sent by rank t / Tn; mode 2 (after S->T): the
+// T-sharded rows [B, Tn, S], row (b, t, s) sent by rank s / Sn.  Waits until that rank's arrival
+// (slot [src] of this rank's pad) reaches this rank's current epoch.  pad == nullptr: no wait.
 struct PeerWait {
   const uint64_t* pad;
-  int T, Tn, S_loc;
+  int mode, T, Tn, S_loc, S, Sn;
   uint64_t timeout_ns;
 };
 // per-row LayerNorm partials over `seg`-column segments, bitwise = the residual epilogue's (R30)

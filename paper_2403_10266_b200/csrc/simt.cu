@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256, kMaxV <= 5 ? 4 : 2) row_stats_bf16_kernel
 // statistics the consuming GEMM combines are the same bits at every N.
 // One thread per (row, segment).
 __device__ __forceinline__ void wait_peer_rows(const PeerWait& pw, uint64_t epoch, long row) {
-  const int src = (int)((row / pw.S_loc) % pw.T) / pw.Tn;
+  const int src = pw.mode == 2 ? (int)(row % pw.S) / pw.Sn : (int)((row / pw.S_loc) % pw.T) / pw.Tn;
   const uint64_t* slot = pw.pad + src;
   uint64_t v = 0, t0 = 0;
   if (pw.timeout_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
