@@ -697,6 +697,127 @@ def run_nd(args):
         dist.destroy_process_group()
 
 
+def train_flops(sh) -> float:
+    """Algorithmic FLOPs of one training step of the block (forward + backward): GEMMs
+    32 tok C^2 forward and twice that backward (dgrad + wgrad); attention 4 B T S^2 C + 4 B S T^2 C
+    forward (QK^T, PV) and 2.5x that backward (S, dP, dV, dK, dQ)."""
+    tok = sh.B * sh.T * sh.S
+    attn = 4 * sh.B * sh.T * sh.S ** 2 * sh.C + 4 * sh.B * sh.S * sh.T ** 2 * sh.C
+    return 96 * tok * sh.C ** 2 + 3.5 * attn
+
+
+def run_train(args):
+    """one training step of the single ST block (configs[1] shape) = forward_train
+    (activations kept) + backward (dx and the twelve fp32 weight gradients) + at N > 1 the ZeRO
+    reduce-scatter of the gradients; CUDA-graph replay, L2 flushed between steps."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2403_10266_b200 as dsp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    sh, N = synth.CONFIGS["blk"], world
+    Tn = sh.T // N
+    ctx = dsp.Context(pg=pg, device=dev)
+    shape = dsp.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, sh.dtype)
+    to_dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16).to(dev)
+    W = {k: to_dev(v) for k, v in synth.make_block_weights(sh, args.seed).items()}
+    X = to_dev(synth.make_x(sh, args.seed, t_range=(rank * Tn, (rank + 1) * Tn)))
+    gen = torch.Generator(device="cpu").manual_seed(args.seed + 1)
+    dY = ((torch.rand(X.shape, generator=gen) * 2 - 1)).to(torch.bfloat16).to(dev)
+    Y, dX = torch.empty_like(X), torch.empty_like(X)
+    ctx.ensure_workspace(dsp.train_workspace_bytes(shape, N))
+    saved = torch.empty(dsp.train_saved_layout(shape, N)["total"], dtype=torch.uint8, device=dev)
+    sizes = [W[n].numel() for n in dsp.GRAD_NAMES]
+    ntot = (sum(sizes) + N - 1) // N * N
+    flat = torch.zeros(ntot, dtype=torch.float32, device=dev)
+    shard = torch.zeros(ntot // N, dtype=torch.float32, device=dev)
+    G, o = {}, 0
+    for n, k in zip(dsp.GRAD_NAMES, sizes):
+        G[n] = flat[o:o + k].view(W[n].shape)
+        o += k
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def fwd():
+        ctx.block_forward_train(shape, W, X, Y, saved, impl="nccl")
+
+    def bwd():
+        flat.zero_()
+        ctx.block_backward(shape, W, saved, X, dY, dX, G, impl="nccl")
+        if N > 1:
+            ctx.grads_reduce(flat, zero_shard=True, out=shard)
+
+    def step():
+        fwd()
+        bwd()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    graphs = {}
+    for name, fn_ in (("step", step), ("fwd", fwd), ("bwd", bwd)):
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        l0 = ctx.launch_count()
+        with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+            fn_()
+        graphs[name] = (g, ctx.launch_count() - l0)
+    torch.cuda.synchronize()
+    K = args.steps
+
+    def timed(g):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+        for a, b in ev:
+            flush.zero_()
+            a.record()
+            g.replay()
+            b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local) as clocks:
+        t_ms = timed(graphs["step"][0])
+    t_f, t_b = timed(graphs["fwd"][0]), timed(graphs["bwd"][0])
+    tokens = sh.B * sh.T * sh.S
+    P, _ = peaks()
+    flops = train_flops(sh)
+    t_roof = flops / N / (P["bf16_tflops"] * 1e12) * 1e3
+    if rank == 0:
+        print(json.dumps({"metric": "ST-block train step (fwd+bwd) tokens/s", "value": tokens * K / (t_ms / 1e3),
+                          "unit": "tokens/s", "n_gpus": N, "steps": K, "warmup": args.warmup, "ms_per_step": t_ms / K,
+                          "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                          "data": "synthetic",
+                          "config": {"workload": "configs[1] single ST block training step: forward_train + backward "
+                                                 "(dx, 12 fp32 weight gradients)" + (" + ZeRO reduce-scatter" if N > 1 else "")
+                                                 + ", B=1 T=16 S=1024 C=1152 16 heads, raw weights",
+                                     "l2": "flushed between timed steps", "launch": "cuda graph replay"},
+                          "breakdown_ms": {"forward_train": round(t_f / K, 4), "backward": round(t_b / K, 4)},
+                          "roofline": {"bound": "tensor", "t_roofline_ms": round(t_roof, 4),
+                                       "frac": round(t_roof / (t_ms / K), 3), "flops_per_step": flops,
+                                       "achieved_tflops": round(flops / N / (t_ms / K / 1e3) / 1e12, 1),
+                                       "peak_tflops": P["bf16_tflops"],
+                                       "basis": "train FLOPs (bench.train_flops) / N / measured bf16 peak"},
+                          "gpu_launches": graphs["step"][1] * K, "clocks": clocks.summary()}), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
 def free_port() -> int:
     import socket
     with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
@@ -738,7 +859,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="dsp", choices=["dsp", "reference"])
-    ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28", "nd"])
+    ap.add_argument("--config", default="blk", choices=list(CONFIGS) + ["model28", "nd", "train"])
     ap.add_argument("--switch", default="nccl", choices=["nccl", "p2p", "fused"])
     ap.add_argument("--schedule", default="dsp", choices=["dsp", "ulysses"],
                     help="ulysses: DeepSpeed-Ulysses on the same kernels (4 all-to-alls per attention stage)")
@@ -761,11 +882,15 @@ def main():
             args.config, args.layers = "blk", 28
         elif args.config == "nd":
             return print(json.dumps({"impl": "reference", "unavailable": "no oracle timing leg for the N-D block"}))
+        elif args.config == "train":
+            return print(json.dumps({"impl": "reference", "unavailable": "no oracle timing leg for the training step"}))
         run_reference(args)
     elif args.config == "model28":
         run_model(args)
     elif args.config == "nd":
         run_nd(args)
+    elif args.config == "train":
+        run_train(args)
     else:
         run_dsp(args)
 

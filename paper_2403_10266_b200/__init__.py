@@ -59,6 +59,21 @@ class BlockWeights(ctypes.Structure):
         (n, ctypes.c_void_p) for n in LATTE_NAMES] + [("pe_t", ctypes.c_void_p)]
 
 
+GRAD_NAMES = ("ln1_w", "ln1_b", "w_qkv_s", "w_o_s", "ln2_w", "ln2_b", "w_qkv_t", "w_o_t", "ln3_w", "ln3_b",
+              "w_fc1", "w_fc2")
+
+
+class BlockGrads(ctypes.Structure):  # dsp_block_grads_t (include/dsp_train.h): fp32 accumulators
+    _fields_ = [(n, ctypes.c_void_p) for n in GRAD_NAMES]
+
+
+SAVED_NAMES = ("h1", "qkv_s", "o_s", "lse_s", "y1s", "h2", "qkv_t", "o_t", "lse_t", "y2", "h3", "u", "g")
+
+
+class SavedLayout(ctypes.Structure):  # dsp_train_saved_layout_t
+    _fields_ = [(n, ctypes.c_int64) for n in SAVED_NAMES + ("total",)]
+
+
 class SwitchPlan(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64 * 3), ("run_bytes", ctypes.c_int64), ("src_stride", ctypes.c_int64 * 3),
                 ("dst_stride", ctypes.c_int64 * 3), ("dst_peer_off", ctypes.c_int64),
@@ -135,6 +150,18 @@ def lib() -> ctypes.CDLL:
             "dsp_ctx_set_stage_clocks": [vp, vp],
             "dsp_ctx_set_collective_emulation": [vp, ctypes.c_int],
             "dsp_st_block_forward_ulysses": [vp, P(Shape), P(BlockWeights), vp, vp, ctypes.c_int, vp],
+            # training path (include/dsp_train.h)
+            "dsp_train_saved_layout": [P(Shape), ctypes.c_int, P(SavedLayout)],
+            "dsp_st_block_forward_train": [vp, P(Shape), P(BlockWeights), vp, vp, vp, ctypes.c_int, vp],
+            "dsp_st_block_backward": [vp, P(Shape), P(BlockWeights), vp, vp, vp, vp, P(BlockGrads), ctypes.c_int,
+                                      vp],
+            "dsp_grads_reduce": [vp, vp, i64, ctypes.c_int, vp, vp],
+            "dsp_linear_dgrad": [vp, i64, i64, i64, vp, vp, vp, vp, vp],
+            "dsp_linear_wgrad": [vp, i64, i64, i64, vp, vp, vp, ctypes.c_int, vp],
+            "dsp_linear_gelu_aux": [vp, i64, i64, i64, vp, vp, vp, vp, vp],
+            "dsp_layer_norm_bwd": [vp, i64, i64, vp, vp, vp, vp, ctypes.c_float, vp, vp, vp],
+            "dsp_attention_core_lse": [vp, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp, vp],
+            "dsp_attention_core_bwd": [vp, i64, i64, i64, i64, i32, ctypes.c_int, vp, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -148,6 +175,12 @@ def lib() -> ctypes.CDLL:
         L.dsp_nd_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_ulysses_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
         L.dsp_ulysses_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_train_workspace_bytes.argtypes = [P(Shape), ctypes.c_int]
+        L.dsp_train_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_wgrad_workspace_bytes.argtypes = [vp, i64, i64, i64]
+        L.dsp_wgrad_workspace_bytes.restype = ctypes.c_size_t
+        L.dsp_attention_bwd_workspace_bytes.argtypes = [i64, i64, i32]
+        L.dsp_attention_bwd_workspace_bytes.restype = ctypes.c_size_t
         L.dsp_block_prepared_bytes.argtypes = [P(Shape)]
         L.dsp_block_prepared_bytes.restype = ctypes.c_size_t
         L.dsp_status_str.argtypes = [ctypes.c_int]
@@ -203,6 +236,22 @@ def workspace_bytes(shape: Shape, world: int) -> int:
 def ulysses_workspace_bytes(shape: Shape, world: int) -> int:
     """dsp_ulysses_workspace_bytes: per-rank workspace of the Ulysses-schedule block."""
     return int(lib().dsp_ulysses_workspace_bytes(ctypes.byref(shape), int(world)))
+
+
+def train_workspace_bytes(shape: Shape, world: int) -> int:
+    """dsp_train_workspace_bytes: per-rank workspace of forward_train / backward."""
+    return int(lib().dsp_train_workspace_bytes(ctypes.byref(shape), int(world)))
+
+
+def train_saved_layout(shape: Shape, world: int) -> dict:
+    """dsp_train_saved_layout: byte offsets of the saved activations (+ "total")."""
+    L = SavedLayout()
+    _check(lib().dsp_train_saved_layout(ctypes.byref(shape), int(world), ctypes.byref(L)))
+    return {n: int(getattr(L, n)) for n in SAVED_NAMES + ("total",)}
+
+
+def attention_bwd_workspace_bytes(tok: int, C: int, num_heads: int) -> int:
+    return int(lib().dsp_attention_bwd_workspace_bytes(int(tok), int(C), int(num_heads)))
 
 
 def prepared_bytes(shape: Shape) -> int:
@@ -411,6 +460,60 @@ class Context:
     def temporal_attn(self, shape, h, w_qkv, w_o, residual, out, stream=None):
         self._call("dsp_temporal_attn", ctypes.byref(shape), _ptr(h), _ptr(w_qkv), _ptr(w_o), _ptr(residual),
                    _ptr(out), _stream(stream))
+
+    # ---- training path (include/dsp_train.h)
+    def block_forward_train(self, shape, W: dict, x_local, y_local, saved, impl="nccl", stream=None):
+        """dsp_st_block_forward_train: the block forward, keeping its activations in `saved` (uint8 CUDA
+        tensor of train_saved_layout(...)["total"] bytes)."""
+        bw = self.block_weights(W)
+        self._call("dsp_st_block_forward_train", ctypes.byref(shape), ctypes.byref(bw), _ptr(x_local), _ptr(y_local),
+                   _ptr(saved), IMPLS[impl] if isinstance(impl, str) else int(impl), _stream(stream))
+
+    def block_backward(self, shape, W: dict, saved, x_local, dy_local, dx_local, grads: dict, impl="nccl",
+                       stream=None):
+        """dsp_st_block_backward: dx_local and grads[name] += dW (fp32 CUDA tensors, GRAD_NAMES)."""
+        bw = self.block_weights(W)
+        g = BlockGrads(*[_ptr(grads[n]) for n in GRAD_NAMES])
+        self._call("dsp_st_block_backward", ctypes.byref(shape), ctypes.byref(bw), _ptr(saved), _ptr(x_local),
+                   _ptr(dy_local), _ptr(dx_local), ctypes.byref(g), IMPLS[impl] if isinstance(impl, str) else int(impl),
+                   _stream(stream))
+
+    def grads_reduce(self, buf, zero_shard: bool = False, out=None, stream=None):
+        """dsp_grads_reduce: NCCL all-reduce (or ZeRO reduce-scatter into out) of fp32 gradients."""
+        self._call("dsp_grads_reduce", _ptr(buf), buf.numel(), int(bool(zero_shard)), _ptr(out), _stream(stream))
+
+    def linear_dgrad(self, dY, W, dX, u=None, stream=None):
+        """dsp_linear_dgrad: dX[M, K] = dY[M, N] W[N, K] (* gelu'(u) if u is given)."""
+        N = W.shape[0]
+        M = dY.numel() // N
+        self._call("dsp_linear_dgrad", M, N, W.shape[1], _ptr(dY), _ptr(W), _ptr(u), _ptr(dX), _stream(stream))
+
+    def linear_wgrad(self, dY, X, dW, accumulate=False, stream=None):
+        """dsp_linear_wgrad: dW[N, K] (+)= dY[M, N]^T X[M, K] in fp32 (needs dsp_wgrad_workspace_bytes)."""
+        N, K = dW.shape
+        M = dY.numel() // N
+        self.ensure_workspace(int(lib().dsp_wgrad_workspace_bytes(self.handle, M, N, K)))
+        self._call("dsp_linear_wgrad", M, N, K, _ptr(dY), _ptr(X), _ptr(dW), int(bool(accumulate)), _stream(stream))
+
+    def linear_gelu_aux(self, A, W, G, U, stream=None):
+        """dsp_linear_gelu_aux: G = gelu_tanh(A W^T), U = A W^T."""
+        N, K = W.shape
+        self._call("dsp_linear_gelu_aux", A.numel() // K, N, K, _ptr(A), _ptr(W), _ptr(G), _ptr(U), _stream(stream))
+
+    def layer_norm_bwd(self, x, gamma, dh, dres, dx, dgamma_dbeta, eps=1e-5, stream=None):
+        """dsp_layer_norm_bwd: dx = dres + LN^T dh; dgamma_dbeta[2C] += (sum dh xhat, sum dh)."""
+        C = x.shape[-1]
+        self._call("dsp_layer_norm_bwd", x.numel() // C, C, _ptr(x), _ptr(gamma), _ptr(dh), _ptr(dres),
+                   ctypes.c_float(eps), _ptr(dx), _ptr(dgamma_dbeta), _stream(stream))
+
+    def attention_core_lse(self, B, T_loc, S_loc, C, num_heads, dim, qkv, o, lse, stream=None):
+        self._call("dsp_attention_core_lse", int(B), int(T_loc), int(S_loc), int(C), int(num_heads), DIMS[dim],
+                   _ptr(qkv), _ptr(o), _ptr(lse), _stream(stream))
+
+    def attention_core_bwd(self, B, T_loc, S_loc, C, num_heads, dim, qkv, o, dout, lse, dqkv, stream=None):
+        self.ensure_workspace(attention_bwd_workspace_bytes(B * T_loc * S_loc, C, num_heads))
+        self._call("dsp_attention_core_bwd", int(B), int(T_loc), int(S_loc), int(C), int(num_heads), DIMS[dim],
+                   _ptr(qkv), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dqkv), _stream(stream))
 
     @staticmethod
     def block_weights(W: dict, eps: float = 1e-5) -> BlockWeights:

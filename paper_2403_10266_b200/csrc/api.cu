@@ -1680,3 +1680,392 @@ dsp_status_t dsp_attention_core(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t B, int64_
 }
 
 }  // extern "C"
+
+// ===================================================================== training path (f4)
+// include/dsp_train.h.  Forward-train = the raw block forward keeping its activations; backward =
+// the chain rule of oracle/backward.py in reverse stage order on the same shards, the switches run
+// in the opposite direction (a permutation's adjoint is its inverse).
+namespace {
+
+struct TrainWs {
+  int64_t dz, big, dh, dyb, dob, dqacc, dvec, lnpart, wpart, send, recv, total;
+};
+
+int64_t wgrad_part_bytes(int64_t M, int64_t N, int64_t K, int num_sms) {
+  return (int64_t)wgrad_splits(M, N, K, num_sms) * M * N * 4;
+}
+
+TrainWs train_ws(const dsp_shape_t* s, int world, int num_sms) {
+  TrainWs w{};
+  const int64_t tok = s->B * s->T * s->S / world, C = s->C, act = tok * C * 2;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { const int64_t r = o; o += align256(bytes); return r; };
+  w.dz = take(act);
+  w.big = take(4 * act);
+  w.dh = take(act);
+  w.dyb = take(act);
+  w.dob = take(act);
+  w.dqacc = take(tok * C * 4);
+  w.dvec = take(tok * s->num_heads * 4);
+  w.lnpart = take((int64_t)ln_bwd_blocks(tok, num_sms) * 2 * C * 4);
+  int64_t wp = 0;
+  const int64_t shapes[4][2] = {{3 * C, C}, {C, C}, {4 * C, C}, {C, 4 * C}};
+  for (auto& sh : shapes) wp = std::max(wp, wgrad_part_bytes(sh[0], sh[1], tok, num_sms));
+  w.wpart = take(wp);
+  w.send = take(act);
+  w.recv = take(act);
+  w.total = o;
+  return w;
+}
+
+dsp_train_saved_layout_t saved_layout(const dsp_shape_t* s, int world) {
+  dsp_train_saved_layout_t L{};
+  const int64_t tok = s->B * s->T * s->S / world, C = s->C, act = tok * C * 2, lse = tok * s->num_heads * 4;
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { const int64_t r = o; o += align256(bytes); return r; };
+  L.h1 = take(act);
+  L.qkv_s = take(3 * act);
+  L.o_s = take(act);
+  L.lse_s = take(lse);
+  L.y1s = take(act);
+  L.h2 = take(act);
+  L.qkv_t = take(3 * act);
+  L.o_t = take(act);
+  L.lse_t = take(lse);
+  L.y2 = take(act);
+  L.h3 = take(act);
+  L.u = take(4 * act);
+  L.g = take(4 * act);
+  L.total = o;
+  return L;
+}
+
+dsp_status_t check_train_call(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_shape(ctx, s));
+  DSP_TRY(check_div(ctx, s, ctx->world));
+  if (!w) return fail(ctx, DSP_ERR_NULL, "weights NULL");
+  if (s->dtype != DSP_BF16) return fail(ctx, DSP_ERR_UNSUPPORTED, "the training path is bf16");
+  if (s->C % s->num_heads || s->C / s->num_heads != 72)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "the training path needs head dim 72 (C / num_heads)");
+  const int64_t Tl = s->T, Sl = s->S;
+  auto okL = [](int64_t L) { return L % 128 == 0 || 128 % L == 0; };
+  if (!okL(Tl) || !okL(Sl)) return fail(ctx, DSP_ERR_UNSUPPORTED, "training path: T and S must divide or be multiples of 128");
+  if (w->prepared || w->ln_c_w || w->w_fc1_s || w->pe_t)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "training path: raw weights only (no prepared / cross / Latte / pe extras)");
+  const void* wp[12] = {w->ln1_w, w->ln1_b, w->w_qkv_s, w->w_o_s, w->ln2_w, w->ln2_b,
+                        w->w_qkv_t, w->w_o_t, w->ln3_w, w->ln3_b, w->w_fc1, w->w_fc2};
+  for (int i = 0; i < 12; ++i) {
+    if (!wp[i]) return fail(ctx, DSP_ERR_NULL, "weight %d is NULL", i);
+    if (!aligned16(wp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "weight %d not 16-B aligned", i);
+  }
+  const size_t need = dsp_train_workspace_bytes(s, ctx->world);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "training needs %zu bytes of workspace", need);
+  return DSP_OK;
+}
+
+// dW[N, K] (+)= dY[M, N]^T X[M, K] through the split-K partials in `part`
+dsp_status_t wgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* X, float* dW,
+                   int accumulate, float* part, cudaStream_t st) {
+  std::string why;
+  const int ks = wgrad_splits(N, K, M, ctx->num_sms);
+  cudaError_t e = launch_gemm_bf16_wgrad(dY, X, part, N, K, M, ks, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wgrad GEMM", why);
+  e = launch_wgrad_reduce(part, ks, N * K, dW, accumulate, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "wgrad reduce");
+  ctx->launches += 2;
+  return DSP_OK;
+}
+
+dsp_status_t dgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* W, const void* u,
+                   void* dX, cudaStream_t st) {
+  std::string why;
+  cudaError_t e = launch_gemm_bf16_dgrad(dY, W, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "dgrad GEMM", why);
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
+dsp_status_t ln_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh,
+                    const void* dres, void* dx, float* dgamma, float* dbeta, float* part, cudaStream_t st) {
+  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, part, 1e-5f, ctx->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm backward");
+  e = launch_wgrad_reduce(part, ln_bwd_blocks(rows, ctx->num_sms), 2 * C, dgamma, 1, st, C, dbeta);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm parameter reduce");
+  ctx->launches += 2;
+  return DSP_OK;
+}
+
+// one attention stage's backward: from dout (gradient of the stage output, also the residual
+// gradient) and the saved h / qkv / o / lse, dres_out = dout + LN^T(W_qkv^T (attn^T (W_o^T dout)))
+dsp_status_t attn_stage_bwd(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim,
+                            const void* zin, const void* ln_w, const void* w_qkv, const void* w_o, const void* h,
+                            const void* qkv, const void* o, const float* lse, const void* dout, void* dres_out,
+                            float* g_lnw, float* g_lnb, float* g_qkv, float* g_o, const TrainWs& L, uint8_t* ws,
+                            cudaStream_t st) {
+  const int64_t tok = s->B * T_loc * S_loc, C = s->C;
+  void* dob = ws + L.dob;
+  void* dqkv = ws + L.big;
+  void* dh = ws + L.dh;
+  float* part = reinterpret_cast<float*>(ws + L.wpart);
+  DSP_TRY(dgrad(ctx, tok, C, C, dout, w_o, nullptr, dob, st));                      // dO = dout W_o
+  DSP_TRY(wgrad(ctx, tok, C, C, dout, o, g_o, 1, part, st));                        // dW_o += dout^T O
+  std::string why;
+  cudaError_t e = launch_fmha_bwd_bf16(qkv, o, dob, lse, dqkv, reinterpret_cast<float*>(ws + L.dvec),
+                                       reinterpret_cast<float*>(ws + L.dqacc), s->B, T_loc, S_loc, C, s->num_heads,
+                                       dim, ctx->num_sms, st, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "attention backward", why);
+  ctx->launches += 4;
+  DSP_TRY(dgrad(ctx, tok, 3 * C, C, dqkv, w_qkv, nullptr, dh, st));                 // dh = dqkv W_qkv
+  DSP_TRY(wgrad(ctx, tok, 3 * C, C, dqkv, h, g_qkv, 1, part, st));                  // dW_qkv += dqkv^T h
+  return ln_bwd(ctx, tok, C, zin, ln_w, dh, dout, dres_out, g_lnw, g_lnb, reinterpret_cast<float*>(ws + L.lnpart), st);
+}
+
+}  // namespace
+
+extern "C" {
+
+dsp_status_t dsp_train_saved_layout(const dsp_shape_t* s, int world, dsp_train_saved_layout_t* out) {
+  if (!s || !out) return fail(nullptr, DSP_ERR_NULL, "NULL argument");
+  if (world < 1 || s->B < 1 || s->T < 1 || s->S < 1 || s->C < 1 || s->num_heads < 1)
+    return fail(nullptr, DSP_ERR_SHAPE, "bad shape or world");
+  *out = saved_layout(s, world);
+  return DSP_OK;
+}
+
+size_t dsp_train_workspace_bytes(const dsp_shape_t* s, int world) {
+  if (!s || world < 1) return 0;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (size_t)train_ws(s, world, sms).total;
+}
+
+dsp_status_t dsp_st_block_forward_train(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w,
+                                        const void* x, void* y, void* saved, dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_train_call(ctx, s, w));
+  if (!x || !y || !saved) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (!aligned16(x) || !aligned16(y) || (reinterpret_cast<uintptr_t>(saved) & 255))
+    return fail(ctx, DSP_ERR_ALIGNMENT, "x, y 16-B and saved 256-B aligned");
+  const int N = ctx->world;
+  const int64_t C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * 2, Tn = s->T / N, Sn = s->S / N;
+  const dsp_train_saved_layout_t SL = saved_layout(s, N);
+  const TrainWs L = train_ws(s, N, ctx->num_sms);
+  uint8_t* sv = static_cast<uint8_t*>(saved);
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  if (overlap(saved, SL.total, x, act) || overlap(saved, SL.total, y, act)) return fail(ctx, DSP_ERR_ALIAS, "saved overlaps x/y");
+  if (overlap(ctx->ws, L.total, x, act) || overlap(ctx->ws, L.total, y, act) || overlap(ctx->ws, L.total, saved, SL.total))
+    return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/y/saved");
+  cudaStream_t st = (cudaStream_t)stream;
+  std::string why;
+  cudaError_t e;
+  auto run = [&](cudaError_t err, const char* what) -> dsp_status_t {
+    if (err != cudaSuccess) return cuda_fail(ctx, err, what, why);
+    ctx->launches += 1;
+    return DSP_OK;
+  };
+  // spatial stage on the T-shard (y1 -> dz scratch when it must be switched)
+  void* y1 = N == 1 ? static_cast<void*>(sv + SL.y1s) : static_cast<void*>(ws + L.dz);
+  DSP_TRY(run(launch_layer_norm(DSP_BF16, tok, C, x, w->ln1_w, w->ln1_b, 1e-5f, sv + SL.h1, st), "LN1"));
+  DSP_TRY(run(launch_gemm_bf16(sv + SL.h1, w->w_qkv_s, nullptr, sv + SL.qkv_s, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why), "QKV_S"));
+  DSP_TRY(run(launch_fmha_bf16(sv + SL.qkv_s, sv + SL.o_s, s->B, Tn, s->S, C, s->num_heads, DSP_DIM_S, ctx->num_sms, st, &why,
+                               reinterpret_cast<float*>(sv + SL.lse_s)), "ATTN_S"));
+  DSP_TRY(run(launch_gemm_bf16(sv + SL.o_s, w->w_o_s, x, y1, tok, C, C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why), "PROJ_S"));
+  if (N > 1) DSP_TRY(do_switch(ctx, s, DSP_DIM_T, y1, sv + SL.y1s, impl, st, ws + L.send, ws + L.recv));
+  // temporal stage + MLP on the S-shard
+  DSP_TRY(run(launch_layer_norm(DSP_BF16, tok, C, sv + SL.y1s, w->ln2_w, w->ln2_b, 1e-5f, sv + SL.h2, st), "LN2"));
+  DSP_TRY(run(launch_gemm_bf16(sv + SL.h2, w->w_qkv_t, nullptr, sv + SL.qkv_t, tok, 3 * C, C, DSP_EPI_NONE, ctx->num_sms, st, &why), "QKV_T"));
+  DSP_TRY(run(launch_fmha_bf16(sv + SL.qkv_t, sv + SL.o_t, s->B, s->T, Sn, C, s->num_heads, DSP_DIM_T, ctx->num_sms, st, &why,
+                               reinterpret_cast<float*>(sv + SL.lse_t)), "ATTN_T"));
+  DSP_TRY(run(launch_gemm_bf16(sv + SL.o_t, w->w_o_t, sv + SL.y1s, sv + SL.y2, tok, C, C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why), "PROJ_T"));
+  DSP_TRY(run(launch_layer_norm(DSP_BF16, tok, C, sv + SL.y2, w->ln3_w, w->ln3_b, 1e-5f, sv + SL.h3, st), "LN3"));
+  DSP_TRY(run(launch_gemm_bf16_gelu_aux(sv + SL.h3, w->w_fc1, sv + SL.g, sv + SL.u, tok, 4 * C, C, ctx->num_sms, st, &why), "FC1"));
+  void* z = N == 1 ? y : static_cast<void*>(ws + L.dz);
+  e = launch_gemm_bf16(sv + SL.g, w->w_fc2, sv + SL.y2, z, tok, C, 4 * C, DSP_EPI_RESIDUAL, ctx->num_sms, st, &why);
+  DSP_TRY(run(e, "FC2"));
+  if (N > 1) DSP_TRY(do_switch(ctx, s, DSP_DIM_S, z, y, impl, st, ws + L.send, ws + L.recv));
+  return DSP_OK;
+}
+
+dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w, const void* saved,
+                                   const void* x, const void* dy, void* dx, const dsp_block_grads_t* g,
+                                   dsp_switch_impl_t impl, void* stream) {
+  DSP_TRY(check_train_call(ctx, s, w));
+  if (!x || !dy || !dx || !saved || !g) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  float* gp[12] = {g->ln1_w, g->ln1_b, g->w_qkv_s, g->w_o_s, g->ln2_w, g->ln2_b,
+                   g->w_qkv_t, g->w_o_t, g->ln3_w, g->ln3_b, g->w_fc1, g->w_fc2};
+  for (int i = 0; i < 12; ++i)
+    if (!gp[i] || !aligned16(gp[i])) return fail(ctx, DSP_ERR_ALIGNMENT, "gradient %d NULL or not 16-B aligned", i);
+  if (!aligned16(x) || !aligned16(dy) || !aligned16(dx)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int N = ctx->world;
+  const int64_t C = s->C, tok = s->B * s->T * s->S / N, act = tok * C * 2, Tn = s->T / N, Sn = s->S / N;
+  const dsp_train_saved_layout_t SL = saved_layout(s, N);
+  const TrainWs L = train_ws(s, N, ctx->num_sms);
+  if (dx != dy && overlap(dx, act, dy, act)) return fail(ctx, DSP_ERR_ALIAS, "dx partially overlaps dy");
+  if (overlap(ctx->ws, L.total, dx, act) || overlap(ctx->ws, L.total, dy, act) || overlap(ctx->ws, L.total, x, act))
+    return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/dy/dx");
+  if (overlap(saved, SL.total, dx, act)) return fail(ctx, DSP_ERR_ALIAS, "dx overlaps saved");
+  const uint8_t* sv = static_cast<const uint8_t*>(saved);
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = reinterpret_cast<float*>(ws + L.wpart);
+  // 1. dz = switch_{T->S}(dy): the adjoint of the forward's closing S->T switch
+  const void* dz = dy;
+  if (N > 1) {
+    DSP_TRY(do_switch(ctx, s, DSP_DIM_T, dy, ws + L.dz, impl, st, ws + L.send, ws + L.recv));
+    dz = ws + L.dz;
+  }
+  // 2. MLP backward: du = (dz W2) * gelu'(u); dW2 += dz^T g; dh3 = du W1; dW1 += du^T h3
+  void* du = ws + L.big;
+  DSP_TRY(dgrad(ctx, tok, C, 4 * C, dz, w->w_fc2, sv + SL.u, du, st));
+  DSP_TRY(wgrad(ctx, tok, C, 4 * C, dz, sv + SL.g, g->w_fc2, 1, part, st));
+  DSP_TRY(dgrad(ctx, tok, 4 * C, C, du, w->w_fc1, nullptr, ws + L.dh, st));
+  DSP_TRY(wgrad(ctx, tok, 4 * C, C, du, sv + SL.h3, g->w_fc1, 1, part, st));
+  // dy2 = dz + LN3^T dh3
+  void* dy2 = ws + L.dyb;
+  DSP_TRY(ln_bwd(ctx, tok, C, sv + SL.y2, w->ln3_w, ws + L.dh, dz, dy2, g->ln3_w, g->ln3_b,
+                 reinterpret_cast<float*>(ws + L.lnpart), st));
+  // 3. temporal stage backward on the S-shard: dy1s = dy2 + LN2^T(...) (in place over dy2)
+  DSP_TRY(attn_stage_bwd(ctx, s, s->T, Sn, DSP_DIM_T, sv + SL.y1s, w->ln2_w, w->w_qkv_t, w->w_o_t, sv + SL.h2,
+                         sv + SL.qkv_t, sv + SL.o_t, reinterpret_cast<const float*>(sv + SL.lse_t), dy2, dy2,
+                         g->ln2_w, g->ln2_b, g->w_qkv_t, g->w_o_t, L, ws, st));
+  // 4. dy1 = switch_{S->T}(dy1s): the adjoint of the forward's T->S switch
+  void* dy1 = dy2;
+  if (N > 1) {
+    DSP_TRY(do_switch(ctx, s, DSP_DIM_S, dy2, ws + L.dz, impl, st, ws + L.send, ws + L.recv));
+    dy1 = ws + L.dz;
+  }
+  // 5. spatial stage backward on the T-shard: dx = dy1 + LN1^T(...)
+  return attn_stage_bwd(ctx, s, Tn, s->S, DSP_DIM_S, x, w->ln1_w, w->w_qkv_s, w->w_o_s, sv + SL.h1, sv + SL.qkv_s,
+                        sv + SL.o_s, reinterpret_cast<const float*>(sv + SL.lse_s), dy1, dx, g->ln1_w, g->ln1_b,
+                        g->w_qkv_s, g->w_o_s, L, ws, st);
+}
+
+dsp_status_t dsp_grads_reduce(dsp_ctx_t ctx, float* buf, int64_t n, int zero_shard, float* out, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!buf || (zero_shard && !out)) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  const int N = ctx->world;
+  if (n < 0 || (zero_shard && n % N)) return fail(ctx, DSP_ERR_SHAPE, "n %% world != 0 for the ZeRO shard");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t shard = n / N;
+  if (N == 1) {
+    if (zero_shard && out != buf) DSP_CUDA(ctx, cudaMemcpyAsync(out, buf, n * 4, cudaMemcpyDeviceToDevice, st), "grads copy");
+    return DSP_OK;
+  }
+  if (ctx->emulate_collectives) return fail(ctx, DSP_ERR_UNSUPPORTED, "gradient reduction under collective emulation");
+  if (!ctx->nccl.ok || !ctx->comm) return fail(ctx, DSP_ERR_NCCL, "gradient reduction without a communicator");
+  constexpr int kF32 = 7, kSum = 0;  // ncclFloat32, ncclSum
+  int r;
+  if (zero_shard) {
+    if (!ctx->nccl.ReduceScatter) return fail(ctx, DSP_ERR_NCCL, "ncclReduceScatter unavailable");
+    r = ctx->nccl.ReduceScatter(buf, out, (size_t)shard, kF32, kSum, ctx->comm, st);
+  } else {
+    if (!ctx->nccl.AllReduce) return fail(ctx, DSP_ERR_NCCL, "ncclAllReduce unavailable");
+    r = ctx->nccl.AllReduce(buf, buf, (size_t)n, kF32, kSum, ctx->comm, st);
+  }
+  if (r) return fail(ctx, DSP_ERR_NCCL, "gradient reduction: %s", ctx->nccl.GetErrorString(r));
+  return DSP_OK;
+}
+
+// ---- building blocks
+dsp_status_t dsp_linear_dgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* W,
+                              const void* u, void* dX, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!dY || !W || !dX) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (M < 0 || N < 1 || K < 1) return fail(ctx, DSP_ERR_SHAPE, "bad dgrad shape");
+  if (K % 128 || N % 8) return fail(ctx, DSP_ERR_UNSUPPORTED, "dgrad needs K %% 128 == 0 and N %% 8 == 0");
+  if (!aligned16(dY) || !aligned16(W) || !aligned16(dX) || (u && !aligned16(u))) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  if (overlap(dX, M * K * 2, dY, M * N * 2) || overlap(dX, M * K * 2, W, N * K * 2)) return fail(ctx, DSP_ERR_ALIAS, "dX overlaps dY or W");
+  return dgrad(ctx, M, N, K, dY, W, u, dX, (cudaStream_t)stream);
+}
+
+size_t dsp_wgrad_workspace_bytes(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K) {
+  const int sms = ctx ? ctx->num_sms : 148;
+  return (size_t)wgrad_part_bytes(N, K, M, sms);
+}
+
+dsp_status_t dsp_linear_wgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* X, float* dW,
+                              int accumulate, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!dY || !X || !dW) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (M < 1 || N < 1 || K < 1) return fail(ctx, DSP_ERR_SHAPE, "bad wgrad shape");
+  if (N % 64 || K % 128) return fail(ctx, DSP_ERR_UNSUPPORTED, "wgrad needs N %% 64 == 0 and K %% 128 == 0");
+  if (!aligned16(dY) || !aligned16(X) || !aligned16(dW)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const size_t need = dsp_wgrad_workspace_bytes(ctx, M, N, K);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "wgrad needs %zu bytes of workspace", need);
+  if (overlap(ctx->ws, need, dW, N * K * 4)) return fail(ctx, DSP_ERR_ALIAS, "dW overlaps the workspace");
+  return wgrad(ctx, M, N, K, dY, X, dW, accumulate, static_cast<float*>(ctx->ws), (cudaStream_t)stream);
+}
+
+dsp_status_t dsp_linear_gelu_aux(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* A, const void* W, void* G,
+                                 void* U, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!A || !W || !G || !U) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (M < 0 || N < 1 || K < 1) return fail(ctx, DSP_ERR_SHAPE, "bad linear shape");
+  if (K % 8 || N % 32) return fail(ctx, DSP_ERR_UNSUPPORTED, "needs K %% 8 == 0 and N %% 32 == 0");
+  if (!aligned16(A) || !aligned16(W) || !aligned16(G) || !aligned16(U)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  std::string why;
+  cudaError_t e = launch_gemm_bf16_gelu_aux(A, W, G, U, M, N, K, ctx->num_sms, (cudaStream_t)stream, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "gelu aux GEMM", why);
+  if (M > 0) ctx->launches += 1;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_layer_norm_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh,
+                                const void* dres, float eps, void* dx, float* dgb, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  if (!x || !gamma || !dh || !dx || !dgb) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  if (rows < 0 || C < 8 || C % 8 || C > 2048) return fail(ctx, DSP_ERR_UNSUPPORTED, "LN backward needs C %% 8 == 0, C <= 2048");
+  const size_t need = (size_t)ln_bwd_blocks(rows, ctx->num_sms) * 2 * C * 4;
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "LN backward needs %zu bytes of workspace", need);
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, static_cast<float*>(ctx->ws), eps, ctx->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm backward");
+  e = launch_wgrad_reduce(static_cast<float*>(ctx->ws), ln_bwd_blocks(rows, ctx->num_sms), 2 * C, dgb, 1, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm parameter reduce");
+  ctx->launches += 2;
+  return DSP_OK;
+}
+
+dsp_status_t dsp_attention_core_lse(dsp_ctx_t ctx, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int32_t NH,
+                                    dsp_dim_t dim, const void* qkv, void* o, float* lse, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_dim(ctx, dim));
+  if (!qkv || !o || !lse) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  dsp_shape_t s{B, T_loc, S_loc, C, NH, DSP_BF16};
+  DSP_TRY(check_shape(ctx, &s));
+  DSP_TRY(check_bf16_attn(ctx, &s, dim == DSP_DIM_S ? S_loc : T_loc));
+  if (!aligned16(qkv) || !aligned16(o) || !aligned16(lse)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  std::string why;
+  cudaError_t e = launch_fmha_bf16(qkv, o, B, T_loc, S_loc, C, NH, dim, ctx->num_sms, (cudaStream_t)stream, &why, lse);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "attention core", why);
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
+size_t dsp_attention_bwd_workspace_bytes(int64_t tok, int64_t C, int32_t NH) {
+  return (size_t)(align256(tok * NH * 4) + align256(tok * C * 4));
+}
+
+dsp_status_t dsp_attention_core_bwd(dsp_ctx_t ctx, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int32_t NH,
+                                    dsp_dim_t dim, const void* qkv, const void* o, const void* dout, const float* lse,
+                                    void* dqkv, void* stream) {
+  DSP_TRY(check_ctx(ctx));
+  DSP_TRY(check_dim(ctx, dim));
+  if (!qkv || !o || !dout || !lse || !dqkv) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
+  dsp_shape_t s{B, T_loc, S_loc, C, NH, DSP_BF16};
+  DSP_TRY(check_shape(ctx, &s));
+  if (!aligned16(qkv) || !aligned16(o) || !aligned16(dout) || !aligned16(dqkv)) return fail(ctx, DSP_ERR_ALIGNMENT, "buffers must be 16-B aligned");
+  const int64_t tok = B * T_loc * S_loc;
+  const size_t need = dsp_attention_bwd_workspace_bytes(tok, C, NH);
+  if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "attention backward needs %zu bytes of workspace", need);
+  uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
+  std::string why;
+  cudaError_t e = launch_fmha_bwd_bf16(qkv, o, dout, lse, dqkv, reinterpret_cast<float*>(ws),
+                                       reinterpret_cast<float*>(ws + align256(tok * NH * 4)), B, T_loc, S_loc, C, NH, dim,
+                                       ctx->num_sms, (cudaStream_t)stream, &why);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "attention backward", why);
+  ctx->launches += 4;
+  return DSP_OK;
+}
+
+}  // extern "C"

@@ -12,6 +12,7 @@
 
 #include "dsp.h"
 #include "dsp_kernels.h"
+#include "dsp_train.h"
 
 namespace dsp {
 
@@ -33,6 +34,9 @@ struct NcclApi {
   int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   int (*CommGetAsyncError)(void*, int*) = nullptr;
+  // gradient reduction (dsp_grads_reduce): (send, recv, count, ncclFloat32, ncclSum, comm, stream)
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*ReduceScatter)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
 };
 bool nccl_load(NcclApi* api, std::string* err);
 constexpr int kNcclUint8 = 1;  // ncclUint8 in nccl.h
@@ -59,7 +63,24 @@ extern thread_local unsigned long long* t_clk;
 cudaError_t launch_gemm_bf16(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
                              int epi, int num_sms, cudaStream_t st, std::string* why);
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
-                             int dim, int num_sms, cudaStream_t st, std::string* why);
+                             int dim, int num_sms, cudaStream_t st, std::string* why, float* lse = nullptr);
+// FMHA backward (f4) over the same token-major q | k | v views: dqkv [tok, 3C] (bf16; padding-free)
+// from qkv, o, do [tok, C], lse [tok][NH] (log2 domain, written by the forward with lse != nullptr);
+// dvec [tok][NH] (f32) and dq_acc [tok, C] (f32, zeroed here when the sequence spans several key
+// tiles) are scratch.  Dh == 72; sequence length L % 128 == 0 or 128 % L == 0.
+cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
+                                 float* dvec, float* dq_acc, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C,
+                                 int NH, int dim, int num_sms, cudaStream_t st, std::string* why);
+// the backward's SIMT helpers (bwd.cu)
+// out (+)= sum_s part[s] (n floats); out1 != nullptr: elements >= split_at go to out1 instead
+cudaError_t launch_wgrad_reduce(const float* part, int nparts, int64_t n, float* out, int accumulate, cudaStream_t st,
+                                int64_t split_at = 0, float* out1 = nullptr);
+int ln_bwd_blocks(int64_t rows, int num_sms);
+cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh, const void* dres,
+                          void* dx, float* part, float eps, int num_sms, cudaStream_t st);
+cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, const void* dout, float* dvec,
+                                 cudaStream_t st);
+cudaError_t launch_dq_convert(int64_t tok, int64_t C, const float* dq_acc, void* dqkv, cudaStream_t st);
 // temporal attention reading q | k | v from the TSEQ layout (launch_gemm_bf16_tseq); o [tok, C]
 cudaError_t launch_fmha_bf16_tseq(const void* qkv_tseq, void* o, int64_t B, int64_t T, int64_t S_loc, int64_t C,
                                   int NH, int num_sms, cudaStream_t st, std::string* why);
@@ -118,7 +139,26 @@ struct AdaFold {
 cudaError_t launch_adaln_fold(int njobs, const AdaFold* jobs, int64_t C, cudaStream_t st);
 cudaError_t launch_fold_ln_weights(int njobs, const LnFold* jobs, int64_t K, cudaStream_t st);
 // GEMM epilogue codes beyond the public dsp_epilogue_t
-enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5, EPI_TSEQ = 6, EPI_LN_TSEQ = 7 };
+enum { EPI_LN = 3, EPI_LN_GELU = 4, EPI_RES_REMOTE = 5, EPI_TSEQ = 6, EPI_LN_TSEQ = 7,
+       // backward (f4): D = acc * gelu'(R) (R = the saved FC1 pre-activation u); D = gelu(acc) with
+       // the raw acc also stored to R (forward-train FC1: u and g in one pass); fp32 partial store
+       EPI_GELU_BWD = 8, EPI_GELU_AUX = 9, EPI_F32 = 10 };
+// Operand majors of the backward GEMMs (bit 0: A is MN-major, stored [K][M]; bit 1: W is MN-major,
+// stored [K][N]).  dgrad dX = dY W uses W [N_fwd, K_fwd] as an MN-major B; wgrad dW = dY^T X
+// reads both token-major activations as MN-major operands (no transposes in HBM).
+enum { MAJ_K = 0, MAJ_A_MN = 1, MAJ_B_MN = 2 };
+// dgrad: D[M, N] = epi(A[M, K] . Wt) with W stored [K, N] (N contiguous); epi = DSP_EPI_NONE or
+// EPI_GELU_BWD (R = u [M, N]); N % 128 == 0
+cudaError_t launch_gemm_bf16_dgrad(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                                   int64_t K, int epi, int num_sms, cudaStream_t st, std::string* why);
+// wgrad: part[s][M, N] (fp32) = sum over the s-th token range of dY[tok, M]^T X[tok, N]; ksplit
+// ranges (ksplit = wgrad_splits(...)); M % 64 == 0, N % 128 == 0
+int wgrad_splits(int64_t M, int64_t N, int64_t K, int num_sms);
+cudaError_t launch_gemm_bf16_wgrad(const void* dY, const void* X, float* part, int64_t M, int64_t N, int64_t K,
+                                   int ksplit, int num_sms, cudaStream_t st, std::string* why);
+// forward-train FC1: G = gelu(A W^T) and U = A W^T (both bf16 [M, N])
+cudaError_t launch_gemm_bf16_gelu_aux(const void* A, const void* W, void* G, void* U, int64_t M, int64_t N,
+                                      int64_t K, int num_sms, cudaStream_t st, std::string* why);
 // Sequence-major temporal layout of q | k | v ("TSEQ", written by the temporal QKV GEMM, read by
 // the temporal FMHA): element (part, b, h, s, t, d) at ((((part*B + b)*NH + h)*S_loc + s)*T + t)*kTseqDP
 // + d, d < Dh = kTseqDh; columns Dh..DP-1 are zero.  Every temporal sequence (b, h, s) is one
@@ -217,6 +257,9 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle swz, std::string* why);
+// f32 tensor map, no swizzle, no L2 promotion change (the FMHA backward's dQ reduce-add target)
+bool make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                   const uint32_t* box, std::string* why);
 
 }  // namespace dsp
 

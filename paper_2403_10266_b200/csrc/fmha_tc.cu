@@ -67,6 +67,7 @@ struct FmhaParams {
   int colfast;   // 1: item order column-fastest (outer before head), for the head-major TSEQ layout
   float scale_log2;
   __nv_bfloat16* o;
+  float* lse;                 // optional [tok][NH]: log2-domain log-sum-exp of the scaled scores (training)
   unsigned long long* trace;  // DSP_FMHA_TRACE builds only: per-phase clock64 stamps of CTA 0
   unsigned long long* clk;    // stage clock (instrumentation, t_clk)
 };
@@ -407,14 +408,20 @@ template <int NA, int RB, int LCOL = -1>  // LCOL >= 0: the row sum l is O's col
 __device__ __forceinline__ void epilogue_tma_store(const FmhaParams& p, const CUtensorMap* to_a,
                                                    const CUtensorMap* to_b, uint8_t* stage, uint32_t tO,
                                                    uint32_t lane_off, int row, float l, uint32_t bar_id,
-                                                   const TileCoord& t, uint64_t* o_free, int& store_pending) {
+                                                   const TileCoord& t, uint64_t* o_free, int& store_pending,
+                                                   float m) {
   constexpr int DP = NA * 64 + RB;
   const uint32_t st0 = smem_u32(stage);
   uint32_t ov[DP];  // all TMEM loads in flight before one wait
 #pragma unroll
   for (int c = 0; c < DP / 16; ++c) tmem_ld16(tO + lane_off + c * 16, *reinterpret_cast<uint32_t(*)[16]>(ov + c * 16));
   tmem_ld_wait();
-  const float inv_l = 1.f / (LCOL >= 0 ? __uint_as_float(ov[LCOL < 0 ? 0 : LCOL]) : l);
+  const float lsum = LCOL >= 0 ? __uint_as_float(ov[LCOL < 0 ? 0 : LCOL]) : l;
+  const float inv_l = 1.f / lsum;
+  if (p.lse) {  // training: P = exp2(s * scale_log2 - lse2) reproduces this row's softmax (m, l consistent)
+    const long tok = row_token(p, t, row);
+    if (tok >= 0) p.lse[tok * p.NH + t.h] = m + __log2f(lsum);
+  }
 #pragma unroll
   for (int c = 0; c < DP / 16; ++c) {
     const uint32_t* o = ov + c * 16;
@@ -755,7 +762,7 @@ __global__ void __launch_bounds__(256, FmhaCfg<NA, RB>::CTAS_PER_SM)
       tc_fence_after();
       FMHA_STAMP(tr, 3);
       epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sP, tO, G.lane_off, G.row, l, 1, tile_coord(p, item, -1), o_free,
-                                 store_pending);
+                                 store_pending, m);
       FMHA_STAMP(tr, 4);
     }
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
@@ -1022,7 +1029,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       FMHA_STAMP(te, 6);
       epilogue_tma_store<NA, RB, ONES ? Cfg::DP - 8 : -1>(p, &to_a, &to_b, sPs, tO, G.lane_off, G.row, l, bar_id,
-                                 tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
+                                 tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending, m);
       FMHA_STAMP(te, 7);
     }
     if (store_leader) bulk_wait_group_read0();
@@ -1365,7 +1372,7 @@ __global__ void __launch_bounds__(384, 1)
         store_pending = 0;
       }
       epilogue_tma_store<NA, RB, Cfg::DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
-                                              tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
+                                              tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending, m);
     }
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
   }
@@ -1598,10 +1605,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       if (G.diag)
         epilogue_tma_store<NA, RB>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, l, bar_id, tile_coord(p, item, -1),
-                                   &o_free[slot], store_pending);
+                                   &o_free[slot], store_pending, m);
       else
         epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, G.row, 0.f, bar_id,
-                                           tile_coord(p, item, -1), &o_free[slot], store_pending);
+                                           tile_coord(p, item, -1), &o_free[slot], store_pending, m);
     }
     if ((threadIdx.x & 127) == 0) bulk_wait_group_read0();
   }
@@ -1981,7 +1988,7 @@ __global__ void __launch_bounds__(640, 1)
           store_pending = 0;
         }
         epilogue_tma_store<NA, RB, DP - 8>(p, &to_a, &to_b, sOs, tO, G.lane_off, row, 0.f, bar_epi,
-                                           tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending);
+                                           tile_coord(p, 2 * ip + slot, -1), &o_free[slot], store_pending, m);
       }
     }
     if (half == 0 && (threadIdx.x & 127) == 0) bulk_wait_group_read0();
@@ -2119,6 +2126,375 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
   return launch_k(kern, dim3(grid), dim3(256), Cfg::SMEM, st, 1, m[0], m[1], m[2], m[3], m[4], m[5], mo[0], mo[1], p);
 }
 
+
+// ===================================================================== backward (f4)
+// FMHA backward for one sequence / head / 128-key tile per work item (P:17 attention, the gradient
+// of oracle/backward.py attention_core_bwd): with the forward's log2-domain row normaliser lse2,
+//   S^T = K Q^T,  P^T = exp2(S^T * scale_log2 - lse2[q]),  dP^T = V dO^T,
+//   dS^T = P^T * (dP^T - D[q]) / sqrt(Dh)   (D = rowsum(dO * O), attn_bwd_dvec_kernel),
+//   dV += P^T dO,  dK += dS^T Q,  dQ_j = dS K   for every 128-query tile j of the sequence.
+// Keys are the TMEM lanes: a compute thread owns one key row of S^T / dP^T and writes its P^T row
+// back into TMEM over the consumed S^T columns (the TS-form A of dV += P^T dO) and its dS^T row
+// into shared memory (SW128 K-major over queries), which is the K-major A of dK += dS^T Q and,
+// read as MN-major, the A of dQ = dS K.  dQ leaves per query tile by a TMA reduce-add (f32) into
+// dq_acc when the sequence has several key tiles, else as one bf16 TMA store; dK, dV leave after
+// the item's last query tile.  TMEM (512 columns): S^T [0,128), dP^T [128,256), dV [256,336),
+// dK [336,416), dQ [416,496).  Roles (256 threads, one CTA per SM): warp 0 TMA producer (K, V
+// per item; {Q, dO} per query tile, two stages), warp 1 TMEM allocator + MMA issuer, warps 4-7
+// compute (P, dS, dQ / dK / dV epilogues).  Block-diagonal packing (G = 128 / L sequences per
+// tile, temporal T = 16) masks P and dS outside each thread's own sequence.
+struct BwdMaps {
+  CUtensorMap q[2], k[2], v[2], dout[2], dq[2], dk[2], dv[2], dq_acc;
+};
+
+template <int NA, int RB>
+struct BwdCfg {
+  using Base = FmhaCfg<NA, RB>;
+  static constexpr int TILE = Base::TILE, DP = Base::DP, TX = Base::TX;
+  static constexpr int OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE;  // stage s: Q at OFF_Q + 2 s TILE, dO next
+  static constexpr int OFF_DS = 6 * TILE;                            // dS^T: 2 x [128 keys][64 queries] SW128
+  static constexpr int OFF_DQ = OFF_DS + 32768;                      // dQ f32 staging [128][DP] / dK, dV bf16
+  static constexpr int OFF_VEC = OFF_DQ + 128 * DP * 4;              // [2 buf][lse2 | D][128] f32
+  static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
+  static constexpr int SMEM = 1024 + OFF_BAR + 256;
+  static constexpr bool OK = SMEM <= 227 * 1024 && RB == 16 && NA == 1;
+  static_assert(2 * TILE <= 128 * DP * 4, "dK and dV staging fit in the dQ staging area");
+};
+
+__device__ __forceinline__ TileCoord bwd_coord(const FmhaParams& p, int outer, int h, int pt) {
+  TileCoord t;
+  t.h = h;
+  if (p.G == 1) {
+    t.x2 = pt * 128;
+    if (p.spatial) { t.x3 = outer; t.x4 = 0; }
+    else { t.x3 = outer % p.S_loc; t.x4 = outer / p.S_loc; }
+  } else {
+    t.x2 = 0;
+    if (p.spatial) { t.x3 = outer * p.G; t.x4 = 0; }
+    else { const int ng = (p.S_loc + p.G - 1) / p.G; t.x3 = (outer % ng) * p.G; t.x4 = outer / ng; }
+  }
+  return t;
+}
+
+// bf16 row of a [128][DP] tile -> the TMA box staging layout (SW128 64-column chunks, then the SW32
+// remainder), scaled by `mul`
+template <int NA, int RB>
+__device__ __forceinline__ void stage_row_bf16(uint32_t st0, int row, const uint32_t* v, float mul) {
+  constexpr int DP = NA * 64 + RB;
+#pragma unroll
+  for (int d = 0; d < DP; d += 8) {
+    const uint32_t a0 = pack_bf16x2(__uint_as_float(v[d]) * mul, __uint_as_float(v[d + 1]) * mul);
+    const uint32_t a1 = pack_bf16x2(__uint_as_float(v[d + 2]) * mul, __uint_as_float(v[d + 3]) * mul);
+    const uint32_t a2 = pack_bf16x2(__uint_as_float(v[d + 4]) * mul, __uint_as_float(v[d + 5]) * mul);
+    const uint32_t a3 = pack_bf16x2(__uint_as_float(v[d + 6]) * mul, __uint_as_float(v[d + 7]) * mul);
+    uint32_t addr;
+    if (d < NA * 64) {
+      const int blk = d >> 6, ch = (d & 63) >> 3;
+      addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
+    } else {
+      const int ch = (d - NA * 64) >> 3;  // RB = 16: SW32, two chunks per 32-B row
+      addr = st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4);
+    }
+    st_shared_v4(addr, a0, a1, a2, a3);
+  }
+}
+
+template <int NA, int RB>
+__device__ __forceinline__ void store_tile(const CUtensorMap* ma, const CUtensorMap* mb, const uint8_t* src,
+                                           const TileCoord& t) {
+#pragma unroll
+  for (int i = 0; i < NA; ++i) tma_store_5d(ma, src + i * 16384, 64 * i, t.h, t.x2, t.x3, t.x4);
+  tma_store_5d(mb, src + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
+}
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(256, 1)
+    fmha_bwd_kernel(const __grid_constant__ BwdMaps mp, const FmhaParams p, const float* __restrict__ lse,
+                    const float* __restrict__ dvec, int accum) {
+  using Cfg = BwdCfg<NA, RB>;
+  using Base = FmhaCfg<NA, RB>;
+  constexpr int DP = Cfg::DP;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + Cfg::OFF_K;
+  uint8_t* sV = smem + Cfg::OFF_V;
+  uint8_t* sDS = smem + Cfg::OFF_DS;
+  uint8_t* sDQ = smem + Cfg::OFF_DQ;
+  float* sVec = reinterpret_cast<float*>(smem + Cfg::OFF_VEC);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* q_full = bars + 2;   // [2]
+  uint64_t* q_empty = bars + 4;  // [2]
+  uint64_t* s_full = bars + 6;
+  uint64_t* p_full = bars + 7;   // count 128
+  uint64_t* dq_full = bars + 8;
+  uint64_t* dq_free = bars + 9;  // count 128
+  uint64_t* kv_free = bars + 10; // count 128
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const int warp = warp_id();
+  if (warp == 0 && lane_id() == 0) {
+    mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 128);
+    mbar_init(kv_free, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  griddep_launch_dependents();
+  griddep_wait();
+  clk_start(p.clk);
+
+  const int nq = p.n_qt;
+  auto decomp = [&](int item, int& outer, int& h, int& kvt) {
+    kvt = item % p.n_kv;
+    const int rest = item / p.n_kv;
+    h = rest % p.NH;
+    outer = rest / p.NH;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      uint32_t it = 0, g = 0;
+      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+        int outer, h, kvt;
+        decomp(item, outer, h, kvt);
+        mbar_wait_sleep(kv_empty, (it & 1) ^ 1);
+        mbar_arrive_expect_tx(kv_full, 2 * Cfg::TX);
+        const TileCoord tk = bwd_coord(p, outer, h, kvt);
+        load_tile<NA, RB>(sK, &mp.k[0], &mp.k[1], kv_full, tk);
+        load_tile<NA, RB>(sV, &mp.v[0], &mp.v[1], kv_full, tk);
+        for (int j = 0; j < nq; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait_sleep(&q_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[st], 2 * Cfg::TX);
+          uint8_t* qb = smem + Cfg::OFF_Q + 2 * st * Cfg::TILE;
+          const TileCoord tq = bwd_coord(p, outer, h, j);
+          load_tile<NA, RB>(qb, &mp.q[0], &mp.q[1], &q_full[st], tq);
+          load_tile<NA, RB>(qb + Cfg::TILE, &mp.dout[0], &mp.dout[1], &q_full[st], tq);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);       // S^T, dP^T
+    constexpr uint32_t idKa = make_idesc_bf16(128, 64, 0, 1);       // dV, dK: A K-major, B MN-major
+    constexpr uint32_t idKb = make_idesc_bf16(128, RB, 0, 1);
+    constexpr uint32_t idQa = make_idesc_bf16(128, 64, 1, 1);       // dQ: A (dS) MN-major, B (K) MN-major
+    constexpr uint32_t idQb = make_idesc_bf16(128, RB, 1, 1);
+    const uint32_t kb = smem_u32(sK), vb = smem_u32(sV), dsb = smem_u32(sDS);
+    const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 336, tdQ = tmem + 416;
+    // D[tmem] = X Y^T over the head dim: X, Y two [128][DP] K-major tiles
+    auto qk = [&](uint32_t d, uint32_t xa, uint32_t ya) {
+      int step = 0;
+#pragma unroll
+      for (int i = 0; i < NA; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk, ++step)
+          umma_bf16_ss(d, make_sdesc(xa + i * 16384 + kk * 32, 16, 1024, SW_128B),
+                       make_sdesc(ya + i * 16384 + kk * 32, 16, 1024, SW_128B), idS, step != 0);
+#pragma unroll
+      for (int kk = 0; kk < RB / 16; ++kk, ++step)
+        umma_bf16_ss(d, make_sdesc(xa + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
+                     make_sdesc(ya + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+    };
+    // MN-major B descriptor of a [128 rows = K][DP] tile: head-dim chunk i, 16-row k-step kk
+    auto bmn = [&](uint32_t base, int i, int kk) {
+      return make_sdesc(base + i * 16384 + kk * 2048, 16384, 1024, SW_128B);
+    };
+    auto bmn_r = [&](uint32_t base, int kk) {
+      return make_sdesc(base + NA * 16384 + kk * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW);
+    };
+    uint32_t it = 0, g = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      for (int j = 0; j < nq; ++j, ++g) {
+        const int st = g & 1;
+        const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
+        if (j == 0) mbar_wait(kv_full, it & 1);
+        mbar_wait(&q_full[st], (g >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          qk(tS, kb, qa);   // S^T = K Q^T
+          qk(tdP, vb, da);  // dP^T = V dO^T
+          umma_commit(s_full);
+        }
+        __syncwarp();
+        mbar_wait(p_full, g & 1);
+        if (g >= 1) mbar_wait(dq_free, (g - 1) & 1);
+        if (j == 0 && it >= 1) mbar_wait(kv_free, (it - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t acc0 = j != 0;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step
+            // dV (+)= P^T dO  (P^T packed in TMEM over S^T's columns: 8 columns per 16 queries)
+#pragma unroll
+            for (int i = 0; i < NA; ++i) umma_bf16_ts(tdV + 64 * i, tS + 8 * kk, bmn(da, i, kk), idKa, acc0 | (kk != 0));
+            umma_bf16_ts(tdV + 64 * NA, tS + 8 * kk, bmn_r(da, kk), idKb, acc0 | (kk != 0));
+            // dK (+)= dS^T Q  (dS^T K-major in smem: query chunk kk / 4, 32 B per 16 queries)
+            const uint64_t ad = make_sdesc(dsb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B);
+#pragma unroll
+            for (int i = 0; i < NA; ++i) umma_bf16_ss(tdK + 64 * i, ad, bmn(qa, i, kk), idKa, acc0 | (kk != 0));
+            umma_bf16_ss(tdK + 64 * NA, ad, bmn_r(qa, kk), idKb, acc0 | (kk != 0));
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
+            const uint64_t ad = make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B);
+#pragma unroll
+            for (int i = 0; i < NA; ++i) umma_bf16_ss(tdQ + 64 * i, ad, bmn(kb, i, kk), idQa, kk != 0);
+            umma_bf16_ss(tdQ + 64 * NA, ad, bmn_r(kb, kk), idQb, kk != 0);
+          }
+          umma_commit(dq_full);
+          umma_commit(&q_empty[st]);
+          if (j == nq - 1) umma_commit(kv_empty);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane_id();
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off, tdV = tmem + 256 + lane_off,
+                   tdK = tmem + 336 + lane_off, tdQ = tmem + 416 + lane_off;
+    const bool elected = threadIdx.x == 128;
+    const float sl2 = p.scale_log2;
+    const float sc = rsqrtf((float)p.Dh);
+    const bool diag = p.G > 1;
+    const int my_blk = row / p.L;
+    const uint32_t dsrow = smem_u32(sDS) + row * 128;
+    uint32_t it = 0, g = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      int outer, h, kvt;
+      decomp(item, outer, h, kvt);
+      for (int j = 0; j < nq; ++j, ++g) {
+        // this query tile's lse2 and D, one value per thread, broadcast through smem
+        float* l2 = sVec + (g & 1) * 256;
+        float* dd = l2 + 128;
+        {
+          const TileCoord tq = bwd_coord(p, outer, h, j);
+          const long tok = row_token(p, tq, row);
+          l2[row] = tok >= 0 ? lse[tok * p.NH + h] : INFINITY;
+          dd[row] = tok >= 0 ? dvec[tok * p.NH + h] : 0.f;
+        }
+        if (!accum && elected) bulk_wait_group_read0();  // the previous direct dQ store has read sDS
+        named_bar_sync(1, 128);
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c32 = 0; c32 < 4; ++c32) {
+          uint32_t sv[32], dv[32];
+          tmem_ld32(tS + c32 * 32, sv);
+          tmem_ld32(tdP + c32 * 32, dv);
+          tmem_ld_wait();
+          uint32_t pk[16], dk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float pp[2], ds[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int q = c32 * 32 + 2 * i + e;
+              const bool ok = !diag || q / p.L == my_blk;
+              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sv[2 * i + e]), sl2, -l2[q])) : 0.f;
+              pp[e] = pe;
+              ds[e] = pe * (__uint_as_float(dv[2 * i + e]) - dd[q]) * sc;
+            }
+            pk[i] = pack_bf16x2(pp[0], pp[1]);
+            dk[i] = pack_bf16x2(ds[0], ds[1]);
+          }
+          tmem_st16(tS + c32 * 16, pk);  // P^T over already-consumed S^T columns
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ch = (c32 & 1) * 4 + u;
+            st_shared_v4(dsrow + (c32 >> 1) * 16384 + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1],
+                         dk[4 * u + 2], dk[4 * u + 3]);
+          }
+        }
+        tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_full);
+        // dQ of this query tile
+        mbar_wait(dq_full, g & 1);
+        tc_fence_after();
+        uint32_t qv[DP];
+#pragma unroll
+        for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdQ + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(dq_free);
+        const TileCoord tq = bwd_coord(p, outer, h, j);
+        if (accum) {
+          if (elected) bulk_wait_group_read0();  // the previous reduce / dK, dV stores have read sDQ
+          named_bar_sync(1, 128);
+          const uint32_t r0 = smem_u32(sDQ) + row * DP * 4;
+#pragma unroll
+          for (int d = 0; d < DP; d += 4) st_shared_v4(r0 + d * 4, qv[d], qv[d + 1], qv[d + 2], qv[d + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (elected) {
+            tma_reduce_add_5d(&mp.dq_acc, sDQ, 0, tq.h, tq.x2, tq.x3, tq.x4);
+            bulk_commit_group();
+          }
+        } else {  // one key tile per sequence: dQ is final, bf16 through the (free) dS^T buffer
+          stage_row_bf16<NA, RB>(smem_u32(sDS), row, qv, 1.f);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (elected) {
+            store_tile<NA, RB>(&mp.dq[0], &mp.dq[1], sDS, tq);
+            bulk_commit_group();
+          }
+        }
+        if (j == nq - 1) {  // dK, dV final (dq_full of the last tile covers every MMA of the item)
+          uint32_t kv[DP];
+#pragma unroll
+          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdK + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
+          tmem_ld_wait();
+          if (elected) bulk_wait_group_read0();
+          named_bar_sync(1, 128);
+          stage_row_bf16<NA, RB>(smem_u32(sDQ), row, kv, 1.f);
+#pragma unroll
+          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdV + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(kv_free);
+          stage_row_bf16<NA, RB>(smem_u32(sDQ + Cfg::TILE), row, kv, 1.f);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (elected) {
+            const TileCoord tk = bwd_coord(p, outer, h, kvt);
+            store_tile<NA, RB>(&mp.dk[0], &mp.dk[1], sDQ, tk);
+            store_tile<NA, RB>(&mp.dv[0], &mp.dv[1], sDQ + Cfg::TILE, tk);
+            bulk_commit_group();
+          }
+        }
+      }
+    }
+    if (elected) bulk_wait_group0();  // reduce-adds and stores complete before the CTA retires
+  }
+  tc_fence_before();
+  __syncthreads();
+  clk_end(p.clk);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 static cudaError_t dispatch_dh(const FmhaViews& vw, const FmhaParams& p, const uint32_t* box_rows, int num_sms,
@@ -2130,8 +2506,9 @@ extern "C" void* dsp_debug_fmha_trace() { return g_fmha_trace; }
 #endif
 
 cudaError_t launch_fmha_bf16(const void* qkv, void* o, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C, int NH,
-                             int dim, int num_sms, cudaStream_t st, std::string* why) {
+                             int dim, int num_sms, cudaStream_t st, std::string* why, float* lse) {
   FmhaParams p{};
+  p.lse = lse;
   p.NH = NH;
   p.Dh = (int)(C / NH);
   p.C = (int)C;
@@ -2311,6 +2688,93 @@ static cudaError_t dispatch_dh(const FmhaViews& vw, const FmhaParams& p, const u
   if (na == 2 && rb == 0) return run_fmha<2, 0>(vw, p, box_rows, num_sms, st, why);    // Dh 104..128
   if (why) *why = "bf16 attention supports head dims up to 128";
   return cudaErrorNotSupported;
+}
+
+
+cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dout, const float* lse, void* dqkv,
+                                 float* dvec, float* dq_acc, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C,
+                                 int NH, int dim, int num_sms, cudaStream_t st, std::string* why) {
+  using Cfg = BwdCfg<1, 16>;
+  FmhaParams p{};
+  p.NH = NH;
+  p.Dh = (int)(C / NH);
+  p.C = (int)C;
+  p.S_loc = (int)S_loc;
+  p.T_loc = (int)T_loc;
+  p.B = (int)B;
+  p.clk = t_clk;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
+  p.spatial = (dim == DSP_DIM_S);
+  p.L = (int)(p.spatial ? S_loc : T_loc);
+  if (NH <= 0 || C % NH != 0 || p.Dh != 72) {
+    if (why) *why = "attention backward: head dim 72 only (the paper's C = 1152, 16 heads)";
+    return cudaErrorNotSupported;
+  }
+  if (p.L <= 0 || !(p.L % 128 == 0 || 128 % p.L == 0)) {
+    if (why) *why = "attention backward: sequence length must divide or be a multiple of 128";
+    return cudaErrorNotSupported;
+  }
+  const int64_t tok = B * T_loc * S_loc;
+  if (tok == 0) return cudaSuccess;
+  if (p.L % 128 == 0) {
+    p.G = 1;
+    p.n_kv = p.n_qt = p.L / 128;
+  } else {
+    p.G = 128 / p.L;
+    p.n_kv = p.n_qt = 1;
+  }
+  const uint64_t e = 2, rowb = 3 * (uint64_t)C * e;
+  uint64_t dims[5], strides[4];
+  if (p.spatial) {
+    dims[0] = p.Dh; dims[1] = NH; dims[2] = S_loc; dims[3] = B * T_loc; dims[4] = 1;
+    strides[0] = p.Dh * e; strides[1] = rowb; strides[2] = S_loc * rowb; strides[3] = B * T_loc * S_loc * rowb;
+    const int64_t frames = B * T_loc;
+    p.n_outer = (int)(p.G == 1 ? frames : (frames + p.G - 1) / p.G);
+  } else {
+    dims[0] = p.Dh; dims[1] = NH; dims[2] = T_loc; dims[3] = S_loc; dims[4] = B;
+    strides[0] = p.Dh * e; strides[1] = S_loc * rowb; strides[2] = rowb; strides[3] = T_loc * S_loc * rowb;
+    p.n_outer = (int)(p.G == 1 ? B * S_loc : B * ((S_loc + p.G - 1) / p.G));
+  }
+  uint64_t ostr[4];
+  for (int i = 0; i < 4; ++i) ostr[i] = i == 0 ? strides[0] : strides[i] / 3;  // [tok, C] views
+  p.items = p.n_outer * NH * p.n_kv;
+  const int accum = p.n_kv > 1;
+  const uint32_t r0 = (uint32_t)(p.G == 1 ? 128 : p.L), r1 = (uint32_t)p.G;
+  uint32_t boxa[5] = {64, 1, r0, r1, 1}, boxb[5] = {16, 1, r0, r1, 1};
+  BwdMaps mp;
+  const auto* qb = static_cast<const __nv_bfloat16*>(qkv);
+  auto* db = static_cast<__nv_bfloat16*>(dqkv);
+  auto pair = [&](CUtensorMap* m, const void* base, const uint64_t* s4) {
+    return make_tmap_bf16(&m[0], base, 5, dims, s4, boxa, CU_TENSOR_MAP_SWIZZLE_128B, why) &&
+           make_tmap_bf16(&m[1], base, 5, dims, s4, boxb, CU_TENSOR_MAP_SWIZZLE_32B, why);
+  };
+  if (!pair(mp.q, qb, strides) || !pair(mp.k, qb + C, strides) || !pair(mp.v, qb + 2 * C, strides) ||
+      !pair(mp.dout, dout, ostr) || !pair(mp.dq, db, strides) || !pair(mp.dk, db + C, strides) ||
+      !pair(mp.dv, db + 2 * C, strides))
+    return cudaErrorInvalidValue;
+  if (accum) {
+    uint64_t fstr[4];
+    for (int i = 0; i < 4; ++i) fstr[i] = 2 * ostr[i];
+    uint32_t boxf[5] = {(uint32_t)Cfg::DP, 1, r0, r1, 1};
+    if (!make_tmap_f32(&mp.dq_acc, dq_acc, 5, dims, fstr, boxf, why)) return cudaErrorInvalidValue;
+  } else {
+    mp.dq_acc = mp.q[0];  // unused
+  }
+  cudaError_t err = launch_attn_bwd_dvec(tok, NH, p.Dh, o, dout, dvec, st);
+  if (err != cudaSuccess) return err;
+  if (accum && (err = cudaMemsetAsync(dq_acc, 0, (size_t)tok * C * sizeof(float), st)) != cudaSuccess) return err;
+  auto kern = fmha_bwd_kernel<1, 16>;
+  static bool attr = false;
+  if (!attr) {
+    if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM)) != cudaSuccess)
+      return err;
+    attr = true;
+  }
+  const int grid = p.items < num_sms ? p.items : num_sms;
+  err = launch_k(kern, dim3(grid), dim3(256), Cfg::SMEM, st, 1, mp, p, lse, (const float*)dvec, accum);
+  if (err != cudaSuccess) return err;
+  if (accum) return launch_dq_convert(tok, C, dq_acc, dqkv, st);
+  return cudaSuccess;
 }
 
 }  // namespace dsp

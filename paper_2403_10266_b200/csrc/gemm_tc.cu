@@ -48,8 +48,13 @@ namespace {
 constexpr int BM = 128;  // rows per CTA (256 per pair)
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SW128 atom row
 
-template <int BN, int EPI>
+template <int BN, int EPI, int MAJ = MAJ_K>
 struct GemmCfg {
+  static constexpr bool A_MN = (MAJ & MAJ_A_MN) != 0;  // A staged as BM/64 MN-major SW128 boxes {64 rows, BK}
+  static constexpr bool B_MN = (MAJ & MAJ_B_MN) != 0;  // W staged as BNH/64 MN-major boxes
+  static_assert(!B_MN || (BN / 2) % 64 == 0, "an MN-major W half-tile is whole 64-column atoms");
+  static constexpr bool AUX = EPI == EPI_GELU_BWD;      // R tile staged by TMA like the residual
+  static constexpr bool F32 = EPI == EPI_F32;           // fp32 partials, per-thread-row stores
   static constexpr int BNH = BN / 2;                    // W rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNH * BK * 2;
@@ -60,12 +65,14 @@ struct GemmCfg {
   // lands there by TMA); the others use a ring of two boxes (store of box i overlaps box i+1),
   // which leaves room for one more mainloop stage at BN = 256
   static constexpr bool TSEQ = EPI == EPI_TSEQ || EPI == EPI_LN_TSEQ;  // temporal q|k|v layout, per-head boxes
-  static constexpr bool RING = EPI != DSP_EPI_RESIDUAL && EPI != EPI_RES_REMOTE && !TSEQ;
-  static constexpr int E_BYTES = TSEQ ? (BN / kTseqDh) * 128 * kTseqDP * 2 : RING ? 2 * 128 * EB * 2 : BN * 256;
+  static constexpr bool RING = EPI != DSP_EPI_RESIDUAL && EPI != EPI_RES_REMOTE && !TSEQ && !AUX && !F32;
+  static constexpr int E_BYTES = TSEQ ? (BN / kTseqDh) * 128 * kTseqDP * 2 : F32 ? 0 : RING ? 2 * 128 * EB * 2 : BN * 256;
   static constexpr int CW = BN % 32 == 0 ? 32 : 16;      // accumulator columns per TMEM load in the epilogue
   static constexpr int E_BOX = 128 * EB * 2;
   static constexpr int NBOX = BN / EB;  // staging boxes per tile (stored / reloaded one by one)
-  static constexpr int SPLIT_MAX = NBOX; // a narrow tail tile is a whole number of EB-column boxes
+  // a narrow tail tile is a whole number of EB-column boxes (MN-major W: whole 64-column atoms,
+  // not cut; fp32 partials: split-K instead)
+  static constexpr int SPLIT_MAX = (B_MN || F32) ? 1 : NBOX;
   // epilogue warpgroups (TMA epilogues: two, each owning every other box; the remote-row
   // epilogue of the fused switch: one)
   static constexpr int EPI_WG = EPI == EPI_LN_GELU ? DSP_GEMM_EPI_WG : 1;
@@ -80,6 +87,12 @@ __device__ __forceinline__ float gelu_tanh_f(float u) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   return 0.5f * u * (1.f + fast_tanh(k0 * (u + k1 * u * u * u)));
 }
+// d/du gelu_tanh(u) = 0.5 (1 + t) + 0.5 u (1 - t^2) k0 (1 + 3 k1 u^2), t = tanh(k0 (u + k1 u^3))
+__device__ __forceinline__ float gelu_tanh_grad_f(float u) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float t = fast_tanh(k0 * (u + k1 * u * u * u));
+  return 0.5f * (1.f + t) + 0.5f * u * (1.f - t * t) * k0 * (1.f + 3.f * k1 * u * u);
+}
 
 // Static tile schedule over P pairs: `full` BN-wide tiles; when the last wave is partial (rem =
 // full % P tiles) and its tiles cut into `split` narrower ones (split | BN/EB, so a narrow tile is
@@ -91,10 +104,11 @@ struct TileSched {
 };
 // most narrow tiles one BN-wide tile may be cut into; 1 for a residual epilogue that writes
 // LayerNorm partials (one partial per BN-wide tile, R30)
-template <int BN, int EPI>
+template <int BN, int EPI, int MAJ = MAJ_K>
 __host__ __device__ inline int gemm_split_max(const EpiVec& ev) {
-  return ((EPI == DSP_EPI_RESIDUAL && ev.part_out != nullptr) || GemmCfg<BN, EPI>::TSEQ) ? 1
-                                                                                        : GemmCfg<BN, EPI>::SPLIT_MAX;
+  return ((EPI == DSP_EPI_RESIDUAL && ev.part_out != nullptr) || GemmCfg<BN, EPI, MAJ>::TSEQ)
+             ? 1
+             : GemmCfg<BN, EPI, MAJ>::SPLIT_MAX;
 }
 __host__ __device__ inline TileSched make_tile_sched(int full, int P, int smax) {
   TileSched t{full, 1, full};
@@ -169,14 +183,14 @@ __device__ __forceinline__ float2 ln_stats_from_parts(const EpiVec& ev, int r) {
   return make_float2(mean, rsqrtf(m2 / (float)(np * ev.part_cnt) + ev.eps));
 }
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
+template <int BN, int EPI, int MAJ>
+__global__ void __launch_bounds__(GemmCfg<BN, EPI, MAJ>::THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmD,
                         const __grid_constant__ CUtensorMap tmR,
                         const __nv_bfloat16* __restrict__ R, __nv_bfloat16* D, int M, int N, int K,
-                        const EpiVec ev, const RemoteMap rm) {
-  using Cfg = GemmCfg<BN, EPI>;
+                        int ksplit, const EpiVec ev, const RemoteMap rm) {
+  using Cfg = GemmCfg<BN, EPI, MAJ>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -203,7 +217,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
   // is cut into `split` narrower tiles when they then fit in one wave (gemm_tail_split), so the
   // idle pairs of that wave share its work.  Every output element is still one tile's K-ordered
   // accumulation: the bits do not depend on the tile width (N-invariance).
-  const TileSched ts = make_tile_sched(tiles_m * tiles_n, num_pairs, gemm_split_max<BN, EPI>(ev));
+  // split-K (fp32 partials, ksplit > 1): tile t computes output tile t % (tiles_m * tiles_n) over
+  // the k-blocks of range t / (tiles_m * tiles_n); concurrently running pairs share a token range
+  const int tmn = tiles_m * tiles_n;
+  const int kbs = (num_kb + ksplit - 1) / ksplit;
+  const TileSched ts = make_tile_sched(tmn * ksplit, num_pairs, gemm_split_max<BN, EPI, MAJ>(ev));
   const int num_tiles = ts.num_tiles;
   auto geom = [&](int t, int& mrow, int& ncol, int& width) {
     int p = t, sub = 0;
@@ -213,8 +231,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       sub = (t - ts.head) % ts.split;
       width = BN / ts.split;
     }
+    p %= tmn;
     mrow = (p / tiles_n) * (2 * BM);
     ncol = (p % tiles_n) * BN + sub * width;
+  };
+  auto krange = [&](int t, int& kb0, int& kb1) {
+    kb0 = ksplit > 1 ? (t / tmn) * kbs : 0;  // ksplit > 1 never has narrow tiles (SPLIT_MAX 1)
+    kb1 = kb0 + kbs < num_kb ? kb0 + kbs : num_kb;
   };
 
   if (warp == 0 && lane_id() == 0) {
@@ -255,11 +278,25 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
         const int n0 = ncol + rank * (width / 2);
         const bool narrow = width != BN;
         const uint32_t bytes = 2 * (Cfg::A_BYTES + (width / 2) * BK * 2);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0, kb1;
+        krange(tile, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-          tma_load_2d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
-          tma_load_2d_2sm(sB + stage * Cfg::B_BYTES, narrow ? &tmW2 : &tmW, &full[stage], kb * BK, n0);
+          if (Cfg::A_MN) {  // A stored [K][M]: BM/64 boxes {64 rows of M, BK k-rows}, 8 KB apart
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d_2sm(sA + stage * Cfg::A_BYTES + j * (BK * 128), &tmA, &full[stage], m0 + 64 * j, kb * BK);
+          } else {
+            tma_load_2d_2sm(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          }
+          if (Cfg::B_MN) {
+#pragma unroll
+            for (int j = 0; j < Cfg::BNH / 64; ++j)
+              tma_load_2d_2sm(sB + stage * Cfg::B_BYTES + j * (BK * 128), &tmW, &full[stage], n0 + 64 * j, kb * BK);
+          } else {
+            tma_load_2d_2sm(sB + stage * Cfg::B_BYTES, narrow ? &tmW2 : &tmW, &full[stage], kb * BK, n0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -269,7 +306,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc_full = make_idesc_bf16(2 * BM, BN, 0, 0);
+      constexpr uint32_t idesc_full = make_idesc_bf16(2 * BM, BN, Cfg::A_MN, Cfg::B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -279,7 +316,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        int kb0, kb1;
+        krange(tile, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
@@ -287,12 +326,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
             const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, SW_128B);
-              const uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, SW_128B);
-              umma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              // K-major: the k-th 16-column slice is 32 B into each 128-B row; MN-major: 16 k-rows
+              // (2 KB) down, 64-element MN groups BK * 128 B apart (LBO), 8-row groups 1 KB (SBO)
+              const uint64_t ad = Cfg::A_MN ? make_sdesc(a0 + k * 2048, BK * 128, 1024, SW_128B)
+                                            : make_sdesc(a0 + k * 32, 16, 1024, SW_128B);
+              const uint64_t bd = Cfg::B_MN ? make_sdesc(b0 + k * 2048, BK * 128, 1024, SW_128B)
+                                            : make_sdesc(b0 + k * 32, 16, 1024, SW_128B);
+              umma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0));
             }
             umma_commit_2sm_mc(&empty[stage], 0x3);
-            if (kb == num_kb - 1) umma_commit_2sm_mc(&tfull[acc], 0x3);
+            if (kb == kb1 - 1) umma_commit_2sm_mc(&tfull[acc], 0x3);
           }
           __syncwarp();
           if (++stage == STAGES) {
@@ -390,7 +433,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
     }
     if (elected) bulk_wait_group_read0();
    }
-  } else if (warp >= 4 && EPI != EPI_RES_REMOTE) {
+  } else if (warp >= 4 && EPI != EPI_RES_REMOTE && !Cfg::F32) {
     // Bulk-tensor epilogue, EPI_WG warpgroups: warpgroup h (warps 4+4h .. 7+4h, TMEM lane quadrant
     // = warp % 4, thread = accumulator row) owns the tile's EB-column boxes b with b % EPI_WG == h.
     // Each thread adds its accumulator row into its box in place (SW128 layout: 16-B chunk c of
@@ -401,8 +444,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
     // loaded).  Other epilogues stage through one slot per warpgroup.  A LayerNorm partial is one
     // box of one row, so the partials' arithmetic does not depend on the warpgroup split.
     constexpr bool kRes = EPI == DSP_EPI_RESIDUAL;
+    constexpr bool kStage = kRes || Cfg::AUX;   // an R tile (residual, or u for gelu') staged by TMA
+    constexpr bool kDual = EPI == EPI_GELU_AUX;  // two stores per box: gelu(acc) -> D, acc -> R
     constexpr bool kLn = EPI == EPI_LN || EPI == EPI_LN_GELU;
     constexpr int WG = Cfg::EPI_WG;
+    static_assert(!kDual || WG == 1, "the dual-store epilogue uses both ring slots per box");
     const int q = warp & 3;
     const int h = (warp - 4) >> 2;
     const int row = q * 32 + lane_id();
@@ -419,7 +465,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       mbar_arrive_expect_tx(&r_full[b], Cfg::E_BOX);
       tma_load_2d(sE + b * Cfg::E_BOX, &tmR, &r_full[b], ncol + Cfg::EB * b, mrow + rank * BM);
     };
-    if (kRes && elected && pair < num_tiles)
+    if (kStage && elected && pair < num_tiles)
       for (int b = h; b < Cfg::NBOX; b += WG) load_res_box(pair, b);
     // LayerNorm folded (kLn): the next tile's row statistics (or its rows' partials, up to 8) are
     // loaded while this tile is processed, so their L2 latency is off the epilogue's critical path
@@ -492,13 +538,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       // (one LayerNorm partial per row per BN-wide tile; the residual epilogue runs one warpgroup,
       // so the row's boxes are summed in column order by one thread)
       const bool kStats = kRes && ev.part_out != nullptr;
-      static_assert(!kRes || WG == 1, "the residual epilogue's row partials assume one warpgroup");
+      static_assert(!kStage || WG == 1, "the residual epilogue's row partials assume one warpgroup");
       float2 sh = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
       constexpr int CW = Cfg::CW;
       for (int b = h; b < nb; b += WG, ++nbox_done) {
         // staging slot: the residual tile's own box; else a ring of two slots (one warpgroup:
         // boxes alternate, so a store overlaps the next box) or one slot per warpgroup
-        const int slot = Cfg::RING ? (WG == 1 ? (nbox_done & 1) : h) : b;
+        const int slot = kDual ? 0 : Cfg::RING ? (WG == 1 ? (nbox_done & 1) : h) : b;
         const uint32_t line = e0 + slot * Cfg::E_BOX + row * (Cfg::EB * 2);
 #pragma unroll
         for (int cb = 0; cb < Cfg::EB / CW; ++cb) {
@@ -508,10 +554,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
           else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + col0, v);
           tmem_ld_wait();
           if (cb == 0) {
-            if (kRes) mbar_wait(&r_full[b], it & 1);
+            if (kStage) mbar_wait(&r_full[b], it & 1);
             if (Cfg::RING) {  // the warpgroup's previous store out of this slot has been read
               if (elected) {
-                if (WG == 1) bulk_wait_group_read1();
+                if (WG == 1 && !kDual) bulk_wait_group_read1();
                 else bulk_wait_group_read0();
               }
               named_bar_sync(bar_wg, 128);
@@ -526,11 +572,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
             float f[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[8 * u + i]);
-            if (kRes) {
+            if (kStage) {
               uint32_t r0, r1, r2, r3;
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-              f[0] += bf16lo(r0); f[1] += bf16hi(r0); f[2] += bf16lo(r1); f[3] += bf16hi(r1);
-              f[4] += bf16lo(r2); f[5] += bf16hi(r2); f[6] += bf16lo(r3); f[7] += bf16hi(r3);
+              const float r[8] = {bf16lo(r0), bf16hi(r0), bf16lo(r1), bf16hi(r1),
+                                  bf16lo(r2), bf16hi(r2), bf16lo(r3), bf16hi(r3)};
+              if (kRes) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] += r[i];
+              } else {  // EPI_GELU_BWD: du = dg * gelu'(u)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] *= gelu_tanh_grad_f(r[i]);
+              }
+            } else if (kDual) {  // u = acc (bf16) into the other ring slot, g = gelu(acc) below
+              st_shared_v4(addr + ((slot ^ 1) - slot) * Cfg::E_BOX, pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                           pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
             } else if (EPI == DSP_EPI_GELU) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) f[i] = gelu_tanh_f(f[i]);
@@ -571,8 +629,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
         named_bar_sync(bar_wg, 128);
         if (elected) {
           tma_store_2d(&tmD, sE + slot * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
+          if (kDual) tma_store_2d(&tmR, sE + (slot ^ 1) * Cfg::E_BOX, n0 + Cfg::EB * b, m0);
           bulk_commit_group();
-          if (kRes && has_next && b >= WG) {
+          if (kStage && has_next && b >= WG) {
             bulk_wait_group_read1();  // box b-WG read out of sE: reload it for the next tile
             load_res_box(tile + num_pairs, b - WG);
           }
@@ -588,7 +647,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[acc]);  // accumulator free for the tile after next
       else mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-      if (kRes && elected && has_next) {
+      if (kStage && elected && has_next) {
         bulk_wait_group_read0();  // the warpgroup's boxes of the next tile not reloaded yet
         int last = -1;
         for (int b = h; b < nb; b += WG) last = b;
@@ -608,6 +667,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
       const int grow = m0 + row;
       const bool live = grow < M;
       __nv_bfloat16* drow = D + (size_t)grow * N + n0;
+      // fp32 partials of split-K range t / tmn: part[ks][M][N]
+      float* frow = reinterpret_cast<float*>(D) + ((size_t)(tile / tmn) * M + grow) * N + n0;
       if (EPI == EPI_RES_REMOTE && live) {
         // switch fused into the epilogue: this row's owner rank q and row index there
         int64_t dst;
@@ -691,11 +752,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI>::THREADS, 1)
               }
             }
           }
-          uint4* dp = reinterpret_cast<uint4*>(drow + c * CW);
+          if constexpr (Cfg::F32) {
+            float4* fp = reinterpret_cast<float4*>(frow + c * CW);
 #pragma unroll
-          for (int j = 0; j < CW / 8; ++j) {
-            dp[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
-                               pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            for (int j = 0; j < CW / 4; ++j) fp[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+          } else {
+            uint4* dp = reinterpret_cast<uint4*>(drow + c * CW);
+#pragma unroll
+            for (int j = 0; j < CW / 8; ++j) {
+              dp[j] = make_uint4(pack_bf16x2(f[8 * j], f[8 * j + 1]), pack_bf16x2(f[8 * j + 2], f[8 * j + 3]),
+                                 pack_bf16x2(f[8 * j + 4], f[8 * j + 5]), pack_bf16x2(f[8 * j + 6], f[8 * j + 7]));
+            }
           }
         }
       }
@@ -767,16 +834,43 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* 
   return true;
 }
 
-template <int BN, int EPI>
+bool make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                   const uint32_t* box, std::string* why) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    if (why) *why = "cuTensorMapEncodeTiled unavailable (driver entry point)";
+    return false;
+  }
+  uint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (why) *why = "cuTensorMapEncodeTiled (f32) failed with CUresult " + std::to_string((int)r);
+    return false;
+  }
+  return true;
+}
+
+template <int BN, int EPI, int MAJ = MAJ_K>
 static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N, int64_t K,
                             int num_sms, cudaStream_t st, std::string* why, const EpiVec& ev = EpiVec{},
-                            const RemoteMap& rm = RemoteMap{}) {
-  using Cfg = GemmCfg<BN, EPI>;
+                            const RemoteMap& rm = RemoteMap{}, int ksplit = 1) {
+  using Cfg = GemmCfg<BN, EPI, MAJ>;
   CUtensorMap ta, tw, tw2, td, tr;
+  // K-major operands: {K, rows}, box {BK, rows}; MN-major ({rows, K} in memory order): box {64, BK}
   uint64_t da[2] = {(uint64_t)K, (uint64_t)M}, sa[1] = {(uint64_t)K * 2};
   uint64_t dw[2] = {(uint64_t)K, (uint64_t)N}, sw[1] = {(uint64_t)K * 2};
   uint64_t dd[2] = {(uint64_t)N, (uint64_t)M}, sd[1] = {(uint64_t)N * 2};
   uint32_t ba[2] = {BK, BM}, bw[2] = {BK, Cfg::BNH}, bd[2] = {Cfg::EB, BM};
+  if (Cfg::A_MN) {
+    da[0] = (uint64_t)M; da[1] = (uint64_t)K; sa[0] = (uint64_t)M * 2;
+    ba[0] = 64; ba[1] = BK;
+  }
+  if (Cfg::B_MN) {
+    dw[0] = (uint64_t)N; dw[1] = (uint64_t)K; sw[0] = (uint64_t)N * 2;
+    bw[0] = 64; bw[1] = BK;
+  }
   const CUtensorMapSwizzle esw = Cfg::EB == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
                                  : Cfg::EB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                  : CU_TENSOR_MAP_SWIZZLE_32B;
@@ -784,9 +878,9 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
   // grid: one pair per tile up to all pairs; a partial last wave becomes narrow tiles (TileSched)
-  const int64_t full = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
+  const int64_t full = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN) * ksplit;
   const int pmax = num_sms / 2;
-  const int smax = gemm_split_max<BN, EPI>(ev);
+  const int smax = gemm_split_max<BN, EPI, MAJ>(ev);
   TileSched tsh = make_tile_sched((int)full, pmax, smax);
   const int64_t pairs = full >= pmax ? pmax : (tsh.num_tiles < pmax ? tsh.num_tiles : pmax);
   tsh = make_tile_sched((int)full, (int)pairs, smax);  // what the kernel will compute
@@ -804,12 +898,12 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
     uint64_t st5[4] = {row, (uint64_t)q.T * row, (uint64_t)q.S_loc * q.T * row, (uint64_t)q.NH * q.S_loc * q.T * row};
     uint32_t bx[5] = {(uint32_t)kTseqDP, 1, BM, 1, 1};
     if (!make_tmap_bf16(&td, D, 5, dt, st5, bx, CU_TENSOR_MAP_SWIZZLE_NONE, why)) return cudaErrorInvalidValue;
-  } else if (EPI != EPI_RES_REMOTE) {
+  } else if (EPI != EPI_RES_REMOTE && !Cfg::F32) {
     if (!make_tmap_bf16(&td, D, 2, dd, sd, bd, esw, why)) return cudaErrorInvalidValue;
-    if (EPI == DSP_EPI_RESIDUAL && !make_tmap_bf16(&tr, R, 2, dd, sd, bd, esw, why))
+    if ((EPI == DSP_EPI_RESIDUAL || Cfg::AUX || EPI == EPI_GELU_AUX) && !make_tmap_bf16(&tr, R, 2, dd, sd, bd, esw, why))
       return cudaErrorInvalidValue;
   }
-  auto kern = gemm_bf16_tc_kernel<BN, EPI>;
+  auto kern = gemm_bf16_tc_kernel<BN, EPI, MAJ>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -819,7 +913,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
   EpiVec evc = ev;
   evc.clk = t_clk;
   return launch_k(kern, dim3((unsigned)(2 * pairs)), dim3(Cfg::THREADS), Cfg::SMEM, st, 2, ta, tw, tw2, td, tr, (const __nv_bfloat16*)R,
-                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, evc, rm);
+                  (__nv_bfloat16*)D, (int)M, (int)N, (int)K, ksplit, evc, rm);
 }
 
 template <int EPI>
@@ -875,6 +969,68 @@ cudaError_t launch_gemm_bf16_ln(const void* A, const void* Wf, const EpiVec& ev,
 }
 
 int gemm_part_cols(int64_t N) { return gemm_bn_for(N); }  // one partial per BN-wide tile
+
+// ----------------------------------------------------------------- backward GEMMs (f4)
+cudaError_t launch_gemm_bf16_dgrad(const void* A, const void* W, const void* R, void* D, int64_t M, int64_t N,
+                                   int64_t K, int epi, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  if (N % 128 != 0 || K % 8 != 0) {
+    if (why) *why = "dgrad GEMM: N % 128 == 0 and K % 8 == 0 required";
+    return cudaErrorNotSupported;
+  }
+  const bool wide = N % 256 == 0;
+  if (epi == EPI_GELU_BWD)
+    return wide ? run_gemm<256, EPI_GELU_BWD, MAJ_B_MN>(A, W, R, D, M, N, K, num_sms, st, why)
+                : run_gemm<128, EPI_GELU_BWD, MAJ_B_MN>(A, W, R, D, M, N, K, num_sms, st, why);
+  if (epi == DSP_EPI_NONE)
+    return wide ? run_gemm<256, DSP_EPI_NONE, MAJ_B_MN>(A, W, R, D, M, N, K, num_sms, st, why)
+                : run_gemm<128, DSP_EPI_NONE, MAJ_B_MN>(A, W, R, D, M, N, K, num_sms, st, why);
+  if (why) *why = "dgrad GEMM: unsupported epilogue";
+  return cudaErrorInvalidValue;
+}
+
+// Split count for the wgrad GEMM: the output has few tiles (dW [3C, C] at C = 1152: 126 tiles of
+// 256 x 128 for 74 CTA pairs) and a long reduction (all tokens), so the token range is cut into
+// ksplit slices, the smallest count whose tiles fill >= 90 % of the last wave (at most 16, each
+// slice >= 8 k-blocks); the fp32 partials are summed in slice order by launch_wgrad_reduce.
+int wgrad_splits(int64_t M, int64_t N, int64_t K, int num_sms) {
+  const int64_t bn = N % 256 == 0 ? 256 : 128;
+  const int64_t tiles = ((M + 255) / 256) * (N / bn), pairs = num_sms / 2, nkb = (K + 63) / 64;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 16 && s <= nkb / 8; ++s) {
+    const int64_t kbs = (nkb + s - 1) / s, se = (nkb + kbs - 1) / kbs;  // slices actually used
+    if (se != s) continue;
+    const int64_t units = tiles * s, waves = (units + pairs - 1) / pairs;
+    const double eff = (double)units / (double)(waves * pairs);
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+    if (eff >= 0.9) break;
+  }
+  return best;
+}
+
+cudaError_t launch_gemm_bf16_wgrad(const void* dY, const void* X, float* part, int64_t M, int64_t N, int64_t K,
+                                   int ksplit, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  if (M % 64 != 0 || N % 128 != 0 || ksplit < 1) {
+    if (why) *why = "wgrad GEMM: M % 64 == 0, N % 128 == 0 required";
+    return cudaErrorNotSupported;
+  }
+  const int64_t nkb = (K + 63) / 64, kbs = (nkb + ksplit - 1) / ksplit;
+  if ((nkb + kbs - 1) / kbs != ksplit) {  // every slice must own k-blocks (an empty one never completes)
+    if (why) *why = "wgrad GEMM: ksplit leaves an empty token slice (use wgrad_splits)";
+    return cudaErrorInvalidValue;
+  }
+  constexpr int MAJ = MAJ_A_MN | MAJ_B_MN;
+  if (N % 256 == 0) return run_gemm<256, EPI_F32, MAJ>(dY, X, nullptr, part, M, N, K, num_sms, st, why, EpiVec{}, RemoteMap{}, ksplit);
+  return run_gemm<128, EPI_F32, MAJ>(dY, X, nullptr, part, M, N, K, num_sms, st, why, EpiVec{}, RemoteMap{}, ksplit);
+}
+
+cudaError_t launch_gemm_bf16_gelu_aux(const void* A, const void* W, void* G, void* U, int64_t M, int64_t N,
+                                      int64_t K, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  return dispatch_bn<EPI_GELU_AUX>(A, W, U, G, M, N, K, num_sms, st, why);
+}
 
 int gemm_bn_for(int64_t N) {
 #ifdef DSP_GEMM_BN_1152

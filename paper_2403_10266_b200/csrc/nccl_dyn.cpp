@@ -38,7 +38,11 @@ bool nccl_load(NcclApi* api, std::string* err) {
          sym(h, "ncclGroupEnd", &api->GroupEnd) && sym(h, "ncclSend", &api->Send) && sym(h, "ncclRecv", &api->Recv) &&
          sym(h, "ncclGetErrorString", &api->GetErrorString);
   }
-  if (ok) sym(h, "ncclCommGetAsyncError", &api->CommGetAsyncError);  // optional: health check only
+  if (ok) {
+    sym(h, "ncclCommGetAsyncError", &api->CommGetAsyncError);  // optional: health check only
+    sym(h, "ncclAllReduce", &api->AllReduce);                  // optional: gradient reduction only
+    sym(h, "ncclReduceScatter", &api->ReduceScatter);
+  }
   if (!ok && err) *err = "libnccl.so.2 lacks the collectives dsp needs";
   api->ok = ok;
   return ok;
