@@ -98,8 +98,9 @@ dsp_status_t dsp_linear_gelu_aux(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K,
 
 /* LayerNorm backward (R3) fused with the residual path: dx = dres + dLN(x)^T dh over
  * rows of C (dres may be NULL), and dgamma_dbeta[0:C] += sum_rows dh * xhat,
- * dgamma_dbeta[C:2C] += sum_rows dh (fp32; summed per CTA, then in CTA order).  bf16 x, gamma,
- * dh, dres, dx [rows, C]; C % 8 == 0, C <= 2048.  Workspace >= 2 C * 4 * 2 * #SMs bytes. */
+ * dgamma_dbeta[C:2C] += sum_rows dh (fp32).  bf16 x, gamma,
+ * dh, dres, dx [rows, C]; C % 8 == 0, C <= 2048.  Workspace >= 8 rows + 2 C * 4 * ceil(rows / 64) bytes
+ * (row statistics, then per-64-row column partials summed in chunk order). */
 dsp_status_t dsp_layer_norm_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const void* x, const void* gamma,
                                 const void* dh, const void* dres, float eps, void* dx, float* dgamma_dbeta,
                                 void* stream);

@@ -1707,7 +1707,7 @@ TrainWs train_ws(const dsp_shape_t* s, int world, int num_sms) {
   w.dob = take(act);
   w.dqacc = take(tok * C * 4);
   w.dvec = take(tok * s->num_heads * 4);
-  w.lnpart = take((int64_t)ln_bwd_blocks(tok, num_sms) * 2 * C * 4);
+  w.lnpart = take(ln_bwd_scratch_bytes(tok, C));
   int64_t wp = 0;
   const int64_t shapes[4][2] = {{3 * C, C}, {C, C}, {4 * C, C}, {C, 4 * C}};
   for (auto& sh : shapes) wp = std::max(wp, wgrad_part_bytes(sh[0], sh[1], tok, num_sms));
@@ -1788,11 +1788,9 @@ dsp_status_t dgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* d
 
 dsp_status_t ln_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh,
                     const void* dres, void* dx, float* dgamma, float* dbeta, float* part, cudaStream_t st) {
-  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, part, 1e-5f, ctx->num_sms, st);
+  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, part, dgamma, dbeta, 1, 1e-5f, ctx->num_sms, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm backward");
-  e = launch_wgrad_reduce(part, ln_bwd_blocks(rows, ctx->num_sms), 2 * C, dgamma, 1, st, C, dbeta);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm parameter reduce");
-  ctx->launches += 2;
+  ctx->launches += 3;
   return DSP_OK;
 }
 
@@ -2015,14 +2013,13 @@ dsp_status_t dsp_layer_norm_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const vo
   DSP_TRY(check_ctx(ctx));
   if (!x || !gamma || !dh || !dx || !dgb) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
   if (rows < 0 || C < 8 || C % 8 || C > 2048) return fail(ctx, DSP_ERR_UNSUPPORTED, "LN backward needs C %% 8 == 0, C <= 2048");
-  const size_t need = (size_t)ln_bwd_blocks(rows, ctx->num_sms) * 2 * C * 4;
+  const size_t need = (size_t)ln_bwd_scratch_bytes(rows, C);
   if (!ctx->ws || ctx->ws_bytes < need) return fail(ctx, DSP_ERR_WORKSPACE, "LN backward needs %zu bytes of workspace", need);
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, static_cast<float*>(ctx->ws), eps, ctx->num_sms, st);
+  cudaError_t e = launch_ln_bwd(rows, C, x, gamma, dh, dres, dx, static_cast<float*>(ctx->ws), dgb, dgb + C, 1, eps,
+                                ctx->num_sms, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm backward");
-  e = launch_wgrad_reduce(static_cast<float*>(ctx->ws), ln_bwd_blocks(rows, ctx->num_sms), 2 * C, dgb, 1, st);
-  if (e != cudaSuccess) return cuda_fail(ctx, e, "layer_norm parameter reduce");
-  ctx->launches += 2;
+  ctx->launches += 3;
   return DSP_OK;
 }
 

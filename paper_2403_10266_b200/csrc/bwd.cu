@@ -44,115 +44,162 @@ __global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float4* __restr
   }
 }
 
-// One warp per row (rows strided over the grid's warps), kMaxV 16-B vectors per lane (C <= 256 kMaxV).
-// Dynamic smem: [warps][2][C] f32 column partials, summed over the warps in warp order at the end.
+// LayerNorm backward, pass 1: one warp per row, kMaxV 16-B vectors per lane (C <= 256 kMaxV); the
+// row's (mean, rstd) is recomputed from x and written to `stats` for pass 2.  No column accumulators
+// here, so the kernel stays small enough for several CTAs per SM (rows in flight hide HBM latency).
 template <int kMaxV>
 __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* __restrict__ x,
                                                           const __nv_bfloat16* __restrict__ gamma,
                                                           const __nv_bfloat16* __restrict__ dh,
                                                           const __nv_bfloat16* __restrict__ dres,
-                                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ part,
+                                                          __nv_bfloat16* __restrict__ dx, float2* __restrict__ stats,
                                                           long rows, int C, float eps) {
-  extern __shared__ float red[];
   griddep_wait();
   griddep_launch_dependents();
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
   const int nv = C / 8;
-  float ag[kMaxV][8], ab[kMaxV][8];  // this lane's dgamma / dbeta column accumulators
-#pragma unroll
-  for (int k = 0; k < kMaxV; ++k)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ag[k][i] = ab[k][i] = 0.f;
   const uint4* gvec = reinterpret_cast<const uint4*>(gamma);
-  for (long r = (long)blockIdx.x * nw + wib; r < rows; r += (long)gridDim.x * nw) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + r * C);
-    const uint4* hr = reinterpret_cast<const uint4*>(dh + r * C);
-    float xv[kMaxV][8], hv[kMaxV][8];
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < kMaxV; ++k) {
-      const int vi = lane + 32 * k;
-      if (vi < nv) {
-        unpack8(xr[vi], xv[k]);
-        unpack8(hr[vi], hv[k]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) s += xv[k][i];
-      }
-    }
-    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    const float mean = s / C;
-    float q = 0.f;
-#pragma unroll
-    for (int k = 0; k < kMaxV; ++k)
-      if (lane + 32 * k < nv) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float d = xv[k][i] - mean;
-          q += d * d;
-        }
-      }
-    for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
-    const float rstd = rsqrtf(q / C + eps);
-    // xhat in place of x, g = dh * gamma in place of dh; sums of g and of g * xhat
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kMaxV; ++k)
-      if (lane + 32 * k < nv) {
-        float gm[8];
-        unpack8(gvec[lane + 32 * k], gm);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float xh = (xv[k][i] - mean) * rstd;
-          xv[k][i] = xh;
-          ag[k][i] += hv[k][i] * xh;
-          ab[k][i] += hv[k][i];
-          const float g = hv[k][i] * gm[i];
-          hv[k][i] = g;
-          s1 += g;
-          s2 += g * xh;
-        }
-      }
-    for (int off = 16; off; off >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, off);
-    }
-    const float m1 = s1 / C, m2 = s2 / C;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + r * C);
-    const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + r * C) : nullptr;
-#pragma unroll
-    for (int k = 0; k < kMaxV; ++k) {
-      const int vi = lane + 32 * k;
-      if (vi < nv) {
-        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (rr) unpack8(rr[vi], rv);
-        uint32_t o[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float a = rv[2 * t] + rstd * (hv[k][2 * t] - m1 - xv[k][2 * t] * m2);
-          const float b = rv[2 * t + 1] + rstd * (hv[k][2 * t + 1] - m1 - xv[k][2 * t + 1] * m2);
-          o[t] = pack_bf16x2(a, b);
-        }
-        dxr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
-      }
-    }
-  }
-  // column partials: warps -> smem -> summed in warp order by the CTA's threads
+  const uint4* xr = reinterpret_cast<const uint4*>(x + r * C);
+  const uint4* hr = reinterpret_cast<const uint4*>(dh + r * C);
+  const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + r * C) : nullptr;
+  float xv[kMaxV][8], hv[kMaxV][8];
+  uint4 rv4[kMaxV];
+  float s = 0.f;
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k) {
     const int vi = lane + 32 * k;
     if (vi < nv) {
+      unpack8(xr[vi], xv[k]);
+      unpack8(hr[vi], hv[k]);
+      if (rr) rv4[k] = rr[vi];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += xv[k][i];
+    }
+  }
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  const float mean = s / C;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        red[(size_t)wib * 2 * C + vi * 8 + i] = ag[k][i];
-        red[(size_t)wib * 2 * C + C + vi * 8 + i] = ab[k][i];
+        const float d = xv[k][i] - mean;
+        q += d * d;
       }
+    }
+  for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+  const float rstd = rsqrtf(q / C + eps);
+  // xhat in place of x, g = dh * gamma in place of dh; sums of g and of g * xhat
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) {
+      float gm[8];
+      unpack8(gvec[lane + 32 * k], gm);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = (xv[k][i] - mean) * rstd;
+        xv[k][i] = xh;
+        const float g = hv[k][i] * gm[i];
+        hv[k][i] = g;
+        s1 += g;
+        s2 += g * xh;
+      }
+    }
+  for (int off = 16; off; off >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+  }
+  const float m1 = s1 / C, m2 = s2 / C;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + r * C);
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (rr) unpack8(rv4[k], rv);
+      uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float a = rv[2 * t] + rstd * (hv[k][2 * t] - m1 - xv[k][2 * t] * m2);
+        const float b = rv[2 * t + 1] + rstd * (hv[k][2 * t + 1] - m1 - xv[k][2 * t + 1] * m2);
+        o[t] = pack_bf16x2(a, b);
+      }
+      dxr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  if (lane == 0) stats[r] = make_float2(mean, rstd);
+}
+
+// LayerNorm backward, pass 2: column partials of dgamma = sum dh xhat and dbeta = sum dh over a chunk
+// of kLnRows rows per CTA.  Thread (x, y) = 8 columns (one 16-B vector of each row: a row group reads
+// whole rows, coalesced) of rows r0 + y, r0 + y + kLnRG, ...; the kLnRG row groups are then added in
+// y order.  part[chunk][0:C] = dgamma, part[chunk][C:2C] = dbeta, summed in chunk order after.
+constexpr int kLnRows = 64, kLnRG = 4;
+__global__ void __launch_bounds__(1024) ln_bwd_param_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            const __nv_bfloat16* __restrict__ dh,
+                                                            const float2* __restrict__ stats,
+                                                            float* __restrict__ part, long rows, int C) {
+  extern __shared__ float red[];  // [kLnRG][2][C]
+  griddep_wait();
+  griddep_launch_dependents();
+  const int nv = C / 8;
+  const int v = threadIdx.x, y = threadIdx.y;
+  const long r0 = (long)blockIdx.x * kLnRows, r1 = r0 + kLnRows < rows ? r0 + kLnRows : rows;
+  float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (v < nv) {
+#pragma unroll 4
+    for (long r = r0 + y; r < r1; r += kLnRG) {
+      const float2 st = stats[r];
+      float xv[8], hv[8];
+      unpack8(reinterpret_cast<const uint4*>(x + r * C)[v], xv);
+      unpack8(reinterpret_cast<const uint4*>(dh + r * C)[v], hv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ag[i] = fmaf(hv[i], (xv[i] - st.x) * st.y, ag[i]);
+        ab[i] += hv[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      red[(size_t)y * 2 * C + 8 * v + i] = ag[i];
+      red[(size_t)y * 2 * C + C + 8 * v + i] = ab[i];
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < 2 * C; c += blockDim.x) {
+  const int nt = blockDim.x * blockDim.y, t = y * blockDim.x + v;
+  for (int c = t; c < 2 * C; c += nt) {
     float a = 0.f;
-    for (int w = 0; w < nw; ++w) a += red[(size_t)w * 2 * C + c];
+#pragma unroll
+    for (int k = 0; k < kLnRG; ++k) a += red[(size_t)k * 2 * C + c];
     part[(size_t)blockIdx.x * 2 * C + c] = a;
+  }
+}
+
+// out[c] (+)= sum_b part[b][c] for few, long columns (nparts large, n small): warp w of the CTA sums
+// parts b = w, w + 8, ... for 32 consecutive columns (lanes), then the 8 warp sums are added in warp
+// order (deterministic).  out1 / split_at as wgrad_reduce_kernel.
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ part, int nparts, long n, long split_at,
+                                                     float* out0, float* out1, int accumulate) {
+  __shared__ float red[8][32];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long c = (long)blockIdx.x * 32 + lane;
+  float a = 0.f;
+  if (c < n)
+    for (int b = w; b < nparts; b += 8) a += part[(long)b * n + c];
+  red[w][lane] = a;
+  __syncthreads();
+  if (w == 0 && c < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    float* o = (out1 && c >= split_at) ? out1 + (c - split_at) : out0 + c;
+    *o = accumulate ? *o + t : t;
   }
 }
 
@@ -206,34 +253,47 @@ cudaError_t launch_wgrad_reduce(const float* part, int nparts, int64_t n, float*
 }
 
 int ln_bwd_blocks(int64_t rows, int num_sms) {
-  const int64_t need = (rows + 7) / 8;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(need, 2 * num_sms));
+  (void)num_sms;
+  return (int)std::max<int64_t>(1, (rows + kLnRows - 1) / kLnRows);  // pass-2 row chunks = partials
 }
 
-template <int kMaxV>
-static cudaError_t run_ln_bwd(int blocks, size_t smem, cudaStream_t st, const void* x, const void* gamma,
-                              const void* dh, const void* dres, void* dx, float* part, int64_t rows, int64_t C,
-                              float eps) {
-  static bool attr = false;  // per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(ln_bwd_bf16_kernel<kMaxV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         8 * 2 * 256 * kMaxV * 4);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  return launch_k(ln_bwd_bf16_kernel<kMaxV>, dim3(blocks), dim3(256), smem, st, 1, (const __nv_bfloat16*)x,
-                  (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)dh, (const __nv_bfloat16*)dres,
-                  (__nv_bfloat16*)dx, part, (long)rows, (int)C, eps);
+int64_t ln_bwd_scratch_bytes(int64_t rows, int64_t C) {
+  return ((rows * 8 + 255) / 256) * 256 + (int64_t)ln_bwd_blocks(rows, 0) * 2 * C * 4;
 }
 
 cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh, const void* dres,
-                          void* dx, float* part, float eps, int num_sms, cudaStream_t st) {
+                          void* dx, float* scratch, float* dgamma, float* dbeta, int accumulate, float eps,
+                          int num_sms, cudaStream_t st) {
+  (void)num_sms;
   if (rows == 0) return cudaSuccess;
   if (C % 8 != 0 || C > 2048) return cudaErrorNotSupported;
-  const int blocks = ln_bwd_blocks(rows, num_sms);
-  const size_t smem = (size_t)8 * 2 * C * sizeof(float);
-  if (C <= 256 * 5) return run_ln_bwd<5>(blocks, smem, st, x, gamma, dh, dres, dx, part, rows, C, eps);
-  return run_ln_bwd<8>(blocks, smem, st, x, gamma, dh, dres, dx, part, rows, C, eps);
+  float2* stats = reinterpret_cast<float2*>(scratch);
+  float* part = scratch + ((rows * 8 + 255) / 256) * 256 / 4;
+  const unsigned blocks = (unsigned)((rows * 32 + 255) / 256);
+  cudaError_t e;
+  if (C <= 256 * 5)
+    e = launch_k(ln_bwd_bf16_kernel<5>, dim3(blocks), dim3(256), 0, st, 1, (const __nv_bfloat16*)x,
+                 (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)dh, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx,
+                 stats, (long)rows, (int)C, eps);
+  else
+    e = launch_k(ln_bwd_bf16_kernel<8>, dim3(blocks), dim3(256), 0, st, 1, (const __nv_bfloat16*)x,
+                 (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)dh, (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx,
+                 stats, (long)rows, (int)C, eps);
+  if (e != cudaSuccess) return e;
+  const int chunks = ln_bwd_blocks(rows, num_sms), nv = (int)(C / 8);
+  const size_t smem = (size_t)kLnRG * 2 * C * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(ln_bwd_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kLnRG * 2 * 2048 * 4)) != cudaSuccess)
+      return e;
+    attr = true;
+  }
+  e = launch_k(ln_bwd_param_kernel, dim3((unsigned)chunks), dim3((unsigned)(((nv + 31) / 32) * 32), kLnRG), smem, st, 1,
+               (const __nv_bfloat16*)x, (const __nv_bfloat16*)dh, (const float2*)stats, part, (long)rows, (int)C);
+  if (e != cudaSuccess) return e;
+  return launch_k(colsum_kernel, dim3((unsigned)((2 * C + 31) / 32)), dim3(256), 0, st, 1, (const float*)part, chunks,
+                  (long)(2 * C), (long)C, dgamma, dbeta, accumulate);
 }
 
 cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, const void* dout, float* dvec,

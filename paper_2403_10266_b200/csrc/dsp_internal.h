@@ -76,8 +76,11 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
 cudaError_t launch_wgrad_reduce(const float* part, int nparts, int64_t n, float* out, int accumulate, cudaStream_t st,
                                 int64_t split_at = 0, float* out1 = nullptr);
 int ln_bwd_blocks(int64_t rows, int num_sms);
+int64_t ln_bwd_scratch_bytes(int64_t rows, int64_t C);  // row statistics + column partials
+// dx = dres + LN^T dh; dgamma (+)= sum dh xhat, dbeta (+)= sum dh (three launches: rows, column chunks, sum)
 cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* gamma, const void* dh, const void* dres,
-                          void* dx, float* part, float eps, int num_sms, cudaStream_t st);
+                          void* dx, float* scratch, float* dgamma, float* dbeta, int accumulate, float eps,
+                          int num_sms, cudaStream_t st);
 cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, const void* dout, float* dvec,
                                  cudaStream_t st);
 cudaError_t launch_dq_convert(int64_t tok, int64_t C, const float* dq_acc, void* dqkv, cudaStream_t st);
@@ -257,9 +260,9 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                     const uint32_t* box, CUtensorMapSwizzle swz, std::string* why);
-// f32 tensor map, no swizzle, no L2 promotion change (the FMHA backward's dQ reduce-add target)
+// f32 tensor map (the FMHA backward's dQ reduce-add target)
 bool make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                   const uint32_t* box, std::string* why);
+                   const uint32_t* box, std::string* why, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE);
 
 }  // namespace dsp
 

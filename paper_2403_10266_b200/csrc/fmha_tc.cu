@@ -2144,7 +2144,8 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
 // compute (P, dS, dQ / dK / dV epilogues).  Block-diagonal packing (G = 128 / L sequences per
 // tile, temporal T = 16) masks P and dS outside each thread's own sequence.
 struct BwdMaps {
-  CUtensorMap q[2], k[2], v[2], dout[2], dq[2], dk[2], dv[2], dq_acc;
+  CUtensorMap q[2], k[2], v[2], dout[2], dq[2], dk[2], dv[2];
+  CUtensorMap dq_acc[2];  // f32 reduce-add boxes: {32 columns, rows} SW128 (x2), {16 columns, rows} SW64
 };
 
 template <int NA, int RB>
@@ -2153,12 +2154,13 @@ struct BwdCfg {
   static constexpr int TILE = Base::TILE, DP = Base::DP, TX = Base::TX;
   static constexpr int OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE;  // stage s: Q at OFF_Q + 2 s TILE, dO next
   static constexpr int OFF_DS = 6 * TILE;                            // dS^T: 2 x [128 keys][64 queries] SW128
-  static constexpr int OFF_DQ = OFF_DS + 32768;                      // dQ f32 staging [128][DP] / dK, dV bf16
+  static constexpr int OFF_DQ = OFF_DS + 32768;                      // dQ f32 staging (3 swizzled boxes) / dK, dV bf16
   static constexpr int OFF_VEC = OFF_DQ + 128 * DP * 4;              // [2 buf][lse2 | D][128] f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
   static constexpr int SMEM = 1024 + OFF_BAR + 256;
   static constexpr bool OK = SMEM <= 227 * 1024 && RB == 16 && NA == 1;
   static_assert(2 * TILE <= 128 * DP * 4, "dK and dV staging fit in the dQ staging area");
+  static constexpr int THREADS = 384;  // warps 0-3: producer, MMA, idle x2; warps 4-11: two compute warpgroups
 };
 
 __device__ __forceinline__ TileCoord bwd_coord(const FmhaParams& p, int outer, int h, int pt) {
@@ -2178,15 +2180,15 @@ __device__ __forceinline__ TileCoord bwd_coord(const FmhaParams& p, int outer, i
 
 // bf16 row of a [128][DP] tile -> the TMA box staging layout (SW128 64-column chunks, then the SW32
 // remainder), scaled by `mul`
-template <int NA, int RB>
+template <int NA, int RB, int D0 = 0, int D1 = NA * 64 + RB>  // columns [D0, D1) of the row; v[0] = column D0
 __device__ __forceinline__ void stage_row_bf16(uint32_t st0, int row, const uint32_t* v, float mul) {
-  constexpr int DP = NA * 64 + RB;
 #pragma unroll
-  for (int d = 0; d < DP; d += 8) {
-    const uint32_t a0 = pack_bf16x2(__uint_as_float(v[d]) * mul, __uint_as_float(v[d + 1]) * mul);
-    const uint32_t a1 = pack_bf16x2(__uint_as_float(v[d + 2]) * mul, __uint_as_float(v[d + 3]) * mul);
-    const uint32_t a2 = pack_bf16x2(__uint_as_float(v[d + 4]) * mul, __uint_as_float(v[d + 5]) * mul);
-    const uint32_t a3 = pack_bf16x2(__uint_as_float(v[d + 6]) * mul, __uint_as_float(v[d + 7]) * mul);
+  for (int d = D0; d < D1; d += 8) {
+    const uint32_t* w = v + (d - D0);
+    const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]) * mul, __uint_as_float(w[1]) * mul);
+    const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]) * mul, __uint_as_float(w[3]) * mul);
+    const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]) * mul, __uint_as_float(w[5]) * mul);
+    const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]) * mul, __uint_as_float(w[7]) * mul);
     uint32_t addr;
     if (d < NA * 64) {
       const int blk = d >> 6, ch = (d & 63) >> 3;
@@ -2208,7 +2210,7 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* ma, const CUtensor
 }
 
 template <int NA, int RB>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     fmha_bwd_kernel(const __grid_constant__ BwdMaps mp, const FmhaParams p, const float* __restrict__ lse,
                     const float* __restrict__ dvec, int accum) {
   using Cfg = BwdCfg<NA, RB>;
@@ -2242,10 +2244,10 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 128);
-    mbar_init(kv_free, 128);
+    mbar_init(dq_free, 256);
+    mbar_init(kv_free, 256);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -2341,10 +2343,12 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t acc0 = j != 0;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step
-            // dV (+)= P^T dO  (P^T packed in TMEM over S^T's columns: 8 columns per 16 queries)
+            // dV (+)= P^T dO  (P^T packed in TMEM over S^T's columns, 8 columns per 16 queries:
+            // queries 0-63 at columns 0-31, queries 64-127 at columns 64-95)
+            const uint32_t pa = tS + 8 * kk + (kk >= 4 ? 32 : 0);
 #pragma unroll
-            for (int i = 0; i < NA; ++i) umma_bf16_ts(tdV + 64 * i, tS + 8 * kk, bmn(da, i, kk), idKa, acc0 | (kk != 0));
-            umma_bf16_ts(tdV + 64 * NA, tS + 8 * kk, bmn_r(da, kk), idKb, acc0 | (kk != 0));
+            for (int i = 0; i < NA; ++i) umma_bf16_ts(tdV + 64 * i, pa, bmn(da, i, kk), idKa, acc0 | (kk != 0));
+            umma_bf16_ts(tdV + 64 * NA, pa, bmn_r(da, kk), idKb, acc0 | (kk != 0));
             // dK (+)= dS^T Q  (dS^T K-major in smem: query chunk kk / 4, 32 B per 16 queries)
             const uint64_t ad = make_sdesc(dsb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B);
 #pragma unroll
@@ -2366,37 +2370,57 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q4 = warp & 3;
+    // Two compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
+    // queries [64 hw, 64 hw + 64) of S^T / dP^T (its P^T columns, its dS^T tile), then dQ columns
+    // [48 hw, ...) (0-47 | 48-79) and, at the item's end, dK (hw = 0) or dV (hw = 1).
+    const int q4 = warp & 3, hw = (warp - 4) >> 2;
     const int row = q4 * 32 + lane_id();
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off, tdV = tmem + 256 + lane_off,
                    tdK = tmem + 336 + lane_off, tdQ = tmem + 416 + lane_off;
-    const bool elected = threadIdx.x == 128;
+    const bool elected = threadIdx.x == 128;    // issues every bulk store / reduce of the CTA
+    const uint32_t bar_wg = 1 + hw, bar_all = 3;  // named barriers: own warpgroup (128), both (256)
     const float sl2 = p.scale_log2;
     const float sc = rsqrtf((float)p.Dh);
     const bool diag = p.G > 1;
     const int my_blk = row / p.L;
-    const uint32_t dsrow = smem_u32(sDS) + row * 128;
+    const uint32_t dsrow = smem_u32(sDS) + hw * 16384 + row * 128;
+    // lse2 / D of the query this thread stages (threads row < 64 of each warpgroup: query 64 hw + row),
+    // loaded one step ahead so the global latency is off the step's critical path
+    auto fetch = [&](int item, int j, float& l, float& d) {
+      l = INFINITY;
+      d = 0.f;
+      if (item >= p.items || row >= 64) return;
+      int outer, h, kvt;
+      decomp(item, outer, h, kvt);
+      const long tok = row_token(p, bwd_coord(p, outer, h, j), 64 * hw + row);
+      if (tok >= 0) {
+        l = __ldg(lse + tok * p.NH + h);
+        d = __ldg(dvec + tok * p.NH + h);
+      }
+    };
+    float nl, nd;
+    fetch(blockIdx.x, 0, nl, nd);
     uint32_t it = 0, g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
       int outer, h, kvt;
       decomp(item, outer, h, kvt);
       for (int j = 0; j < nq; ++j, ++g) {
-        // this query tile's lse2 and D, one value per thread, broadcast through smem
-        float* l2 = sVec + (g & 1) * 256;
+        float* l2 = sVec + (g & 1) * 256 + hw * 64;  // this warpgroup's 64 queries
         float* dd = l2 + 128;
-        {
-          const TileCoord tq = bwd_coord(p, outer, h, j);
-          const long tok = row_token(p, tq, row);
-          l2[row] = tok >= 0 ? lse[tok * p.NH + h] : INFINITY;
-          dd[row] = tok >= 0 ? dvec[tok * p.NH + h] : 0.f;
+        if (row < 64) {
+          l2[row] = nl;
+          dd[row] = nd;
         }
+        if (j + 1 < nq) fetch(item, j + 1, nl, nd);
+        else fetch(item + gridDim.x, 0, nl, nd);
         if (!accum && elected) bulk_wait_group_read0();  // the previous direct dQ store has read sDS
-        named_bar_sync(1, 128);
+        named_bar_sync(accum ? bar_wg : bar_all, accum ? 128 : 256);
         mbar_wait(s_full, g & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int c32 = 0; c32 < 4; ++c32) {
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c32 = 2 * hw + cc;
           uint32_t sv[32], dv[32];
           tmem_ld32(tS + c32 * 32, sv);
           tmem_ld32(tdP + c32 * 32, dv);
@@ -2407,74 +2431,85 @@ __global__ void __launch_bounds__(256, 1)
             float pp[2], ds[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int q = c32 * 32 + 2 * i + e;
-              const bool ok = !diag || q / p.L == my_blk;
-              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sv[2 * i + e]), sl2, -l2[q])) : 0.f;
+              const int qc = cc * 32 + 2 * i + e;  // query within the warpgroup's 64
+              const bool ok = !diag || (64 * hw + qc) / p.L == my_blk;
+              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sv[2 * i + e]), sl2, -l2[qc])) : 0.f;
               pp[e] = pe;
-              ds[e] = pe * (__uint_as_float(dv[2 * i + e]) - dd[q]) * sc;
+              ds[e] = pe * (__uint_as_float(dv[2 * i + e]) - dd[qc]) * sc;
             }
             pk[i] = pack_bf16x2(pp[0], pp[1]);
             dk[i] = pack_bf16x2(ds[0], ds[1]);
           }
-          tmem_st16(tS + c32 * 16, pk);  // P^T over already-consumed S^T columns
+          // P^T over S^T columns this warpgroup has already consumed: queries [64 hw, 64 hw + 64)
+          // packed into columns [64 hw, 64 hw + 32) (the other warpgroup may still read its own)
+          tmem_st16(tS + hw * 64 + cc * 16, pk);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int ch = (c32 & 1) * 4 + u;
-            st_shared_v4(dsrow + (c32 >> 1) * 16384 + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1],
-                         dk[4 * u + 2], dk[4 * u + 3]);
+            const int ch = cc * 4 + u;
+            st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
           }
         }
         tmem_st_wait();
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(p_full);
-        // dQ of this query tile
+        // dQ of this query tile: warpgroup 0 columns 0-47, warpgroup 1 columns 48-79
         mbar_wait(dq_full, g & 1);
         tc_fence_after();
-        uint32_t qv[DP];
+        uint32_t qv[48];
 #pragma unroll
-        for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdQ + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
+        for (int c = 0; c < 3; ++c)
+          if (hw == 0 || c < 2) tmem_ld16(tdQ + hw * 48 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(dq_free);
         const TileCoord tq = bwd_coord(p, outer, h, j);
         if (accum) {
+          // f32 staging as three swizzled TMA boxes (conflict-free row writes): columns 0-31 and 32-63
+          // SW128 (128 B rows), 64-79 SW64 (64 B rows); reduce-added into dq_acc
           if (elected) bulk_wait_group_read0();  // the previous reduce / dK, dV stores have read sDQ
-          named_bar_sync(1, 128);
-          const uint32_t r0 = smem_u32(sDQ) + row * DP * 4;
+          named_bar_sync(bar_all, 256);
+          const uint32_t s0 = smem_u32(sDQ);
 #pragma unroll
-          for (int d = 0; d < DP; d += 4) st_shared_v4(r0 + d * 4, qv[d], qv[d + 1], qv[d + 2], qv[d + 3]);
+          for (int c4 = 0; c4 < 12; ++c4) {
+            if (hw == 1 && c4 >= 8) break;
+            const int col = hw * 48 + c4 * 4;  // 4 floats = one 16-B chunk
+            uint32_t addr;
+            if (col < 64) addr = s0 + (col >> 5) * 16384 + row * 128 + ((((col & 31) >> 2) ^ (row & 7)) << 4);
+            else addr = s0 + 32768 + row * 64 + ((((col - 64) >> 2) ^ ((row >> 1) & 3)) << 4);
+            st_shared_v4(addr, qv[4 * c4], qv[4 * c4 + 1], qv[4 * c4 + 2], qv[4 * c4 + 3]);
+          }
           fence_proxy_async_smem();
-          named_bar_sync(1, 128);
+          named_bar_sync(bar_all, 256);
           if (elected) {
-            tma_reduce_add_5d(&mp.dq_acc, sDQ, 0, tq.h, tq.x2, tq.x3, tq.x4);
+            tma_reduce_add_5d(&mp.dq_acc[0], sDQ, 0, tq.h, tq.x2, tq.x3, tq.x4);
+            tma_reduce_add_5d(&mp.dq_acc[0], sDQ + 16384, 32, tq.h, tq.x2, tq.x3, tq.x4);
+            tma_reduce_add_5d(&mp.dq_acc[1], sDQ + 32768, 64, tq.h, tq.x2, tq.x3, tq.x4);
             bulk_commit_group();
           }
         } else {  // one key tile per sequence: dQ is final, bf16 through the (free) dS^T buffer
-          stage_row_bf16<NA, RB>(smem_u32(sDS), row, qv, 1.f);
+          if (hw == 0) stage_row_bf16<NA, RB, 0, 48>(smem_u32(sDS), row, qv, 1.f);
+          else stage_row_bf16<NA, RB, 48, 80>(smem_u32(sDS), row, qv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(1, 128);
+          named_bar_sync(bar_all, 256);
           if (elected) {
             store_tile<NA, RB>(&mp.dq[0], &mp.dq[1], sDS, tq);
             bulk_commit_group();
           }
         }
-        if (j == nq - 1) {  // dK, dV final (dq_full of the last tile covers every MMA of the item)
+        if (j == nq - 1) {  // dK (warpgroup 0) or dV (1) final: dq_full of the last tile covers every MMA
           uint32_t kv[DP];
 #pragma unroll
-          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdK + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
-          tmem_ld_wait();
-          if (elected) bulk_wait_group_read0();
-          named_bar_sync(1, 128);
-          stage_row_bf16<NA, RB>(smem_u32(sDQ), row, kv, 1.f);
-#pragma unroll
-          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdV + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
+          for (int c = 0; c < DP / 16; ++c)
+            tmem_ld16((hw == 0 ? tdK : tdV) + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(kv_free);
-          stage_row_bf16<NA, RB>(smem_u32(sDQ + Cfg::TILE), row, kv, 1.f);
+          if (elected) bulk_wait_group_read0();
+          named_bar_sync(bar_all, 256);
+          stage_row_bf16<NA, RB>(smem_u32(sDQ + hw * Cfg::TILE), row, kv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(1, 128);
+          named_bar_sync(bar_all, 256);
           if (elected) {
             const TileCoord tk = bwd_coord(p, outer, h, kvt);
             store_tile<NA, RB>(&mp.dk[0], &mp.dk[1], sDQ, tk);
@@ -2755,10 +2790,12 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
   if (accum) {
     uint64_t fstr[4];
     for (int i = 0; i < 4; ++i) fstr[i] = 2 * ostr[i];
-    uint32_t boxf[5] = {(uint32_t)Cfg::DP, 1, r0, r1, 1};
-    if (!make_tmap_f32(&mp.dq_acc, dq_acc, 5, dims, fstr, boxf, why)) return cudaErrorInvalidValue;
+    uint32_t boxf0[5] = {32, 1, r0, r1, 1}, boxf1[5] = {16, 1, r0, r1, 1};
+    if (!make_tmap_f32(&mp.dq_acc[0], dq_acc, 5, dims, fstr, boxf0, why, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !make_tmap_f32(&mp.dq_acc[1], dq_acc, 5, dims, fstr, boxf1, why, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
   } else {
-    mp.dq_acc = mp.q[0];  // unused
+    mp.dq_acc[0] = mp.dq_acc[1] = mp.q[0];  // unused
   }
   cudaError_t err = launch_attn_bwd_dvec(tok, NH, p.Dh, o, dout, dvec, st);
   if (err != cudaSuccess) return err;
@@ -2771,7 +2808,7 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
     attr = true;
   }
   const int grid = p.items < num_sms ? p.items : num_sms;
-  err = launch_k(kern, dim3(grid), dim3(256), Cfg::SMEM, st, 1, mp, p, lse, (const float*)dvec, accum);
+  err = launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, mp, p, lse, (const float*)dvec, accum);
   if (err != cudaSuccess) return err;
   if (accum) return launch_dq_convert(tok, C, dq_acc, dqkv, st);
   return cudaSuccess;

@@ -835,7 +835,7 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, int rank, const uint64_t* 
 }
 
 bool make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                   const uint32_t* box, std::string* why) {
+                   const uint32_t* box, std::string* why, CUtensorMapSwizzle swz) {
   auto enc = tensor_map_encoder();
   if (!enc) {
     if (why) *why = "cuTensorMapEncodeTiled unavailable (driver entry point)";
@@ -843,7 +843,7 @@ bool make_tmap_f32(CUtensorMap* m, const void* base, int rank, const uint64_t* d
   }
   uint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     if (why) *why = "cuTensorMapEncodeTiled (f32) failed with CUresult " + std::to_string((int)r);
