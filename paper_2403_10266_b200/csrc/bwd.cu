@@ -7,8 +7,8 @@
 //                          dbeta = sum dh, summed in CTA order by wgrad_reduce_kernel.
 //   wgrad_reduce_kernel    out (+)= sum_s part[s] in slice order (split-K weight gradients and the
 //                          LayerNorm parameter partials: deterministic, no atomics).
-//   attn_bwd_dvec_kernel   D[tok, h] = sum_d dO * O (the softmax-backward row term
-//                          rowsum(dP * P) = dO . O, oracle/backward.py attention_core_bwd).
+//   attn_bwd_dvec_kernel   D[tok, h] = sum_d dO * O / sqrt(Dh) (the softmax-backward row term
+//                          rowsum(dP * P) = dO . O, oracle/backward.py attention_core_bwd, pre-scaled).
 //   dq_convert_kernel      dQ accumulated in fp32 by the FMHA backward -> bf16 into dqkv[:, 0:C].
 // All bound by HBM bytes: one 16-B vector per lane access, rows across warps.
 #include <cuda_bf16.h>
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(256) attn_bwd_dvec_kernel(const __nv_bfloat16*
 #pragma unroll
     for (int t = 0; t < 8; ++t) acc = fmaf(a[t], b[t], acc);
   }
-  dvec[i] = acc;
+  dvec[i] = acc * rsqrtf((float)Dh);  // pre-scaled by 1 / sqrt(Dh): dS = P (dP - D) / sqrt(Dh) in the FMHA backward
 }
 
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ dq, uint2* __restrict__ dqkv,

@@ -2143,6 +2143,12 @@ cudaError_t run_fmha(const FmhaViews& vw, const FmhaParams& p, const uint32_t* b
 // per item; {Q, dO} per query tile, two stages), warp 1 TMEM allocator + MMA issuer, warps 4-7
 // compute (P, dS, dQ / dK / dV epilogues).  Block-diagonal packing (G = 128 / L sequences per
 // tile, temporal T = 16) masks P and dS outside each thread's own sequence.
+#ifdef DSP_FMHA_BWD_TRACE  // per-step clock64 stamps of CTA 0 (scripts/fmha_bwd_trace.py)
+#define BWD_STAMP(idx) \
+  do { if (p.trace && blockIdx.x == 0 && g < 64) p.trace[g * 8 + (idx)] = clock64(); } while (0)
+#else
+#define BWD_STAMP(idx) do { } while (0)
+#endif
 struct BwdMaps {
   CUtensorMap q[2], k[2], v[2], dout[2], dq[2], dk[2], dv[2];
   CUtensorMap dq_acc[2];  // f32 reduce-add boxes: {32 columns, rows} SW128 (x2), {16 columns, rows} SW64
@@ -2154,13 +2160,16 @@ struct BwdCfg {
   static constexpr int TILE = Base::TILE, DP = Base::DP, TX = Base::TX;
   static constexpr int OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE;  // stage s: Q at OFF_Q + 2 s TILE, dO next
   static constexpr int OFF_DS = 6 * TILE;                            // dS^T: 2 x [128 keys][64 queries] SW128
-  static constexpr int OFF_DQ = OFF_DS + 32768;                      // dQ f32 staging (3 swizzled boxes) / dK, dV bf16
+  static constexpr int OFF_P = OFF_DS + 32768;                       // P^T: same layout
+  static constexpr int OFF_DQ = OFF_P + 32768;                       // dQ f32 staging (3 swizzled boxes) / dK, dV bf16
   static constexpr int OFF_VEC = OFF_DQ + 128 * DP * 4;              // [2 buf][lse2 | D][128] f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
-  static constexpr int SMEM = 1024 + OFF_BAR + 256;
+  // no alignment slack: dynamic smem starts 1024-B aligned after the system-reserved block (checked)
+  static constexpr int SMEM = OFF_BAR + 256;
   static constexpr bool OK = SMEM <= 227 * 1024 && RB == 16 && NA == 1;
   static_assert(2 * TILE <= 128 * DP * 4, "dK and dV staging fit in the dQ staging area");
-  static constexpr int THREADS = 384;  // warps 0-3: producer, MMA, idle x2; warps 4-11: two compute warpgroups
+  // warps 0-3: producer, MMA, idle x2; warps 4-11: two compute warpgroups; warps 12-15: epilogue warpgroup
+  static constexpr int THREADS = 512;
 };
 
 __device__ __forceinline__ TileCoord bwd_coord(const FmhaParams& p, int outer, int h, int pt) {
@@ -2209,18 +2218,31 @@ __device__ __forceinline__ void store_tile(const CUtensorMap* ma, const CUtensor
   tma_store_5d(mb, src + NA * 16384, 64 * NA, t.h, t.x2, t.x3, t.x4);
 }
 
+// The backward's Q, K, V, dO tiles: DP / 16 boxes of [rows][16 columns], SW32, 4 KB apart.  One
+// layout serves as the K-major operand (one box per 16-column k-step, SBO 256 B) and as an MN-major
+// operand with N = DP in ONE instruction (16-column groups LBO = 4 KB apart, 8-row groups 256 B):
+// the dV / dK / dQ products take one N = 80 MMA per 16-row k-step instead of N = 64 + N = 16.
 template <int NA, int RB>
-__global__ void __launch_bounds__(384, 1)
+__device__ __forceinline__ void load_tile_sw32(uint8_t* dst, const CUtensorMap* mb, uint64_t* bar, const TileCoord& t) {
+  constexpr int DP = NA * 64 + RB;
+#pragma unroll
+  for (int i = 0; i < DP / 16; ++i) tma_load_5d(dst + i * 4096, mb, bar, 16 * i, t.h, t.x2, t.x3, t.x4);
+}
+
+template <int NA, int RB, bool DIAG>
+__global__ void __launch_bounds__(512, 1)
     fmha_bwd_kernel(const __grid_constant__ BwdMaps mp, const FmhaParams p, const float* __restrict__ lse,
                     const float* __restrict__ dvec, int accum) {
   using Cfg = BwdCfg<NA, RB>;
   using Base = FmhaCfg<NA, RB>;
   constexpr int DP = Cfg::DP;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if ((smem_u32(smem_raw) & 1023) != 0) __trap();  // layout assumes a 1024-B aligned base
+  uint8_t* smem = smem_raw;
   uint8_t* sK = smem + Cfg::OFF_K;
   uint8_t* sV = smem + Cfg::OFF_V;
   uint8_t* sDS = smem + Cfg::OFF_DS;
+  uint8_t* sP = smem + Cfg::OFF_P;
   uint8_t* sDQ = smem + Cfg::OFF_DQ;
   float* sVec = reinterpret_cast<float*>(smem + Cfg::OFF_VEC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -2233,7 +2255,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* dq_full = bars + 8;
   uint64_t* dq_free = bars + 9;  // count 128
   uint64_t* kv_free = bars + 10; // count 128
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* s_free = bars + 11;  // count 256: the compute warpgroups have read S^T / dP^T out of TMEM
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = warp_id();
   if (warp == 0 && lane_id() == 0) {
@@ -2246,8 +2269,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(s_full, 1);
     mbar_init(p_full, 256);
     mbar_init(dq_full, 1);
-    mbar_init(dq_free, 256);
-    mbar_init(kv_free, 256);
+    mbar_init(dq_free, 128);
+    mbar_init(kv_free, 128);
+    mbar_init(s_free, 256);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -2270,6 +2294,10 @@ __global__ void __launch_bounds__(384, 1)
     outer = rest / p.NH;
   };
 
+  // launch allocation 128 regs x 512 threads: 80 x 128 (warps 0-3) + 152 x 256 (compute) + 128 x 128 (epilogue)
+  if (warp < 4) setmaxnreg_dec<80>();
+  else if (warp < 12) setmaxnreg_inc<152>();
+  // (the epilogue warpgroup keeps the launch allocation of 128)
   if (warp == 0) {
     if (elect_one()) {
       uint32_t it = 0, g = 0;
@@ -2279,237 +2307,288 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait_sleep(kv_empty, (it & 1) ^ 1);
         mbar_arrive_expect_tx(kv_full, 2 * Cfg::TX);
         const TileCoord tk = bwd_coord(p, outer, h, kvt);
-        load_tile<NA, RB>(sK, &mp.k[0], &mp.k[1], kv_full, tk);
-        load_tile<NA, RB>(sV, &mp.v[0], &mp.v[1], kv_full, tk);
+        load_tile_sw32<NA, RB>(sK, &mp.k[1], kv_full, tk);
+        load_tile_sw32<NA, RB>(sV, &mp.v[1], kv_full, tk);
         for (int j = 0; j < nq; ++j, ++g) {
           const int st = g & 1;
           mbar_wait_sleep(&q_empty[st], ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&q_full[st], 2 * Cfg::TX);
           uint8_t* qb = smem + Cfg::OFF_Q + 2 * st * Cfg::TILE;
           const TileCoord tq = bwd_coord(p, outer, h, j);
-          load_tile<NA, RB>(qb, &mp.q[0], &mp.q[1], &q_full[st], tq);
-          load_tile<NA, RB>(qb + Cfg::TILE, &mp.dout[0], &mp.dout[1], &q_full[st], tq);
+          load_tile_sw32<NA, RB>(qb, &mp.q[1], &q_full[st], tq);
+          load_tile_sw32<NA, RB>(qb + Cfg::TILE, &mp.dout[1], &q_full[st], tq);
         }
       }
     }
   } else if (warp == 1) {
+    constexpr int DP = Cfg::DP;
     constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);       // S^T, dP^T
-    constexpr uint32_t idKa = make_idesc_bf16(128, 64, 0, 1);       // dV, dK: A K-major, B MN-major
-    constexpr uint32_t idKb = make_idesc_bf16(128, RB, 0, 1);
-    constexpr uint32_t idQa = make_idesc_bf16(128, 64, 1, 1);       // dQ: A (dS) MN-major, B (K) MN-major
-    constexpr uint32_t idQb = make_idesc_bf16(128, RB, 1, 1);
+    constexpr uint32_t idK = make_idesc_bf16(128, DP, 0, 1);        // dV, dK: A K-major, B MN-major (N = 80)
+    constexpr uint32_t idQ = make_idesc_bf16(128, DP, 1, 1);        // dQ: A (dS) MN-major, B (K) MN-major
     const uint32_t kb = smem_u32(sK), vb = smem_u32(sV), dsb = smem_u32(sDS);
     const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 336, tdQ = tmem + 416;
-    // D[tmem] = X Y^T over the head dim: X, Y two [128][DP] K-major tiles
+    // D[tmem] = X Y^T over the head dim: X, Y two [128][DP] tiles of SW32 boxes (one box per k-step)
     auto qk = [&](uint32_t d, uint32_t xa, uint32_t ya) {
-      int step = 0;
 #pragma unroll
-      for (int i = 0; i < NA; ++i)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk, ++step)
-          umma_bf16_ss(d, make_sdesc(xa + i * 16384 + kk * 32, 16, 1024, SW_128B),
-                       make_sdesc(ya + i * 16384 + kk * 32, 16, 1024, SW_128B), idS, step != 0);
-#pragma unroll
-      for (int kk = 0; kk < RB / 16; ++kk, ++step)
-        umma_bf16_ss(d, make_sdesc(xa + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW),
-                     make_sdesc(ya + NA * 16384 + kk * 32, 16, 8 * Base::RB_ROW, Base::RB_SW), idS, step != 0);
+      for (int kk = 0; kk < DP / 16; ++kk)
+        umma_bf16_ss(d, make_sdesc(xa + kk * 4096, 16, 256, SW_32B), make_sdesc(ya + kk * 4096, 16, 256, SW_32B), idS,
+                     kk != 0);
     };
-    // MN-major B descriptor of a [128 rows = K][DP] tile: head-dim chunk i, 16-row k-step kk
-    auto bmn = [&](uint32_t base, int i, int kk) {
-      return make_sdesc(base + i * 16384 + kk * 2048, 16384, 1024, SW_128B);
+    // MN-major B descriptor of a [128 rows = K][DP] tile, all DP columns, 16-row k-step kk
+    auto bmn = [&](uint32_t base, int kk) { return make_sdesc(base + kk * 512, 4096, 256, SW_32B); };
+    // Issue order: S^T/dP^T of tile g + 1 as soon as the compute warps have read tile g's out of TMEM
+    // (s_free), BEFORE dV/dK/dQ of tile g, so tile g + 1's exponentials overlap tile g's products
+    // (P^T and dS^T live in shared memory).  Across an item boundary the next K, V land only after
+    // the item's last products (single K/V buffer), so there the order is the plain one.
+    const uint32_t pbb = smem_u32(sP);
+    auto issue_a = [&](uint32_t gg, bool first_of_item, uint32_t itx) {
+      const int st = gg & 1;
+      const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
+      if (first_of_item) mbar_wait(kv_full, itx & 1);
+      mbar_wait(&q_full[st], (gg >> 1) & 1);
+      if (gg >= 1) mbar_wait(s_free, (gg - 1) & 1);  // S^T / dP^T of the previous tile read out of TMEM
+      tc_fence_after();
+      if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(3); }
+      if (elect_one()) {
+        qk(tS, kb, qa);   // S^T = K Q^T
+        qk(tdP, vb, da);  // dP^T = V dO^T
+        umma_commit(s_full);
+      }
+      __syncwarp();
     };
-    auto bmn_r = [&](uint32_t base, int kk) {
-      return make_sdesc(base + NA * 16384 + kk * 16 * Base::RB_ROW, 16384, 8 * Base::RB_ROW, Base::RB_SW);
+    auto issue_bc = [&](uint32_t gg, int j, uint32_t itx) {
+      const int st = gg & 1;
+      const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
+      mbar_wait(p_full, gg & 1);
+      if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(4); }
+      if (gg >= 1) mbar_wait(dq_free, (gg - 1) & 1);
+      if (j == 0 && itx >= 1) mbar_wait(kv_free, (itx - 1) & 1);
+      tc_fence_after();
+      if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(5); }
+      if (elect_one()) {
+        const uint32_t acc0 = j != 0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step; P^T, dS^T K-major in smem (chunk kk / 4)
+          const uint32_t co = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16_ss(tdV, make_sdesc(pbb + co, 16, 1024, SW_128B), bmn(da, kk), idK, acc0 | (kk != 0));   // dV += P^T dO
+          umma_bf16_ss(tdK, make_sdesc(dsb + co, 16, 1024, SW_128B), bmn(qa, kk), idK, acc0 | (kk != 0));   // dK += dS^T Q
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
+          umma_bf16_ss(tdQ, make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B), bmn(kb, kk), idQ, kk != 0);
+        umma_commit(dq_full);
+        umma_commit(&q_empty[st]);
+        if (j == nq - 1) umma_commit(kv_empty);
+      }
+      __syncwarp();
     };
     uint32_t it = 0, g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      issue_a(g, true, it);
       for (int j = 0; j < nq; ++j, ++g) {
-        const int st = g & 1;
-        const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
-        if (j == 0) mbar_wait(kv_full, it & 1);
-        mbar_wait(&q_full[st], (g >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          qk(tS, kb, qa);   // S^T = K Q^T
-          qk(tdP, vb, da);  // dP^T = V dO^T
-          umma_commit(s_full);
-        }
-        __syncwarp();
-        mbar_wait(p_full, g & 1);
-        if (g >= 1) mbar_wait(dq_free, (g - 1) & 1);
-        if (j == 0 && it >= 1) mbar_wait(kv_free, (it - 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t acc0 = j != 0;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step
-            // dV (+)= P^T dO  (P^T packed in TMEM over S^T's columns, 8 columns per 16 queries:
-            // queries 0-63 at columns 0-31, queries 64-127 at columns 64-95)
-            const uint32_t pa = tS + 8 * kk + (kk >= 4 ? 32 : 0);
-#pragma unroll
-            for (int i = 0; i < NA; ++i) umma_bf16_ts(tdV + 64 * i, pa, bmn(da, i, kk), idKa, acc0 | (kk != 0));
-            umma_bf16_ts(tdV + 64 * NA, pa, bmn_r(da, kk), idKb, acc0 | (kk != 0));
-            // dK (+)= dS^T Q  (dS^T K-major in smem: query chunk kk / 4, 32 B per 16 queries)
-            const uint64_t ad = make_sdesc(dsb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B);
-#pragma unroll
-            for (int i = 0; i < NA; ++i) umma_bf16_ss(tdK + 64 * i, ad, bmn(qa, i, kk), idKa, acc0 | (kk != 0));
-            umma_bf16_ss(tdK + 64 * NA, ad, bmn_r(qa, kk), idKb, acc0 | (kk != 0));
-          }
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
-            const uint64_t ad = make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B);
-#pragma unroll
-            for (int i = 0; i < NA; ++i) umma_bf16_ss(tdQ + 64 * i, ad, bmn(kb, i, kk), idQa, kk != 0);
-            umma_bf16_ss(tdQ + 64 * NA, ad, bmn_r(kb, kk), idQb, kk != 0);
-          }
-          umma_commit(dq_full);
-          umma_commit(&q_empty[st]);
-          if (j == nq - 1) umma_commit(kv_empty);
-        }
-        __syncwarp();
+        if (j + 1 < nq) issue_a(g + 1, false, it);
+        issue_bc(g, j, it);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 12) {
     // Two compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
-    // queries [64 hw, 64 hw + 64) of S^T / dP^T (its P^T columns, its dS^T tile), then dQ columns
-    // [48 hw, ...) (0-47 | 48-79) and, at the item's end, dK (hw = 0) or dV (hw = 1).
+    // queries [64 hw, 64 hw + 64) of S^T / dP^T (its P^T columns, its dS^T tile).
     const int q4 = warp & 3, hw = (warp - 4) >> 2;
     const int row = q4 * 32 + lane_id();
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off, tdV = tmem + 256 + lane_off,
-                   tdK = tmem + 336 + lane_off, tdQ = tmem + 416 + lane_off;
-    const bool elected = threadIdx.x == 128;    // issues every bulk store / reduce of the CTA
-    const uint32_t bar_wg = 1 + hw, bar_all = 3;  // named barriers: own warpgroup (128), both (256)
+    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+    const uint32_t bar_wg = 1 + hw;  // named barrier of the own warpgroup (128)
     const float sl2 = p.scale_log2;
     const float sc = rsqrtf((float)p.Dh);
-    const bool diag = p.G > 1;
-    const int my_blk = row / p.L;
+    // block-diagonal packing: this key row's sequence owns queries [qlo, qhi) of the warpgroup's 64
+    const int qlo = p.G > 1 ? (row / p.L) * p.L - 64 * hw : 0;
+    const int qhi = p.G > 1 ? qlo + p.L : 64;
     const uint32_t dsrow = smem_u32(sDS) + hw * 16384 + row * 128;
+    const uint32_t prow = smem_u32(sP) + hw * 16384 + row * 128;
     // lse2 / D of the query this thread stages (threads row < 64 of each warpgroup: query 64 hw + row),
     // loaded one step ahead so the global latency is off the step's critical path
-    auto fetch = [&](int item, int j, float& l, float& d) {
-      l = INFINITY;
-      d = 0.f;
-      if (item >= p.items || row >= 64) return;
-      int outer, h, kvt;
-      decomp(item, outer, h, kvt);
-      const long tok = row_token(p, bwd_coord(p, outer, h, j), 64 * hw + row);
+    // lse2 and D / sqrt(Dh) of the query this thread stages (threads row < 64 of each warpgroup: query
+    // 64 hw + row), copied global -> smem by cp.async one tile ahead (no registers held across the tile,
+    // the latency off the critical path); padding queries get lse2 = +inf (P = 0), D = 0
+    auto fetch = [&](int item, int j, uint32_t vbuf) {
+      if (row >= 64) return;
+      long tok = -1;
+      int h = 0;
+      if (item < p.items) {
+        int outer, kvt;
+        decomp(item, outer, h, kvt);
+        tok = row_token(p, bwd_coord(p, outer, h, j), 64 * hw + row);
+      }
       if (tok >= 0) {
-        l = __ldg(lse + tok * p.NH + h);
-        d = __ldg(dvec + tok * p.NH + h);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(vbuf + row * 4), "l"(lse + tok * p.NH + h) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(vbuf + 512 + row * 4), "l"(dvec + tok * p.NH + h)
+                     : "memory");
+      } else {
+        st_shared_f32(vbuf + row * 4, INFINITY);
+        st_shared_f32(vbuf + 512 + row * 4, 0.f);
       }
     };
-    float nl, nd;
-    fetch(blockIdx.x, 0, nl, nd);
-    uint32_t it = 0, g = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+    fetch(blockIdx.x, 0, smem_u32(sVec + hw * 64));
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+      for (int j = 0; j < nq; ++j, ++g) {
+        const uint32_t vb = smem_u32(sVec + (g & 1) * 256 + hw * 64);  // this warpgroup's 64 queries
+        asm volatile("cp.async.wait_all;" ::: "memory");               // this tile's lse2 / D landed
+        const uint32_t vnext = smem_u32(sVec + ((g + 1) & 1) * 256 + hw * 64);
+        if (threadIdx.x == 128) BWD_STAMP(0);
+        named_bar_sync(bar_wg, 128);
+        // the next tile's values go to the other buffer (its readers finished before this barrier)
+        if (j + 1 < nq) fetch(item, j + 1, vnext);
+        else fetch(item + gridDim.x, 0, vnext);
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+        if (threadIdx.x == 128) BWD_STAMP(1);
+        // four 16-query chunks; the TMEM loads of chunk k + 1 are in flight while chunk k is computed
+        // (tcgen05.wait::ld waits for every load issued, so the next pair is issued after the wait)
+        uint32_t sa[16], da[16], sb[16], db[16];
+        tmem_ld16(tS + hw * 64, sa);
+        tmem_ld16(tdP + hw * 64, da);
+        tmem_ld_wait();
+        uint32_t pk[16], dk[16];
+        auto chunk = [&](int k, const uint32_t (&sv)[16], const uint32_t (&dv)[16]) {
+          // packed pairs (FFMA2 / FMUL2): x = s scale_log2 - lse2, P = 2^x, dS = P (dP / sqrt(Dh) - D / sqrt(Dh))
+          const float2 sl22 = make_float2(sl2, sl2), sc2 = make_float2(sc, sc);
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {  // 4 queries per step: lse2 and D / sqrt(Dh) as 16-B shared loads
+            const int q0 = k * 16 + 4 * i4;
+            const float4 l4 = ld_shared_f32x4(vb + q0 * 4), d4 = ld_shared_f32x4(vb + 512 + q0 * 4);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int e = 4 * i4 + 2 * h2;
+              const float2 s2 = make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
+              const float2 p2 = make_float2(__uint_as_float(dv[e]), __uint_as_float(dv[e + 1]));
+              const float2 nl = h2 ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y);
+              const float2 nd = h2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y);
+              float2 x = ffma2(s2, sl22, nl);
+              if (DIAG) {
+                const int qc = q0 + 2 * h2;
+                if (qc < qlo || qc >= qhi) x.x = -INFINITY;
+                if (qc + 1 < qlo || qc + 1 >= qhi) x.y = -INFINITY;
+              }
+              const float2 pe = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              const float2 ds = fmul2(pe, ffma2(p2, sc2, nd));
+              const int kk = (k & 1) * 8 + 2 * i4 + h2;
+              pk[kk] = pack_bf16x2(pe.x, pe.y);
+              dk[kk] = pack_bf16x2(ds.x, ds.y);
+            }
+          }
+          if (k & 1) {  // P^T and dS^T of 32 queries -> smem (SW128 K-major over queries)
+            const int cc = k >> 1;
+            if (cc == 0 && g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products read them
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int ch = cc * 4 + u;
+              st_shared_v4(prow + ((ch ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+              st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+            }
+          }
+        };
+        tmem_ld16(tS + hw * 64 + 16, sb);
+        tmem_ld16(tdP + hw * 64 + 16, db);
+        chunk(0, sa, da);
+        tmem_ld_wait();
+        tmem_ld16(tS + hw * 64 + 32, sa);
+        tmem_ld16(tdP + hw * 64 + 32, da);
+        chunk(1, sb, db);
+        tmem_ld_wait();
+        tmem_ld16(tS + hw * 64 + 48, sb);
+        tmem_ld16(tdP + hw * 64 + 48, db);
+        chunk(2, sa, da);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's may be issued
+        chunk(3, sb, db);
+        fence_proxy_async_smem();
+        if (threadIdx.x == 128) BWD_STAMP(2);
+        mbar_arrive(p_full);
+      }
+    }
+  } else if (warp >= 12) {
+    // Epilogue warpgroup (thread = TMEM lane = query row for dQ, key row for dK / dV): dQ of every
+    // query tile leaves as three swizzled f32 TMA reduce-adds into dq_acc (several key tiles) or
+    // as one bf16 TMA store (one key tile); dK, dV as bf16 TMA stores after the item's last tile.
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane_id();
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tdV = tmem + 256 + lane_off, tdK = tmem + 336 + lane_off, tdQ = tmem + 416 + lane_off;
+    const bool elected = threadIdx.x == 384;  // issues every bulk store / reduce of the CTA
+    const uint32_t s0 = smem_u32(sDQ);
+    uint32_t g = 0;
+    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       int outer, h, kvt;
       decomp(item, outer, h, kvt);
       for (int j = 0; j < nq; ++j, ++g) {
-        float* l2 = sVec + (g & 1) * 256 + hw * 64;  // this warpgroup's 64 queries
-        float* dd = l2 + 128;
-        if (row < 64) {
-          l2[row] = nl;
-          dd[row] = nd;
-        }
-        if (j + 1 < nq) fetch(item, j + 1, nl, nd);
-        else fetch(item + gridDim.x, 0, nl, nd);
-        if (!accum && elected) bulk_wait_group_read0();  // the previous direct dQ store has read sDS
-        named_bar_sync(accum ? bar_wg : bar_all, accum ? 128 : 256);
-        mbar_wait(s_full, g & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c32 = 2 * hw + cc;
-          uint32_t sv[32], dv[32];
-          tmem_ld32(tS + c32 * 32, sv);
-          tmem_ld32(tdP + c32 * 32, dv);
-          tmem_ld_wait();
-          uint32_t pk[16], dk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float pp[2], ds[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int qc = cc * 32 + 2 * i + e;  // query within the warpgroup's 64
-              const bool ok = !diag || (64 * hw + qc) / p.L == my_blk;
-              const float pe = ok ? fast_exp2(fmaf(__uint_as_float(sv[2 * i + e]), sl2, -l2[qc])) : 0.f;
-              pp[e] = pe;
-              ds[e] = pe * (__uint_as_float(dv[2 * i + e]) - dd[qc]) * sc;
-            }
-            pk[i] = pack_bf16x2(pp[0], pp[1]);
-            dk[i] = pack_bf16x2(ds[0], ds[1]);
-          }
-          // P^T over S^T columns this warpgroup has already consumed: queries [64 hw, 64 hw + 64)
-          // packed into columns [64 hw, 64 hw + 32) (the other warpgroup may still read its own)
-          tmem_st16(tS + hw * 64 + cc * 16, pk);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int ch = cc * 4 + u;
-            st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
-          }
-        }
-        tmem_st_wait();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        mbar_arrive(p_full);
-        // dQ of this query tile: warpgroup 0 columns 0-47, warpgroup 1 columns 48-79
         mbar_wait(dq_full, g & 1);
         tc_fence_after();
-        uint32_t qv[48];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (hw == 0 || c < 2) tmem_ld16(tdQ + hw * 48 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(dq_free);
+        if (elected) BWD_STAMP(6);
         const TileCoord tq = bwd_coord(p, outer, h, j);
+        if (elected) bulk_wait_group_read0();  // the previous reduce / stores have read sDQ
+        named_bar_sync(3, 128);
         if (accum) {
           // f32 staging as three swizzled TMA boxes (conflict-free row writes): columns 0-31 and 32-63
-          // SW128 (128 B rows), 64-79 SW64 (64 B rows); reduce-added into dq_acc
-          if (elected) bulk_wait_group_read0();  // the previous reduce / dK, dV stores have read sDQ
-          named_bar_sync(bar_all, 256);
-          const uint32_t s0 = smem_u32(sDQ);
+          // SW128 (128 B rows), 64-79 SW64 (64 B rows); reduce-added into dq_acc.  16 columns per
+          // TMEM load (register budget).
 #pragma unroll
-          for (int c4 = 0; c4 < 12; ++c4) {
-            if (hw == 1 && c4 >= 8) break;
-            const int col = hw * 48 + c4 * 4;  // 4 floats = one 16-B chunk
-            uint32_t addr;
-            if (col < 64) addr = s0 + (col >> 5) * 16384 + row * 128 + ((((col & 31) >> 2) ^ (row & 7)) << 4);
-            else addr = s0 + 32768 + row * 64 + ((((col - 64) >> 2) ^ ((row >> 1) & 3)) << 4);
-            st_shared_v4(addr, qv[4 * c4], qv[4 * c4 + 1], qv[4 * c4 + 2], qv[4 * c4 + 3]);
+          for (int c = 0; c < DP / 16; ++c) {
+            uint32_t qv[16];
+            tmem_ld16(tdQ + c * 16, qv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int col = c * 16 + k * 4;  // 4 floats = one 16-B chunk
+              uint32_t addr;
+              if (col < 64) addr = s0 + (col >> 5) * 16384 + row * 128 + ((((col & 31) >> 2) ^ (row & 7)) << 4);
+              else addr = s0 + 32768 + row * 64 + ((((col - 64) >> 2) ^ ((row >> 1) & 3)) << 4);
+              st_shared_v4(addr, qv[4 * k], qv[4 * k + 1], qv[4 * k + 2], qv[4 * k + 3]);
+            }
           }
+          tc_fence_before();
+          mbar_arrive(dq_free);
           fence_proxy_async_smem();
-          named_bar_sync(bar_all, 256);
+          named_bar_sync(3, 128);
           if (elected) {
             tma_reduce_add_5d(&mp.dq_acc[0], sDQ, 0, tq.h, tq.x2, tq.x3, tq.x4);
             tma_reduce_add_5d(&mp.dq_acc[0], sDQ + 16384, 32, tq.h, tq.x2, tq.x3, tq.x4);
             tma_reduce_add_5d(&mp.dq_acc[1], sDQ + 32768, 64, tq.h, tq.x2, tq.x3, tq.x4);
             bulk_commit_group();
+            BWD_STAMP(7);
           }
-        } else {  // one key tile per sequence: dQ is final, bf16 through the (free) dS^T buffer
-          if (hw == 0) stage_row_bf16<NA, RB, 0, 48>(smem_u32(sDS), row, qv, 1.f);
-          else stage_row_bf16<NA, RB, 48, 80>(smem_u32(sDS), row, qv, 1.f);
+        } else {  // one key tile per sequence: dQ is final (bf16)
+          uint32_t qv[DP];
+#pragma unroll
+          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdQ + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(dq_free);
+          stage_row_bf16<NA, RB>(s0, row, qv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(bar_all, 256);
+          named_bar_sync(3, 128);
           if (elected) {
-            store_tile<NA, RB>(&mp.dq[0], &mp.dq[1], sDS, tq);
+            store_tile<NA, RB>(&mp.dq[0], &mp.dq[1], sDQ, tq);
             bulk_commit_group();
           }
         }
-        if (j == nq - 1) {  // dK (warpgroup 0) or dV (1) final: dq_full of the last tile covers every MMA
+        if (j == nq - 1) {  // dK, dV final: dq_full of the last tile covers every MMA of the item
+          if (elected) bulk_wait_group_read0();
+          named_bar_sync(3, 128);
           uint32_t kv[DP];
 #pragma unroll
-          for (int c = 0; c < DP / 16; ++c)
-            tmem_ld16((hw == 0 ? tdK : tdV) + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
+          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdK + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
+          tmem_ld_wait();
+          stage_row_bf16<NA, RB>(s0, row, kv, 1.f);
+#pragma unroll
+          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdV + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(kv_free);
-          if (elected) bulk_wait_group_read0();
-          named_bar_sync(bar_all, 256);
-          stage_row_bf16<NA, RB>(smem_u32(sDQ + hw * Cfg::TILE), row, kv, 1.f);
+          stage_row_bf16<NA, RB>(s0 + Cfg::TILE, row, kv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(bar_all, 256);
+          named_bar_sync(3, 128);
           if (elected) {
             const TileCoord tk = bwd_coord(p, outer, h, kvt);
             store_tile<NA, RB>(&mp.dk[0], &mp.dk[1], sDQ, tk);
@@ -2797,15 +2876,25 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
   } else {
     mp.dq_acc[0] = mp.dq_acc[1] = mp.q[0];  // unused
   }
+#ifdef DSP_FMHA_BWD_TRACE
+  {
+    static unsigned long long* tbuf = nullptr;
+    if (!tbuf) cudaMalloc(&tbuf, 64 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(tbuf, 0, 64 * 8 * sizeof(unsigned long long), st);
+    p.trace = tbuf;
+    extern unsigned long long* g_fmha_trace;
+    g_fmha_trace = tbuf;
+  }
+#endif
   cudaError_t err = launch_attn_bwd_dvec(tok, NH, p.Dh, o, dout, dvec, st);
   if (err != cudaSuccess) return err;
   if (accum && (err = cudaMemsetAsync(dq_acc, 0, (size_t)tok * C * sizeof(float), st)) != cudaSuccess) return err;
-  auto kern = fmha_bwd_kernel<1, 16>;
-  static bool attr = false;
-  if (!attr) {
+  auto kern = p.G > 1 ? fmha_bwd_kernel<1, 16, true> : fmha_bwd_kernel<1, 16, false>;
+  static bool attr[2] = {false, false};
+  if (!attr[p.G > 1]) {
     if ((err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM)) != cudaSuccess)
       return err;
-    attr = true;
+    attr[p.G > 1] = true;
   }
   const int grid = p.items < num_sms ? p.items : num_sms;
   err = launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, mp, p, lse, (const float*)dvec, accum);

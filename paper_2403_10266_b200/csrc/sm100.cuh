@@ -408,6 +408,11 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
   return f2_unpack(r);
 }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(r);
+}
 // poly_exp2 on a pair, FFMA2/FADD2 for the arithmetic
 __device__ __forceinline__ float2 poly_exp2_x2(float2 x) {
   x.x = fmaxf(x.x, -126.f);  // see poly_exp2: -127 would wrap to NaN
