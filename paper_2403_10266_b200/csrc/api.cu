@@ -443,6 +443,9 @@ dsp_ctx::~dsp_ctx() {
     for (void* e : {ev_in[b], ev_xfree[b], ev_out[b], ev_yfree[b]})
       if (e) cudaEventDestroy((cudaEvent_t)e);
   if (h2d_stream) cudaStreamDestroy((cudaStream_t)h2d_stream);
+  for (void* e : wg_ev)
+    if (e) cudaEventDestroy((cudaEvent_t)e);
+  if (wg_stream) cudaStreamDestroy((cudaStream_t)wg_stream);
   if (d2h_stream) cudaStreamDestroy((cudaStream_t)d2h_stream);
 }
 
@@ -1688,7 +1691,7 @@ dsp_status_t dsp_attention_core(dsp_ctx_t ctx, dsp_dtype_t dt, int64_t B, int64_
 namespace {
 
 struct TrainWs {
-  int64_t dz, big, dh, dyb, dob, dqacc, dvec, lnpart, wpart, send, recv, total;
+  int64_t dz, big, dh, dyb, dob, dqacc, dvec, lnpart, wpart, wt, send, recv, total;
 };
 
 int64_t wgrad_part_bytes(int64_t M, int64_t N, int64_t K, int num_sms) {
@@ -1712,6 +1715,7 @@ TrainWs train_ws(const dsp_shape_t* s, int world, int num_sms) {
   const int64_t shapes[4][2] = {{3 * C, C}, {C, C}, {4 * C, C}, {C, 4 * C}};
   for (auto& sh : shapes) wp = std::max(wp, wgrad_part_bytes(sh[0], sh[1], tok, num_sms));
   w.wpart = take(wp);
+  w.wt = take(4 * C * C * 2);  // one transposed weight (dgrad on the K-major GEMM path)
   w.send = take(act);
   w.recv = take(act);
   w.total = o;
@@ -1778,9 +1782,17 @@ dsp_status_t wgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* d
 }
 
 dsp_status_t dgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* W, const void* u,
-                   void* dX, cudaStream_t st) {
+                   void* dX, cudaStream_t st, void* wt = nullptr) {
   std::string why;
-  cudaError_t e = launch_gemm_bf16_dgrad(dY, W, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
+  cudaError_t e;
+  if (wt) {  // W^T [K, N] once (16 C^2 elements per block step, ~13 us in all), then the forward's K-major GEMM
+    e = launch_transpose_bf16(W, wt, N, K, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "weight transpose");
+    e = launch_gemm_bf16_dgrad_kmajor(dY, wt, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
+    ctx->launches += 1;
+  } else {  // W read as an MN-major operand
+    e = launch_gemm_bf16_dgrad(dY, W, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
+  }
   if (e != cudaSuccess) return cuda_fail(ctx, e, "dgrad GEMM", why);
   ctx->launches += 1;
   return DSP_OK;
@@ -1794,28 +1806,68 @@ dsp_status_t ln_bwd(dsp_ctx_t ctx, int64_t rows, int64_t C, const void* x, const
   return DSP_OK;
 }
 
+// Weight-gradient GEMMs beside the dgrad chain: each wgrad is forked onto the context's side stream
+// when its inputs are ready and joined back before the main stream overwrites what it reads (the
+// side stream runs them in order, so waiting for wgrad k also covers every earlier one).
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, done[7] = {};
+};
+dsp_status_t side_init(dsp_ctx_t ctx, Side* sd) {
+  if (!ctx->wg_stream) {
+    cudaStream_t s;
+    DSP_CUDA(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "side stream");
+    ctx->wg_stream = s;
+    for (auto& e : ctx->wg_ev) {
+      cudaEvent_t ev;
+      DSP_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "side events");
+      e = ev;
+    }
+  }
+  sd->s = (cudaStream_t)ctx->wg_stream;
+  sd->fork = (cudaEvent_t)ctx->wg_ev[0];
+  for (int i = 0; i < 7; ++i) sd->done[i] = (cudaEvent_t)ctx->wg_ev[i + 1];
+  return DSP_OK;
+}
+// wgrad k on the side stream once the main stream (st) has produced its inputs
+dsp_status_t side_wgrad(dsp_ctx_t ctx, const Side& sd, int k, int64_t M, int64_t N, int64_t K, const void* dY,
+                        const void* X, float* dW, float* part, cudaStream_t st) {
+  DSP_CUDA(ctx, cudaEventRecord(sd.fork, st), "fork");
+  DSP_CUDA(ctx, cudaStreamWaitEvent(sd.s, sd.fork, 0), "fork wait");
+  DSP_TRY(wgrad(ctx, M, N, K, dY, X, dW, 1, part, sd.s));
+  DSP_CUDA(ctx, cudaEventRecord(sd.done[k], sd.s), "wgrad done");
+  return DSP_OK;
+}
+dsp_status_t side_join(dsp_ctx_t ctx, const Side& sd, int k, cudaStream_t st) {
+  DSP_CUDA(ctx, cudaStreamWaitEvent(st, sd.done[k], 0), "join");
+  return DSP_OK;
+}
+
 // one attention stage's backward: from dout (gradient of the stage output, also the residual
-// gradient) and the saved h / qkv / o / lse, dres_out = dout + LN^T(W_qkv^T (attn^T (W_o^T dout)))
+// gradient) and the saved h / qkv / o / lse, dres_out = dout + LN^T(W_qkv^T (attn^T (W_o^T dout))).
+// Side-stream wgrads k_o (W_o) and k_o + 1 (W_qkv); join_big: the wgrad that last read ws.big.
 dsp_status_t attn_stage_bwd(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, int64_t S_loc, int dim,
                             const void* zin, const void* ln_w, const void* w_qkv, const void* w_o, const void* h,
                             const void* qkv, const void* o, const float* lse, const void* dout, void* dres_out,
                             float* g_lnw, float* g_lnb, float* g_qkv, float* g_o, const TrainWs& L, uint8_t* ws,
-                            cudaStream_t st) {
+                            cudaStream_t st, const Side& sd, int k_o, int join_big) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   void* dob = ws + L.dob;
   void* dqkv = ws + L.big;
   void* dh = ws + L.dh;
   float* part = reinterpret_cast<float*>(ws + L.wpart);
-  DSP_TRY(dgrad(ctx, tok, C, C, dout, w_o, nullptr, dob, st));                      // dO = dout W_o
-  DSP_TRY(wgrad(ctx, tok, C, C, dout, o, g_o, 1, part, st));                        // dW_o += dout^T O
+  DSP_TRY(dgrad(ctx, tok, C, C, dout, w_o, nullptr, dob, st, ws + L.wt));           // dO = dout W_o
+  DSP_TRY(side_wgrad(ctx, sd, k_o, tok, C, C, dout, o, g_o, part, st));             // dW_o += dout^T O
+  DSP_TRY(side_join(ctx, sd, join_big, st));                                        // ws.big free
   std::string why;
   cudaError_t e = launch_fmha_bwd_bf16(qkv, o, dob, lse, dqkv, reinterpret_cast<float*>(ws + L.dvec),
                                        reinterpret_cast<float*>(ws + L.dqacc), s->B, T_loc, S_loc, C, s->num_heads,
                                        dim, ctx->num_sms, st, &why);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "attention backward", why);
   ctx->launches += 4;
-  DSP_TRY(dgrad(ctx, tok, 3 * C, C, dqkv, w_qkv, nullptr, dh, st));                 // dh = dqkv W_qkv
-  DSP_TRY(wgrad(ctx, tok, 3 * C, C, dqkv, h, g_qkv, 1, part, st));                  // dW_qkv += dqkv^T h
+  DSP_TRY(dgrad(ctx, tok, 3 * C, C, dqkv, w_qkv, nullptr, dh, st, ws + L.wt));      // dh = dqkv W_qkv
+  DSP_TRY(side_wgrad(ctx, sd, k_o + 1, tok, 3 * C, C, dqkv, h, g_qkv, part, st));   // dW_qkv += dqkv^T h
+  if (dres_out == dout) DSP_TRY(side_join(ctx, sd, k_o, st));                       // in place over dout
   return ln_bwd(ctx, tok, C, zin, ln_w, dh, dout, dres_out, g_lnw, g_lnb, reinterpret_cast<float*>(ws + L.lnpart), st);
 }
 
@@ -1912,12 +1964,14 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
     DSP_TRY(do_switch(ctx, s, DSP_DIM_T, dy, ws + L.dz, impl, st, ws + L.send, ws + L.recv));
     dz = ws + L.dz;
   }
-  // 2. MLP backward: du = (dz W2) * gelu'(u); dW2 += dz^T g; dh3 = du W1; dW1 += du^T h3
+  Side sd;
+  DSP_TRY(side_init(ctx, &sd));
+  // 2. MLP backward: du = (dz W2) * gelu'(u); dW2 += dz^T g; dh3 = du W1; dW1 += du^T h3 (wgrads 0, 1 aside)
   void* du = ws + L.big;
-  DSP_TRY(dgrad(ctx, tok, C, 4 * C, dz, w->w_fc2, sv + SL.u, du, st));
-  DSP_TRY(wgrad(ctx, tok, C, 4 * C, dz, sv + SL.g, g->w_fc2, 1, part, st));
-  DSP_TRY(dgrad(ctx, tok, 4 * C, C, du, w->w_fc1, nullptr, ws + L.dh, st));
-  DSP_TRY(wgrad(ctx, tok, 4 * C, C, du, sv + SL.h3, g->w_fc1, 1, part, st));
+  DSP_TRY(side_wgrad(ctx, sd, 0, tok, C, 4 * C, dz, sv + SL.g, g->w_fc2, part, st));
+  DSP_TRY(dgrad(ctx, tok, C, 4 * C, dz, w->w_fc2, sv + SL.u, du, st, ws + L.wt));
+  DSP_TRY(side_wgrad(ctx, sd, 1, tok, 4 * C, C, du, sv + SL.h3, g->w_fc1, part, st));
+  DSP_TRY(dgrad(ctx, tok, 4 * C, C, du, w->w_fc1, nullptr, ws + L.dh, st, ws + L.wt));
   // dy2 = dz + LN3^T dh3
   void* dy2 = ws + L.dyb;
   DSP_TRY(ln_bwd(ctx, tok, C, sv + SL.y2, w->ln3_w, ws + L.dh, dz, dy2, g->ln3_w, g->ln3_b,
@@ -1925,17 +1979,19 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   // 3. temporal stage backward on the S-shard: dy1s = dy2 + LN2^T(...) (in place over dy2)
   DSP_TRY(attn_stage_bwd(ctx, s, s->T, Sn, DSP_DIM_T, sv + SL.y1s, w->ln2_w, w->w_qkv_t, w->w_o_t, sv + SL.h2,
                          sv + SL.qkv_t, sv + SL.o_t, reinterpret_cast<const float*>(sv + SL.lse_t), dy2, dy2,
-                         g->ln2_w, g->ln2_b, g->w_qkv_t, g->w_o_t, L, ws, st));
+                         g->ln2_w, g->ln2_b, g->w_qkv_t, g->w_o_t, L, ws, st, sd, 2, 1));
   // 4. dy1 = switch_{S->T}(dy1s): the adjoint of the forward's T->S switch
   void* dy1 = dy2;
   if (N > 1) {
+    DSP_TRY(side_join(ctx, sd, 0, st));  // wgrad FC2 read dz
     DSP_TRY(do_switch(ctx, s, DSP_DIM_S, dy2, ws + L.dz, impl, st, ws + L.send, ws + L.recv));
     dy1 = ws + L.dz;
   }
   // 5. spatial stage backward on the T-shard: dx = dy1 + LN1^T(...)
-  return attn_stage_bwd(ctx, s, Tn, s->S, DSP_DIM_S, x, w->ln1_w, w->w_qkv_s, w->w_o_s, sv + SL.h1, sv + SL.qkv_s,
-                        sv + SL.o_s, reinterpret_cast<const float*>(sv + SL.lse_s), dy1, dx, g->ln1_w, g->ln1_b,
-                        g->w_qkv_s, g->w_o_s, L, ws, st);
+  DSP_TRY(attn_stage_bwd(ctx, s, Tn, s->S, DSP_DIM_S, x, w->ln1_w, w->w_qkv_s, w->w_o_s, sv + SL.h1, sv + SL.qkv_s,
+                         sv + SL.o_s, reinterpret_cast<const float*>(sv + SL.lse_s), dy1, dx, g->ln1_w, g->ln1_b,
+                         g->w_qkv_s, g->w_o_s, L, ws, st, sd, 4, 3));
+  return side_join(ctx, sd, 5, st);  // every weight gradient done before the call returns (stream order)
 }
 
 dsp_status_t dsp_grads_reduce(dsp_ctx_t ctx, float* buf, int64_t n, int zero_shard, float* out, void* stream) {

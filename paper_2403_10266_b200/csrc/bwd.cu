@@ -227,6 +227,35 @@ __global__ void __launch_bounds__(256) attn_bwd_dvec_kernel(const __nv_bfloat16*
   dvec[i] = acc * rsqrtf((float)Dh);  // pre-scaled by 1 / sqrt(Dh): dS = P (dP - D) / sqrt(Dh) in the FMHA backward
 }
 
+// out[c][r] = in[r][c] (bf16), 64 x 64 tiles through padded smem: 16-B row-segment loads, 4-B stores
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in,
+                                                             __nv_bfloat16* __restrict__ out, int R, int Cc) {
+  __shared__ __nv_bfloat16 t[64][66];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
+  for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {  // 64 rows x 8 vectors of 8
+    const int r = i >> 3, v = i & 7;
+    if (r0 + r < R && c0 + 8 * v < Cc) {
+      const uint4 w = *reinterpret_cast<const uint4*>(in + (size_t)(r0 + r) * Cc + c0 + 8 * v);
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&w);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[r][8 * v + k] = e[k];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) {  // 64 output rows (columns of in) x 32 pairs
+    const int c = i >> 5, rp = i & 31;
+    if (c0 + c < Cc && r0 + 2 * rp + 1 < R + 1) {
+      __nv_bfloat162 v2;
+      v2.x = t[2 * rp][c];
+      v2.y = t[2 * rp + 1][c];
+      if (r0 + 2 * rp + 1 < R) *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(c0 + c) * R + r0 + 2 * rp) = v2;
+      else if (r0 + 2 * rp < R) out[(size_t)(c0 + c) * R + r0 + 2 * rp] = v2.x;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ dq, uint2* __restrict__ dqkv,
                                                          long tok, int C4) {
   griddep_wait();
@@ -303,6 +332,13 @@ cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, con
   if (Dh % 8 != 0) return cudaErrorNotSupported;
   return launch_k(attn_bwd_dvec_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
                   (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, n, NH, Dh);
+}
+
+cudaError_t launch_transpose_bf16(const void* in, void* out, int64_t R, int64_t Cc, cudaStream_t st) {
+  if (R == 0 || Cc == 0) return cudaSuccess;
+  if (Cc % 8 != 0 || R % 2 != 0) return cudaErrorNotSupported;
+  return launch_k(transpose_bf16_kernel, dim3((unsigned)((Cc + 63) / 64), (unsigned)((R + 63) / 64)), dim3(256), 0, st, 1,
+                  (const __nv_bfloat16*)in, (__nv_bfloat16*)out, (int)R, (int)Cc);
 }
 
 cudaError_t launch_dq_convert(int64_t tok, int64_t C, const float* dq_acc, void* dqkv, cudaStream_t st) {

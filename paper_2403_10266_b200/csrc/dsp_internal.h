@@ -84,6 +84,12 @@ cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* ga
 cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, const void* dout, float* dvec,
                                  cudaStream_t st);
 cudaError_t launch_dq_convert(int64_t tok, int64_t C, const float* dq_acc, void* dqkv, cudaStream_t st);
+// out [Cc, R] = in [R, Cc]^T (bf16; Cc % 8 == 0, R even)
+cudaError_t launch_transpose_bf16(const void* in, void* out, int64_t R, int64_t Cc, cudaStream_t st);
+// dgrad on pre-transposed weights: D[M, N] = epi(A[M, K] Wt[N, K]^T) -- the forward GEMM's K-major path
+// (BN by gemm_bn_for, narrow tail tiles), epi = DSP_EPI_NONE or EPI_GELU_BWD (R = u [M, N])
+cudaError_t launch_gemm_bf16_dgrad_kmajor(const void* A, const void* Wt, const void* R, void* D, int64_t M, int64_t N,
+                                          int64_t K, int epi, int num_sms, cudaStream_t st, std::string* why);
 // temporal attention reading q | k | v from the TSEQ layout (launch_gemm_bf16_tseq); o [tok, C]
 cudaError_t launch_fmha_bf16_tseq(const void* qkv_tseq, void* o, int64_t B, int64_t T, int64_t S_loc, int64_t C,
                                   int NH, int num_sms, cudaStream_t st, std::string* why);
@@ -291,6 +297,9 @@ struct dsp_ctx {
   void* ev_xfree[2] = {};   // x_dev[b] consumed by the block (compute stream)
   void* ev_out[2] = {};     // y_dev[b] written by the block (compute stream)
   void* ev_yfree[2] = {};   // y_dev[b] copied out (copy-out stream)
+  // block backward: the weight-gradient GEMMs run on a side stream beside the dgrad chain
+  void* wg_stream = nullptr;
+  void* wg_ev[8] = {};       // [0] fork, [1..6] wgrad k done
   std::string last_error;
   ~dsp_ctx();
 };

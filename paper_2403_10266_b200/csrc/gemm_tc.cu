@@ -989,6 +989,15 @@ cudaError_t launch_gemm_bf16_dgrad(const void* A, const void* W, const void* R, 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_gemm_bf16_dgrad_kmajor(const void* A, const void* Wt, const void* R, void* D, int64_t M, int64_t N,
+                                          int64_t K, int epi, int num_sms, cudaStream_t st, std::string* why) {
+  if (M == 0) return cudaSuccess;
+  if (epi == EPI_GELU_BWD) return dispatch_bn<EPI_GELU_BWD>(A, Wt, R, D, M, N, K, num_sms, st, why);
+  if (epi == DSP_EPI_NONE) return dispatch_bn<DSP_EPI_NONE>(A, Wt, R, D, M, N, K, num_sms, st, why);
+  if (why) *why = "dgrad GEMM: unsupported epilogue";
+  return cudaErrorInvalidValue;
+}
+
 // Split count for the wgrad GEMM: the output has few tiles (dW [3C, C] at C = 1152: 126 tiles of
 // 256 x 128 for 74 CTA pairs) and a long reduction (all tokens), so the token range is cut into
 // ksplit slices, the smallest count whose tiles fill >= 90 % of the last wave (at most 16, each
