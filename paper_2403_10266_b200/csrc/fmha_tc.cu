@@ -2168,8 +2168,8 @@ struct BwdCfg {
   static constexpr int SMEM = OFF_BAR + 256;
   static constexpr bool OK = SMEM <= 227 * 1024 && RB == 16 && NA == 1;
   static_assert(2 * TILE <= 128 * DP * 4, "dK and dV staging fit in the dQ staging area");
-  // warps 0-3: producer, MMA, idle x2; warps 4-11: two compute warpgroups; warps 12-15: epilogue warpgroup
-  static constexpr int THREADS = 512;
+  // warps 0-3: producer, MMA, idle x2; warps 4-19: four compute warpgroups; warps 20-23: epilogue
+  static constexpr int NWG = 4, THREADS = 128 + 128 * NWG + 128;
 };
 
 __device__ __forceinline__ TileCoord bwd_coord(const FmhaParams& p, int outer, int h, int pt) {
@@ -2210,6 +2210,29 @@ __device__ __forceinline__ void stage_row_bf16(uint32_t st0, int row, const uint
   }
 }
 
+// 16 columns [d0, d0 + 16) of a bf16 row into the TMA box staging layout (as stage_row_bf16)
+template <int NA, int RB>
+__device__ __forceinline__ void stage_cols16_bf16(uint32_t st0, int row, const uint32_t* v, int d0) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int d = d0 + 8 * h;
+    const uint32_t* w = v + 8 * h;
+    const uint32_t a0 = pack_bf16x2(__uint_as_float(w[0]), __uint_as_float(w[1]));
+    const uint32_t a1 = pack_bf16x2(__uint_as_float(w[2]), __uint_as_float(w[3]));
+    const uint32_t a2 = pack_bf16x2(__uint_as_float(w[4]), __uint_as_float(w[5]));
+    const uint32_t a3 = pack_bf16x2(__uint_as_float(w[6]), __uint_as_float(w[7]));
+    uint32_t addr;
+    if (d < NA * 64) {
+      const int blk = d >> 6, ch = (d & 63) >> 3;
+      addr = st0 + blk * 16384 + row * 128 + ((ch ^ (row & 7)) << 4);
+    } else {
+      const int ch = (d - NA * 64) >> 3;  // RB = 16: SW32, two chunks per 32-B row
+      addr = st0 + NA * 16384 + row * 32 + ((ch ^ ((row >> 2) & 1)) << 4);
+    }
+    st_shared_v4(addr, a0, a1, a2, a3);
+  }
+}
+
 template <int NA, int RB>
 __device__ __forceinline__ void store_tile(const CUtensorMap* ma, const CUtensorMap* mb, const uint8_t* src,
                                            const TileCoord& t) {
@@ -2230,7 +2253,7 @@ __device__ __forceinline__ void load_tile_sw32(uint8_t* dst, const CUtensorMap* 
 }
 
 template <int NA, int RB, bool DIAG>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     fmha_bwd_kernel(const __grid_constant__ BwdMaps mp, const FmhaParams p, const float* __restrict__ lse,
                     const float* __restrict__ dvec, int accum) {
   using Cfg = BwdCfg<NA, RB>;
@@ -2267,11 +2290,11 @@ __global__ void __launch_bounds__(512, 1)
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 256);
+    mbar_init(p_full, 128 * Cfg::NWG);
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 128);
     mbar_init(kv_free, 128);
-    mbar_init(s_free, 256);
+    mbar_init(s_free, 128 * Cfg::NWG);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -2294,10 +2317,7 @@ __global__ void __launch_bounds__(512, 1)
     outer = rest / p.NH;
   };
 
-  // launch allocation 128 regs x 512 threads: 80 x 128 (warps 0-3) + 152 x 256 (compute) + 128 x 128 (epilogue)
-  if (warp < 4) setmaxnreg_dec<80>();
-  else if (warp < 12) setmaxnreg_inc<152>();
-  // (the epilogue warpgroup keeps the launch allocation of 128)
+  // 768 threads: every role fits the launch allocation of 80 registers (no setmaxnreg)
   if (warp == 0) {
     if (elect_one()) {
       uint32_t it = 0, g = 0;
@@ -2390,34 +2410,33 @@ __global__ void __launch_bounds__(512, 1)
         issue_bc(g, j, it);
       }
     }
-  } else if (warp >= 4 && warp < 12) {
-    // Two compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
-    // queries [64 hw, 64 hw + 64) of S^T / dP^T (its P^T columns, its dS^T tile).
+  } else if (warp >= 4 && warp < 4 + 4 * Cfg::NWG) {
+    // Four compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
+    // queries [32 hw, 32 hw + 32) of S^T / dP^T, i.e. chunks (hw & 1) * 4 .. + 3 of the 64-query P^T /
+    // dS^T smem tile hw >> 1.  Four warps per SMSP keep the TMEM-load latency of each covered.
     const int q4 = warp & 3, hw = (warp - 4) >> 2;
     const int row = q4 * 32 + lane_id();
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+    const uint32_t tS = tmem + lane_off + hw * 32, tdP = tmem + 128 + lane_off + hw * 32;
     const uint32_t bar_wg = 1 + hw;  // named barrier of the own warpgroup (128)
     const float sl2 = p.scale_log2;
     const float sc = rsqrtf((float)p.Dh);
-    // block-diagonal packing: this key row's sequence owns queries [qlo, qhi) of the warpgroup's 64
-    const int qlo = p.G > 1 ? (row / p.L) * p.L - 64 * hw : 0;
-    const int qhi = p.G > 1 ? qlo + p.L : 64;
-    const uint32_t dsrow = smem_u32(sDS) + hw * 16384 + row * 128;
-    const uint32_t prow = smem_u32(sP) + hw * 16384 + row * 128;
-    // lse2 / D of the query this thread stages (threads row < 64 of each warpgroup: query 64 hw + row),
-    // loaded one step ahead so the global latency is off the step's critical path
-    // lse2 and D / sqrt(Dh) of the query this thread stages (threads row < 64 of each warpgroup: query
-    // 64 hw + row), copied global -> smem by cp.async one tile ahead (no registers held across the tile,
+    // block-diagonal packing: this key row's sequence owns queries [qlo, qhi) of the warpgroup's 32
+    const int qlo = p.G > 1 ? (row / p.L) * p.L - 32 * hw : 0;
+    const int qhi = p.G > 1 ? qlo + p.L : 32;
+    const uint32_t tile_off = (hw >> 1) * 16384 + row * 128;
+    const uint32_t dsrow = smem_u32(sDS) + tile_off, prow = smem_u32(sP) + tile_off;
+    // lse2 and D / sqrt(Dh) of the query this thread stages (threads row < 32 of each warpgroup: query
+    // 32 hw + row), copied global -> smem by cp.async one tile ahead (no registers held across the tile,
     // the latency off the critical path); padding queries get lse2 = +inf (P = 0), D = 0
     auto fetch = [&](int item, int j, uint32_t vbuf) {
-      if (row >= 64) return;
+      if (row >= 32) return;
       long tok = -1;
       int h = 0;
       if (item < p.items) {
         int outer, kvt;
         decomp(item, outer, h, kvt);
-        tok = row_token(p, bwd_coord(p, outer, h, j), 64 * hw + row);
+        tok = row_token(p, bwd_coord(p, outer, h, j), 32 * hw + row);
       }
       if (tok >= 0) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(vbuf + row * 4), "l"(lse + tok * p.NH + h) : "memory");
@@ -2428,13 +2447,13 @@ __global__ void __launch_bounds__(512, 1)
         st_shared_f32(vbuf + 512 + row * 4, 0.f);
       }
     };
-    fetch(blockIdx.x, 0, smem_u32(sVec + hw * 64));
+    fetch(blockIdx.x, 0, smem_u32(sVec + hw * 32));
     uint32_t g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
       for (int j = 0; j < nq; ++j, ++g) {
-        const uint32_t vb = smem_u32(sVec + (g & 1) * 256 + hw * 64);  // this warpgroup's 64 queries
+        const uint32_t vb = smem_u32(sVec + (g & 1) * 256 + hw * 32);  // this warpgroup's 32 queries
         asm volatile("cp.async.wait_all;" ::: "memory");               // this tile's lse2 / D landed
-        const uint32_t vnext = smem_u32(sVec + ((g + 1) & 1) * 256 + hw * 64);
+        const uint32_t vnext = smem_u32(sVec + ((g + 1) & 1) * 256 + hw * 32);
         if (threadIdx.x == 128) BWD_STAMP(0);
         named_bar_sync(bar_wg, 128);
         // the next tile's values go to the other buffer (its readers finished before this barrier)
@@ -2443,14 +2462,18 @@ __global__ void __launch_bounds__(512, 1)
         mbar_wait(s_full, g & 1);
         tc_fence_after();
         if (threadIdx.x == 128) BWD_STAMP(1);
-        // four 16-query chunks; the TMEM loads of chunk k + 1 are in flight while chunk k is computed
-        // (tcgen05.wait::ld waits for every load issued, so the next pair is issued after the wait)
-        uint32_t sa[16], da[16], sb[16], db[16];
-        tmem_ld16(tS + hw * 64, sa);
-        tmem_ld16(tdP + hw * 64, da);
-        tmem_ld_wait();
+        if (threadIdx.x == 128 + 128 * (Cfg::NWG - 1)) BWD_STAMP(6);  // the last warpgroup saw S
         uint32_t pk[16], dk[16];
-        auto chunk = [&](int k, const uint32_t (&sv)[16], const uint32_t (&dv)[16]) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {  // two 16-query chunks
+          uint32_t sv[16], dv[16];
+          tmem_ld16(tS + k * 16, sv);
+          tmem_ld16(tdP + k * 16, dv);
+          tmem_ld_wait();
+          if (k == 1) {
+            tc_fence_before();
+            mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's may be issued
+          }
           // packed pairs (FFMA2 / FMUL2): x = s scale_log2 - lse2, P = 2^x, dS = P (dP / sqrt(Dh) - D / sqrt(Dh))
           const float2 sl22 = make_float2(sl2, sl2), sc2 = make_float2(sc, sc);
 #pragma unroll
@@ -2472,43 +2495,27 @@ __global__ void __launch_bounds__(512, 1)
               }
               const float2 pe = make_float2(fast_exp2(x.x), fast_exp2(x.y));
               const float2 ds = fmul2(pe, ffma2(p2, sc2, nd));
-              const int kk = (k & 1) * 8 + 2 * i4 + h2;
+              const int kk = k * 8 + 2 * i4 + h2;
               pk[kk] = pack_bf16x2(pe.x, pe.y);
               dk[kk] = pack_bf16x2(ds.x, ds.y);
             }
           }
-          if (k & 1) {  // P^T and dS^T of 32 queries -> smem (SW128 K-major over queries)
-            const int cc = k >> 1;
-            if (cc == 0 && g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products read them
+        }
+        // P^T and dS^T of the warpgroup's 32 queries -> smem (SW128 K-major over queries)
+        if (g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products have read them
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int ch = cc * 4 + u;
-              st_shared_v4(prow + ((ch ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-              st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
-            }
-          }
-        };
-        tmem_ld16(tS + hw * 64 + 16, sb);
-        tmem_ld16(tdP + hw * 64 + 16, db);
-        chunk(0, sa, da);
-        tmem_ld_wait();
-        tmem_ld16(tS + hw * 64 + 32, sa);
-        tmem_ld16(tdP + hw * 64 + 32, da);
-        chunk(1, sb, db);
-        tmem_ld_wait();
-        tmem_ld16(tS + hw * 64 + 48, sb);
-        tmem_ld16(tdP + hw * 64 + 48, db);
-        chunk(2, sa, da);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's may be issued
-        chunk(3, sb, db);
+        for (int u = 0; u < 4; ++u) {
+          const int ch = (hw & 1) * 4 + u;
+          st_shared_v4(prow + ((ch ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
         fence_proxy_async_smem();
         if (threadIdx.x == 128) BWD_STAMP(2);
+        if (threadIdx.x == 128 + 128 * (Cfg::NWG - 1)) BWD_STAMP(7);  // the last warpgroup's P done
         mbar_arrive(p_full);
       }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 4 + 4 * Cfg::NWG) {
     // Epilogue warpgroup (thread = TMEM lane = query row for dQ, key row for dK / dV): dQ of every
     // query tile leaves as three swizzled f32 TMA reduce-adds into dq_acc (several key tiles) or
     // as one bf16 TMA store (one key tile); dK, dV as bf16 TMA stores after the item's last tile.
@@ -2516,7 +2523,8 @@ __global__ void __launch_bounds__(512, 1)
     const int row = q4 * 32 + lane_id();
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t tdV = tmem + 256 + lane_off, tdK = tmem + 336 + lane_off, tdQ = tmem + 416 + lane_off;
-    const bool elected = threadIdx.x == 384;  // issues every bulk store / reduce of the CTA
+    const bool elected = threadIdx.x == 128 + 128 * Cfg::NWG;  // issues every bulk store / reduce of the CTA
+    constexpr uint32_t kBarEpi = 1 + Cfg::NWG;
     const uint32_t s0 = smem_u32(sDQ);
     uint32_t g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
@@ -2525,10 +2533,9 @@ __global__ void __launch_bounds__(512, 1)
       for (int j = 0; j < nq; ++j, ++g) {
         mbar_wait(dq_full, g & 1);
         tc_fence_after();
-        if (elected) BWD_STAMP(6);
         const TileCoord tq = bwd_coord(p, outer, h, j);
         if (elected) bulk_wait_group_read0();  // the previous reduce / stores have read sDQ
-        named_bar_sync(3, 128);
+        named_bar_sync(kBarEpi, 128);
         if (accum) {
           // f32 staging as three swizzled TMA boxes (conflict-free row writes): columns 0-31 and 32-63
           // SW128 (128 B rows), 64-79 SW64 (64 B rows); reduce-added into dq_acc.  16 columns per
@@ -2550,24 +2557,25 @@ __global__ void __launch_bounds__(512, 1)
           tc_fence_before();
           mbar_arrive(dq_free);
           fence_proxy_async_smem();
-          named_bar_sync(3, 128);
+          named_bar_sync(kBarEpi, 128);
           if (elected) {
             tma_reduce_add_5d(&mp.dq_acc[0], sDQ, 0, tq.h, tq.x2, tq.x3, tq.x4);
             tma_reduce_add_5d(&mp.dq_acc[0], sDQ + 16384, 32, tq.h, tq.x2, tq.x3, tq.x4);
             tma_reduce_add_5d(&mp.dq_acc[1], sDQ + 32768, 64, tq.h, tq.x2, tq.x3, tq.x4);
             bulk_commit_group();
-            BWD_STAMP(7);
           }
-        } else {  // one key tile per sequence: dQ is final (bf16)
-          uint32_t qv[DP];
+        } else {  // one key tile per sequence: dQ is final (bf16), 16 columns per TMEM load
 #pragma unroll
-          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdQ + c * 16, *reinterpret_cast<uint32_t(*)[16]>(qv + c * 16));
-          tmem_ld_wait();
+          for (int c = 0; c < DP / 16; ++c) {
+            uint32_t qv[16];
+            tmem_ld16(tdQ + c * 16, qv);
+            tmem_ld_wait();
+            stage_cols16_bf16<NA, RB>(s0, row, qv, c * 16);
+          }
           tc_fence_before();
           mbar_arrive(dq_free);
-          stage_row_bf16<NA, RB>(s0, row, qv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(3, 128);
+          named_bar_sync(kBarEpi, 128);
           if (elected) {
             store_tile<NA, RB>(&mp.dq[0], &mp.dq[1], sDQ, tq);
             bulk_commit_group();
@@ -2575,20 +2583,19 @@ __global__ void __launch_bounds__(512, 1)
         }
         if (j == nq - 1) {  // dK, dV final: dq_full of the last tile covers every MMA of the item
           if (elected) bulk_wait_group_read0();
-          named_bar_sync(3, 128);
-          uint32_t kv[DP];
+          named_bar_sync(kBarEpi, 128);
 #pragma unroll
-          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdK + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
-          tmem_ld_wait();
-          stage_row_bf16<NA, RB>(s0, row, kv, 1.f);
-#pragma unroll
-          for (int c = 0; c < DP / 16; ++c) tmem_ld16(tdV + c * 16, *reinterpret_cast<uint32_t(*)[16]>(kv + c * 16));
-          tmem_ld_wait();
+          for (int c = 0; c < 2 * (DP / 16); ++c) {  // dK then dV, 16 columns per TMEM load
+            const int cc = c % (DP / 16);
+            uint32_t kv[16];
+            tmem_ld16((c < DP / 16 ? tdK : tdV) + cc * 16, kv);
+            tmem_ld_wait();
+            stage_cols16_bf16<NA, RB>(s0 + (c < DP / 16 ? 0 : Cfg::TILE), row, kv, cc * 16);
+          }
           tc_fence_before();
           mbar_arrive(kv_free);
-          stage_row_bf16<NA, RB>(s0 + Cfg::TILE, row, kv, 1.f);
           fence_proxy_async_smem();
-          named_bar_sync(3, 128);
+          named_bar_sync(kBarEpi, 128);
           if (elected) {
             const TileCoord tk = bwd_coord(p, outer, h, kvt);
             store_tile<NA, RB>(&mp.dk[0], &mp.dk[1], sDQ, tk);

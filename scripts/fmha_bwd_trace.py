@@ -26,7 +26,7 @@ rt = ctypes.CDLL("libcudart.so.12")
 rt.cudaMemcpy(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(ptr), ctypes.c_size_t(buf.nbytes), 2)
 t = buf.reshape(64, 8).astype(np.int64)
 base = t[t > 0].min()
-names = ["c.start", "c.Srdy", "c.Pdone", "m.qfull", "m.pfull", "m.Bgo", "e.dqfull", "e.red"]
+names = ["c.start", "c.Srdy", "c.Pdone", "m.qfull", "m.pfull", "m.Bgo", "w1.Srdy", "w1.Pdone"]
 print("step " + " ".join(f"{n:>8s}" for n in names) + "   softmax  S->Bgo  Bgo->dq  dq->red  step")
 prev = None
 for g in range(40):
