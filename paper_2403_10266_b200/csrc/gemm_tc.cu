@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI, MAJ>::THREADS, 1)
   const uint32_t rank = cluster_ctarank();  // 0 = leader of the CTA pair
   const bool leader = rank == 0;
   const int tiles_m = (M + 2 * BM - 1) / (2 * BM);
-  const int tiles_n = N / BN;
+  // a ragged last column tile only for the f32 wgrad partials (zero-filled W columns, guarded stores)
+  const int tiles_n = Cfg::F32 ? (N + BN - 1) / BN : N / BN;
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
   // Tile schedule (static round robin over the pairs): the last, partial wave of BN-wide tiles
@@ -712,6 +713,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, EPI, MAJ>::THREADS, 1)
 #pragma unroll
       for (int c = 0; c < BN / CW; ++c) {
         if (c * CW >= width) break;  // narrow tail tile
+        if (Cfg::F32 && n0 + c * CW >= N) break;  // ragged last column tile (wgrad)
         uint32_t v[CW];
         if constexpr (CW == 32) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
         else tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c * CW, v);
@@ -878,7 +880,7 @@ static cudaError_t run_gemm(const void* A, const void* W, const void* R, void* D
       !make_tmap_bf16(&tw, W, 2, dw, sw, bw, CU_TENSOR_MAP_SWIZZLE_128B, why))
     return cudaErrorInvalidValue;
   // grid: one pair per tile up to all pairs; a partial last wave becomes narrow tiles (TileSched)
-  const int64_t full = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN) * ksplit;
+  const int64_t full = ((M + 2 * BM - 1) / (2 * BM)) * (Cfg::F32 ? (N + BN - 1) / BN : N / BN) * ksplit;
   const int pmax = num_sms / 2;
   const int smax = gemm_split_max<BN, EPI, MAJ>(ev);
   TileSched tsh = make_tile_sched((int)full, pmax, smax);
@@ -1003,8 +1005,8 @@ cudaError_t launch_gemm_bf16_dgrad_kmajor(const void* A, const void* Wt, const v
 // ksplit slices, the smallest count whose tiles fill >= 90 % of the last wave (at most 16, each
 // slice >= 8 k-blocks); the fp32 partials are summed in slice order by launch_wgrad_reduce.
 int wgrad_splits(int64_t M, int64_t N, int64_t K, int num_sms) {
-  const int64_t bn = N % 256 == 0 ? 256 : 128;
-  const int64_t tiles = ((M + 255) / 256) * (N / bn), pairs = num_sms / 2, nkb = (K + 63) / 64;
+  const int64_t bn = N % 256 == 0 || N > 256 ? 256 : 128;  // as launch_gemm_bf16_wgrad
+  const int64_t tiles = ((M + 255) / 256) * ((N + bn - 1) / bn), pairs = num_sms / 2, nkb = (K + 63) / 64;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 16 && s <= nkb / 8; ++s) {
@@ -1031,7 +1033,11 @@ cudaError_t launch_gemm_bf16_wgrad(const void* dY, const void* X, float* part, i
     return cudaErrorInvalidValue;
   }
   constexpr int MAJ = MAJ_A_MN | MAJ_B_MN;
-  if (N % 256 == 0) return run_gemm<256, EPI_F32, MAJ>(dY, X, nullptr, part, M, N, K, num_sms, st, why, EpiVec{}, RemoteMap{}, ksplit);
+  // BN = 256 (a ragged last column tile when 256 does not divide N: 10 % idle MMA columns at N = 1152)
+  // halves the operand bytes each CTA pulls from L2 per MMA cycle against BN = 128 (measured 66 % vs
+  // 88 % tensor-active: the 128-wide tiles are bound by L2 -> SM bandwidth)
+  if (N % 256 == 0 || N > 256)
+    return run_gemm<256, EPI_F32, MAJ>(dY, X, nullptr, part, M, N, K, num_sms, st, why, EpiVec{}, RemoteMap{}, ksplit);
   return run_gemm<128, EPI_F32, MAJ>(dY, X, nullptr, part, M, N, K, num_sms, st, why, EpiVec{}, RemoteMap{}, ksplit);
 }
 

@@ -81,7 +81,7 @@ def test_linear_wgrad_vs_oracle(M, N, K):
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-4, np.abs(got - ref).max()
     ctx.linear_wgrad(dY, X, dW, accumulate=True)
     torch.cuda.synchronize()
-    np.testing.assert_allclose(to_f64(dW), 2 * got, rtol=1e-6, atol=1e-5)
+    np.testing.assert_allclose(to_f64(dW), 2 * got, rtol=2e-5, atol=1e-4)  # slice sums re-rounded
     assert m.lib().dsp_wgrad_workspace_bytes(ctx.handle, M, N, K) >= N * K * 4
 
 
