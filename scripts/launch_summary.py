@@ -14,10 +14,12 @@ ROLE = {"3": "QKV_S/QKV_T", "1": "PROJ_S/PROJ_T/FC2", "4": "FC1", "2": "FC1 (raw
 
 
 def kind(name):
-    m = re.search(r"gemm_bf16_tc_kernel<(\d+), (\d+)>", name)
+    m = re.search(r"gemm_bf16_tc_kernel<(\d+), (\d+)(?:, \d+)?>", name)
     if m:
         return f"gemm BN={m.group(1)} {EPI.get(m.group(2), m.group(2))} [{ROLE.get(m.group(2), '?')}]"
-    for k in ("fmha_pt_kernel", "fmha_split_kernel", "fmha_pair_kernel", "fmha_bf16_tc_kernel", "row_partials", "row_stats", "layer_norm", "run_copy", "p2p_barrier",
+    for k in ("fmha_pt_kernel", "fmha_seq_kernel", "fmha_split_kernel", "fmha_pair_kernel", "fmha_bf16_tc_kernel", "fmha_bwd_kernel",
+              "row_partials", "row_stats", "layer_norm", "ln_bwd", "wgrad_reduce", "colsum", "transpose", "attn_bwd_dvec",
+              "dq_convert", "run_copy", "p2p_barrier",
               "p2p_put", "fold_ln_weights"):
         if k in name:
             return k
