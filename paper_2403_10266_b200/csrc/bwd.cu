@@ -64,18 +64,21 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
   const uint4* xr = reinterpret_cast<const uint4*>(x + r * C);
   const uint4* hr = reinterpret_cast<const uint4*>(dh + r * C);
   const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + r * C) : nullptr;
-  float xv[kMaxV][8], hv[kMaxV][8];
-  uint4 rv4[kMaxV];
+  // the row stays packed (bf16) in registers and is unpacked per pass: ~half the registers of fp32
+  // copies, so three CTAs fit per SM and more rows are in flight
+  uint4 xp[kMaxV], hp[kMaxV], rp[kMaxV];
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k) {
     const int vi = lane + 32 * k;
     if (vi < nv) {
-      unpack8(xr[vi], xv[k]);
-      unpack8(hr[vi], hv[k]);
-      if (rr) rv4[k] = rr[vi];
+      xp[k] = xr[vi];
+      hp[k] = hr[vi];
+      if (rr) rp[k] = rr[vi];
+      float f[8];
+      unpack8(xp[k], f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s += xv[k][i];
+      for (int i = 0; i < 8; ++i) s += f[i];
     }
   }
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -84,29 +87,30 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k)
     if (lane + 32 * k < nv) {
+      float f[8];
+      unpack8(xp[k], f);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float d = xv[k][i] - mean;
+        const float d = f[i] - mean;
         q += d * d;
       }
     }
   for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
   const float rstd = rsqrtf(q / C + eps);
-  // xhat in place of x, g = dh * gamma in place of dh; sums of g and of g * xhat
+  // sums of g = dh * gamma and of g * xhat
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k)
     if (lane + 32 * k < nv) {
-      float gm[8];
+      float xf[8], hf[8], gm[8];
+      unpack8(xp[k], xf);
+      unpack8(hp[k], hf);
       unpack8(gvec[lane + 32 * k], gm);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float xh = (xv[k][i] - mean) * rstd;
-        xv[k][i] = xh;
-        const float g = hv[k][i] * gm[i];
-        hv[k][i] = g;
+        const float g = hf[i] * gm[i];
         s1 += g;
-        s2 += g * xh;
+        s2 += g * ((xf[i] - mean) * rstd);
       }
     }
   for (int off = 16; off; off >>= 1) {
@@ -119,13 +123,17 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
   for (int k = 0; k < kMaxV; ++k) {
     const int vi = lane + 32 * k;
     if (vi < nv) {
-      float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (rr) unpack8(rv4[k], rv);
+      float xf[8], hf[8], gm[8], rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      unpack8(xp[k], xf);
+      unpack8(hp[k], hf);
+      unpack8(gvec[vi], gm);
+      if (rr) unpack8(rp[k], rv);
       uint32_t o[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const float a = rv[2 * t] + rstd * (hv[k][2 * t] - m1 - xv[k][2 * t] * m2);
-        const float b = rv[2 * t + 1] + rstd * (hv[k][2 * t + 1] - m1 - xv[k][2 * t + 1] * m2);
+        const float a = rv[2 * t] + rstd * (hf[2 * t] * gm[2 * t] - m1 - (xf[2 * t] - mean) * rstd * m2);
+        const float b = rv[2 * t + 1] +
+                        rstd * (hf[2 * t + 1] * gm[2 * t + 1] - m1 - (xf[2 * t + 1] - mean) * rstd * m2);
         o[t] = pack_bf16x2(a, b);
       }
       dxr[vi] = make_uint4(o[0], o[1], o[2], o[3]);

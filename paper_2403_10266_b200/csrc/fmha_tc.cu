@@ -2393,11 +2393,11 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
           umma_bf16_ss(tdV, make_sdesc(pbb + co, 16, 1024, SW_128B), bmn(da, kk), idK, acc0 | (kk != 0));   // dV += P^T dO
           umma_bf16_ss(tdK, make_sdesc(dsb + co, 16, 1024, SW_128B), bmn(qa, kk), idK, acc0 | (kk != 0));   // dK += dS^T Q
         }
+        umma_commit(&q_empty[st]);  // Q and dO read (dV, dK issued): the producer may refill the stage
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
           umma_bf16_ss(tdQ, make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B), bmn(kb, kk), idQ, kk != 0);
         umma_commit(dq_full);
-        umma_commit(&q_empty[st]);
         if (j == nq - 1) umma_commit(kv_empty);
       }
       __syncwarp();
