@@ -146,12 +146,12 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
 // of kLnRows rows per CTA.  Thread (x, y) = 8 columns (one 16-B vector of each row: a row group reads
 // whole rows, coalesced) of rows r0 + y, r0 + y + kLnRG, ...; the kLnRG row groups are then added in
 // y order.  part[chunk][0:C] = dgamma, part[chunk][C:2C] = dbeta, summed in chunk order after.
-constexpr int kLnRows = 64, kLnRG = 4;
+constexpr int kLnRows = 64, kLnRG = 6;
 __global__ void __launch_bounds__(1024) ln_bwd_param_kernel(const __nv_bfloat16* __restrict__ x,
                                                             const __nv_bfloat16* __restrict__ dh,
                                                             const float2* __restrict__ stats,
                                                             float* __restrict__ part, long rows, int C) {
-  extern __shared__ float red[];  // [kLnRG][2][C]
+  extern __shared__ float red[];  // [blockDim.y row groups][2][C]
   griddep_wait();
   griddep_launch_dependents();
   const int nv = C / 8;
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(1024) ln_bwd_param_kernel(const __nv_bfloat16*
   float ag[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, ab[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (v < nv) {
 #pragma unroll 4
-    for (long r = r0 + y; r < r1; r += kLnRG) {
+    for (long r = r0 + y; r < r1; r += blockDim.y) {
       const float2 st = stats[r];
       float xv[8], hv[8];
       unpack8(reinterpret_cast<const uint4*>(x + r * C)[v], xv);
@@ -181,8 +181,7 @@ __global__ void __launch_bounds__(1024) ln_bwd_param_kernel(const __nv_bfloat16*
   const int nt = blockDim.x * blockDim.y, t = y * blockDim.x + v;
   for (int c = t; c < 2 * C; c += nt) {
     float a = 0.f;
-#pragma unroll
-    for (int k = 0; k < kLnRG; ++k) a += red[(size_t)k * 2 * C + c];
+    for (int k = 0; k < (int)blockDim.y; ++k) a += red[(size_t)k * 2 * C + c];
     part[(size_t)blockIdx.x * 2 * C + c] = a;
   }
 }
@@ -318,7 +317,8 @@ cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* ga
                  stats, (long)rows, (int)C, eps);
   if (e != cudaSuccess) return e;
   const int chunks = ln_bwd_blocks(rows, num_sms), nv = (int)(C / 8);
-  const size_t smem = (size_t)kLnRG * 2 * C * sizeof(float);
+  const int bx = ((nv + 31) / 32) * 32, rg = std::min(kLnRG, 1024 / bx);  // row groups per CTA
+  const size_t smem = (size_t)rg * 2 * C * sizeof(float);
   static bool attr = false;
   if (!attr) {
     if ((e = cudaFuncSetAttribute(ln_bwd_param_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -326,7 +326,7 @@ cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* ga
       return e;
     attr = true;
   }
-  e = launch_k(ln_bwd_param_kernel, dim3((unsigned)chunks), dim3((unsigned)(((nv + 31) / 32) * 32), kLnRG), smem, st, 1,
+  e = launch_k(ln_bwd_param_kernel, dim3((unsigned)chunks), dim3((unsigned)bx, (unsigned)rg), smem, st, 1,
                (const __nv_bfloat16*)x, (const __nv_bfloat16*)dh, (const float2*)stats, part, (long)rows, (int)C);
   if (e != cudaSuccess) return e;
   return launch_k(colsum_kernel, dim3((unsigned)((2 * C + 31) / 32)), dim3(256), 0, st, 1, (const float*)part, chunks,
