@@ -1954,6 +1954,9 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   if (overlap(ctx->ws, L.total, dx, act) || overlap(ctx->ws, L.total, dy, act) || overlap(ctx->ws, L.total, x, act))
     return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps x/dy/dx");
   if (overlap(saved, SL.total, dx, act)) return fail(ctx, DSP_ERR_ALIAS, "dx overlaps saved");
+  if (overlap(ctx->ws, L.total, saved, SL.total)) return fail(ctx, DSP_ERR_ALIAS, "workspace overlaps saved");
+  for (int i = 0; i < 12; ++i)
+    if (overlap(ctx->ws, L.total, gp[i], 4)) return fail(ctx, DSP_ERR_ALIAS, "gradient %d inside the workspace", i);
   const uint8_t* sv = static_cast<const uint8_t*>(saved);
   uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
   cudaStream_t st = (cudaStream_t)stream;
