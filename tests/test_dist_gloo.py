@@ -112,3 +112,68 @@ def test_bench_self_spawns_n_ranks(n):
     assert len(lines) == 1, r.stdout  # rank 0 only
     out = json.loads(lines[0])
     assert out["world"] == n and out["ranks"] == list(range(n))
+
+
+def _bwd_worker(rank, world, port, q):
+    """One rank of the DSP backward (f4) on CPU: the oracle's per-stage backward pieces run on this rank's
+    shards; the two switches of the backward go through the library's plan (dsp_switch_plan) and a real
+    gloo all_to_all, T->S for dy (the adjoint of the forward's S->T) and S->T for dy1 (adjoint of T->S);
+    the weight gradients are all-reduced (the sum ZeRO reduce-scatters)."""
+    try:
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path.insert(0, root)
+        import paper_2403_10266_b200 as m
+        import synth
+        from oracle import backward as bw
+        from oracle import block as ob
+        from oracle import switch as osw
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        sh = synth.BlockShape(1, 4, 8, 16, 2, "f32")
+        shape = m.make_shape(sh.B, sh.T, sh.S, sh.C, sh.NH, "f32")
+        W = {k: synth.to_f64(v, "f32") for k, v in synth.make_block_weights(sh, 5).items()}
+        x = synth.to_f64(synth.make_x(sh, 5), "f32")
+        dy = np.random.default_rng(9).standard_normal(x.shape)
+        dx_ref, g_ref = bw.st_block_bwd(x, W, sh.NH, dy)
+        xs = osw.split(x, osw.DIM_T, world)[rank]
+        y1 = ob.spatial_stage(xs, W, sh.NH)                                       # forward on this rank
+        y1s = _switch_via_plan(m, shape, world, rank, osw.DIM_T, osw.DIM_S, y1.astype(np.float32)).astype(np.float64)
+        y1s = y1s.reshape(sh.B, sh.T, sh.S // world, sh.C)
+        y2 = ob.temporal_stage(y1s, W, sh.NH)
+        dys = osw.split(dy, osw.DIM_T, world)[rank].astype(np.float32)
+        dz = _switch_via_plan(m, shape, world, rank, osw.DIM_T, osw.DIM_S, dys).astype(np.float64)
+        dz = dz.reshape(y2.shape)
+        dy2, gm = bw.mlp_stage_bwd(y2, W, dz)
+        dy1s, gt = bw.temporal_stage_bwd(y1s, W, sh.NH, dy2)
+        dy1 = _switch_via_plan(m, shape, world, rank, osw.DIM_S, osw.DIM_T, dy1s.astype(np.float32)).astype(np.float64)
+        dx, gs = bw.spatial_stage_bwd(xs, W, sh.NH, dy1.reshape(xs.shape))
+        ok_dx = np.allclose(dx, osw.split(dx_ref, osw.DIM_T, world)[rank], rtol=1e-5, atol=1e-5)
+        worst = 0.0
+        for n, v in {**gm, **gt, **gs}.items():
+            t = torch.from_numpy(np.ascontiguousarray(v))
+            dist.all_reduce(t)
+            worst = max(worst, float(np.abs(t.numpy() - g_ref[n]).max() / max(np.abs(g_ref[n]).max(), 1e-30)))
+        q.put((rank, bool(ok_dx), worst))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(e), 1.0))
+
+
+def test_backward_schedule_world2_gloo():
+    """The DSP backward over two processes (library switch plans + gloo all_to_all + all_reduce of the
+    weight gradients) equals the unsharded oracle backward (the f32 wire format rounds the exchanged
+    activations: 1e-5)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bwd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, worst in res:
+        assert ok is True, (rank, ok)
+        assert worst < 1e-4, (rank, worst)
