@@ -2252,6 +2252,21 @@ __device__ __forceinline__ void load_tile_sw32(uint8_t* dst, const CUtensorMap* 
   for (int i = 0; i < DP / 16; ++i) tma_load_5d(dst + i * 4096, mb, bar, 16 * i, t.h, t.x2, t.x3, t.x4);
 }
 
+// Slot schedule shared by the producer and the MMA issuer (both walk it in the same order): item i
+// keeps K, V in slot kv; query tile j uses slot o[j % 2]; item i + 1 puts K, V into o[nq % 2] (free
+// once tile nq - 2 is done) and its query tiles use {kv, o[(nq - 1) % 2]}, both freed by the item's last
+// products.  Per-slot use counters give the mbarrier phases.
+struct SlotRing {
+  int kv = 0, o[2] = {1, 2};
+  uint32_t use[3] = {0, 0, 0};
+  __device__ __forceinline__ void next_item(int nq) {
+    const int nkv = o[nq & 1], last = o[(nq - 1) & 1];
+    o[0] = kv;
+    o[1] = last;
+    kv = nkv;
+  }
+};
+
 template <int NA, int RB, bool DIAG>
 __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     fmha_bwd_kernel(const __grid_constant__ BwdMaps mp, const FmhaParams p, const float* __restrict__ lse,
@@ -2269,10 +2284,11 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
   uint8_t* sDQ = smem + Cfg::OFF_DQ;
   float* sVec = reinterpret_cast<float*>(smem + Cfg::OFF_VEC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* kv_full = bars;
-  uint64_t* kv_empty = bars + 1;
-  uint64_t* q_full = bars + 2;   // [2]
-  uint64_t* q_empty = bars + 4;  // [2]
+  // Three 40 KB slots (two tiles each) hold an item's {K, V} and its query tiles' {Q, dO}: the item's K, V
+  // take one slot, its query tiles alternate in the other two, and the next item's K, V go into the slot
+  // the last query tile does not use -- loaded while that tile is computed (SlotRing)
+  uint64_t* slot_full = bars;       // [3]
+  uint64_t* slot_empty = bars + 3;  // [3]
   uint64_t* s_full = bars + 6;
   uint64_t* p_full = bars + 7;   // count 128
   uint64_t* dq_full = bars + 8;
@@ -2283,11 +2299,9 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
 
   const int warp = warp_id();
   if (warp == 0 && lane_id() == 0) {
-    mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&slot_full[i], 1);
+      mbar_init(&slot_empty[i], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 128 * Cfg::NWG);
@@ -2320,23 +2334,30 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
   // 768 threads: every role fits the launch allocation of 80 registers (no setmaxnreg)
   if (warp == 0) {
     if (elect_one()) {
-      uint32_t it = 0, g = 0;
-      for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
+      SlotRing rg;
+      auto fill = [&](int slot, const CUtensorMap* ma, const CUtensorMap* mb, const TileCoord& t) {
+        mbar_wait_sleep(&slot_empty[slot], (rg.use[slot] & 1) ^ 1);
+        ++rg.use[slot];
+        mbar_arrive_expect_tx(&slot_full[slot], 2 * Cfg::TX);
+        uint8_t* b = smem + slot * 2 * Cfg::TILE;
+        load_tile_sw32<NA, RB>(b, ma, &slot_full[slot], t);
+        load_tile_sw32<NA, RB>(b + Cfg::TILE, mb, &slot_full[slot], t);
+      };
+      int item = blockIdx.x;
+      if (item < p.items) {
         int outer, h, kvt;
         decomp(item, outer, h, kvt);
-        mbar_wait_sleep(kv_empty, (it & 1) ^ 1);
-        mbar_arrive_expect_tx(kv_full, 2 * Cfg::TX);
-        const TileCoord tk = bwd_coord(p, outer, h, kvt);
-        load_tile_sw32<NA, RB>(sK, &mp.k[1], kv_full, tk);
-        load_tile_sw32<NA, RB>(sV, &mp.v[1], kv_full, tk);
-        for (int j = 0; j < nq; ++j, ++g) {
-          const int st = g & 1;
-          mbar_wait_sleep(&q_empty[st], ((g >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&q_full[st], 2 * Cfg::TX);
-          uint8_t* qb = smem + Cfg::OFF_Q + 2 * st * Cfg::TILE;
-          const TileCoord tq = bwd_coord(p, outer, h, j);
-          load_tile_sw32<NA, RB>(qb, &mp.q[1], &q_full[st], tq);
-          load_tile_sw32<NA, RB>(qb + Cfg::TILE, &mp.dout[1], &q_full[st], tq);
+        fill(rg.kv, &mp.k[1], &mp.v[1], bwd_coord(p, outer, h, kvt));
+      }
+      for (; item < p.items; item += gridDim.x) {
+        int outer, h, kvt;
+        decomp(item, outer, h, kvt);
+        for (int j = 0; j < nq; ++j) fill(rg.o[j & 1], &mp.q[1], &mp.dout[1], bwd_coord(p, outer, h, j));
+        rg.next_item(nq);
+        if (item + (int)gridDim.x < p.items) {  // the next item's K, V behind the last query tile
+          int o2, h2, k2;
+          decomp(item + gridDim.x, o2, h2, k2);
+          fill(rg.kv, &mp.k[1], &mp.v[1], bwd_coord(p, o2, h2, k2));
         }
       }
     }
@@ -2345,7 +2366,7 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     constexpr uint32_t idS = make_idesc_bf16(128, 128, 0, 0);       // S^T, dP^T
     constexpr uint32_t idK = make_idesc_bf16(128, DP, 0, 1);        // dV, dK: A K-major, B MN-major (N = 80)
     constexpr uint32_t idQ = make_idesc_bf16(128, DP, 1, 1);        // dQ: A (dS) MN-major, B (K) MN-major
-    const uint32_t kb = smem_u32(sK), vb = smem_u32(sV), dsb = smem_u32(sDS);
+    const uint32_t dsb = smem_u32(sDS);
     const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 336, tdQ = tmem + 416;
     // D[tmem] = X Y^T over the head dim: X, Y two [128][DP] tiles of SW32 boxes (one box per k-step)
     auto qk = [&](uint32_t d, uint32_t xa, uint32_t ya) {
@@ -2361,11 +2382,17 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     // (P^T and dS^T live in shared memory).  Across an item boundary the next K, V land only after
     // the item's last products (single K/V buffer), so there the order is the plain one.
     const uint32_t pbb = smem_u32(sP);
-    auto issue_a = [&](uint32_t gg, bool first_of_item, uint32_t itx) {
-      const int st = gg & 1;
-      const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
-      if (first_of_item) mbar_wait(kv_full, itx & 1);
-      mbar_wait(&q_full[st], (gg >> 1) & 1);
+    SlotRing rg;
+    uint32_t cons[3] = {0, 0, 0};  // full-barrier waits per slot
+    auto wait_slot = [&](int slot) {
+      mbar_wait(&slot_full[slot], cons[slot] & 1);
+      ++cons[slot];
+    };
+    auto issue_a = [&](uint32_t gg, int j, bool first_of_item) {
+      const uint32_t qa = smem_u32(smem + rg.o[j & 1] * 2 * Cfg::TILE), da = qa + Cfg::TILE;
+      const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE), vb = kb + Cfg::TILE;
+      if (first_of_item) wait_slot(rg.kv);
+      wait_slot(rg.o[j & 1]);
       if (gg >= 1) mbar_wait(s_free, (gg - 1) & 1);  // S^T / dP^T of the previous tile read out of TMEM
       tc_fence_after();
       if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(3); }
@@ -2377,8 +2404,9 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
       __syncwarp();
     };
     auto issue_bc = [&](uint32_t gg, int j, uint32_t itx) {
-      const int st = gg & 1;
-      const uint32_t qa = smem_u32(smem + Cfg::OFF_Q + 2 * st * Cfg::TILE), da = qa + Cfg::TILE;
+      const int qs = rg.o[j & 1];
+      const uint32_t qa = smem_u32(smem + qs * 2 * Cfg::TILE), da = qa + Cfg::TILE;
+      const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE);
       mbar_wait(p_full, gg & 1);
       if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(4); }
       if (gg >= 1) mbar_wait(dq_free, (gg - 1) & 1);
@@ -2393,22 +2421,23 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
           umma_bf16_ss(tdV, make_sdesc(pbb + co, 16, 1024, SW_128B), bmn(da, kk), idK, acc0 | (kk != 0));   // dV += P^T dO
           umma_bf16_ss(tdK, make_sdesc(dsb + co, 16, 1024, SW_128B), bmn(qa, kk), idK, acc0 | (kk != 0));   // dK += dS^T Q
         }
-        umma_commit(&q_empty[st]);  // Q and dO read (dV, dK issued): the producer may refill the stage
+        umma_commit(&slot_empty[qs]);  // Q and dO read (dV, dK issued): the producer may refill the slot
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
           umma_bf16_ss(tdQ, make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B), bmn(kb, kk), idQ, kk != 0);
         umma_commit(dq_full);
-        if (j == nq - 1) umma_commit(kv_empty);
+        if (j == nq - 1) umma_commit(&slot_empty[rg.kv]);  // the item's K, V read
       }
       __syncwarp();
     };
     uint32_t it = 0, g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-      issue_a(g, true, it);
+      issue_a(g, 0, true);
       for (int j = 0; j < nq; ++j, ++g) {
-        if (j + 1 < nq) issue_a(g + 1, false, it);
+        if (j + 1 < nq) issue_a(g + 1, j + 1, false);
         issue_bc(g, j, it);
       }
+      rg.next_item(nq);
     }
   } else if (warp >= 4 && warp < 4 + 4 * Cfg::NWG) {
     // Four compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
