@@ -807,11 +807,13 @@ def run_train(args):
                                                  + ", B=1 T=16 S=1024 C=1152 16 heads, raw weights",
                                      "l2": "flushed between timed steps", "launch": "cuda graph replay"},
                           "breakdown_ms": {"forward_train": round(t_f / K, 4), "backward": round(t_b / K, 4)},
-                          "roofline": {"bound": "tensor", "t_roofline_ms": round(t_roof, 4),
-                                       "frac": round(t_roof / (t_ms / K), 3), "flops_per_step": flops,
-                                       "achieved_tflops": round(flops / N / (t_ms / K / 1e3) / 1e12, 1),
-                                       "peak_tflops": P["bf16_tflops"],
-                                       "basis": "train FLOPs (bench.train_flops) / N / measured bf16 peak"},
+                          "roofline": {"bound": "tensor", "achieved": round(flops / N / (t_ms / K / 1e3) / 1e12, 1),
+                                       "peak": P["bf16_tflops"], "unit": "TFLOP/s",
+                                       "frac": round(t_roof / (t_ms / K), 3), "traffic": None,
+                                       "t_roofline_ms": round(t_roof, 4), "flops_per_step": flops,
+                                       "basis": "whole training step: train FLOPs (bench.train_flops) / N over the "
+                                                "device-timed step, against the measured bf16 peak (per-kernel "
+                                                "shares: profiles/r02/train/launches_train_step.txt)"},
                           "gpu_launches": graphs["step"][1] * K, "clocks": clocks.summary()}), flush=True)
     if world > 1:
         dist.barrier(device_ids=[local])
