@@ -1832,6 +1832,8 @@ dsp_status_t side_init(dsp_ctx_t ctx, Side* sd) {
 // wgrad k on the side stream once the main stream (st) has produced its inputs
 dsp_status_t side_wgrad(dsp_ctx_t ctx, const Side& sd, int k, int64_t M, int64_t N, int64_t K, const void* dY,
                         const void* X, float* dW, float* part, cudaStream_t st) {
+  static const bool off = [] { const char* e = std::getenv("DSP_BWD_SIDE"); return e && e[0] == '0'; }();
+  if (off) return wgrad(ctx, M, N, K, dY, X, dW, 1, part, st);  // A/B: everything on the caller's stream
   DSP_CUDA(ctx, cudaEventRecord(sd.fork, st), "fork");
   DSP_CUDA(ctx, cudaStreamWaitEvent(sd.s, sd.fork, 0), "fork wait");
   DSP_TRY(wgrad(ctx, M, N, K, dY, X, dW, 1, part, sd.s));
@@ -1839,6 +1841,8 @@ dsp_status_t side_wgrad(dsp_ctx_t ctx, const Side& sd, int k, int64_t M, int64_t
   return DSP_OK;
 }
 dsp_status_t side_join(dsp_ctx_t ctx, const Side& sd, int k, cudaStream_t st) {
+  static const bool off = [] { const char* e = std::getenv("DSP_BWD_SIDE"); return e && e[0] == '0'; }();
+  if (off) return DSP_OK;
   DSP_CUDA(ctx, cudaStreamWaitEvent(st, sd.done[k], 0), "join");
   return DSP_OK;
 }
@@ -1961,6 +1965,11 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   uint8_t* ws = static_cast<uint8_t*>(ctx->ws);
   cudaStream_t st = (cudaStream_t)stream;
   float* part = reinterpret_cast<float*>(ws + L.wpart);
+  struct NoPdl {  // the backward's kernels launch without programmatic dependent launch (dsp_internal.h)
+    bool prev = t_no_pdl;
+    NoPdl() { t_no_pdl = true; }
+    ~NoPdl() { t_no_pdl = prev; }
+  } no_pdl;
   // 1. dz = switch_{T->S}(dy): the adjoint of the forward's closing S->T switch
   const void* dz = dy;
   if (N > 1) {

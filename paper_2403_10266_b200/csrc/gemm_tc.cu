@@ -36,6 +36,7 @@
 namespace dsp {
 
 thread_local unsigned long long* t_clk = nullptr;
+thread_local bool t_no_pdl = false;
 
 namespace {
 
