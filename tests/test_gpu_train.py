@@ -302,3 +302,19 @@ def test_block_train_virtual_ranks(N):
         tot = sum(to_f64(G[r][n]) for r in range(N))
         ref = to_f64(G1[n])
         assert np.abs(tot - ref).max() <= 1e-4 * np.abs(ref).max() + 1e-5, n
+
+
+def test_block_train_benchmarked_shape_vs_oracle():
+    """The exact configuration `bench.py --config train` times (configs[1]: B=1 T=16 S=1024 C=1152,
+    16 heads; the spatial attention backward on its multi-key-tile path with the f32 dQ reduce-add)
+    against the float64 oracle backward: dx and all twelve weight gradients (R40)."""
+    sh = synth.BlockShape(1, 16, 1024, 1152, 16, "bf16")
+    xs, Ws = synth.make_x(sh, 7), synth.make_block_weights(sh, 7)
+    dys = _rand((sh.B, sh.T, sh.S, sh.C), 1.0, 43)
+    Y, dX, G = _train_n1(sh, xs, Ws, dys)
+    x64, W64 = synth.to_f64(xs, "bf16"), weights_f64(Ws, "bf16")
+    dy64 = to_f64(_bf16(dys)).reshape(dys.shape)
+    dx_ref, g_ref = bw.st_block_bwd(x64, W64, sh.NH, dy64)
+    print(grad_close(to_f64(dX).reshape(xs.shape), dx_ref, name="dx"))
+    for n in bw.GRAD_NAMES:
+        print(grad_close(to_f64(G[n]), g_ref[n], rel_l2=2e-2, rel_max=5e-2, name=n))
