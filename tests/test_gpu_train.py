@@ -318,3 +318,30 @@ def test_block_train_benchmarked_shape_vs_oracle():
     print(grad_close(to_f64(dX).reshape(xs.shape), dx_ref, name="dx"))
     for n in bw.GRAD_NAMES:
         print(grad_close(to_f64(G[n]), g_ref[n], rel_l2=2e-2, rel_max=5e-2, name=n))
+
+
+def test_training_path_rejects_what_it_does_not_support():
+    """Documented limits (include/dsp_train.h) fail loudly with the right status, before any launch."""
+    m = dsp()
+    ctx = m.Context()
+    ok = synth.BlockShape(1, 16, 128, 1152, 16, "bf16")
+    Ws = weights_dev(synth.make_block_weights(ok, 1), "bf16")
+    X = to_dev(synth.make_x(ok, 1), "bf16")
+    Y = torch.empty_like(X)
+
+    def call(shape, W=Ws, ws=True):
+        if ws:
+            ctx.ensure_workspace(m.train_workspace_bytes(shape, 1))
+        saved = torch.empty(m.train_saved_layout(shape, 1)["total"] + 256, dtype=torch.uint8, device="cuda")
+        with pytest.raises(m.DSPError) as e:
+            ctx.block_forward_train(shape, W, X, Y, saved)
+        return e.value.name
+
+    assert call(m.make_shape(1, 16, 128, 1152, 12, "bf16")) == "DSP_ERR_UNSUPPORTED"   # Dh = 96
+    assert call(m.make_shape(1, 16, 100, 1152, 16, "bf16")) == "DSP_ERR_UNSUPPORTED"   # S neither divides nor is a multiple of 128
+    assert call(m.make_shape(1, 16, 128, 1152, 16, "f32")) == "DSP_ERR_UNSUPPORTED"    # f32
+    W2 = dict(Ws)
+    W2["pe_t"] = torch.zeros(16, 1152, dtype=torch.bfloat16, device="cuda")
+    assert call(m.make_shape(1, 16, 128, 1152, 16, "bf16"), W=W2) == "DSP_ERR_UNSUPPORTED"  # forward-only extras
+    ctx.set_workspace(torch.empty(1024, dtype=torch.uint8, device="cuda"))
+    assert call(m.make_shape(1, 16, 128, 1152, 16, "bf16"), ws=False) == "DSP_ERR_WORKSPACE"
