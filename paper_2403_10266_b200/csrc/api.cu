@@ -1967,7 +1967,10 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   float* part = reinterpret_cast<float*>(ws + L.wpart);
   struct NoPdl {  // the backward's kernels launch without programmatic dependent launch (dsp_internal.h)
     bool prev = t_no_pdl;
-    NoPdl() { t_no_pdl = true; }
+    NoPdl() {
+      static const bool keep = [] { const char* e = std::getenv("DSP_BWD_PDL"); return e && e[0] == '1'; }();
+      t_no_pdl = !keep;  // A/B: DSP_BWD_PDL=1 keeps PDL
+    }
     ~NoPdl() { t_no_pdl = prev; }
   } no_pdl;
   // 1. dz = switch_{T->S}(dy): the adjoint of the forward's closing S->T switch
