@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float4* __restr
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
     float4* o = i < h4 ? out0 + i : out1 + (i - h4);
     float4 a = accumulate ? *o : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
     for (int s = 0; s < nparts; ++s) {
       const float4 b = part[(long)s * n4 + i];
       a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
