@@ -2160,8 +2160,7 @@ struct BwdCfg {
   static constexpr int TILE = Base::TILE, DP = Base::DP, TX = Base::TX;
   static constexpr int OFF_K = 0, OFF_V = TILE, OFF_Q = 2 * TILE;  // stage s: Q at OFF_Q + 2 s TILE, dO next
   static constexpr int OFF_DS = 6 * TILE;                            // dS^T: 2 x [128 keys][64 queries] SW128
-  static constexpr int OFF_P = OFF_DS + 32768;                       // P^T: same layout
-  static constexpr int OFF_DQ = OFF_P + 32768;                       // dQ f32 staging (3 swizzled boxes) / dK, dV bf16
+  static constexpr int OFF_DQ = OFF_DS + 32768;                      // dQ f32 staging (3 swizzled boxes) / dK, dV bf16
   static constexpr int OFF_VEC = OFF_DQ + 128 * DP * 4;              // [2 buf][lse2 | D][128] f32
   static constexpr int OFF_BAR = OFF_VEC + 2 * 2 * 128 * 4;
   // no alignment slack: dynamic smem starts 1024-B aligned after the system-reserved block (checked)
@@ -2280,7 +2279,6 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
   uint8_t* sK = smem + Cfg::OFF_K;
   uint8_t* sV = smem + Cfg::OFF_V;
   uint8_t* sDS = smem + Cfg::OFF_DS;
-  uint8_t* sP = smem + Cfg::OFF_P;
   uint8_t* sDQ = smem + Cfg::OFF_DQ;
   float* sVec = reinterpret_cast<float*>(smem + Cfg::OFF_VEC);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
@@ -2294,8 +2292,9 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
   uint64_t* dq_full = bars + 8;
   uint64_t* dq_free = bars + 9;  // count 128
   uint64_t* kv_free = bars + 10; // count 128
-  uint64_t* s_free = bars + 11;  // count 256: the compute warpgroups have read S^T / dP^T out of TMEM
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* s_free = bars + 11;  // the compute warpgroups have read S^T / dP^T out of TMEM
+  uint64_t* dp_full = bars + 12; // dP^T of the tile in TMEM (issued behind the previous tile's dV)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 13);
 
   const int warp = warp_id();
   if (warp == 0 && lane_id() == 0) {
@@ -2309,6 +2308,7 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     mbar_init(dq_free, 128);
     mbar_init(kv_free, 128);
     mbar_init(s_free, 128 * Cfg::NWG);
+    mbar_init(dp_full, 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -2381,16 +2381,17 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     // (s_free), BEFORE dV/dK/dQ of tile g, so tile g + 1's exponentials overlap tile g's products
     // (P^T and dS^T live in shared memory).  Across an item boundary the next K, V land only after
     // the item's last products (single K/V buffer), so there the order is the plain one.
-    const uint32_t pbb = smem_u32(sP);
     SlotRing rg;
     uint32_t cons[3] = {0, 0, 0};  // full-barrier waits per slot
     auto wait_slot = [&](int slot) {
       mbar_wait(&slot_full[slot], cons[slot] & 1);
       ++cons[slot];
     };
-    auto issue_a = [&](uint32_t gg, int j, bool first_of_item) {
-      const uint32_t qa = smem_u32(smem + rg.o[j & 1] * 2 * Cfg::TILE), da = qa + Cfg::TILE;
-      const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE), vb = kb + Cfg::TILE;
+    // S^T of tile g + 1 goes out as soon as the compute warps have read tile g out of TMEM; dP^T of
+    // tile g + 1 behind tile g's dV, which reads P^T from dP^T's columns (TS form: no smem for P)
+    auto issue_s = [&](uint32_t gg, int j, bool first_of_item) {
+      const uint32_t qa = smem_u32(smem + rg.o[j & 1] * 2 * Cfg::TILE);
+      const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE);
       if (first_of_item) wait_slot(rg.kv);
       wait_slot(rg.o[j & 1]);
       if (gg >= 1) mbar_wait(s_free, (gg - 1) & 1);  // S^T / dP^T of the previous tile read out of TMEM
@@ -2398,8 +2399,16 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
       if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(3); }
       if (elect_one()) {
         qk(tS, kb, qa);   // S^T = K Q^T
-        qk(tdP, vb, da);  // dP^T = V dO^T
         umma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int j) {
+      const uint32_t da = smem_u32(smem + rg.o[j & 1] * 2 * Cfg::TILE) + Cfg::TILE;
+      const uint32_t vb = smem_u32(smem + rg.kv * 2 * Cfg::TILE) + Cfg::TILE;
+      if (elect_one()) {
+        qk(tdP, vb, da);  // dP^T = V dO^T
+        umma_commit(dp_full);
       }
       __syncwarp();
     };
@@ -2416,10 +2425,12 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
       if (elect_one()) {
         const uint32_t acc0 = j != 0;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step; P^T, dS^T K-major in smem (chunk kk / 4)
-          const uint32_t co = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16_ss(tdV, make_sdesc(pbb + co, 16, 1024, SW_128B), bmn(da, kk), idK, acc0 | (kk != 0));   // dV += P^T dO
-          umma_bf16_ss(tdK, make_sdesc(dsb + co, 16, 1024, SW_128B), bmn(qa, kk), idK, acc0 | (kk != 0));   // dK += dS^T Q
+        for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step
+          // dV += P^T dO: P^T packed in TMEM over dP^T's columns (queries 32 w .. 32 w + 31 of compute
+          // warpgroup w at columns 32 w .. 32 w + 15); dK += dS^T Q: dS^T K-major in smem (chunk kk / 4)
+          umma_bf16_ts(tdV, tdP + 32 * (kk >> 1) + 8 * (kk & 1), bmn(da, kk), idK, acc0 | (kk != 0));
+          umma_bf16_ss(tdK, make_sdesc(dsb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B), bmn(qa, kk), idK,
+                       acc0 | (kk != 0));
         }
         umma_commit(&slot_empty[qs]);  // Q and dO read (dV, dK issued): the producer may refill the slot
 #pragma unroll
@@ -2432,10 +2443,12 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     };
     uint32_t it = 0, g = 0;
     for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-      issue_a(g, 0, true);
+      issue_s(g, 0, true);
+      issue_dp(0);
       for (int j = 0; j < nq; ++j, ++g) {
-        if (j + 1 < nq) issue_a(g + 1, j + 1, false);
+        if (j + 1 < nq) issue_s(g + 1, j + 1, false);
         issue_bc(g, j, it);
+        if (j + 1 < nq) issue_dp(j + 1);
       }
       rg.next_item(nq);
     }
@@ -2454,7 +2467,7 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     const int qlo = p.G > 1 ? (row / p.L) * p.L - 32 * hw : 0;
     const int qhi = p.G > 1 ? qlo + p.L : 32;
     const uint32_t tile_off = (hw >> 1) * 16384 + row * 128;
-    const uint32_t dsrow = smem_u32(sDS) + tile_off, prow = smem_u32(sP) + tile_off;
+    const uint32_t dsrow = smem_u32(sDS) + tile_off;
     // lse2 and D / sqrt(Dh) of the query this thread stages (threads row < 32 of each warpgroup: query
     // 32 hw + row), copied global -> smem by cp.async one tile ahead (no registers held across the tile,
     // the latency off the critical path); padding queries get lse2 = +inf (P = 0), D = 0
@@ -2492,52 +2505,68 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         tc_fence_after();
         if (threadIdx.x == 128) BWD_STAMP(1);
         if (threadIdx.x == 128 + 128 * (Cfg::NWG - 1)) BWD_STAMP(6);  // the last warpgroup saw S
+        // phase 1: P from S^T (two 16-query chunks), packed bf16 (kept for dS and stored for dV)
         uint32_t pk[16], dk[16];
+        const float2 sl22 = make_float2(sl2, sl2), sc2 = make_float2(sc, sc);
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {  // two 16-query chunks
-          uint32_t sv[16], dv[16];
+        for (int k = 0; k < 2; ++k) {
+          uint32_t sv[16];
           tmem_ld16(tS + k * 16, sv);
-          tmem_ld16(tdP + k * 16, dv);
           tmem_ld_wait();
-          if (k == 1) {
-            tc_fence_before();
-            mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's may be issued
-          }
-          // packed pairs (FFMA2 / FMUL2): x = s scale_log2 - lse2, P = 2^x, dS = P (dP / sqrt(Dh) - D / sqrt(Dh))
-          const float2 sl22 = make_float2(sl2, sl2), sc2 = make_float2(sc, sc);
 #pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {  // 4 queries per step: lse2 and D / sqrt(Dh) as 16-B shared loads
+          for (int i4 = 0; i4 < 4; ++i4) {
             const int q0 = k * 16 + 4 * i4;
-            const float4 l4 = ld_shared_f32x4(vb + q0 * 4), d4 = ld_shared_f32x4(vb + 512 + q0 * 4);
+            const float4 l4 = ld_shared_f32x4(vb + q0 * 4);
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
               const int e = 4 * i4 + 2 * h2;
               const float2 s2 = make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
-              const float2 p2 = make_float2(__uint_as_float(dv[e]), __uint_as_float(dv[e + 1]));
               const float2 nl = h2 ? make_float2(-l4.z, -l4.w) : make_float2(-l4.x, -l4.y);
-              const float2 nd = h2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y);
               float2 x = ffma2(s2, sl22, nl);
               if (DIAG) {
                 const int qc = q0 + 2 * h2;
                 if (qc < qlo || qc >= qhi) x.x = -INFINITY;
                 if (qc + 1 < qlo || qc + 1 >= qhi) x.y = -INFINITY;
               }
-              const float2 pe = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              pk[k * 8 + 2 * i4 + h2] = pack_bf16x2(fast_exp2(x.x), fast_exp2(x.y));
+            }
+          }
+        }
+        // phase 2: dS = P (dP / sqrt(Dh) - D / sqrt(Dh)) with the bf16 P the dV product uses
+        mbar_wait(dp_full, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          uint32_t dv[16];
+          tmem_ld16(tdP + k * 16, dv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const int q0 = k * 16 + 4 * i4;
+            const float4 d4 = ld_shared_f32x4(vb + 512 + q0 * 4);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int e = 4 * i4 + 2 * h2, kk = k * 8 + 2 * i4 + h2;
+              const float2 p2 = make_float2(__uint_as_float(dv[e]), __uint_as_float(dv[e + 1]));
+              const float2 nd = h2 ? make_float2(-d4.z, -d4.w) : make_float2(-d4.x, -d4.y);
+              const float2 pe = make_float2(bf16lo(pk[kk]), bf16hi(pk[kk]));
               const float2 ds = fmul2(pe, ffma2(p2, sc2, nd));
-              const int kk = k * 8 + 2 * i4 + h2;
-              pk[kk] = pack_bf16x2(pe.x, pe.y);
               dk[kk] = pack_bf16x2(ds.x, ds.y);
             }
           }
         }
-        // P^T and dS^T of the warpgroup's 32 queries -> smem (SW128 K-major over queries)
-        if (g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products have read them
+        tc_fence_before();
+        mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's S may be issued
+        tmem_st16(tdP, pk);   // P^T over this warpgroup's consumed dP^T columns (read by dV, TS form)
+        // dS^T of the warpgroup's 32 queries -> smem (SW128 K-major over queries)
+        if (g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products have read it
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int ch = (hw & 1) * 4 + u;
-          st_shared_v4(prow + ((ch ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
           st_shared_v4(dsrow + ((ch ^ (row & 7)) << 4), dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
         }
+        tmem_st_wait();
+        tc_fence_before();
         fence_proxy_async_smem();
         if (threadIdx.x == 128) BWD_STAMP(2);
         if (threadIdx.x == 128 + 128 * (Cfg::NWG - 1)) BWD_STAMP(7);  // the last warpgroup's P done
