@@ -2426,11 +2426,11 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         const uint32_t acc0 = j != 0;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // 16 queries per step
-          // dV += P^T dO: P^T packed in TMEM over dP^T's columns (queries 32 w .. 32 w + 31 of compute
-          // warpgroup w at columns 32 w .. 32 w + 15); dK += dS^T Q: dS^T K-major in smem (chunk kk / 4)
-          umma_bf16_ts(tdV, tdP + 32 * (kk >> 1) + 8 * (kk & 1), bmn(da, kk), idK, acc0 | (kk != 0));
-          umma_bf16_ss(tdK, make_sdesc(dsb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SW_128B), bmn(qa, kk), idK,
-                       acc0 | (kk != 0));
+          // dV += P^T dO and dK += dS^T Q, both A operands packed in TMEM over dP^T's consumed columns:
+          // compute warpgroup w's 32 queries at columns 32 w .. 32 w + 15 (P^T) and + 16 .. + 31 (dS^T)
+          const uint32_t pa = tdP + 32 * (kk >> 1) + 8 * (kk & 1);
+          umma_bf16_ts(tdV, pa, bmn(da, kk), idK, acc0 | (kk != 0));
+          umma_bf16_ts(tdK, pa + 16, bmn(qa, kk), idK, acc0 | (kk != 0));
         }
         umma_commit(&slot_empty[qs]);  // Q and dO read (dV, dK issued): the producer may refill the slot
 #pragma unroll
@@ -2557,7 +2557,8 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         }
         tc_fence_before();
         mbar_arrive(s_free);  // S^T / dP^T of this tile are in registers: the next tile's S may be issued
-        tmem_st16(tdP, pk);   // P^T over this warpgroup's consumed dP^T columns (read by dV, TS form)
+        tmem_st16(tdP, pk);       // P^T over this warpgroup's consumed dP^T columns (dV, TS form)
+        tmem_st16(tdP + 16, dk);  // dS^T beside it (dK, TS form); dQ reads the smem copy (MN-major)
         // dS^T of the warpgroup's 32 queries -> smem (SW128 K-major over queries)
         if (g >= 1) mbar_wait(dq_full, (g - 1) & 1);  // the previous tile's products have read it
 #pragma unroll
