@@ -7,8 +7,9 @@ txt = txt[txt.index('"ID"'):]
 rows = [r for r in csv.DictReader(io.StringIO(txt)) if r["Metric Name"] == "gpu__time_duration.sum"]
 names = [r["Kernel Name"] for r in rows]
 # the step starts at the last forward LayerNorm preceded by the bench's flat.zero_ fill of a previous bwd
-starts = [i for i, n in enumerate(names) if "layer_norm_bf16_vec_kernel" in n and i + 1 < len(names)
-          and "gemm_bf16_tc_kernel<192, 0, 0>" in names[i + 1]]
+# a step starts at LN1: LayerNorm -> QKV GEMM -> the spatial FMHA (fmha_pt_kernel)
+starts = [i for i, n in enumerate(names) if "layer_norm_bf16_vec_kernel" in n and i + 2 < len(names)
+          and "fmha_pt_kernel" in names[i + 2]]
 s0 = starts[1] if len(starts) >= 3 else starts[0]  # a warm-up step (the list may end mid-step)
 step = rows[s0:]
 # stop before the next forward (if any)
