@@ -54,7 +54,7 @@ size_t dsp_train_workspace_bytes(const dsp_shape_t* shape, int world);
  * (>= dsp_train_saved_layout().total bytes, device, 256-B aligned).  x_local, y_local T-sharded
  * [B, T/N, S, C]; they must not overlap `saved` or the workspace.
  * Errors: NULL, SHAPE, DIVISIBILITY, ALIGNMENT, ALIAS, UNSUPPORTED (f32, Dh != 72, extras set,
- * sequence length neither dividing nor a multiple of 128), WORKSPACE, CUDA, NCCL. */
+ * sequence length neither dividing nor a multiple of 128, impl DSP_SWITCH_FUSED), WORKSPACE, CUDA, NCCL. */
 dsp_status_t dsp_st_block_forward_train(dsp_ctx_t ctx, const dsp_shape_t* shape, const dsp_block_weights_t* w,
                                         const void* x_local, void* y_local, void* saved,
                                         dsp_switch_impl_t impl, void* stream);

@@ -1768,6 +1768,12 @@ dsp_status_t check_train_call(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_blo
   return DSP_OK;
 }
 
+dsp_status_t check_train_impl(dsp_ctx_t ctx, dsp_switch_impl_t impl) {
+  if (impl != DSP_SWITCH_NCCL && impl != DSP_SWITCH_P2P)
+    return fail(ctx, DSP_ERR_UNSUPPORTED, "training path: switch impl NCCL or P2P (the fused epilogues are forward-only)");
+  return DSP_OK;
+}
+
 // dW[N, K] (+)= dY[M, N]^T X[M, K] through the split-K partials in `part`
 dsp_status_t wgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* X, float* dW,
                    int accumulate, float* part, cudaStream_t st) {
@@ -1897,6 +1903,7 @@ size_t dsp_train_workspace_bytes(const dsp_shape_t* s, int world) {
 dsp_status_t dsp_st_block_forward_train(dsp_ctx_t ctx, const dsp_shape_t* s, const dsp_block_weights_t* w,
                                         const void* x, void* y, void* saved, dsp_switch_impl_t impl, void* stream) {
   DSP_TRY(check_train_call(ctx, s, w));
+  DSP_TRY(check_train_impl(ctx, impl));
   if (!x || !y || !saved) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
   if (!aligned16(x) || !aligned16(y) || (reinterpret_cast<uintptr_t>(saved) & 255))
     return fail(ctx, DSP_ERR_ALIGNMENT, "x, y 16-B and saved 256-B aligned");
@@ -1944,6 +1951,7 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
                                    const void* x, const void* dy, void* dx, const dsp_block_grads_t* g,
                                    dsp_switch_impl_t impl, void* stream) {
   DSP_TRY(check_train_call(ctx, s, w));
+  DSP_TRY(check_train_impl(ctx, impl));
   if (!x || !dy || !dx || !saved || !g) return fail(ctx, DSP_ERR_NULL, "NULL buffer");
   float* gp[12] = {g->ln1_w, g->ln1_b, g->w_qkv_s, g->w_o_s, g->ln2_w, g->ln2_b,
                    g->w_qkv_t, g->w_o_t, g->ln3_w, g->ln3_b, g->w_fc1, g->w_fc2};

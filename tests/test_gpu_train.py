@@ -343,5 +343,10 @@ def test_training_path_rejects_what_it_does_not_support():
     W2 = dict(Ws)
     W2["pe_t"] = torch.zeros(16, 1152, dtype=torch.bfloat16, device="cuda")
     assert call(m.make_shape(1, 16, 128, 1152, 16, "bf16"), W=W2) == "DSP_ERR_UNSUPPORTED"  # forward-only extras
+    shape = m.make_shape(1, 16, 128, 1152, 16, "bf16")
+    saved = torch.empty(m.train_saved_layout(shape, 1)["total"] + 256, dtype=torch.uint8, device="cuda")
+    with pytest.raises(m.DSPError) as e:  # the fused switch epilogues are forward-only
+        ctx.block_forward_train(shape, Ws, X, Y, saved, impl="fused")
+    assert e.value.name == "DSP_ERR_UNSUPPORTED"
     ctx.set_workspace(torch.empty(1024, dtype=torch.uint8, device="cuda"))
     assert call(m.make_shape(1, 16, 128, 1152, 16, "bf16"), ws=False) == "DSP_ERR_WORKSPACE"
