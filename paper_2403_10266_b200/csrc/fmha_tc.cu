@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "dsp_internal.h"
 #include "sm100.cuh"
@@ -65,6 +66,7 @@ struct FmhaParams {
   int kv_last;   // valid keys in the last K/V tile (128 unless the key length is ragged: cross-attention)
   int cross;     // 1: cross-attention views (queries and keys from different tensors)
   int colfast;   // 1: item order column-fastest (outer before head), for the head-major TSEQ layout
+  int walk_ch;   // backward: consecutive items per CTA chunk (BwdWalk; 0: one contiguous range per CTA)
   float scale_log2;
   __nv_bfloat16* o;
   float* lse;                 // optional [tok][NH]: log2-domain log-sum-exp of the scaled scores (training)
@@ -2258,11 +2260,52 @@ __device__ __forceinline__ void load_tile_sw32(uint8_t* dst, const CUtensorMap* 
 struct SlotRing {
   int kv = 0, o[2] = {1, 2};
   uint32_t use[3] = {0, 0, 0};
-  __device__ __forceinline__ void next_item(int nq) {
+  // reuse: the next item's first query tile is this item's last (BwdWalk), still in its slot, so
+  // the next item starts in that slot and its second tile goes to this item's K, V slot
+  __device__ __forceinline__ void next_item(int nq, bool reuse) {
     const int nkv = o[nq & 1], last = o[(nq - 1) & 1];
-    o[0] = kv;
-    o[1] = last;
+    o[0] = reuse ? last : kv;
+    o[1] = reuse ? kv : last;
     kv = nkv;
+  }
+};
+
+// A CTA's items: chunks of walk_ch consecutive items of the item list (key tile fastest), chunk c on
+// CTA c mod grid (walk_ch = 1: plain grid stride; 0: one contiguous range per CTA).  Consecutive items
+// of a chunk mostly share (sequence group, head) and differ in the key tile; such a follower walks its
+// query tiles in the opposite order, its first tile being its predecessor's last: that tile's {Q, dO}
+// stay in their slot and the item boundary waits for no load.  Concurrent CTAs still cover
+// neighbouring key tiles of the same sequences (their {Q, dO} read once from HBM, then from L2).
+struct BwdWalk {
+  int item, end, chunk, ch, items, nq, n_kv;
+  bool rev = false, reuse = false;  // query order of the current item; its first tile is the previous one's last
+  __device__ __forceinline__ explicit BwdWalk(const FmhaParams& p)
+      : ch(p.walk_ch), items(p.items), nq(p.n_qt), n_kv(p.n_kv) {
+    if (ch > 0) {
+      chunk = blockIdx.x;
+      item = chunk * ch;
+      end = min(item + ch, items);
+    } else {
+      item = (int)((long long)blockIdx.x * items / gridDim.x);
+      end = (int)((long long)(blockIdx.x + 1) * items / gridDim.x);
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return item < end; }
+  __device__ __forceinline__ int qt(int j) const { return rev ? nq - 1 - j : j; }
+  __device__ __forceinline__ bool next_reuses() const {
+    return nq > 1 && item + 1 < end && (item + 1) / n_kv == item / n_kv;
+  }
+  __device__ __forceinline__ void advance() {
+    const bool r = next_reuses();
+    rev = r && !rev;
+    reuse = r;
+    if (item + 1 < end || ch == 0) {
+      ++item;
+    } else {  // this CTA's next chunk
+      chunk += gridDim.x;
+      item = chunk * ch;
+      end = min(item + ch, items);
+    }
   }
 };
 
@@ -2343,20 +2386,22 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         load_tile_sw32<NA, RB>(b, ma, &slot_full[slot], t);
         load_tile_sw32<NA, RB>(b + Cfg::TILE, mb, &slot_full[slot], t);
       };
-      int item = blockIdx.x;
-      if (item < p.items) {
+      BwdWalk wk(p);
+      if (wk.valid()) {
         int outer, h, kvt;
-        decomp(item, outer, h, kvt);
+        decomp(wk.item, outer, h, kvt);
         fill(rg.kv, &mp.k[1], &mp.v[1], bwd_coord(p, outer, h, kvt));
       }
-      for (; item < p.items; item += gridDim.x) {
+      while (wk.valid()) {
         int outer, h, kvt;
-        decomp(item, outer, h, kvt);
-        for (int j = 0; j < nq; ++j) fill(rg.o[j & 1], &mp.q[1], &mp.dout[1], bwd_coord(p, outer, h, j));
-        rg.next_item(nq);
-        if (item + (int)gridDim.x < p.items) {  // the next item's K, V behind the last query tile
+        decomp(wk.item, outer, h, kvt);
+        for (int j = wk.reuse ? 1 : 0; j < nq; ++j)
+          fill(rg.o[j & 1], &mp.q[1], &mp.dout[1], bwd_coord(p, outer, h, wk.qt(j)));
+        rg.next_item(nq, wk.next_reuses());
+        wk.advance();
+        if (wk.valid()) {  // the next item's K, V behind the last query tile
           int o2, h2, k2;
-          decomp(item + gridDim.x, o2, h2, k2);
+          decomp(wk.item, o2, h2, k2);
           fill(rg.kv, &mp.k[1], &mp.v[1], bwd_coord(p, o2, h2, k2));
         }
       }
@@ -2389,11 +2434,11 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     };
     // S^T of tile g + 1 goes out as soon as the compute warps have read tile g out of TMEM; dP^T of
     // tile g + 1 behind tile g's dV, which reads P^T from dP^T's columns (TS form: no smem for P)
-    auto issue_s = [&](uint32_t gg, int j, bool first_of_item) {
+    auto issue_s = [&](uint32_t gg, int j, bool first_of_item, bool reused) {
       const uint32_t qa = smem_u32(smem + rg.o[j & 1] * 2 * Cfg::TILE);
       const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE);
       if (first_of_item) wait_slot(rg.kv);
-      wait_slot(rg.o[j & 1]);
+      if (!reused) wait_slot(rg.o[j & 1]);  // a reused tile's {Q, dO} are in the slot already
       if (gg >= 1) mbar_wait(s_free, (gg - 1) & 1);  // S^T / dP^T of the previous tile read out of TMEM
       tc_fence_after();
       if (lane_id() == 0) { const uint32_t g = gg; BWD_STAMP(3); }
@@ -2412,7 +2457,7 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
       }
       __syncwarp();
     };
-    auto issue_bc = [&](uint32_t gg, int j, uint32_t itx) {
+    auto issue_bc = [&](uint32_t gg, int j, uint32_t itx, bool keep) {
       const int qs = rg.o[j & 1];
       const uint32_t qa = smem_u32(smem + qs * 2 * Cfg::TILE), da = qa + Cfg::TILE;
       const uint32_t kb = smem_u32(smem + rg.kv * 2 * Cfg::TILE);
@@ -2432,7 +2477,7 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
           umma_bf16_ts(tdV, pa, bmn(da, kk), idK, acc0 | (kk != 0));
           umma_bf16_ts(tdK, pa + 16, bmn(qa, kk), idK, acc0 | (kk != 0));
         }
-        umma_commit(&slot_empty[qs]);  // Q and dO read (dV, dK issued): the producer may refill the slot
+        if (!keep) umma_commit(&slot_empty[qs]);  // Q and dO read (dV, dK issued): the producer may refill the slot
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ = dS K: 16 keys per step; dS MN-major (queries contiguous)
           umma_bf16_ss(tdQ, make_sdesc(dsb + kk * 2048, 16384, 1024, SW_128B), bmn(kb, kk), idQ, kk != 0);
@@ -2442,15 +2487,16 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
       __syncwarp();
     };
     uint32_t it = 0, g = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x, ++it) {
-      issue_s(g, 0, true);
+    for (BwdWalk wk(p); wk.valid(); wk.advance(), ++it) {
+      const bool rn = wk.next_reuses();  // the last tile's slot is kept for the next item
+      issue_s(g, 0, true, wk.reuse);
       issue_dp(0);
       for (int j = 0; j < nq; ++j, ++g) {
-        if (j + 1 < nq) issue_s(g + 1, j + 1, false);
-        issue_bc(g, j, it);
+        if (j + 1 < nq) issue_s(g + 1, j + 1, false, false);
+        issue_bc(g, j, it, rn && j == nq - 1);
         if (j + 1 < nq) issue_dp(j + 1);
       }
-      rg.next_item(nq);
+      rg.next_item(nq, rn);
     }
   } else if (warp >= 4 && warp < 4 + 4 * Cfg::NWG) {
     // Four compute warpgroups share each key row (TMEM lane quadrant = warp % 4): warpgroup hw owns
@@ -2471,11 +2517,11 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     // lse2 and D / sqrt(Dh) of the query this thread stages (threads row < 32 of each warpgroup: query
     // 32 hw + row), copied global -> smem by cp.async one tile ahead (no registers held across the tile,
     // the latency off the critical path); padding queries get lse2 = +inf (P = 0), D = 0
-    auto fetch = [&](int item, int j, uint32_t vbuf) {
+    auto fetch = [&](bool valid, int item, int j, uint32_t vbuf) {
       if (row >= 32) return;
       long tok = -1;
       int h = 0;
-      if (item < p.items) {
+      if (valid) {
         int outer, kvt;
         decomp(item, outer, h, kvt);
         tok = row_token(p, bwd_coord(p, outer, h, j), 32 * hw + row);
@@ -2489,9 +2535,10 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         st_shared_f32(vbuf + 512 + row * 4, 0.f);
       }
     };
-    fetch(blockIdx.x, 0, smem_u32(sVec + hw * 32));
     uint32_t g = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    BwdWalk wk(p);
+    fetch(wk.valid(), wk.item, wk.qt(0), smem_u32(sVec + hw * 32));
+    for (; wk.valid(); wk.advance()) {
       for (int j = 0; j < nq; ++j, ++g) {
         const uint32_t vb = smem_u32(sVec + (g & 1) * 256 + hw * 32);  // this warpgroup's 32 queries
         asm volatile("cp.async.wait_all;" ::: "memory");               // this tile's lse2 / D landed
@@ -2499,8 +2546,13 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
         if (threadIdx.x == 128) BWD_STAMP(0);
         named_bar_sync(bar_wg, 128);
         // the next tile's values go to the other buffer (its readers finished before this barrier)
-        if (j + 1 < nq) fetch(item, j + 1, vnext);
-        else fetch(item + gridDim.x, 0, vnext);
+        if (j + 1 < nq) {
+          fetch(true, wk.item, wk.qt(j + 1), vnext);
+        } else {
+          BwdWalk nx = wk;
+          nx.advance();
+          fetch(nx.valid(), nx.item, nx.qt(0), vnext);
+        }
         mbar_wait(s_full, g & 1);
         tc_fence_after();
         if (threadIdx.x == 128) BWD_STAMP(1);
@@ -2586,13 +2638,13 @@ __global__ void __launch_bounds__(BwdCfg<NA, RB>::THREADS, 1)
     constexpr uint32_t kBarEpi = 1 + Cfg::NWG;
     const uint32_t s0 = smem_u32(sDQ);
     uint32_t g = 0;
-    for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+    for (BwdWalk wk(p); wk.valid(); wk.advance()) {
       int outer, h, kvt;
-      decomp(item, outer, h, kvt);
+      decomp(wk.item, outer, h, kvt);
       for (int j = 0; j < nq; ++j, ++g) {
         mbar_wait(dq_full, g & 1);
         tc_fence_after();
-        const TileCoord tq = bwd_coord(p, outer, h, j);
+        const TileCoord tq = bwd_coord(p, outer, h, wk.qt(j));
         if (elected) bulk_wait_group_read0();  // the previous reduce / stores have read sDQ
         named_bar_sync(kBarEpi, 128);
         if (accum) {
@@ -2962,7 +3014,14 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
       return err;
     attr[p.G > 1] = true;
   }
-  const int grid = p.items < num_sms ? p.items : num_sms;
+  // item walk (BwdWalk): pairs of key tiles when a sequence has several (the second reuses the first's
+  // last {Q, dO}: scripts/fmha_bwd_walk_ab.py measured 387 -> 384 us spatial; longer chunks lose L2
+  // locality, 447-464 us); one contiguous range per CTA for one-tile sequences (consecutive items are
+  // the heads of the same tokens: temporal 107 -> 102 us).  DSP_FMHA_BWD_CH overrides (A/B).
+  static const int walk_env = [] { const char* e = std::getenv("DSP_FMHA_BWD_CH"); return e ? std::atoi(e) : -1; }();
+  p.walk_ch = walk_env >= 0 ? walk_env : (p.n_qt > 1 ? 2 : 0);
+  const int units = p.walk_ch > 0 ? (p.items + p.walk_ch - 1) / p.walk_ch : p.items;
+  const int grid = units < num_sms ? units : num_sms;
   err = launch_k(kern, dim3(grid), dim3(Cfg::THREADS), Cfg::SMEM, st, 1, mp, p, lse, (const float*)dvec, accum);
   if (err != cudaSuccess) return err;
   if (accum) return launch_dq_convert(tok, C, dq_acc, dqkv, st);
