@@ -115,7 +115,8 @@ dsp_status_t dsp_attention_core_lse(dsp_ctx_t ctx, int64_t B, int64_t T_loc, int
  * S^T = K Q^T, P^T = exp2(S^T scale - lse), dP^T = V dO^T, dS^T = P^T (dP^T - rowsum(dO o O)) / sqrt(Dh)
  * (P^T rounded to bf16 once, the same values in dV and dS), dV += P^T dO, dK += dS^T Q, dQ += dS K
  * (f32 TMA reduce-add across key tiles; one bf16 store when the sequence is one key tile).  Workspace >=
- * dsp_attention_bwd_workspace_bytes.  Errors: NULL, UNSUPPORTED, ALIGNMENT, WORKSPACE, CUDA. */
+ * dsp_attention_bwd_workspace_bytes.  Errors: NULL, UNSUPPORTED (head dim != 72, C > 2048, sequence
+ * length neither dividing nor a multiple of 128), ALIGNMENT, WORKSPACE, CUDA. */
 size_t dsp_attention_bwd_workspace_bytes(int64_t tok, int64_t C, int32_t num_heads);
 dsp_status_t dsp_attention_core_bwd(dsp_ctx_t ctx, int64_t B, int64_t T_loc, int64_t S_loc, int64_t C,
                                     int32_t num_heads, dsp_dim_t dim, const void* qkv, const void* o,

@@ -211,28 +211,48 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ p
   }
 }
 
-// one thread per (token, head): Dh / 8 vectors of dO and O
+// one warp per token row: lane l reads the row's 16-B vectors l, l + 32, ... of O and dO (each
+// warp load instruction covers 512 contiguous bytes), the per-vector dot products go to shared memory
+// and lane h adds its head's Dh / 8 of them in column order.  C <= 8 * 32 * kDvecV.
+constexpr int kDvecV = 8;
 __global__ void __launch_bounds__(256) attn_bwd_dvec_kernel(const __nv_bfloat16* __restrict__ o,
                                                             const __nv_bfloat16* __restrict__ dout,
-                                                            float* __restrict__ dvec, long n, int NH, int Dh) {
+                                                            float* __restrict__ dvec, long tok, int NH, int Dh) {
+  __shared__ float part[8][32 * kDvecV];
   griddep_wait();
   griddep_launch_dependents();
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const long tok = i / NH;
-  const int h = (int)(i % NH);
-  const size_t base = (size_t)tok * NH * Dh + (size_t)h * Dh;
-  const uint4* ov = reinterpret_cast<const uint4*>(o + base);
-  const uint4* dv = reinterpret_cast<const uint4*>(dout + base);
-  float acc = 0.f;
-  for (int j = 0; j < Dh / 8; ++j) {
-    float a[8], b[8];
-    unpack8(ov[j], a);
-    unpack8(dv[j], b);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long r = (long)blockIdx.x * 8 + w;
+  if (r >= tok) return;
+  const int nv = NH * Dh / 8;
+  const uint4* ov = reinterpret_cast<const uint4*>(o + r * NH * Dh);
+  const uint4* dv = reinterpret_cast<const uint4*>(dout + r * NH * Dh);
+  uint4 a[kDvecV], b[kDvecV];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) acc = fmaf(a[t], b[t], acc);
+  for (int k = 0; k < kDvecV; ++k)
+    if (lane + 32 * k < nv) {
+      a[k] = ov[lane + 32 * k];
+      b[k] = dv[lane + 32 * k];
+    }
+#pragma unroll
+  for (int k = 0; k < kDvecV; ++k)
+    if (lane + 32 * k < nv) {
+      float fa[8], fb[8];
+      unpack8(a[k], fa);
+      unpack8(b[k], fb);
+      float acc = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc = fmaf(fa[t], fb[t], acc);
+      part[w][lane + 32 * k] = acc;
+    }
+  __syncwarp();
+  const int vh = Dh / 8;
+  const float sc = rsqrtf((float)Dh);  // pre-scaled: dS = P (dP - D) / sqrt(Dh) in the FMHA backward
+  for (int h = lane; h < NH; h += 32) {
+    float acc = 0.f;
+    for (int j = 0; j < vh; ++j) acc += part[w][h * vh + j];
+    dvec[r * NH + h] = acc * sc;
   }
-  dvec[i] = acc * rsqrtf((float)Dh);  // pre-scaled by 1 / sqrt(Dh): dS = P (dP - D) / sqrt(Dh) in the FMHA backward
 }
 
 // out[c][r] = in[r][c] (bf16), 64 x 64 tiles through padded smem: 16-B row-segment loads, 4-B stores
@@ -336,11 +356,10 @@ cudaError_t launch_ln_bwd(int64_t rows, int64_t C, const void* x, const void* ga
 
 cudaError_t launch_attn_bwd_dvec(int64_t tok, int NH, int Dh, const void* o, const void* dout, float* dvec,
                                  cudaStream_t st) {
-  const long n = tok * NH;
-  if (n == 0) return cudaSuccess;
-  if (Dh % 8 != 0) return cudaErrorNotSupported;
-  return launch_k(attn_bwd_dvec_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1,
-                  (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, n, NH, Dh);
+  if (tok == 0 || NH == 0) return cudaSuccess;
+  if (Dh % 8 != 0 || (int64_t)NH * Dh > 8 * 32 * kDvecV) return cudaErrorNotSupported;
+  return launch_k(attn_bwd_dvec_kernel, dim3((unsigned)((tok + 7) / 8)), dim3(256), 0, st, 1,
+                  (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, (long)tok, NH, Dh);
 }
 
 cudaError_t launch_transpose_bf16(const void* in, void* out, int64_t R, int64_t Cc, cudaStream_t st) {

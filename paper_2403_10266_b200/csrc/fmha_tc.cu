@@ -2938,8 +2938,8 @@ cudaError_t launch_fmha_bwd_bf16(const void* qkv, const void* o, const void* dou
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)p.Dh));
   p.spatial = (dim == DSP_DIM_S);
   p.L = (int)(p.spatial ? S_loc : T_loc);
-  if (NH <= 0 || C % NH != 0 || p.Dh != 72) {
-    if (why) *why = "attention backward: head dim 72 only (the paper's C = 1152, 16 heads)";
+  if (NH <= 0 || C % NH != 0 || p.Dh != 72 || C > 2048) {
+    if (why) *why = "attention backward: head dim 72 only (the paper's C = 1152, 16 heads), C <= 2048";
     return cudaErrorNotSupported;
   }
   if (p.L <= 0 || !(p.L % 128 == 0 || 128 % p.L == 0)) {
