@@ -1715,7 +1715,7 @@ TrainWs train_ws(const dsp_shape_t* s, int world, int num_sms) {
   const int64_t shapes[4][2] = {{3 * C, C}, {C, C}, {4 * C, C}, {C, 4 * C}};
   for (auto& sh : shapes) wp = std::max(wp, wgrad_part_bytes(sh[0], sh[1], tok, num_sms));
   w.wpart = take(wp);
-  w.wt = take(4 * C * C * 2);  // one transposed weight (dgrad on the K-major GEMM path)
+  w.wt = take(16 * C * C * 2);  // the six transposed weights (dgrad on the K-major GEMM path; WtOff)
   w.send = take(act);
   w.recv = take(act);
   w.total = o;
@@ -1787,15 +1787,28 @@ dsp_status_t wgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* d
   return DSP_OK;
 }
 
+// element offsets of the transposed weights in ws.wt (C^2 units): fc2, fc1, o_t, qkv_t, o_s, qkv_s
+struct WtOff {
+  static constexpr int64_t fc2 = 0, fc1 = 4, o_t = 8, qkv_t = 9, o_s = 12, qkv_s = 13;
+};
+
+// W^T [K, N] of W [N, K] (the dgrad's K-major operand)
+dsp_status_t transpose_w(dsp_ctx_t ctx, const void* W, int64_t N, int64_t K, void* wt, cudaStream_t st) {
+  cudaError_t e = launch_transpose_bf16(W, wt, N, K, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "weight transpose");
+  ctx->launches += 1;
+  return DSP_OK;
+}
+
+// dX = dY W: wt == nullptr reads W as an MN-major operand; else wt holds W^T for the forward's
+// K-major GEMM, transposed here unless wt_ready (the block backward transposes them up front)
 dsp_status_t dgrad(dsp_ctx_t ctx, int64_t M, int64_t N, int64_t K, const void* dY, const void* W, const void* u,
-                   void* dX, cudaStream_t st, void* wt = nullptr) {
+                   void* dX, cudaStream_t st, void* wt = nullptr, bool wt_ready = false) {
   std::string why;
   cudaError_t e;
-  if (wt) {  // W^T [K, N] once (16 C^2 elements per block step, ~13 us in all), then the forward's K-major GEMM
-    e = launch_transpose_bf16(W, wt, N, K, st);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "weight transpose");
+  if (wt) {
+    if (!wt_ready) DSP_TRY(transpose_w(ctx, W, N, K, wt, st));
     e = launch_gemm_bf16_dgrad_kmajor(dY, wt, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
-    ctx->launches += 1;
   } else {  // W read as an MN-major operand
     e = launch_gemm_bf16_dgrad(dY, W, u, dX, M, K, N, u ? EPI_GELU_BWD : DSP_EPI_NONE, ctx->num_sms, st, &why);
   }
@@ -1852,6 +1865,17 @@ dsp_status_t side_join(dsp_ctx_t ctx, const Side& sd, int k, cudaStream_t st) {
   DSP_CUDA(ctx, cudaStreamWaitEvent(st, sd.done[k], 0), "join");
   return DSP_OK;
 }
+// fn(stream) on the side stream after what st has issued so far, completion recorded as done[k]
+template <class F>
+dsp_status_t side_run(dsp_ctx_t ctx, const Side& sd, int k, cudaStream_t st, F&& fn) {
+  static const bool off = [] { const char* e = std::getenv("DSP_BWD_SIDE"); return e && e[0] == '0'; }();
+  if (off) return fn(st);
+  DSP_CUDA(ctx, cudaEventRecord(sd.fork, st), "fork");
+  DSP_CUDA(ctx, cudaStreamWaitEvent(sd.s, sd.fork, 0), "fork wait");
+  DSP_TRY(fn(sd.s));
+  DSP_CUDA(ctx, cudaEventRecord(sd.done[k], sd.s), "side done");
+  return DSP_OK;
+}
 
 // one attention stage's backward: from dout (gradient of the stage output, also the residual
 // gradient) and the saved h / qkv / o / lse, dres_out = dout + LN^T(W_qkv^T (attn^T (W_o^T dout))).
@@ -1860,13 +1884,13 @@ dsp_status_t attn_stage_bwd(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, 
                             const void* zin, const void* ln_w, const void* w_qkv, const void* w_o, const void* h,
                             const void* qkv, const void* o, const float* lse, const void* dout, void* dres_out,
                             float* g_lnw, float* g_lnb, float* g_qkv, float* g_o, const TrainWs& L, uint8_t* ws,
-                            cudaStream_t st, const Side& sd, int k_o, int join_big) {
+                            cudaStream_t st, const Side& sd, int k_o, int join_big, void* wt_o, void* wt_qkv) {
   const int64_t tok = s->B * T_loc * S_loc, C = s->C;
   void* dob = ws + L.dob;
   void* dqkv = ws + L.big;
   void* dh = ws + L.dh;
   float* part = reinterpret_cast<float*>(ws + L.wpart);
-  DSP_TRY(dgrad(ctx, tok, C, C, dout, w_o, nullptr, dob, st, ws + L.wt));           // dO = dout W_o
+  DSP_TRY(dgrad(ctx, tok, C, C, dout, w_o, nullptr, dob, st, wt_o, true));          // dO = dout W_o
   DSP_TRY(side_wgrad(ctx, sd, k_o, tok, C, C, dout, o, g_o, part, st));             // dW_o += dout^T O
   DSP_TRY(side_join(ctx, sd, join_big, st));                                        // ws.big free
   std::string why;
@@ -1875,7 +1899,7 @@ dsp_status_t attn_stage_bwd(dsp_ctx_t ctx, const dsp_shape_t* s, int64_t T_loc, 
                                        dim, ctx->num_sms, st, &why);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "attention backward", why);
   ctx->launches += 4;
-  DSP_TRY(dgrad(ctx, tok, 3 * C, C, dqkv, w_qkv, nullptr, dh, st, ws + L.wt));      // dh = dqkv W_qkv
+  DSP_TRY(dgrad(ctx, tok, 3 * C, C, dqkv, w_qkv, nullptr, dh, st, wt_qkv, true));   // dh = dqkv W_qkv
   DSP_TRY(side_wgrad(ctx, sd, k_o + 1, tok, 3 * C, C, dqkv, h, g_qkv, part, st));   // dW_qkv += dqkv^T h
   if (dres_out == dout) DSP_TRY(side_join(ctx, sd, k_o, st));                       // in place over dout
   return ln_bwd(ctx, tok, C, zin, ln_w, dh, dout, dres_out, g_lnw, g_lnb, reinterpret_cast<float*>(ws + L.lnpart), st);
@@ -1989,12 +2013,25 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   }
   Side sd;
   DSP_TRY(side_init(ctx, &sd));
+  // the dgrads' transposed weights: W2^T here, the other five on the side stream ahead of its wgrads
+  // (event done[6]), so they run beside the first dgrad instead of in front of each
+  const int64_t C2 = C * C;
+  auto wt = [&](int64_t off) -> void* { return ws + L.wt + off * C2 * 2; };  // bf16, WtOff units
+  DSP_TRY(transpose_w(ctx, w->w_fc2, C, 4 * C, wt(WtOff::fc2), st));
+  DSP_TRY(side_run(ctx, sd, 6, st, [&](cudaStream_t ss) -> dsp_status_t {
+    DSP_TRY(transpose_w(ctx, w->w_fc1, 4 * C, C, wt(WtOff::fc1), ss));
+    DSP_TRY(transpose_w(ctx, w->w_o_t, C, C, wt(WtOff::o_t), ss));
+    DSP_TRY(transpose_w(ctx, w->w_qkv_t, 3 * C, C, wt(WtOff::qkv_t), ss));
+    DSP_TRY(transpose_w(ctx, w->w_o_s, C, C, wt(WtOff::o_s), ss));
+    return transpose_w(ctx, w->w_qkv_s, 3 * C, C, wt(WtOff::qkv_s), ss);
+  }));
   // 2. MLP backward: du = (dz W2) * gelu'(u); dW2 += dz^T g; dh3 = du W1; dW1 += du^T h3 (wgrads 0, 1 aside)
   void* du = ws + L.big;
   DSP_TRY(side_wgrad(ctx, sd, 0, tok, C, 4 * C, dz, sv + SL.g, g->w_fc2, part, st));
-  DSP_TRY(dgrad(ctx, tok, C, 4 * C, dz, w->w_fc2, sv + SL.u, du, st, ws + L.wt));
+  DSP_TRY(dgrad(ctx, tok, C, 4 * C, dz, w->w_fc2, sv + SL.u, du, st, wt(WtOff::fc2), true));
   DSP_TRY(side_wgrad(ctx, sd, 1, tok, 4 * C, C, du, sv + SL.h3, g->w_fc1, part, st));
-  DSP_TRY(dgrad(ctx, tok, 4 * C, C, du, w->w_fc1, nullptr, ws + L.dh, st, ws + L.wt));
+  DSP_TRY(side_join(ctx, sd, 6, st));  // the five transposes done
+  DSP_TRY(dgrad(ctx, tok, 4 * C, C, du, w->w_fc1, nullptr, ws + L.dh, st, wt(WtOff::fc1), true));
   // dy2 = dz + LN3^T dh3
   void* dy2 = ws + L.dyb;
   DSP_TRY(ln_bwd(ctx, tok, C, sv + SL.y2, w->ln3_w, ws + L.dh, dz, dy2, g->ln3_w, g->ln3_b,
@@ -2002,7 +2039,8 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   // 3. temporal stage backward on the S-shard: dy1s = dy2 + LN2^T(...) (in place over dy2)
   DSP_TRY(attn_stage_bwd(ctx, s, s->T, Sn, DSP_DIM_T, sv + SL.y1s, w->ln2_w, w->w_qkv_t, w->w_o_t, sv + SL.h2,
                          sv + SL.qkv_t, sv + SL.o_t, reinterpret_cast<const float*>(sv + SL.lse_t), dy2, dy2,
-                         g->ln2_w, g->ln2_b, g->w_qkv_t, g->w_o_t, L, ws, st, sd, 2, 1));
+                         g->ln2_w, g->ln2_b, g->w_qkv_t, g->w_o_t, L, ws, st, sd, 2, 1, wt(WtOff::o_t),
+                         wt(WtOff::qkv_t)));
   // 4. dy1 = switch_{S->T}(dy1s): the adjoint of the forward's T->S switch
   void* dy1 = dy2;
   if (N > 1) {
@@ -2013,7 +2051,7 @@ dsp_status_t dsp_st_block_backward(dsp_ctx_t ctx, const dsp_shape_t* s, const ds
   // 5. spatial stage backward on the T-shard: dx = dy1 + LN1^T(...)
   DSP_TRY(attn_stage_bwd(ctx, s, Tn, s->S, DSP_DIM_S, x, w->ln1_w, w->w_qkv_s, w->w_o_s, sv + SL.h1, sv + SL.qkv_s,
                          sv + SL.o_s, reinterpret_cast<const float*>(sv + SL.lse_s), dy1, dx, g->ln1_w, g->ln1_b,
-                         g->w_qkv_s, g->w_o_s, L, ws, st, sd, 4, 3));
+                         g->w_qkv_s, g->w_o_s, L, ws, st, sd, 4, 3, wt(WtOff::o_s), wt(WtOff::qkv_s)));
   return side_join(ctx, sd, 5, st);  // every weight gradient done before the call returns (stream order)
 }
 
