@@ -13,6 +13,7 @@
 // All bound by HBM bytes: one 16-B vector per lane access, rows across warps.
 #include <cuda_bf16.h>
 
+
 #include "dsp_internal.h"
 #include "sm100.cuh"
 
@@ -147,7 +148,9 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
 // of kLnRows rows per CTA.  Thread (x, y) = 8 columns (one 16-B vector of each row: a row group reads
 // whole rows, coalesced) of rows r0 + y, r0 + y + kLnRG, ...; the kLnRG row groups are then added in
 // y order.  part[chunk][0:C] = dgamma, part[chunk][C:2C] = dbeta, summed in chunk order after.
-constexpr int kLnRows = 64, kLnRG = 6;
+// kLnRG = 3: 480 threads at C = 1152, two CTAs per SM (the 256 chunks in one wave); measured per
+// dsp_layer_norm_bwd call (scripts/ln_bwd_ab.py): 6 groups 55.9 us, 4 59.5, 3 52.8, 2 58.1, 1 78.8
+constexpr int kLnRows = 64, kLnRG = 3;
 __global__ void __launch_bounds__(1024) ln_bwd_param_kernel(const __nv_bfloat16* __restrict__ x,
                                                             const __nv_bfloat16* __restrict__ dh,
                                                             const float2* __restrict__ stats,
