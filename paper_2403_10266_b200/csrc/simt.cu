@@ -134,11 +134,15 @@ __global__ void layer_norm_kernel(const T* __restrict__ x, const T* __restrict__
   }
 }
 
-// bf16 LayerNorm specialised for C % 256 == 0 ... general C handled above; this variant
-// keeps 16-B vector accesses (C*2 % 16 == 0) and the whole row in registers (C <= 2048).
-__global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
-                                           const __nv_bfloat16* __restrict__ b, float eps, __nv_bfloat16* y, long rows,
-                                           int C) {
+// bf16 LayerNorm for C % 8 == 0: 16-B vector accesses and the whole row in registers (C <= 256
+// kMaxV), the arithmetic on bf16 pairs with packed f32x2 adds / multiplies / FMAs (ncu of the scalar
+// version: issue-active 75 %, i.e. bound by its instruction count, not by HBM).
+__device__ __forceinline__ float2 bf16x2_f2(uint32_t v) { return make_float2(bf16lo(v), bf16hi(v)); }
+template <int kMaxV>
+__global__ void __launch_bounds__(256) layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                  const __nv_bfloat16* __restrict__ g,
+                                                                  const __nv_bfloat16* __restrict__ b, float eps,
+                                                                  __nv_bfloat16* y, long rows, int C) {
   griddep_wait();
   griddep_launch_dependents();
   const long r = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -146,36 +150,36 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
   if (r >= rows) return;
   const int nv = C / 8;  // 16-B vectors per row
   const uint4* xr = reinterpret_cast<const uint4*>(x + r * C);
-  constexpr int kMaxV = 8;  // up to 8 vectors per lane -> C <= 2048
   uint4 buf[kMaxV];
-  float s = 0.f;
+  float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < kMaxV; ++k) {
-    const int vi = lane + 32 * k;
-    if (vi < nv) {
-      buf[k] = xr[vi];
-      const uint32_t w[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) buf[k] = xr[lane + 32 * k];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) s += __uint_as_float(w[t] << 16) + __uint_as_float(w[t] & 0xFFFF0000u);
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) {
+      s2 = fadd2(s2, fadd2(bf16x2_f2(buf[k].x), bf16x2_f2(buf[k].y)));
+      s2 = fadd2(s2, fadd2(bf16x2_f2(buf[k].z), bf16x2_f2(buf[k].w)));
     }
-  }
+  float s = s2.x + s2.y;
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   const float mean = s / C;
-  float q = 0.f;
+  const float2 nm = make_float2(-mean, -mean);
+  float2 q2 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int k = 0; k < kMaxV; ++k) {
-    const int vi = lane + 32 * k;
-    if (vi < nv) {
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) {
       const uint32_t w[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const float a = __uint_as_float(w[t] << 16) - mean, c = __uint_as_float(w[t] & 0xFFFF0000u) - mean;
-        q += a * a + c * c;
+        const float2 d = fadd2(bf16x2_f2(w[t]), nm);
+        q2 = ffma2(d, d, q2);
       }
     }
-  }
+  float q = q2.x + q2.y;
   for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
   const float rstd = rsqrtf(q / C + eps);
+  const float2 rs = make_float2(rstd, rstd);
   const uint4* gv = reinterpret_cast<const uint4*>(g);
   const uint4* bv = reinterpret_cast<const uint4*>(b);
   uint4* yr = reinterpret_cast<uint4*>(y + r * C);
@@ -190,18 +194,14 @@ __global__ void layer_norm_bf16_vec_kernel(const __nv_bfloat16* __restrict__ x, 
       uint32_t o[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const float lo = (__uint_as_float(w[t] << 16) - mean) * rstd * __uint_as_float(gw[t] << 16) +
-                         __uint_as_float(bw[t] << 16);
-        const float hi = (__uint_as_float(w[t] & 0xFFFF0000u) - mean) * rstd * __uint_as_float(gw[t] & 0xFFFF0000u) +
-                         __uint_as_float(bw[t] & 0xFFFF0000u);
-        __nv_bfloat162 p2 = __floats2bfloat162_rn(lo, hi);
-        o[t] = *reinterpret_cast<uint32_t*>(&p2);
+        const float2 xh = fmul2(fadd2(bf16x2_f2(w[t]), nm), rs);
+        const float2 v = ffma2(xh, bf16x2_f2(gw[t]), bf16x2_f2(bw[t]));
+        o[t] = pack_bf16x2(v.x, v.y);
       }
       yr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
-
 
 #ifndef DSP_ROWSTATS_R
 #define DSP_ROWSTATS_R 1  // measured: 1 row per warp 14.2 us, 2: 16.2, 4: 28.5 (LN1 stage, blk N=1)
@@ -426,8 +426,9 @@ cudaError_t launch_layer_norm(int dtype, int64_t rows, int64_t C, const void* x,
     return launch_k(layer_norm_kernel<float>, dim3(blocks), dim3(threads), 0, st, 1, (const float*)x, (const float*)g,
                     (const float*)b, eps, (float*)y, rows, (int)C);
   } else if (C % 8 == 0 && C <= 2048) {
-    return launch_k(layer_norm_bf16_vec_kernel, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x,
-                    (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows, (int)C);
+    auto kern = C <= 256 * 5 ? layer_norm_bf16_vec_kernel<5> : layer_norm_bf16_vec_kernel<8>;
+    return launch_k(kern, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
+                    (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows, (int)C);
   } else {
     return launch_k(layer_norm_kernel<__nv_bfloat16>, dim3(blocks), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x,
                     (const __nv_bfloat16*)g, (const __nv_bfloat16*)b, eps, (__nv_bfloat16*)y, rows, (int)C);
