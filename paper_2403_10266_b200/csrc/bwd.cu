@@ -69,7 +69,6 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
   // the row stays packed (bf16) in registers and is unpacked per pass: ~half the registers of fp32
   // copies, so three CTAs fit per SM and more rows are in flight
   uint4 xp[kMaxV], hp[kMaxV], rp[kMaxV];
-  float s = 0.f;
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k) {
     const int vi = lane + 32 * k;
@@ -77,66 +76,71 @@ __global__ void __launch_bounds__(256) ln_bwd_bf16_kernel(const __nv_bfloat16* _
       xp[k] = xr[vi];
       hp[k] = hr[vi];
       if (rr) rp[k] = rr[vi];
-      float f[8];
-      unpack8(xp[k], f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s += f[i];
     }
   }
+  // arithmetic on bf16 pairs with packed f32x2 operations (the kernel is issue-bound, not HBM-bound)
+  auto f2 = [](uint32_t v) { return make_float2(bf16lo(v), bf16hi(v)); };
+  auto w4 = [](const uint4& u, int t) { return t == 0 ? u.x : t == 1 ? u.y : t == 2 ? u.z : u.w; };
+  float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < kMaxV; ++k)
+    if (lane + 32 * k < nv) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s2 = fadd2(s2, f2(w4(xp[k], t)));
+    }
+  float s = s2.x + s2.y;
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   const float mean = s / C;
-  float q = 0.f;
+  const float2 nm = make_float2(-mean, -mean);
+  float2 q2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k)
     if (lane + 32 * k < nv) {
-      float f[8];
-      unpack8(xp[k], f);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float d = f[i] - mean;
-        q += d * d;
+      for (int t = 0; t < 4; ++t) {
+        const float2 d = fadd2(f2(w4(xp[k], t)), nm);
+        q2 = ffma2(d, d, q2);
       }
     }
+  float q = q2.x + q2.y;
   for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
   const float rstd = rsqrtf(q / C + eps);
+  const float2 rs = make_float2(rstd, rstd);
   // sums of g = dh * gamma and of g * xhat
-  float s1 = 0.f, s2 = 0.f;
+  float2 a1 = make_float2(0.f, 0.f), a2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k)
     if (lane + 32 * k < nv) {
-      float xf[8], hf[8], gm[8];
-      unpack8(xp[k], xf);
-      unpack8(hp[k], hf);
-      unpack8(gvec[lane + 32 * k], gm);
+      const uint4 gm = gvec[lane + 32 * k];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float g = hf[i] * gm[i];
-        s1 += g;
-        s2 += g * ((xf[i] - mean) * rstd);
+      for (int t = 0; t < 4; ++t) {
+        const float2 g = fmul2(f2(w4(hp[k], t)), f2(w4(gm, t)));
+        a1 = fadd2(a1, g);
+        a2 = ffma2(g, fmul2(fadd2(f2(w4(xp[k], t)), nm), rs), a2);
       }
     }
+  float s1 = a1.x + a1.y, s2s = a2.x + a2.y;
   for (int off = 16; off; off >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    s2s += __shfl_xor_sync(0xffffffffu, s2s, off);
   }
-  const float m1 = s1 / C, m2 = s2 / C;
+  const float m1 = s1 / C, m2 = s2s / C;
+  const float2 nm1 = make_float2(-m1, -m1), nm2 = make_float2(-m2, -m2);
   uint4* dxr = reinterpret_cast<uint4*>(dx + r * C);
 #pragma unroll
   for (int k = 0; k < kMaxV; ++k) {
     const int vi = lane + 32 * k;
     if (vi < nv) {
-      float xf[8], hf[8], gm[8], rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      unpack8(xp[k], xf);
-      unpack8(hp[k], hf);
-      unpack8(gvec[vi], gm);
-      if (rr) unpack8(rp[k], rv);
+      const uint4 gm = gvec[vi];
       uint32_t o[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const float a = rv[2 * t] + rstd * (hf[2 * t] * gm[2 * t] - m1 - (xf[2 * t] - mean) * rstd * m2);
-        const float b = rv[2 * t + 1] +
-                        rstd * (hf[2 * t + 1] * gm[2 * t + 1] - m1 - (xf[2 * t + 1] - mean) * rstd * m2);
-        o[t] = pack_bf16x2(a, b);
+        // dx = dres + rstd (g - m1 - xhat m2)
+        const float2 g = fmul2(f2(w4(hp[k], t)), f2(w4(gm, t)));
+        const float2 xh = fmul2(fadd2(f2(w4(xp[k], t)), nm), rs);
+        const float2 u = ffma2(xh, nm2, fadd2(g, nm1));
+        const float2 v = rr ? ffma2(u, rs, f2(w4(rp[k], t))) : fmul2(u, rs);
+        o[t] = pack_bf16x2(v.x, v.y);
       }
       dxr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
     }
